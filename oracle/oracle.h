@@ -1,0 +1,104 @@
+/*
+ * oracle.h — CPU restatement of the reference lseforge loss path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Nothing in paper_2509_09682_b200/ links, loads or
+ * calls this code; only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may use it, and only as the checker.
+ *
+ * Parity status: PINNED.  Every function below is checked bit-for-bit against
+ * the reference itself compiled in place (oracle/_ref/liblseforge_ref.so, see
+ * oracle/Makefile and tests/test_oracle.py) and against golden vectors from the
+ * reference's own tests (SplitMix64 streams, test_core.cpp:21-52; known answers
+ * in test_cce.cpp / test_ccem.cpp / test_oracles.cpp).
+ *
+ * Layout conventions follow the REFERENCE (not the B200 library):
+ *   E    : n x d  float, row-major   (reference "E", hidden states; B200 "X")
+ *   C    : d x v  float, row-major   (reference "C", classifier;  B200 "E"^T)
+ *   dE   : n x d  double             (GradPair::d_embeddings)
+ *   dC   : d x v  double             (GradPair::d_classifier)
+ *   inds : n x w  int64, slot 0 = positive (NegIndexMatrix)
+ * All accumulation is double, k ascending, exactly as the reference orders it.
+ */
+#ifndef LSEFORGE_ORACLE_H
+#define LSEFORGE_ORACLE_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- SplitMix64 (proj/include/lseforge/rng.hpp:13-60) -------------------- */
+typedef struct {
+  uint64_t seed;
+  uint64_t state;
+} orc_rng;
+
+void orc_rng_init(orc_rng* r, uint64_t seed);              /* rng.hpp:15 */
+uint64_t orc_rng_next(orc_rng* r);                         /* rng.hpp:17-20 */
+uint64_t orc_rng_bounded(orc_rng* r, uint64_t bound);      /* rng.hpp:23-38 */
+double orc_rng_uniform(orc_rng* r);                        /* rng.hpp:41 */
+void orc_rng_derived(const orc_rng* r, uint64_t index, orc_rng* out); /* rng.hpp:45-47 */
+uint64_t orc_mix64(uint64_t z);                            /* rng.hpp:51-55 */
+
+/* ---- test fixtures (proj/tests/support.hpp:27-56) ------------------------- */
+/* Fills E (n*d), C (d*v), targets (n) in the reference draw order. */
+void orc_make_instance(orc_rng* r, size_t n, size_t d, size_t v, double half_width,
+                       float* E, float* C, int64_t* targets);
+/* make_candidates: slot 0 = target, negatives uniform with rejection. */
+void orc_make_candidates(orc_rng* r, const int64_t* targets, size_t n, size_t ns, size_t v,
+                         int64_t* inds);
+/* sample_uniform (proj/src/sampler.cpp:44-75): per-row derived(i) streams.
+ * Returns 0 on success, -1 if a row exhausts retry_cap. */
+int orc_sample_uniform(const int64_t* positives, size_t n, size_t ns, size_t catalog,
+                       uint64_t rng_seed, int retry_cap, int64_t* inds);
+
+/* ---- CCE (proj/src/cce.cpp) ----------------------------------------------- */
+/* cce_forward (cce.cpp:65-145).  pos, lse: n doubles.  Returns the mean loss.
+ * Tiling does not change any per-row operation order in the forward, so no
+ * block parameters are needed for bitwise parity. */
+double orc_cce_forward(const float* E, const float* C, const int64_t* x, size_t n, size_t d,
+                       size_t v, double* pos, double* lse);
+
+/* cce_backward (cce.cpp:147-272).  dE (n*d) and dC (d*v) are OVERWRITTEN.
+ * col_block reproduces the reference's per-column-block partial sums for dE
+ * (cce.cpp:222-231), which is what makes dE bitwise comparable.
+ * Returns skipped_fraction (cce.cpp:264-268); *skipped gets the raw count. */
+double orc_cce_backward(const float* E, const float* C, const int64_t* x, const double* lse,
+                        double upstream, double filter_eps, size_t col_block, size_t n, size_t d,
+                        size_t v, double* dE, double* dC, uint64_t* skipped);
+
+/* Per-shard forward partials for catalog sharding: over columns [v0, v1)
+ * of C only.  m = running max, s = rescaled sum (OnlineLse, numeric.hpp:15-30),
+ * t = target logit if x[i] in [v0,v1) else 0, has_t = 1/0. */
+void orc_cce_forward_partial(const float* E, const float* C, const int64_t* x, size_t n,
+                             size_t d, size_t v, size_t v0, size_t v1, double* m, double* s,
+                             double* t, int32_t* has_t);
+
+/* ---- CCE- (proj/src/ccem.cpp) --------------------------------------------- */
+/* ccem_forward (ccem.cpp:48-105).  inds: n*w.  Returns the mean loss. */
+double orc_ccem_forward(const float* E, const float* C, const int64_t* inds, size_t n, size_t d,
+                        size_t v, size_t w, double* pos, double* lse);
+
+/* ccem_backward_rows (ccem.cpp:107-194).  dE, dC overwritten. */
+void orc_ccem_backward_rows(const float* E, const float* C, const int64_t* inds,
+                            const double* lse, const double* row_upstream, size_t n, size_t d,
+                            size_t v, size_t w, double* dE, double* dC);
+
+/* ---- validation (losses.cpp:48-69, neg_index.cpp:8-28) --------------------
+ * Return 0 if valid, else the first offending row index + 1 (message text is
+ * produced by the host library; the oracle only locates the row). */
+int64_t orc_validate_targets(const int64_t* x, size_t n, size_t v);
+int64_t orc_validate_inds(const int64_t* inds, size_t n, size_t w, size_t v);
+
+/* ---- closed forms (ccem.cpp:207-235, memory_model.cpp:26-74) -------------- */
+/* backend: 0 ce, 1 cem, 2 cce, 3 ccem, 4 bce (backend.hpp:10-16) */
+void orc_estimate_flops(size_t n, size_t d, size_t v, size_t ns, int backend, uint64_t* fwd,
+                        uint64_t* bwd);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,345 @@
+"""ctypes bindings for the CPU checkers under oracle/ (TEST INFRASTRUCTURE).
+
+Two libraries:
+  * ``oracle/liboracle.so``            — the C restatement (oracle/oracle.c)
+  * ``oracle/_ref/liblseforge_ref.so`` — the unmodified reference hot-path sources
+                                          compiled in place (oracle/Makefile)
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline legs import
+this module.  Layouts are the reference's: E n×d float32, C d×v float32,
+outputs float64 (proj/include/lseforge/losses.hpp:15-27).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ORACLE_SO = os.path.join(ROOT, "oracle", "liboracle.so")
+REF_SO = os.path.join(ROOT, "oracle", "_ref", "liblseforge_ref.so")
+
+_f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+_i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
+_i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+_u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+_sz = C.c_size_t
+
+
+def _load(path):
+    if not os.path.exists(path):
+        raise FileNotFoundError(f"{path} missing: run `make -C oracle` (or __graft_entry__.build())")
+    return C.CDLL(path)
+
+
+class _Rng(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("state", C.c_uint64)]
+
+
+_orc = None
+
+
+def orc():
+    global _orc
+    if _orc is None:
+        L = _load(ORACLE_SO)
+        L.orc_rng_init.argtypes = [C.POINTER(_Rng), C.c_uint64]
+        L.orc_rng_next.argtypes = [C.POINTER(_Rng)]
+        L.orc_rng_next.restype = C.c_uint64
+        L.orc_rng_bounded.argtypes = [C.POINTER(_Rng), C.c_uint64]
+        L.orc_rng_bounded.restype = C.c_uint64
+        L.orc_rng_uniform.argtypes = [C.POINTER(_Rng)]
+        L.orc_rng_uniform.restype = C.c_double
+        L.orc_make_instance.argtypes = [C.POINTER(_Rng), _sz, _sz, _sz, C.c_double, _f32p, _f32p, _i64p]
+        L.orc_make_candidates.argtypes = [C.POINTER(_Rng), _i64p, _sz, _sz, _sz, _i64p]
+        L.orc_sample_uniform.argtypes = [_i64p, _sz, _sz, _sz, C.c_uint64, C.c_int, _i64p]
+        L.orc_sample_uniform.restype = C.c_int
+        L.orc_cce_forward.argtypes = [_f32p, _f32p, _i64p, _sz, _sz, _sz, _f64p, _f64p]
+        L.orc_cce_forward.restype = C.c_double
+        L.orc_cce_backward.argtypes = [_f32p, _f32p, _i64p, _f64p, C.c_double, C.c_double, _sz,
+                                       _sz, _sz, _sz, _f64p, _f64p, C.POINTER(C.c_uint64)]
+        L.orc_cce_backward.restype = C.c_double
+        L.orc_cce_forward_partial.argtypes = [_f32p, _f32p, _i64p, _sz, _sz, _sz, _sz, _sz,
+                                              _f64p, _f64p, _f64p, _i32p]
+        L.orc_ccem_forward.argtypes = [_f32p, _f32p, _i64p, _sz, _sz, _sz, _sz, _f64p, _f64p]
+        L.orc_ccem_forward.restype = C.c_double
+        L.orc_ccem_backward_rows.argtypes = [_f32p, _f32p, _i64p, _f64p, _f64p, _sz, _sz, _sz, _sz,
+                                             _f64p, _f64p]
+        L.orc_validate_targets.argtypes = [_i64p, _sz, _sz]
+        L.orc_validate_targets.restype = C.c_int64
+        L.orc_validate_inds.argtypes = [_i64p, _sz, _sz, _sz]
+        L.orc_validate_inds.restype = C.c_int64
+        L.orc_estimate_flops.argtypes = [_sz, _sz, _sz, _sz, C.c_int, C.POINTER(C.c_uint64),
+                                         C.POINTER(C.c_uint64)]
+        _orc = L
+    return _orc
+
+
+_ref = None
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def ref():
+    global _ref
+    if _ref is None:
+        L = _load(REF_SO)
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_rng_stream.argtypes = [C.c_uint64, _u64p, C.c_int]
+        L.ref_make_instance.argtypes = [C.c_uint64, _sz, _sz, _sz, C.c_double, _f32p, _f32p, _i64p]
+        L.ref_make_instance_candidates.argtypes = [C.c_uint64, _sz, _sz, _sz, _sz, _f32p, _f32p,
+                                                   _i64p, _i64p]
+        L.ref_sample_uniform.argtypes = [_i64p, _sz, _sz, _sz, C.c_uint64, _i64p]
+        L.ref_cce_forward.argtypes = [_f32p, _f32p, _i64p, _sz, _sz, _sz, _sz, _sz, C.c_int,
+                                      _f64p, _f64p, C.POINTER(C.c_double)]
+        L.ref_cce_backward.argtypes = [_f32p, _f32p, _i64p, _f64p, C.c_double, C.c_double, _sz,
+                                       _sz, _sz, _sz, _sz, C.c_int, _f64p, _f64p,
+                                       C.POINTER(C.c_double)]
+        L.ref_ccem_forward.argtypes = [_f32p, _f32p, _i64p, _sz, _sz, _sz, _sz, _sz, C.c_int,
+                                       _f64p, _f64p, C.POINTER(C.c_double)]
+        L.ref_ccem_backward_rows.argtypes = [_f32p, _f32p, _i64p, _f64p, _f64p, _sz, _sz, _sz,
+                                             _sz, _sz, C.c_int, _f64p, _f64p]
+        L.ref_ce_full.argtypes = [_f32p, _f32p, _i64p, _sz, _sz, _sz, C.c_double, _f64p, _f64p,
+                                  C.POINTER(C.c_double), C.c_void_p, C.c_void_p]
+        L.ref_ce_sampled.argtypes = [_f32p, _f32p, _i64p, _sz, _sz, _sz, _sz, C.c_double, _f64p,
+                                     _f64p, C.POINTER(C.c_double), C.c_void_p, C.c_void_p]
+        L.ref_validate_targets.argtypes = [_sz, _sz, _sz, _i64p, _sz]
+        L.ref_validate_inds.argtypes = [_i64p, _sz, _sz, _sz]
+        L.ref_estimate_flops.argtypes = [_sz, _sz, _sz, _sz, C.c_int, C.POINTER(C.c_uint64),
+                                         C.POINTER(C.c_uint64)]
+        _ref = L
+    return _ref
+
+
+def _chk(rc, lib):
+    if rc != 0:
+        raise ValueError(lib.ref_last_error().decode())
+
+
+# ---------------------------------------------------------------------------
+# Restatement (oracle.c) wrappers — numpy in, numpy out
+# ---------------------------------------------------------------------------
+class Rng:
+    """SplitMix64 (rng.hpp:13-60) backed by the C restatement."""
+
+    def __init__(self, seed: int):
+        self._s = _Rng()
+        orc().orc_rng_init(C.byref(self._s), C.c_uint64(seed & 0xFFFFFFFFFFFFFFFF))
+
+    def next(self) -> int:
+        return orc().orc_rng_next(C.byref(self._s))
+
+    def bounded(self, b: int) -> int:
+        return orc().orc_rng_bounded(C.byref(self._s), b)
+
+    def uniform(self) -> float:
+        return orc().orc_rng_uniform(C.byref(self._s))
+
+
+@dataclass
+class Instance:
+    E: np.ndarray        # n×d float32 (reference "E" = B200 "X")
+    C: np.ndarray        # d×v float32 (reference "C" = B200 "E"^T)
+    targets: np.ndarray  # n int64
+
+
+def make_instance(rng: Rng, n: int, d: int, v: int, half_width: float = 1.0) -> Instance:
+    """support.hpp:27-37, same draw order (E, then C, then targets)."""
+    E = np.empty((n, d), np.float32)
+    Cm = np.empty((d, v), np.float32)
+    t = np.empty(n, np.int64)
+    orc().orc_make_instance(C.byref(rng._s), n, d, v, half_width, E, Cm, t)
+    return Instance(E, Cm, t)
+
+
+def make_candidates(rng: Rng, targets: np.ndarray, ns: int, v: int) -> np.ndarray:
+    """support.hpp:41-56."""
+    n = targets.shape[0]
+    inds = np.empty((n, 1 + ns), np.int64)
+    orc().orc_make_candidates(C.byref(rng._s), np.ascontiguousarray(targets), n, ns, v, inds)
+    return inds
+
+
+def sample_uniform(positives: np.ndarray, ns: int, catalog: int, seed: int, retry_cap: int = 100):
+    """sampler.cpp:44-75 (per-row derived(i) streams)."""
+    n = positives.shape[0]
+    inds = np.empty((n, 1 + ns), np.int64)
+    rc = orc().orc_sample_uniform(np.ascontiguousarray(positives), n, ns, catalog, seed,
+                                  retry_cap, inds)
+    if rc != 0:
+        raise RuntimeError("sampler: retry cap exhausted")
+    return inds
+
+
+def cce_forward(E, Cm, x):
+    n, d = E.shape
+    v = Cm.shape[1]
+    pos = np.empty(n)
+    lse = np.empty(n)
+    loss = orc().orc_cce_forward(E, Cm, x, n, d, v, pos, lse)
+    return loss, pos, lse
+
+
+def cce_backward(E, Cm, x, lse, upstream=1.0, eps=0.0, col_block=256):
+    n, d = E.shape
+    v = Cm.shape[1]
+    dE = np.empty((n, d))
+    dC = np.empty((d, v))
+    sk = C.c_uint64()
+    frac = orc().orc_cce_backward(E, Cm, x, np.ascontiguousarray(lse, np.float64), upstream, eps,
+                                  col_block, n, d, v, dE, dC, C.byref(sk))
+    return dE, dC, frac, sk.value
+
+
+def cce_forward_partial(E, Cm, x, v0, v1):
+    n, d = E.shape
+    v = Cm.shape[1]
+    m = np.empty(n)
+    s = np.empty(n)
+    t = np.empty(n)
+    h = np.empty(n, np.int32)
+    orc().orc_cce_forward_partial(E, Cm, x, n, d, v, v0, v1, m, s, t, h)
+    return m, s, t, h
+
+
+def ccem_forward(E, Cm, inds):
+    n, d = E.shape
+    v = Cm.shape[1]
+    w = inds.shape[1]
+    pos = np.empty(n)
+    lse = np.empty(n)
+    loss = orc().orc_ccem_forward(E, Cm, np.ascontiguousarray(inds), n, d, v, w, pos, lse)
+    return loss, pos, lse
+
+
+def ccem_backward_rows(E, Cm, inds, lse, row_upstream):
+    n, d = E.shape
+    v = Cm.shape[1]
+    w = inds.shape[1]
+    dE = np.empty((n, d))
+    dC = np.empty((d, v))
+    orc().orc_ccem_backward_rows(E, Cm, np.ascontiguousarray(inds),
+                                 np.ascontiguousarray(lse, np.float64),
+                                 np.ascontiguousarray(row_upstream, np.float64), n, d, v, w, dE,
+                                 dC)
+    return dE, dC
+
+
+def ccem_backward(E, Cm, inds, lse, upstream=1.0):
+    n = E.shape[0]
+    return ccem_backward_rows(E, Cm, inds, lse, np.full(n, upstream / n))
+
+
+def estimate_flops(n, d, v, ns, backend: int):
+    f, b = C.c_uint64(), C.c_uint64()
+    orc().orc_estimate_flops(n, d, v, ns, backend, C.byref(f), C.byref(b))
+    return f.value, b.value
+
+
+# ---------------------------------------------------------------------------
+# Reference (oracle/_ref) wrappers
+# ---------------------------------------------------------------------------
+def ref_cce_forward(E, Cm, x, rb=128, cb=256, workers=1):
+    L = ref()
+    n, d = E.shape
+    v = Cm.shape[1]
+    pos = np.empty(n)
+    lse = np.empty(n)
+    loss = C.c_double()
+    _chk(L.ref_cce_forward(E, Cm, x, n, d, v, rb, cb, workers, pos, lse, C.byref(loss)), L)
+    return loss.value, pos, lse
+
+
+def ref_cce_backward(E, Cm, x, lse, upstream=1.0, eps=0.0, rb=128, cb=256, workers=1):
+    L = ref()
+    n, d = E.shape
+    v = Cm.shape[1]
+    dE = np.empty((n, d))
+    dC = np.empty((d, v))
+    frac = C.c_double()
+    _chk(L.ref_cce_backward(E, Cm, x, np.ascontiguousarray(lse, np.float64), upstream, eps, n, d,
+                            v, rb, cb, workers, dE, dC, C.byref(frac)), L)
+    return dE, dC, frac.value
+
+
+def ref_ccem_forward(E, Cm, inds, rb=128, workers=1):
+    L = ref()
+    n, d = E.shape
+    v = Cm.shape[1]
+    w = inds.shape[1]
+    pos = np.empty(n)
+    lse = np.empty(n)
+    loss = C.c_double()
+    _chk(L.ref_ccem_forward(E, Cm, np.ascontiguousarray(inds), n, d, v, w, rb, workers, pos, lse,
+                            C.byref(loss)), L)
+    return loss.value, pos, lse
+
+
+def ref_ccem_backward_rows(E, Cm, inds, lse, row_upstream, rb=128, workers=1):
+    L = ref()
+    n, d = E.shape
+    v = Cm.shape[1]
+    w = inds.shape[1]
+    dE = np.empty((n, d))
+    dC = np.empty((d, v))
+    _chk(L.ref_ccem_backward_rows(E, Cm, np.ascontiguousarray(inds),
+                                  np.ascontiguousarray(lse, np.float64),
+                                  np.ascontiguousarray(row_upstream, np.float64), n, d, v, w, rb,
+                                  workers, dE, dC), L)
+    return dE, dC
+
+
+def ref_ce_full(E, Cm, x, upstream=1.0, grads=True):
+    L = ref()
+    n, d = E.shape
+    v = Cm.shape[1]
+    pos = np.empty(n)
+    lse = np.empty(n)
+    loss = C.c_double()
+    dE = np.empty((n, d)) if grads else None
+    dC = np.empty((d, v)) if grads else None
+    _chk(L.ref_ce_full(E, Cm, x, n, d, v, upstream, pos, lse, C.byref(loss),
+                       dE.ctypes.data if grads else None, dC.ctypes.data if grads else None), L)
+    return loss.value, pos, lse, dE, dC
+
+
+def ref_ce_sampled(E, Cm, inds, upstream=1.0, grads=True):
+    L = ref()
+    n, d = E.shape
+    v = Cm.shape[1]
+    w = inds.shape[1]
+    pos = np.empty(n)
+    lse = np.empty(n)
+    loss = C.c_double()
+    dE = np.empty((n, d)) if grads else None
+    dC = np.empty((d, v)) if grads else None
+    _chk(L.ref_ce_sampled(E, Cm, np.ascontiguousarray(inds), n, d, v, w, upstream, pos, lse,
+                          C.byref(loss), dE.ctypes.data if grads else None,
+                          dC.ctypes.data if grads else None), L)
+    return loss.value, pos, lse, dE, dC
+
+
+def ref_rng_stream(seed, count=16):
+    out = np.empty(count, np.uint64)
+    ref().ref_rng_stream(seed, out, count)
+    return out
+
+
+def ref_sample_uniform(positives, ns, catalog, seed):
+    L = ref()
+    n = positives.shape[0]
+    inds = np.empty((n, 1 + ns), np.int64)
+    _chk(L.ref_sample_uniform(np.ascontiguousarray(positives), n, ns, catalog, seed, inds), L)
+    return inds
+
+
+def rel_err(got, want):
+    """support.hpp:74-77 / acceptance.cpp:69-71: |got-want| / max(1, |want|)."""
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    return np.abs(got - want) / np.maximum(1.0, np.abs(want))
