@@ -1,0 +1,176 @@
+/*
+ * lseforge_b200.h — C-ABI of the B200-native (sm_100a) CCE / CCE- loss path.
+ *
+ * This is the drop-in boundary for the reference library's hot path
+ * (lseforge, /root/reference/proj).  Each entry point replaces one reference
+ * C++ function; the citation is given beside it.  Plain pointers and sizes
+ * only; every pointer named `d_*` is DEVICE memory on the current CUDA device,
+ * every call is stream-ordered on `stream` (a cudaStream_t, NULL = legacy
+ * default stream) and does not synchronize unless documented.
+ *
+ * Layout (B200 naming; the reference's letters are swapped):
+ *   X  [n x d]  hidden states, row-major       (reference "E", cce.hpp:36)
+ *   E  [v x d]  item embeddings, row-major     (reference "C" is d x v = E^T)
+ *   targets [n] int64, item index of each row's positive (reference "x")
+ *   inds [n x w] int64, slot 0 = positive, w = 1 + K (NegIndexMatrix,
+ *                neg_index.hpp:10-44)
+ *   lse, pos [n] double (LossOutput::lse / pos_logits, losses.hpp:15-19)
+ *   dX [n x d], dE [v x d]: float (dtype bf16/f32) or double (dtype f64)
+ *                (GradPair, losses.hpp:24-27; dE = reference d_classifier^T)
+ *
+ * Element types (lf_dtype):
+ *   LF_BF16 — tcgen05/TMEM/TMA tensor-core kernels, fp32 accumulate
+ *             (requires d % 64 == 0, d <= 256)
+ *   LF_F32  — fp32 SIMT (FFMA) kernels, any d
+ *   LF_F64  — "exact" mode: fp64, reference operand order (k ascending,
+ *             no FMA contraction) so pos logits are bitwise equal to the
+ *             reference's double results for float-representable inputs.
+ *
+ * Status: every function returns 0 on success or a negative LF_E* code;
+ * lf_last_error() returns a thread-local message (the reference's
+ * std::invalid_argument text where one exists, e.g. "loss: row 1 targets item
+ * 9, outside catalog of 8" — losses.cpp:59-66).
+ */
+#ifndef LSEFORGE_B200_H
+#define LSEFORGE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LF_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define LF_API __attribute__((visibility("default")))
+#else
+#define LF_API
+#endif
+
+enum lf_status {
+  LF_OK = 0,
+  LF_EINVAL = -1,      /* bad argument (shape, range, config) */
+  LF_EUNSUPPORTED = -2, /* valid request this build cannot serve (e.g. bf16 with d % 64) */
+  LF_ECUDA = -3,       /* CUDA runtime / driver error */
+  LF_ENOMEM = -4
+};
+
+enum lf_dtype { LF_F32 = 0, LF_F64 = 1, LF_BF16 = 2 };
+
+/* Mirrors lseforge::CceConfig (cce.hpp:18-31).  row_block / col_block /
+ * workers are CPU tiling knobs with no effect on results; they are accepted
+ * and ignored (the GPU picks its own tiles, and results are bitwise identical
+ * run to run for any value, matching test_cce.cpp:170-196). */
+typedef struct {
+  double filter_eps; /* CceConfig::filter_eps; 0 = exact backward (cce.hpp:21) */
+  int32_t dtype;     /* lf_dtype of X and E */
+  int32_t flags;     /* LF_FLAG_* */
+} lf_cce_config;
+
+#define LF_FLAG_NONE 0
+/* CCE-: accumulate dE with red.global.add (non-deterministic bit order)
+ * instead of the default deterministic bucket + ordered segment reduce. */
+#define LF_FLAG_ATOMIC_DE 1
+
+/* Backward statistics (device-side counters are copied into this host struct
+ * only when the caller passes a non-NULL pointer; that forces a stream sync). */
+typedef struct {
+  uint64_t skipped_elems;  /* off-target (row,item) pairs with softmax < eps (cce.cpp:197-200) */
+  uint64_t skipped_tiles;  /* 128x128 tiles whose MMA+exp work was skipped entirely */
+  uint64_t total_tiles;    /* tiles visited by the dX pass */
+  double skipped_fraction; /* skipped_elems / (n * (v_total - 1)), cce.cpp:264-268 */
+} lf_cce_stats;
+
+LF_API int lf_abi_version(void);
+LF_API const char* lf_last_error(void);
+
+/* ---------------------------------------------------------------- CCE ---- */
+
+/* Replaces lseforge::cce_forward (cce.hpp:36-38, cce.cpp:65-145).
+ * Writes d_lse[n], d_pos[n] and the mean loss d_loss[0] (all double). */
+LF_API int lf_cce_forward(const void* d_X, const void* d_E, const int64_t* d_targets, int64_t n,
+                   int64_t d, int64_t v, const lf_cce_config* cfg, double* d_lse, double* d_pos,
+                   double* d_loss, void* stream);
+
+/* Replaces lseforge::cce_backward (cce.hpp:51-54, cce.cpp:147-272) with
+ * upstream = dL/dloss (scale = upstream / n, cce.cpp:174).  d_dX [n x d] and
+ * d_dE [v x d] are OVERWRITTEN (the reference returns fresh zeroed matrices).
+ * stats may be NULL (no sync). */
+LF_API int lf_cce_backward(const void* d_X, const void* d_E, const int64_t* d_targets,
+                    const double* d_lse, double upstream, int64_t n, int64_t d, int64_t v,
+                    const lf_cce_config* cfg, void* d_dX, void* d_dE, lf_cce_stats* stats,
+                    void* stream);
+
+/* ------------------------------------------------ catalog-sharded CCE ---- */
+/* Rank p owns E rows [v_offset, v_offset + v_shard) of a catalog of v_total
+ * items; targets are GLOBAL item indices.  Forward: per-row partial triples
+ * d_part[n] = {m (max logit * log2 e), s (sum of 2^(logit*log2e - m)),
+ * t (target logit if the target lies in this shard, else 0), has_t} as float4;
+ * exchange them across ranks (e.g. one ncclAllGather of n*16 bytes), then
+ * lf_cce_combine over the P gathered blocks gives lse/pos/loss. */
+LF_API int lf_cce_forward_partial(const void* d_X, const void* d_E_shard, const int64_t* d_targets,
+                           int64_t n, int64_t d, int64_t v_shard, int64_t v_offset,
+                           const lf_cce_config* cfg, float* d_part, void* stream);
+
+/* d_parts: P consecutive blocks of n float4 partials. */
+LF_API int lf_cce_combine(const float* d_parts, int32_t P, int64_t n, double* d_lse, double* d_pos,
+                   double* d_loss, void* stream);
+
+/* Sharded backward: dE rows for the local shard are complete; dX is this
+ * shard's PARTIAL sum over its items and must be summed across ranks
+ * (ncclAllReduce sum of n*d floats).  scale = upstream / n. */
+LF_API int lf_cce_backward_shard(const void* d_X, const void* d_E_shard, const int64_t* d_targets,
+                          const double* d_lse, double upstream, int64_t n, int64_t d,
+                          int64_t v_shard, int64_t v_offset, int64_t v_total,
+                          const lf_cce_config* cfg, void* d_dX_partial, void* d_dE_shard,
+                          lf_cce_stats* stats, void* stream);
+
+/* ---------------------------------------------------------------- CCE- --- */
+
+/* Replaces lseforge::ccem_forward (ccem.hpp:19-20, ccem.cpp:48-105). */
+LF_API int lf_ccem_forward(const void* d_X, const void* d_E, const int64_t* d_inds, int64_t n,
+                    int64_t d, int64_t v, int64_t w, const lf_cce_config* cfg, double* d_lse,
+                    double* d_pos, double* d_loss, void* stream);
+
+/* Replaces lseforge::ccem_backward_rows (ccem.hpp:34-36, ccem.cpp:107-194):
+ * d_row_upstream[n] (double).  Passing d_row_upstream == NULL means the scalar
+ * form lseforge::ccem_backward (ccem.hpp:27-29): row_upstream[i] = upstream/n.
+ * Gradient filtering does not apply to CCE- (ccem.hpp:22-26).  d_dX and d_dE
+ * are OVERWRITTEN; d_dE is full width (v x d) with exact zeros for untouched
+ * items. */
+LF_API int lf_ccem_backward(const void* d_X, const void* d_E, const int64_t* d_inds, const double* d_lse,
+                     const double* d_row_upstream, double upstream, int64_t n, int64_t d,
+                     int64_t v, int64_t w, const lf_cce_config* cfg, void* d_dX, void* d_dE,
+                     void* stream);
+
+/* ----------------------------------------------------------- validation --- */
+/* Replaces validate_loss_inputs' index scan (losses.cpp:58-67) for device
+ * targets.  Synchronizes `stream`.  On failure returns LF_EINVAL with the
+ * reference's message naming the first offending row. */
+LF_API int lf_validate_targets(const int64_t* d_targets, int64_t n, int64_t v, void* stream);
+/* Replaces NegIndexMatrix::validate (neg_index.cpp:8-28). Synchronizes. */
+LF_API int lf_validate_inds(const int64_t* d_inds, int64_t n, int64_t w, int64_t v, void* stream);
+
+/* -------------------------------------------------------- accounting ----- */
+/* Replaces lseforge::estimate_flops (ccem.hpp:43-49, ccem.cpp:207-235):
+ * backend 0 ce, 1 cem, 2 cce, 3 ccem, 4 bce (backend.hpp:10-16). */
+LF_API int lf_estimate_flops(int64_t n, int64_t d, int64_t v, int64_t ns, int32_t backend,
+                      uint64_t* forward, uint64_t* backward);
+
+/* Device scratch the library itself allocates (stream-ordered pool):
+ * current and high-water bytes since the last reset. */
+LF_API int lf_workspace_stats(uint64_t* current_bytes, uint64_t* peak_bytes);
+LF_API int lf_workspace_reset_peak(void);
+
+/* Number of library kernel launches issued since the last reset (for the
+ * bench's gpu_launches evidence). */
+LF_API uint64_t lf_launch_count(void);
+LF_API void lf_launch_count_reset(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LSEFORGE_B200_H */

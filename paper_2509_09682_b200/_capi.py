@@ -1,0 +1,92 @@
+"""ctypes binding of liblseforge_b200.so (include/lseforge_b200.h).
+
+The shared library is built in-tree (``make -C paper_2509_09682_b200``, or
+``__graft_entry__.build()``).  There is no fallback: if the library is missing
+every entry point raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblseforge_b200.so")
+
+LF_OK, LF_EINVAL, LF_EUNSUPPORTED, LF_ECUDA, LF_ENOMEM = 0, -1, -2, -3, -4
+LF_F32, LF_F64, LF_BF16 = 0, 1, 2
+LF_FLAG_NONE, LF_FLAG_ATOMIC_DE = 0, 1
+
+# Every symbol include/lseforge_b200.h declares (checked by tests/test_capi.py).
+EXPORTS = (
+    "lf_abi_version", "lf_last_error", "lf_cce_forward", "lf_cce_backward",
+    "lf_cce_forward_partial", "lf_cce_combine", "lf_cce_backward_shard", "lf_ccem_forward",
+    "lf_ccem_backward", "lf_validate_targets", "lf_validate_inds", "lf_estimate_flops",
+    "lf_workspace_stats", "lf_workspace_reset_peak", "lf_launch_count", "lf_launch_count_reset",
+)
+
+
+class CceConfigC(C.Structure):
+    _fields_ = [("filter_eps", C.c_double), ("dtype", C.c_int32), ("flags", C.c_int32)]
+
+
+class CceStatsC(C.Structure):
+    _fields_ = [("skipped_elems", C.c_uint64), ("skipped_tiles", C.c_uint64),
+                ("total_tiles", C.c_uint64), ("skipped_fraction", C.c_double)]
+
+
+class LfError(RuntimeError):
+    """Raised for LF_ECUDA / LF_ENOMEM / LF_EUNSUPPORTED statuses."""
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `make -C {_HERE}` or "
+                "`python -c 'import __graft_entry__ as g; g.build()'` (there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        vp, i64, dp = C.c_void_p, C.c_int64, C.c_void_p
+        cfgp = C.POINTER(CceConfigC)
+        stp = C.POINTER(CceStatsC)
+        L.lf_abi_version.restype = C.c_int
+        L.lf_last_error.restype = C.c_char_p
+        L.lf_cce_forward.argtypes = [vp, vp, vp, i64, i64, i64, cfgp, dp, dp, dp, vp]
+        L.lf_cce_backward.argtypes = [vp, vp, vp, dp, C.c_double, i64, i64, i64, cfgp, vp, vp,
+                                      stp, vp]
+        L.lf_cce_forward_partial.argtypes = [vp, vp, vp, i64, i64, i64, i64, cfgp, vp, vp]
+        L.lf_cce_combine.argtypes = [vp, C.c_int32, i64, dp, dp, dp, vp]
+        L.lf_cce_backward_shard.argtypes = [vp, vp, vp, dp, C.c_double, i64, i64, i64, i64, i64,
+                                            cfgp, vp, vp, stp, vp]
+        L.lf_ccem_forward.argtypes = [vp, vp, vp, i64, i64, i64, i64, cfgp, dp, dp, dp, vp]
+        L.lf_ccem_backward.argtypes = [vp, vp, vp, dp, dp, C.c_double, i64, i64, i64, i64, cfgp,
+                                       vp, vp, vp]
+        L.lf_validate_targets.argtypes = [vp, i64, i64, vp]
+        L.lf_validate_inds.argtypes = [vp, i64, i64, i64, vp]
+        L.lf_estimate_flops.argtypes = [i64, i64, i64, i64, C.c_int32, C.POINTER(C.c_uint64),
+                                        C.POINTER(C.c_uint64)]
+        L.lf_workspace_stats.argtypes = [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        L.lf_launch_count.restype = C.c_uint64
+        for name in ("lf_cce_forward", "lf_cce_backward", "lf_cce_forward_partial",
+                     "lf_cce_combine", "lf_cce_backward_shard", "lf_ccem_forward",
+                     "lf_ccem_backward", "lf_validate_targets", "lf_validate_inds",
+                     "lf_estimate_flops", "lf_workspace_stats", "lf_workspace_reset_peak"):
+            getattr(L, name).restype = C.c_int
+        if L.lf_abi_version() != 1:
+            raise ImportError("liblseforge_b200.so ABI mismatch")
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    """Map a status code to the reference's exception types (std::invalid_argument
+    -> ValueError)."""
+    if rc == LF_OK:
+        return
+    msg = lib().lf_last_error().decode()
+    if rc == LF_EINVAL:
+        raise ValueError(msg)
+    raise LfError(f"[status {rc}] {msg}")

@@ -1,0 +1,321 @@
+// lf_capi.cu — extern "C" entry points of liblseforge_b200.so (declared in
+// include/lseforge_b200.h) plus the library's error, scratch and launch
+// bookkeeping.  Argument checks reproduce the reference's validation
+// (losses.cpp:48-69, cce.cpp:17-27, ccem.cpp:16-31) with the same messages;
+// the index scans themselves are separate calls (lf_validate_*) because they
+// need a device->host sync.
+#include <atomic>
+#include <cmath>
+#include <mutex>
+#include <string>
+
+#include "lf_internal.cuh"
+#include "lf_kernels.cuh"
+
+namespace lf {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+std::atomic<uint64_t> g_ws_current{0};
+std::atomic<uint64_t> g_ws_peak{0};
+}  // namespace
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  g_last_error = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? LF_ENOMEM : LF_ECUDA;
+}
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int Scratch::alloc(size_t nbytes, cudaStream_t s) {
+  if (ptr) return fail(LF_EINVAL, "internal: scratch reused");
+  if (nbytes == 0) nbytes = 16;
+  cudaError_t e = cudaMallocAsync(&ptr, nbytes, s);
+  if (e != cudaSuccess) {
+    ptr = nullptr;
+    return cuda_fail(e, "cudaMallocAsync(scratch)");
+  }
+  bytes = nbytes;
+  stream = s;
+  const uint64_t cur = g_ws_current.fetch_add(nbytes) + nbytes;
+  uint64_t pk = g_ws_peak.load();
+  while (cur > pk && !g_ws_peak.compare_exchange_weak(pk, cur)) {
+  }
+  return LF_OK;
+}
+Scratch::~Scratch() {
+  if (ptr) {
+    cudaFreeAsync(ptr, stream);
+    g_ws_current.fetch_sub(bytes);
+  }
+}
+
+int num_sms() {
+  static int cached = [] {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+  }();
+  return cached;
+}
+
+namespace {
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+int check_cfg(const lf_cce_config* cfg) {
+  if (!cfg) return fail(LF_EINVAL, "CceConfig: null config");
+  if (!(cfg->filter_eps >= 0.0))  // cce.cpp:23-26 (also rejects NaN)
+    return fail(LF_EINVAL, "CceConfig: filter_eps must be >= 0, got " + std::to_string(cfg->filter_eps));
+  if (cfg->dtype != LF_F32 && cfg->dtype != LF_F64 && cfg->dtype != LF_BF16)
+    return fail(LF_EINVAL, "lf_cce_config: unknown dtype " + std::to_string(cfg->dtype));
+  return LF_OK;
+}
+
+// losses.cpp:48-57 shape checks (index range: lf_validate_targets).
+int check_shapes(int64_t n, int64_t d, int64_t v) {
+  if (n <= 0) return fail(LF_EINVAL, "loss: embedding matrix has zero rows; the mean loss is undefined");
+  if (d <= 0) return fail(LF_EINVAL, "loss: embedding width must be >= 1");
+  if (v <= 0) return fail(LF_EINVAL, "loss: catalog must hold at least one item");
+  return LF_OK;
+}
+
+int check_bf16_d(int64_t d) {
+  if (d % 64 != 0 || d > 256)
+    return fail(LF_EUNSUPPORTED,
+                "bf16 tensor-core path needs d in {64, 128, 192, 256} (got " + std::to_string(d) +
+                    "); use dtype f32 or f64");
+  return LF_OK;
+}
+
+struct Counters {
+  Scratch buf;
+  int init(cudaStream_t st) {
+    int rc = buf.alloc(4 * sizeof(unsigned long long), st);
+    if (rc) return rc;
+    LF_CUDA(cudaMemsetAsync(buf.ptr, 0, 4 * sizeof(unsigned long long), st));
+    return LF_OK;
+  }
+  unsigned long long* ptr() { return buf.as<unsigned long long>(); }
+};
+
+int read_stats(Counters& c, lf_cce_stats* stats, int64_t n, int64_t v_total, cudaStream_t st) {
+  unsigned long long h[4] = {0, 0, 0, 0};
+  LF_CUDA(cudaMemcpyAsync(h, c.ptr(), sizeof(h), cudaMemcpyDeviceToHost, st));
+  LF_CUDA(cudaStreamSynchronize(st));
+  stats->skipped_elems = h[0];
+  stats->skipped_tiles = h[1];
+  stats->total_tiles = h[2];
+  const double off_target = static_cast<double>(n) * static_cast<double>(v_total - 1);
+  stats->skipped_fraction = off_target == 0.0 ? 0.0 : static_cast<double>(h[0]) / off_target;
+  return LF_OK;
+}
+
+int backward_impl(const void* X, const void* E, const int64_t* targets, const double* lse,
+                  double upstream, int64_t n, int64_t d, int64_t v_shard, int64_t v_offset,
+                  int64_t v_total, const lf_cce_config* cfg, void* dX, void* dE,
+                  lf_cce_stats* stats, cudaStream_t st) {
+  int rc = check_cfg(cfg);
+  if (!rc) rc = check_shapes(n, d, v_shard);
+  if (rc) return rc;
+  if (!lse) return fail(LF_EINVAL, "cce_backward: LSE vector is null");
+  const double scale = upstream / static_cast<double>(n);  // cce.cpp:174
+  Counters c;
+  rc = c.init(st);
+  if (rc) return rc;
+  switch (cfg->dtype) {
+    case LF_BF16:
+      rc = check_bf16_d(d);
+      if (!rc)
+        rc = tc_cce_backward(X, E, targets, lse, scale, cfg->filter_eps, n, static_cast<int>(d),
+                             v_shard, v_offset, static_cast<float*>(dX), static_cast<float*>(dE),
+                             c.ptr(), st);
+      break;
+    case LF_F32:
+      rc = simt_cce_backward<float>(static_cast<const float*>(X), static_cast<const float*>(E),
+                                    targets, lse, scale, cfg->filter_eps, n, static_cast<int>(d),
+                                    v_shard, v_offset, static_cast<float*>(dX),
+                                    static_cast<float*>(dE), c.ptr(), st);
+      break;
+    default:
+      rc = simt_cce_backward<double>(static_cast<const double*>(X),
+                                     static_cast<const double*>(E), targets, lse, scale,
+                                     cfg->filter_eps, n, static_cast<int>(d), v_shard, v_offset,
+                                     static_cast<double*>(dX), static_cast<double*>(dE), c.ptr(),
+                                     st);
+  }
+  if (rc) return rc;
+  if (stats) return read_stats(c, stats, n, v_total, st);
+  return LF_OK;
+}
+
+}  // namespace
+}  // namespace lf
+
+using namespace lf;
+
+extern "C" {
+
+int lf_abi_version(void) { return LF_ABI_VERSION; }
+const char* lf_last_error(void) { return g_last_error.c_str(); }
+
+int lf_cce_forward(const void* d_X, const void* d_E, const int64_t* d_targets, int64_t n,
+                   int64_t d, int64_t v, const lf_cce_config* cfg, double* d_lse, double* d_pos,
+                   double* d_loss, void* stream) {
+  int rc = check_cfg(cfg);
+  if (!rc) rc = check_shapes(n, d, v);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  switch (cfg->dtype) {
+    case LF_BF16: {
+      rc = check_bf16_d(d);
+      if (rc) return rc;
+      Scratch ws;
+      float* part = nullptr;
+      int P = 0;
+      rc = tc_cce_forward_partials(d_X, d_E, d_targets, n, static_cast<int>(d), v, 0, ws, &part,
+                                   &P, st);
+      if (rc) return rc;
+      return launch_combine_f32log2(part, P, n, d_lse, d_pos, d_loss, st);
+    }
+    case LF_F32:
+      return simt_cce_forward_full<float>(static_cast<const float*>(d_X),
+                                          static_cast<const float*>(d_E), d_targets, n,
+                                          static_cast<int>(d), v, d_lse, d_pos, d_loss, st);
+    default:
+      return simt_cce_forward_full<double>(static_cast<const double*>(d_X),
+                                           static_cast<const double*>(d_E), d_targets, n,
+                                           static_cast<int>(d), v, d_lse, d_pos, d_loss, st);
+  }
+}
+
+int lf_cce_backward(const void* d_X, const void* d_E, const int64_t* d_targets,
+                    const double* d_lse, double upstream, int64_t n, int64_t d, int64_t v,
+                    const lf_cce_config* cfg, void* d_dX, void* d_dE, lf_cce_stats* stats,
+                    void* stream) {
+  return backward_impl(d_X, d_E, d_targets, d_lse, upstream, n, d, v, 0, v, cfg, d_dX, d_dE,
+                       stats, as_stream(stream));
+}
+
+int lf_cce_forward_partial(const void* d_X, const void* d_E_shard, const int64_t* d_targets,
+                           int64_t n, int64_t d, int64_t v_shard, int64_t v_offset,
+                           const lf_cce_config* cfg, float* d_part, void* stream) {
+  int rc = check_cfg(cfg);
+  if (!rc) rc = check_shapes(n, d, v_shard);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  switch (cfg->dtype) {
+    case LF_BF16: {
+      rc = check_bf16_d(d);
+      if (rc) return rc;
+      Scratch ws;
+      float* part = nullptr;
+      int P = 0;
+      rc = tc_cce_forward_partials(d_X, d_E_shard, d_targets, n, static_cast<int>(d), v_shard,
+                                   v_offset, ws, &part, &P, st);
+      if (rc) return rc;
+      // fold the per-chunk partials into one per row (log2 units)
+      return launch_fold_partials(part, P, n, d_part, st);
+    }
+    case LF_F32:
+      return simt_cce_forward_partial_log2<float>(static_cast<const float*>(d_X),
+                                                  static_cast<const float*>(d_E_shard), d_targets,
+                                                  n, static_cast<int>(d), v_shard, v_offset,
+                                                  d_part, st);
+    default:
+      return simt_cce_forward_partial_log2<double>(static_cast<const double*>(d_X),
+                                                   static_cast<const double*>(d_E_shard),
+                                                   d_targets, n, static_cast<int>(d), v_shard,
+                                                   v_offset, d_part, st);
+  }
+}
+
+int lf_cce_combine(const float* d_parts, int32_t P, int64_t n, double* d_lse, double* d_pos,
+                   double* d_loss, void* stream) {
+  if (P < 1) return fail(LF_EINVAL, "combine: P must be >= 1");
+  return launch_combine_f32log2(d_parts, P, n, d_lse, d_pos, d_loss, as_stream(stream));
+}
+
+int lf_cce_backward_shard(const void* d_X, const void* d_E_shard, const int64_t* d_targets,
+                          const double* d_lse, double upstream, int64_t n, int64_t d,
+                          int64_t v_shard, int64_t v_offset, int64_t v_total,
+                          const lf_cce_config* cfg, void* d_dX_partial, void* d_dE_shard,
+                          lf_cce_stats* stats, void* stream) {
+  return backward_impl(d_X, d_E_shard, d_targets, d_lse, upstream, n, d, v_shard, v_offset,
+                       v_total, cfg, d_dX_partial, d_dE_shard, stats, as_stream(stream));
+}
+
+int lf_ccem_forward(const void* d_X, const void* d_E, const int64_t* d_inds, int64_t n,
+                    int64_t d, int64_t v, int64_t w, const lf_cce_config* cfg, double* d_lse,
+                    double* d_pos, double* d_loss, void* stream) {
+  int rc = check_cfg(cfg);
+  if (rc) return rc;
+  if (n <= 0) return fail(LF_EINVAL, "fused sampled loss: zero rows; the mean loss is undefined");
+  if (w < 1) return fail(LF_EINVAL, "NegIndexMatrix: width must be at least 1 (the positive slot)");
+  if (d <= 0 || v <= 0) return fail(LF_EINVAL, "fused sampled loss: empty embedding or catalog");
+  return ccem_forward(cfg->dtype, d_X, d_E, d_inds, n, static_cast<int>(d), v, w, d_lse, d_pos,
+                      d_loss, as_stream(stream));
+}
+
+int lf_ccem_backward(const void* d_X, const void* d_E, const int64_t* d_inds, const double* d_lse,
+                     const double* d_row_upstream, double upstream, int64_t n, int64_t d,
+                     int64_t v, int64_t w, const lf_cce_config* cfg, void* d_dX, void* d_dE,
+                     void* stream) {
+  int rc = check_cfg(cfg);
+  if (rc) return rc;
+  if (n <= 0) return fail(LF_EINVAL, "fused sampled loss: zero rows; the mean loss is undefined");
+  if (w < 1) return fail(LF_EINVAL, "NegIndexMatrix: width must be at least 1 (the positive slot)");
+  if (d <= 0 || v <= 0) return fail(LF_EINVAL, "fused sampled loss: empty embedding or catalog");
+  if (!d_lse) return fail(LF_EINVAL, "ccem_backward: LSE vector is null");
+  return ccem_backward(cfg->dtype, d_X, d_E, d_inds, d_lse, d_row_upstream, upstream, n,
+                       static_cast<int>(d), v, w, (cfg->flags & LF_FLAG_ATOMIC_DE) != 0, d_dX,
+                       d_dE, as_stream(stream));
+}
+
+int lf_validate_targets(const int64_t* d_targets, int64_t n, int64_t v, void* stream) {
+  if (n <= 0) return fail(LF_EINVAL, "loss: embedding matrix has zero rows; the mean loss is undefined");
+  return validate_targets(d_targets, n, v, as_stream(stream));
+}
+
+int lf_validate_inds(const int64_t* d_inds, int64_t n, int64_t w, int64_t v, void* stream) {
+  return validate_inds(d_inds, n, w, v, as_stream(stream));
+}
+
+int lf_estimate_flops(int64_t n, int64_t d, int64_t v, int64_t ns, int32_t backend,
+                      uint64_t* forward, uint64_t* backward) {
+  // ccem.cpp:207-235
+  if (n < 1 || d < 1 || v < 1) return fail(LF_EINVAL, "estimate_flops: N, D, V must all be >= 1");
+  uint64_t scored = 0, factor = 2;
+  switch (backend) {
+    case 0: scored = static_cast<uint64_t>(v); break;
+    case 1: scored = 1 + static_cast<uint64_t>(ns); break;
+    case 2: scored = static_cast<uint64_t>(v); factor = 3; break;
+    case 3: scored = 1 + static_cast<uint64_t>(ns); factor = 3; break;
+    case 4: scored = 2; break;
+    default: return fail(LF_EINVAL, "estimate_flops: unknown backend " + std::to_string(backend));
+  }
+  const uint64_t f = static_cast<uint64_t>(n) * static_cast<uint64_t>(d) * scored;
+  if (forward) *forward = f;
+  if (backward) *backward = factor * f;
+  return LF_OK;
+}
+
+int lf_workspace_stats(uint64_t* current_bytes, uint64_t* peak_bytes) {
+  if (current_bytes) *current_bytes = g_ws_current.load();
+  if (peak_bytes) *peak_bytes = g_ws_peak.load();
+  return LF_OK;
+}
+int lf_workspace_reset_peak(void) {
+  g_ws_peak.store(g_ws_current.load());
+  return LF_OK;
+}
+uint64_t lf_launch_count(void) { return g_launches.load(); }
+void lf_launch_count_reset(void) { g_launches.store(0); }
+
+}  // extern "C"

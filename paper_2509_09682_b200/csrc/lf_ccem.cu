@@ -1,0 +1,668 @@
+// lf_ccem.cu — CCE- (negative-sampled fused CE, paper Alg. 1-2) and device
+// input validation.
+//
+// Reference semantics (proj/src/ccem.cpp):
+//   forward  (ccem.cpp:48-105): per row i, logits o_is = X_i . E_{inds(i,s)}
+//            for s = 0..w-1, online LSE, pos_i = o_i0.
+//   backward (ccem.cpp:107-194): g_is = (softmax_is - [s==0]) * u_i;
+//            dX_i = sum_s g_is E_{inds(i,s)} (slot order);
+//            dE_v = sum over (i,s) with inds(i,s)=v, (i,s) ascending, of g_is X_i.
+//            Duplicates accumulate additively; untouched items get exact zeros.
+// B200 design:
+//   * bf16 / f32 with d % 64 == 0: 8 lanes cooperate on one gathered 2d-byte
+//     row (coalesced 16-B vector loads), 4 slots per warp step.
+//   * exact (f64) / any d: one lane per slot, k-ascending dot (bitwise pos).
+//   * dE (default): deterministic — a stable LSD radix sort of the
+//     (item, slot-key) pairs (keys arrive ascending, so a stable sort by item
+//     keeps (i,s) order inside each item), then one warp per item reduces its
+//     segment in that order.  LF_FLAG_ATOMIC_DE selects red.global.add.v4.f32.
+#include <cfloat>
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "lf_internal.cuh"
+#include "lf_kernels.cuh"
+
+namespace lf {
+
+namespace {
+
+// ------------------------------------------------------------------ loads --
+template <class T>
+struct Vec8;  // 8 consecutive elements of row storage, widened to float
+template <>
+struct Vec8<__nv_bfloat16> {
+  static __device__ __forceinline__ void load(const __nv_bfloat16* p, float (&f)[8]) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      f[2 * i] = __uint_as_float(w[i] << 16);
+      f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+    }
+  }
+};
+template <>
+struct Vec8<float> {
+  static __device__ __forceinline__ void load(const float* p, float (&f)[8]) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+    f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+  }
+};
+
+// ------------------------------------------------- vectorized (bf16 / f32) --
+// Warp per row; lane = 8*g + c: slot group g (4 slots per step), dim chunk c
+// covering dims [c*DPL, (c+1)*DPL), DPL = D/8.
+template <class TE, int D>
+__global__ void __launch_bounds__(256) ccem_fwd_vec(const TE* __restrict__ X,
+                                                    const TE* __restrict__ E,
+                                                    const int64_t* __restrict__ inds, int64_t n,
+                                                    int64_t w, double* __restrict__ lse,
+                                                    double* __restrict__ pos) {
+  constexpr int DPL = D / 8;
+  const int lane = threadIdx.x & 31, g = lane >> 3, c = lane & 7;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (row >= n) return;
+  float xr[DPL];
+#pragma unroll
+  for (int b = 0; b < DPL / 8; ++b) {
+    float f[8];
+    Vec8<TE>::load(X + row * D + c * DPL + 8 * b, f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) xr[8 * b + i] = f[i];
+  }
+  const int64_t* irow = inds + row * w;
+  float m = -INFINITY, s = 0.f, p0 = 0.f;
+  for (int64_t s0 = 0; s0 < w; s0 += 16) {
+    float o[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t slot = s0 + 4 * u + g;
+      float acc = 0.f;
+      if (slot < w) {
+        const int64_t item = __ldg(irow + slot);
+        const TE* er = E + item * D + c * DPL;
+#pragma unroll
+        for (int b = 0; b < DPL / 8; ++b) {
+          float f[8];
+          Vec8<TE>::load(er + 8 * b, f);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc = fmaf(xr[8 * b + i], f[i], acc);
+        }
+      }
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+      o[u] = slot < w ? acc : -INFINITY;
+      if (slot == 0) p0 = acc;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (o[u] == -INFINITY) continue;
+      if (o[u] <= m) {
+        s += __expf(o[u] - m);
+      } else {
+        s = s * __expf(m - o[u]) + 1.f;
+        m = o[u];
+      }
+    }
+  }
+  // merge the 4 slot groups (lanes differing in bits 3,4)
+#pragma unroll
+  for (int off = 8; off <= 16; off <<= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, off);
+    const float s2 = __shfl_xor_sync(0xffffffffu, s, off);
+    const float M = fmaxf(m, m2);
+    s = (m == -INFINITY ? 0.f : s * __expf(m - M)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - M));
+    m = M;
+  }
+  p0 = __shfl_sync(0xffffffffu, p0, 0);
+  if (lane == 0) {
+    lse[row] = static_cast<double>(m) + log(static_cast<double>(s));
+    pos[row] = p0;
+  }
+}
+
+// Backward rows pass: recompute, g = (softmax - [s==0]) * u; dX row; coeff
+// per slot (fp32) for the dE pass, or atomic scatter when ATOMIC.
+template <class TE, int D, bool ATOMIC>
+__global__ void __launch_bounds__(256) ccem_bwd_rows_vec(
+    const TE* __restrict__ X, const TE* __restrict__ E, const int64_t* __restrict__ inds,
+    int64_t n, int64_t w, const double* __restrict__ lse, const double* __restrict__ row_up,
+    double upstream_over_n, float* __restrict__ dX, float* __restrict__ coeff,
+    float* __restrict__ dE) {
+  constexpr int DPL = D / 8;
+  const int lane = threadIdx.x & 31, g = lane >> 3, c = lane & 7;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (row >= n) return;
+  float xr[DPL], acc[DPL];
+#pragma unroll
+  for (int b = 0; b < DPL / 8; ++b) {
+    float f[8];
+    Vec8<TE>::load(X + row * D + c * DPL + 8 * b, f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      xr[8 * b + i] = f[i];
+      acc[8 * b + i] = 0.f;
+    }
+  }
+  const float rl = static_cast<float>(lse[row]);
+  const float u = static_cast<float>(row_up ? row_up[row] : upstream_over_n);
+  const int64_t* irow = inds + row * w;
+  for (int64_t s0 = 0; s0 < w; s0 += 4) {
+    const int64_t slot = s0 + g;
+    if (slot < w) {  // uniform within each 8-lane group
+      const int64_t item = __ldg(irow + slot);
+      const TE* er = E + item * D + c * DPL;
+      float ev[DPL];
+      float dot = 0.f;
+#pragma unroll
+      for (int b = 0; b < DPL / 8; ++b) {
+        float f[8];
+        Vec8<TE>::load(er + 8 * b, f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          ev[8 * b + i] = f[i];
+          dot = fmaf(xr[8 * b + i], f[i], dot);
+        }
+      }
+      const unsigned gm = 0xFFu << (8 * g);
+      dot += __shfl_xor_sync(gm, dot, 1);
+      dot += __shfl_xor_sync(gm, dot, 2);
+      dot += __shfl_xor_sync(gm, dot, 4);
+      const float soft = __expf(dot - rl);
+      const float gcoef = (slot == 0 ? soft - 1.f : soft) * u;
+#pragma unroll
+      for (int i = 0; i < DPL; ++i) acc[i] = fmaf(gcoef, ev[i], acc[i]);
+      if (ATOMIC) {
+        float* dst = dE + item * D + c * DPL;
+#pragma unroll
+        for (int i = 0; i < DPL; i += 4) {
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + i),
+                       "f"(gcoef * xr[i]), "f"(gcoef * xr[i + 1]), "f"(gcoef * xr[i + 2]),
+                       "f"(gcoef * xr[i + 3])
+                       : "memory");
+        }
+      } else if (c == 0) {
+        coeff[row * w + slot] = gcoef;
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) {
+    acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 8);
+    acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 16);
+  }
+  if (g == 0) {
+#pragma unroll
+    for (int i = 0; i < DPL; i += 4)
+      *reinterpret_cast<float4*>(dX + row * D + c * DPL + i) =
+          make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+  }
+}
+
+// ------------------------------------------------- generic / exact (T) -----
+template <class T>
+__device__ __forceinline__ T mac(T acc, T a, T b) { return fmaf(a, b, acc); }
+template <>
+__device__ __forceinline__ double mac<double>(double acc, double a, double b) {
+  return __dadd_rn(acc, __dmul_rn(a, b));  // ccem.cpp:38-44 order, no contraction
+}
+template <class T>
+__device__ __forceinline__ T t_exp(T x) { return expf(x); }
+template <>
+__device__ __forceinline__ double t_exp<double>(double x) { return exp(x); }
+
+// Warp per row, lane per slot; the per-lane (m,s) states are merged at the end.
+template <class T>
+__global__ void __launch_bounds__(256) ccem_fwd_generic(const T* __restrict__ X,
+                                                        const T* __restrict__ E,
+                                                        const int64_t* __restrict__ inds,
+                                                        int64_t n, int D, int64_t w,
+                                                        double* __restrict__ lse,
+                                                        double* __restrict__ pos) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (row >= n) return;
+  const T* xr = X + row * D;
+  T m = -INFINITY, s = T(0), p0 = T(0);
+  for (int64_t slot = lane; slot < w; slot += 32) {
+    const T* er = E + inds[row * w + slot] * D;
+    T o = T(0);
+    for (int k = 0; k < D; ++k) o = mac(o, xr[k], er[k]);
+    if (slot == 0) p0 = o;
+    if (o <= m) {
+      s += t_exp(o - m);
+    } else {
+      s = s * t_exp(m - o) + T(1);
+      m = o;
+    }
+  }
+  for (int off = 1; off < 32; off <<= 1) {
+    const T m2 = __shfl_xor_sync(0xffffffffu, m, off);
+    const T s2 = __shfl_xor_sync(0xffffffffu, s, off);
+    const T M = m > m2 ? m : m2;
+    s = (m == -INFINITY ? T(0) : s * t_exp(m - M)) + (m2 == -INFINITY ? T(0) : s2 * t_exp(m2 - M));
+    m = M;
+  }
+  p0 = __shfl_sync(0xffffffffu, p0, 0);
+  if (lane == 0) {
+    lse[row] = static_cast<double>(m) + log(static_cast<double>(s));
+    pos[row] = static_cast<double>(p0);
+  }
+}
+
+// Rows pass: coefficient per slot (lane per slot, exact dot), then dX with
+// lanes owning dims and slots in ascending order (reference order).
+template <class T>
+__global__ void __launch_bounds__(256) ccem_bwd_rows_generic(
+    const T* __restrict__ X, const T* __restrict__ E, const int64_t* __restrict__ inds,
+    int64_t n, int D, int64_t w, const double* __restrict__ lse, const double* __restrict__ row_up,
+    double upstream_over_n, T* __restrict__ dX, T* __restrict__ coeff) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (row >= n) return;
+  const T* xr = X + row * D;
+  const T rl = static_cast<T>(lse[row]);
+  const T u = static_cast<T>(row_up ? row_up[row] : upstream_over_n);
+  for (int64_t slot = lane; slot < w; slot += 32) {
+    const T* er = E + inds[row * w + slot] * D;
+    T o = T(0);
+    for (int k = 0; k < D; ++k) o = mac(o, xr[k], er[k]);
+    const T soft = t_exp(o - rl);
+    coeff[row * w + slot] = (slot == 0 ? soft - T(1) : soft) * u;
+  }
+  __syncwarp();
+  for (int k = lane; k < D; k += 32) {
+    T acc = T(0);
+    for (int64_t slot = 0; slot < w; ++slot)
+      acc = mac(acc, coeff[row * w + slot], E[inds[row * w + slot] * D + k]);
+    dX[row * D + k] = acc;
+  }
+}
+
+// ------------------------------------------------- stable radix sort --------
+constexpr int kSortThreads = 256;
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kPerWarp = 512;  // contiguous elements per warp
+constexpr int kSortTile = kSortWarps * kPerWarp;
+
+__device__ __forceinline__ uint32_t load_item(const int64_t* inds, const uint32_t* keys, int64_t i) {
+  return keys ? keys[i] : static_cast<uint32_t>(inds[i]);
+}
+
+// hist[digit * nblocks + block]
+__global__ void __launch_bounds__(kSortThreads) radix_hist(const int64_t* __restrict__ inds,
+                                                           const uint32_t* __restrict__ keys,
+                                                           int64_t count, int shift,
+                                                           uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[256];
+  for (int i = threadIdx.x; i < 256; i += kSortThreads) h[i] = 0;
+  __syncthreads();
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kSortTile;
+  for (int j = threadIdx.x; j < kSortTile; j += kSortThreads) {
+    const int64_t i = base + j;
+    if (i < count) atomicAdd(&h[(load_item(inds, keys, i) >> shift) & 0xFF], 1u);
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < 256; d += kSortThreads) hist[d * gridDim.x + blockIdx.x] = h[d];
+}
+
+// Stable scatter: element order inside the tile = warp-major, then 32-wide
+// steps, then lane — exactly index order.
+__global__ void __launch_bounds__(kSortThreads) radix_scatter(
+    const int64_t* __restrict__ inds, const uint32_t* __restrict__ keys_in,
+    const uint32_t* __restrict__ vals_in, int64_t count, int shift,
+    const uint32_t* __restrict__ offs, uint32_t* __restrict__ keys_out,
+    uint32_t* __restrict__ vals_out) {
+  __shared__ uint32_t wcnt[kSortWarps][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < kSortWarps * 256; i += kSortThreads) (&wcnt[0][0])[i] = 0;
+  __syncthreads();
+  const int64_t wbase = static_cast<int64_t>(blockIdx.x) * kSortTile + warp * kPerWarp;
+  const unsigned lt = (1u << lane) - 1u;
+  // pass A: per-warp digit counts
+  for (int st = 0; st < kPerWarp; st += 32) {
+    const int64_t i = wbase + st + lane;
+    const bool ok = i < count;
+    const uint32_t dg = ok ? (load_item(inds, keys_in, i) >> shift) & 0xFF : 256u + lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, dg);
+    if (ok && (peers & lt) == 0) wcnt[warp][dg] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // exclusive prefix over warps per digit, plus the block's global offset
+  for (int d = threadIdx.x; d < 256; d += kSortThreads) {
+    uint32_t run = offs[d * gridDim.x + blockIdx.x];
+    for (int wi = 0; wi < kSortWarps; ++wi) {
+      const uint32_t c = wcnt[wi][d];
+      wcnt[wi][d] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  // pass B: scatter with running per-warp counters
+  for (int st = 0; st < kPerWarp; st += 32) {
+    const int64_t i = wbase + st + lane;
+    const bool ok = i < count;
+    const uint32_t key = ok ? load_item(inds, keys_in, i) : 0u;
+    const uint32_t dg = ok ? (key >> shift) & 0xFF : 256u + lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, dg);
+    if (ok) {
+      const uint32_t dst = wcnt[warp][dg] + __popc(peers & lt);
+      keys_out[dst] = key;
+      vals_out[dst] = vals_in ? vals_in[i] : static_cast<uint32_t>(i);
+    }
+    __syncwarp();
+    if (ok && (peers & lt) == 0) wcnt[warp][dg] += __popc(peers);
+    __syncwarp();
+  }
+}
+
+// Exclusive scan of uint32 (3-level: tiles of 2048 -> block sums -> add).
+__global__ void scan_tiles(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                           int64_t count, uint32_t* __restrict__ sums) {
+  __shared__ uint32_t s[1024];
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * 2048;
+  const int64_t i0 = base + 2 * threadIdx.x;
+  const uint32_t a = i0 < count ? in[i0] : 0u;
+  const uint32_t b = i0 + 1 < count ? in[i0 + 1] : 0u;
+  s[threadIdx.x] = a + b;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    const uint32_t t = threadIdx.x >= off ? s[threadIdx.x - off] : 0u;
+    __syncthreads();
+    s[threadIdx.x] += t;
+    __syncthreads();
+  }
+  const uint32_t excl = s[threadIdx.x] - (a + b);
+  if (i0 < count) out[i0] = excl;
+  if (i0 + 1 < count) out[i0 + 1] = excl + a;
+  if (threadIdx.x == 1023 && sums) sums[blockIdx.x] = s[1023];
+}
+__global__ void scan_add(uint32_t* __restrict__ out, int64_t count,
+                         const uint32_t* __restrict__ sums_scanned) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < count) out[i] += sums_scanned[i / 2048];
+}
+
+int exclusive_scan(const uint32_t* in, uint32_t* out, int64_t count, cudaStream_t st) {
+  const int64_t tiles = ceil_div(count, 2048);
+  if (tiles == 1) {
+    scan_tiles<<<1, 1024, 0, st>>>(in, out, count, nullptr);
+    LF_LAUNCHED();
+    return LF_OK;
+  }
+  Scratch sums, sums_scan;
+  int rc = sums.alloc(sizeof(uint32_t) * tiles, st);
+  if (!rc) rc = sums_scan.alloc(sizeof(uint32_t) * tiles, st);
+  if (rc) return rc;
+  scan_tiles<<<tiles, 1024, 0, st>>>(in, out, count, sums.as<uint32_t>());
+  LF_LAUNCHED();
+  rc = exclusive_scan(sums.as<uint32_t>(), sums_scan.as<uint32_t>(), tiles, st);
+  if (rc) return rc;
+  scan_add<<<ceil_div(count, 256), 256, 0, st>>>(out, count, sums_scan.as<uint32_t>());
+  LF_LAUNCHED();
+  return LF_OK;
+}
+
+__global__ void item_hist(const int64_t* __restrict__ inds, int64_t count,
+                          uint32_t* __restrict__ counts) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    atomicAdd(&counts[inds[i]], 1u);
+}
+
+// Warp per item: dE_v = sum over its (i,s) entries in ascending order of
+// coeff[i,s] * X_i.  Items with no entry get exact zeros.
+template <class TX, class TG, class TO>
+__global__ void __launch_bounds__(256) segment_reduce(const TX* __restrict__ X,
+                                                      const TG* __restrict__ coeff,
+                                                      const uint32_t* __restrict__ sorted_vals,
+                                                      const uint32_t* __restrict__ item_off,
+                                                      int64_t v, int D, int64_t w,
+                                                      TO* __restrict__ dE) {
+  const int lane = threadIdx.x & 31;
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (item >= v) return;
+  const uint32_t b = item_off[item], e = item_off[item + 1];
+  for (int k0 = 0; k0 < D; k0 += 64) {
+    TG acc0 = TG(0), acc1 = TG(0);
+    const int ka = k0 + lane, kb = k0 + 32 + lane;
+    for (uint32_t p = b; p < e; ++p) {
+      const uint32_t key = sorted_vals[p];
+      const TG gk = coeff[key];
+      const TX* xr = X + static_cast<int64_t>(key / w) * D;
+      if (ka < D) acc0 = mac(acc0, gk, static_cast<TG>(to_f32_or_self(xr[ka])));
+      if (kb < D) acc1 = mac(acc1, gk, static_cast<TG>(to_f32_or_self(xr[kb])));
+    }
+    if (ka < D) dE[item * D + ka] = static_cast<TO>(acc0);
+    if (kb < D) dE[item * D + kb] = static_cast<TO>(acc1);
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+int ccem_forward(int dtype, const void* X, const void* E, const int64_t* inds, int64_t n, int D,
+                 int64_t v, int64_t w, double* lse, double* pos, double* loss, cudaStream_t st) {
+  (void)v;
+  const dim3 grid(static_cast<unsigned>(ceil_div(n, 8)));
+  if (dtype == LF_BF16 || (dtype == LF_F32 && D % 64 == 0 && D <= 256)) {
+#define LF_FWD_VEC(TE, DD)                                                                     \
+  ccem_fwd_vec<TE, DD><<<grid, 256, 0, st>>>(static_cast<const TE*>(X),                        \
+                                            static_cast<const TE*>(E), inds, n, w, lse, pos)
+    if (dtype == LF_BF16) {
+      if (D == 64) LF_FWD_VEC(__nv_bfloat16, 64);
+      else if (D == 128) LF_FWD_VEC(__nv_bfloat16, 128);
+      else if (D == 256) LF_FWD_VEC(__nv_bfloat16, 256);
+      else return fail(LF_EUNSUPPORTED, "ccem bf16: d must be 64, 128 or 256");
+    } else {
+      if (D == 64) LF_FWD_VEC(float, 64);
+      else if (D == 128) LF_FWD_VEC(float, 128);
+      else LF_FWD_VEC(float, 256);
+    }
+#undef LF_FWD_VEC
+  } else if (dtype == LF_F32) {
+    ccem_fwd_generic<float><<<grid, 256, 0, st>>>(static_cast<const float*>(X),
+                                                   static_cast<const float*>(E), inds, n, D, w,
+                                                   lse, pos);
+  } else {
+    ccem_fwd_generic<double><<<grid, 256, 0, st>>>(static_cast<const double*>(X),
+                                                    static_cast<const double*>(E), inds, n, D, w,
+                                                    lse, pos);
+  }
+  LF_LAUNCHED();
+  if (loss) return launch_mean_loss(lse, pos, n, loss, st);
+  return LF_OK;
+}
+
+// Sort (item, key) pairs stably by item; returns sorted keys (slot ids) and
+// per-item offsets (v+1).
+static int sort_by_item(const int64_t* inds, int64_t count, int64_t v, Scratch& sorted_vals,
+                        Scratch& item_off, cudaStream_t st) {
+  if (count >= (int64_t(1) << 32)) return fail(LF_EUNSUPPORTED, "ccem: n*w must be < 2^32");
+  Scratch k0, k1, v1, hist, offs;
+  int rc = k0.alloc(sizeof(uint32_t) * count, st);
+  if (!rc) rc = k1.alloc(sizeof(uint32_t) * count, st);
+  if (!rc) rc = v1.alloc(sizeof(uint32_t) * count, st);
+  if (!rc) rc = sorted_vals.alloc(sizeof(uint32_t) * count, st);
+  const int64_t blocks = ceil_div(count, kSortTile);
+  if (!rc) rc = hist.alloc(sizeof(uint32_t) * 256 * blocks, st);
+  if (!rc) rc = offs.alloc(sizeof(uint32_t) * 256 * blocks, st);
+  if (!rc) rc = item_off.alloc(sizeof(uint32_t) * (v + 1), st);
+  if (rc) return rc;
+  int passes = 1;
+  while (passes < 4 && ((static_cast<uint64_t>(v - 1) >> (8 * passes)) != 0)) ++passes;
+  // ping-pong so the final pass lands in sorted_vals (pass p writes S when
+  // passes-1-p is even, else the spare buffer); keys alternate k0/k1.
+  uint32_t* kin = nullptr;
+  uint32_t* vin = nullptr;
+  for (int p = 0; p < passes; ++p) {
+    const bool even_from_end = ((passes - 1 - p) % 2) == 0;
+    uint32_t* kout = even_from_end ? k0.as<uint32_t>() : k1.as<uint32_t>();
+    uint32_t* vout = even_from_end ? sorted_vals.as<uint32_t>() : v1.as<uint32_t>();
+    radix_hist<<<blocks, kSortThreads, 0, st>>>(inds, kin, count, 8 * p, hist.as<uint32_t>());
+    LF_LAUNCHED();
+    rc = exclusive_scan(hist.as<uint32_t>(), offs.as<uint32_t>(), 256 * blocks, st);
+    if (rc) return rc;
+    radix_scatter<<<blocks, kSortThreads, 0, st>>>(inds, kin, vin, count, 8 * p,
+                                                   offs.as<uint32_t>(), kout, vout);
+    LF_LAUNCHED();
+    kin = kout;
+    vin = vout;
+  }
+  // item offsets
+  Scratch counts;
+  rc = counts.alloc(sizeof(uint32_t) * (v + 1), st);
+  if (rc) return rc;
+  LF_CUDA(cudaMemsetAsync(counts.ptr, 0, sizeof(uint32_t) * (v + 1), st));
+  item_hist<<<std::min<int64_t>(ceil_div(count, 256), 8 * num_sms()), 256, 0, st>>>(
+      inds, count, counts.as<uint32_t>());
+  LF_LAUNCHED();
+  return exclusive_scan(counts.as<uint32_t>(), item_off.as<uint32_t>(), v + 1, st);
+}
+
+int ccem_backward(int dtype, const void* X, const void* E, const int64_t* inds,
+                  const double* lse, const double* row_upstream, double upstream, int64_t n,
+                  int D, int64_t v, int64_t w, bool atomic_de, void* dX, void* dE,
+                  cudaStream_t st) {
+  const double u_n = upstream / static_cast<double>(n);
+  const dim3 grid(static_cast<unsigned>(ceil_div(n, 8)));
+  const int64_t count = n * w;
+  const bool vec = dtype == LF_BF16 || (dtype == LF_F32 && D % 64 == 0 && D <= 256);
+  if (dtype == LF_BF16 && !(D == 64 || D == 128 || D == 256))
+    return fail(LF_EUNSUPPORTED, "ccem bf16: d must be 64, 128 or 256");
+  if (dtype == LF_F64) atomic_de = false;  // exact mode is always ordered
+  Scratch coeff;
+  if (!atomic_de) {
+    int rc = coeff.alloc((dtype == LF_F64 ? sizeof(double) : sizeof(float)) * count, st);
+    if (rc) return rc;
+  } else {
+    LF_CUDA(cudaMemsetAsync(dE, 0, sizeof(float) * v * D, st));
+  }
+  if (vec) {
+#define LF_ROWS(TE, DD, AT)                                                                      \
+  ccem_bwd_rows_vec<TE, DD, AT><<<grid, 256, 0, st>>>(                                           \
+      static_cast<const TE*>(X), static_cast<const TE*>(E), inds, n, w, lse, row_upstream, u_n,   \
+      static_cast<float*>(dX), coeff.as<float>(), static_cast<float*>(dE))
+#define LF_ROWS_D(TE, AT)                 \
+  if (D == 64) LF_ROWS(TE, 64, AT);        \
+  else if (D == 128) LF_ROWS(TE, 128, AT); \
+  else LF_ROWS(TE, 256, AT);
+    if (dtype == LF_BF16) {
+      if (atomic_de) { LF_ROWS_D(__nv_bfloat16, true) } else { LF_ROWS_D(__nv_bfloat16, false) }
+    } else {
+      if (atomic_de) { LF_ROWS_D(float, true) } else { LF_ROWS_D(float, false) }
+    }
+#undef LF_ROWS_D
+#undef LF_ROWS
+    LF_LAUNCHED();
+    if (atomic_de) return LF_OK;
+  } else if (dtype == LF_F32) {
+    if (atomic_de) return fail(LF_EUNSUPPORTED, "ccem: atomic dE needs d % 64 == 0");
+    ccem_bwd_rows_generic<float><<<grid, 256, 0, st>>>(
+        static_cast<const float*>(X), static_cast<const float*>(E), inds, n, D, w, lse,
+        row_upstream, u_n, static_cast<float*>(dX), coeff.as<float>());
+    LF_LAUNCHED();
+  } else {
+    ccem_bwd_rows_generic<double><<<grid, 256, 0, st>>>(
+        static_cast<const double*>(X), static_cast<const double*>(E), inds, n, D, w, lse,
+        row_upstream, u_n, static_cast<double*>(dX), coeff.as<double>());
+    LF_LAUNCHED();
+  }
+  Scratch sorted_vals, item_off;
+  int rc = sort_by_item(inds, count, v, sorted_vals, item_off, st);
+  if (rc) return rc;
+  const dim3 sgrid(static_cast<unsigned>(ceil_div(v, 8)));
+  if (dtype == LF_BF16) {
+    segment_reduce<__nv_bfloat16, float, float><<<sgrid, 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(X), coeff.as<float>(), sorted_vals.as<uint32_t>(),
+        item_off.as<uint32_t>(), v, D, w, static_cast<float*>(dE));
+  } else if (dtype == LF_F32) {
+    segment_reduce<float, float, float><<<sgrid, 256, 0, st>>>(
+        static_cast<const float*>(X), coeff.as<float>(), sorted_vals.as<uint32_t>(),
+        item_off.as<uint32_t>(), v, D, w, static_cast<float*>(dE));
+  } else {
+    segment_reduce<double, double, double><<<sgrid, 256, 0, st>>>(
+        static_cast<const double*>(X), coeff.as<double>(), sorted_vals.as<uint32_t>(),
+        item_off.as<uint32_t>(), v, D, w, static_cast<double*>(dE));
+  }
+  LF_LAUNCHED();
+  return LF_OK;
+}
+
+// ------------------------------------------------------------ validation ---
+namespace {
+__global__ void find_bad_targets(const int64_t* __restrict__ t, int64_t n, int64_t v,
+                                 unsigned long long* __restrict__ first) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    if (t[i] < 0 || t[i] >= v) atomicMin(first, static_cast<unsigned long long>(i));
+}
+__global__ void find_bad_inds(const int64_t* __restrict__ inds, int64_t n, int64_t w, int64_t v,
+                              unsigned long long* __restrict__ first) {
+  const int64_t total = n * w;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / w, s = i % w;
+    const int64_t x = inds[i];
+    if (x < 0 || x >= v || (s > 0 && x == inds[r * w]))
+      atomicMin(first, static_cast<unsigned long long>(r));
+  }
+}
+}  // namespace
+
+int validate_targets(const int64_t* targets, int64_t n, int64_t v, cudaStream_t st) {
+  Scratch first;
+  int rc = first.alloc(sizeof(unsigned long long), st);
+  if (rc) return rc;
+  LF_CUDA(cudaMemsetAsync(first.ptr, 0xFF, sizeof(unsigned long long), st));
+  find_bad_targets<<<std::min<int64_t>(ceil_div(n, 256), 4 * num_sms()) + 0, 256, 0, st>>>(
+      targets, n, v, first.as<unsigned long long>());
+  LF_LAUNCHED();
+  unsigned long long bad = 0;
+  LF_CUDA(cudaMemcpyAsync(&bad, first.ptr, sizeof(bad), cudaMemcpyDeviceToHost, st));
+  LF_CUDA(cudaStreamSynchronize(st));
+  if (bad == ~0ull) return LF_OK;
+  int64_t x = 0;
+  LF_CUDA(cudaMemcpy(&x, targets + bad, sizeof(x), cudaMemcpyDeviceToHost));
+  // losses.cpp:62-65
+  return fail(LF_EINVAL, "loss: row " + std::to_string(bad) + " targets item " +
+                             std::to_string(x) + ", outside catalog of " + std::to_string(v));
+}
+
+int validate_inds(const int64_t* inds, int64_t n, int64_t w, int64_t v, cudaStream_t st) {
+  if (w < 1) return fail(LF_EINVAL, "NegIndexMatrix: width must be at least 1 (the positive slot)");
+  Scratch first;
+  int rc = first.alloc(sizeof(unsigned long long), st);
+  if (rc) return rc;
+  LF_CUDA(cudaMemsetAsync(first.ptr, 0xFF, sizeof(unsigned long long), st));
+  find_bad_inds<<<std::min<int64_t>(ceil_div(n * w, 256), 8 * num_sms()), 256, 0, st>>>(
+      inds, n, w, v, first.as<unsigned long long>());
+  LF_LAUNCHED();
+  unsigned long long bad = 0;
+  LF_CUDA(cudaMemcpyAsync(&bad, first.ptr, sizeof(bad), cudaMemcpyDeviceToHost, st));
+  LF_CUDA(cudaStreamSynchronize(st));
+  if (bad == ~0ull) return LF_OK;
+  std::vector<int64_t> row(static_cast<size_t>(w));
+  LF_CUDA(cudaMemcpy(row.data(), inds + bad * w, sizeof(int64_t) * w, cudaMemcpyDeviceToHost));
+  // neg_index.cpp:13-25, same first-failure order within the row
+  for (int64_t s = 0; s < w; ++s) {
+    const int64_t x = row[static_cast<size_t>(s)];
+    if (x < 0 || x >= v)
+      return fail(LF_EINVAL, "NegIndexMatrix: row " + std::to_string(bad) + " slot " +
+                                 std::to_string(s) + " holds " + std::to_string(x) +
+                                 ", outside catalog of " + std::to_string(v));
+    if (s > 0 && x == row[0])
+      return fail(LF_EINVAL, "NegIndexMatrix: row " + std::to_string(bad) +
+                                 " repeats its positive item " + std::to_string(row[0]) +
+                                 " in negative slot " + std::to_string(s));
+  }
+  return fail(LF_EINVAL, "NegIndexMatrix: row " + std::to_string(bad) + " invalid");
+}
+
+}  // namespace lf

@@ -1,0 +1,62 @@
+// lf_kernels.cuh — internal launcher declarations shared by the C-ABI layer.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "lf_internal.cuh"
+
+namespace lf {
+
+// Per-(chunk,row) forward partial: running max m, rescaled sum s, target
+// logit t and a has-target flag.  SIMT path: natural-log units; tensor-core
+// path: float, log2 units (m = max logit * log2 e, s = sum 2^(o log2e - m)).
+template <class T>
+struct alignas(sizeof(T) * 4) Partial {
+  T m, s, t, has;
+};
+
+// ---- SIMT (lf_simt.cu) ----
+template <class T>
+int simt_cce_forward_full(const T* X, const T* E, const int64_t* targets, int64_t n, int D,
+                          int64_t v, double* lse, double* pos, double* loss, cudaStream_t st);
+template <class T>
+int simt_cce_forward_partial_log2(const T* X, const T* E, const int64_t* targets, int64_t n,
+                                  int D, int64_t v, int64_t v_offset, float* out,
+                                  cudaStream_t st);
+template <class T>
+int simt_cce_backward(const T* X, const T* E, const int64_t* targets, const double* lse,
+                      double scale, double eps, int64_t n, int D, int64_t v, int64_t v_offset,
+                      T* dX, T* dE, unsigned long long* skip_counter, cudaStream_t st);
+
+int launch_combine_f32log2(const float* part, int P, int64_t n, double* lse, double* pos,
+                           double* loss, cudaStream_t st);
+int launch_reduce_f32(const float* part, int P, int64_t count, float* out, cudaStream_t st);
+int launch_fold_partials(const float* part, int P, int64_t n, float* out, cudaStream_t st);
+int launch_negate(float* x, int64_t count, cudaStream_t st);
+int launch_mean_loss(const double* lse, const double* pos, int64_t n, double* loss,
+                     cudaStream_t st);
+
+// ---- tensor-core bf16 path (lf_tc.cu) ----
+// Forward partials over the local shard: writes float4 log2-unit partials
+// into `part` (P blocks of n), returns P via *P_out.
+int tc_cce_forward_partials(const void* X, const void* E, const int64_t* targets, int64_t n,
+                            int D, int64_t v, int64_t v_offset, Scratch& ws, float** part_out,
+                            int* P_out, cudaStream_t st);
+int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const double* lse,
+                    double scale, double eps, int64_t n, int D, int64_t v, int64_t v_offset,
+                    float* dX, float* dE, unsigned long long* counters, cudaStream_t st);
+
+// ---- CCE- (lf_ccem.cu) ----
+int ccem_forward(int dtype, const void* X, const void* E, const int64_t* inds, int64_t n, int D,
+                 int64_t v, int64_t w, double* lse, double* pos, double* loss, cudaStream_t st);
+int ccem_backward(int dtype, const void* X, const void* E, const int64_t* inds,
+                  const double* lse, const double* row_upstream, double upstream, int64_t n,
+                  int D, int64_t v, int64_t w, bool atomic_de, void* dX, void* dE,
+                  cudaStream_t st);
+
+// ---- validation (lf_ccem.cu) ----
+int validate_targets(const int64_t* targets, int64_t n, int64_t v, cudaStream_t st);
+int validate_inds(const int64_t* inds, int64_t n, int64_t w, int64_t v, cudaStream_t st);
+
+}  // namespace lf

@@ -1,0 +1,585 @@
+// lf_simt.cu — CUDA-core (SIMT) CCE kernels for the fp32 and fp64 "exact"
+// element types, plus the partial-combine and dX-reduce kernels shared with
+// the tensor-core path.
+//
+// Semantics follow the reference exactly (proj/src/cce.cpp):
+//   logit  o_ij = sum_k X_ik * E_jk, k ascending                (cce.cpp:40-55)
+//   lse_i  = log sum_j exp(o_ij); pos_i = o_{i, x_i} taken from the SAME
+//            tile value that feeds the LSE                       (cce.cpp:111-131)
+//   g_ij   = s*scale, (s-1)*scale at the target, 0 (and counted) for
+//            off-target s < eps                                  (cce.cpp:189-204)
+//   dX = G E (row-owned), dE = G^T X (item-owned): two recompute passes with
+//            single ownership and NO atomics on the gradients    (cce.cpp:206-262)
+// In exact mode (T = double) every product/sum is __dmul_rn/__dadd_rn in the
+// reference's order, so pos is bitwise equal to the CPU's double result.
+#include <cfloat>
+#include <cmath>
+
+#include "lf_internal.cuh"
+#include "lf_kernels.cuh"
+
+namespace lf {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+template <class T>
+__device__ __forceinline__ T mul_rn(T a, T b) { return a * b; }
+template <>
+__device__ __forceinline__ double mul_rn<double>(double a, double b) { return __dmul_rn(a, b); }
+template <class T>
+__device__ __forceinline__ T add_rn(T a, T b) { return a + b; }
+template <>
+__device__ __forceinline__ double add_rn<double>(double a, double b) { return __dadd_rn(a, b); }
+template <class T>
+__device__ __forceinline__ T fma_acc(T acc, T a, T b) { return fmaf(a, b, acc); }
+template <>
+__device__ __forceinline__ double fma_acc<double>(double acc, double a, double b) {
+  return __dadd_rn(acc, __dmul_rn(a, b));  // reference order: acc += a*b, no contraction
+}
+template <class T>
+__device__ __forceinline__ T t_exp(T x) { return expf(x); }
+template <>
+__device__ __forceinline__ double t_exp<double>(double x) { return exp(x); }
+template <class T>
+__device__ __forceinline__ T t_log(T x) { return logf(x); }
+template <>
+__device__ __forceinline__ double t_log<double>(double x) { return log(x); }
+template <class T>
+__device__ __forceinline__ T neg_inf() { return -INFINITY; }
+
+// Stage rows [r0, r0+R) of a row-major [rows x D] matrix into smem laid out
+// [D][R+1] (transposed, padded); rows past `rows` are zero.
+template <class T, int R>
+__device__ __forceinline__ void stage_T(T* s, const T* __restrict__ g, int64_t r0, int64_t rows,
+                                        int D) {
+  for (int idx = threadIdx.x; idx < R * D; idx += kThreads) {
+    const int r = idx / D, k = idx % D;
+    const int64_t row = r0 + r;
+    s[k * (R + 1) + r] = row < rows ? g[row * D + k] : T(0);
+  }
+}
+
+// R x C logit tile from staged Xs [D][R+1] and Es [D][C+1]; each of the 256
+// threads owns RPT rows x CPT columns (RPT*CPT = 8).  Exact mode: k ascending.
+template <class T, int R, int C>
+struct TileMap {
+  static constexpr int RPT = 2;
+  static constexpr int CPT = 4;
+  static constexpr int CG = C / CPT;
+  static_assert((R / RPT) * CG == kThreads, "tile map must cover 256 threads");
+  __device__ static int row(int i) { return (threadIdx.x / CG) * RPT + i; }
+  __device__ static int col(int q) { return (threadIdx.x % CG) + CG * q; }
+  __device__ static void logits(const T* Xs, const T* Es, int D, T (&o)[RPT][CPT]) {
+#pragma unroll
+    for (int i = 0; i < RPT; ++i)
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) o[i][q] = T(0);
+    for (int k = 0; k < D; ++k) {
+      T xv[RPT], ev[CPT];
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) xv[i] = Xs[k * (R + 1) + row(i)];
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) ev[q] = Es[k * (C + 1) + col(q)];
+#pragma unroll
+      for (int i = 0; i < RPT; ++i)
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) o[i][q] = fma_acc(o[i][q], xv[i], ev[q]);
+    }
+  }
+};
+
+// Online LSE update, numeric.hpp:19-27 (branch structure kept).
+template <class T>
+__device__ __forceinline__ void lse_update(T& m, T& s, T o) {
+  if (o <= m) {
+    s += t_exp(o - m);
+  } else {
+    s = s * t_exp(m - o) + T(1);
+    m = o;
+  }
+}
+template <class T>
+__device__ __forceinline__ void lse_merge(T& m, T& s, T m2, T s2) {
+  if (m2 == neg_inf<T>()) return;
+  if (m == neg_inf<T>()) { m = m2; s = s2; return; }
+  const T M = m > m2 ? m : m2;
+  s = s * t_exp(m - M) + s2 * t_exp(m2 - M);
+  m = M;
+}
+
+// ---------------------------------------------------------------------------
+// Forward: block = 32 rows x one V chunk; writes Partial<T> per (chunk, row).
+// ---------------------------------------------------------------------------
+template <class T>
+__global__ void __launch_bounds__(kThreads) cce_simt_fwd(const T* __restrict__ X,
+                                                         const T* __restrict__ E,
+                                                         const int64_t* __restrict__ targets,
+                                                         int64_t n, int D, int64_t v,
+                                                         int64_t v_offset, int64_t chunk,
+                                                         Partial<T>* __restrict__ part) {
+  constexpr int R = 32, C = 64;
+  using M = TileMap<T, R, C>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* Xs = reinterpret_cast<T*>(smem_raw);
+  T* Es = Xs + D * (R + 1);
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * R;
+  const int64_t c_begin = static_cast<int64_t>(blockIdx.y) * chunk;
+  const int64_t c_end = min(v, c_begin + chunk);
+  stage_T<T, R>(Xs, X, r0, n, D);
+
+  T m[M::RPT], s[M::RPT], t[M::RPT], has[M::RPT];
+  int64_t tgt[M::RPT];
+#pragma unroll
+  for (int i = 0; i < M::RPT; ++i) {
+    m[i] = neg_inf<T>();
+    s[i] = T(0);
+    t[i] = T(0);
+    has[i] = T(0);
+    const int64_t row = r0 + M::row(i);
+    tgt[i] = row < n ? targets[row] - v_offset : -1;
+  }
+  for (int64_t c0 = c_begin; c0 < c_end; c0 += C) {
+    __syncthreads();
+    stage_T<T, C>(Es, E, c0, c_end, D);
+    __syncthreads();
+    T o[M::RPT][M::CPT];
+    M::logits(Xs, Es, D, o);
+#pragma unroll
+    for (int i = 0; i < M::RPT; ++i)
+#pragma unroll
+      for (int q = 0; q < M::CPT; ++q) {
+        const int64_t col = c0 + M::col(q);
+        if (col < c_end) {
+          lse_update(m[i], s[i], o[i][q]);
+          if (col == tgt[i]) { t[i] = o[i][q]; has[i] = T(1); }
+        }
+      }
+  }
+  // Merge the CG threads that share each row (consecutive lanes).
+#pragma unroll
+  for (int i = 0; i < M::RPT; ++i) {
+    for (int off = M::CG / 2; off > 0; off >>= 1) {
+      const T m2 = __shfl_xor_sync(0xffffffffu, m[i], off);
+      const T s2 = __shfl_xor_sync(0xffffffffu, s[i], off);
+      const T t2 = __shfl_xor_sync(0xffffffffu, t[i], off);
+      const T h2 = __shfl_xor_sync(0xffffffffu, has[i], off);
+      lse_merge(m[i], s[i], m2, s2);
+      if (h2 != T(0)) { t[i] = t2; has[i] = T(1); }
+    }
+    const int64_t row = r0 + M::row(i);
+    if ((threadIdx.x % M::CG) == 0 && row < n) {
+      Partial<T> p;
+      p.m = m[i];
+      p.s = s[i];
+      p.t = t[i];
+      p.has = has[i];
+      part[static_cast<int64_t>(blockIdx.y) * n + row] = p;
+    }
+  }
+}
+
+// Coefficient of one element (cce.cpp:189-204).
+template <class T>
+__device__ __forceinline__ T coeff(T o, T row_lse, bool is_target, T eps, T scale,
+                                   unsigned& skips) {
+  const T s = t_exp(o - row_lse);
+  if (is_target) return (s - T(1)) * scale;
+  if (eps > T(0) && s < eps) {
+    ++skips;
+    return T(0);
+  }
+  return s * scale;
+}
+
+// ---------------------------------------------------------------------------
+// Backward dX: block = 32 rows x one V chunk; dX partial per chunk.
+// ---------------------------------------------------------------------------
+template <class T>
+__global__ void __launch_bounds__(kThreads) cce_simt_bwd_dx(
+    const T* __restrict__ X, const T* __restrict__ E, const int64_t* __restrict__ targets,
+    const double* __restrict__ lse, int64_t n, int D, int64_t v, int64_t v_offset, int64_t chunk,
+    T scale, T eps, T* __restrict__ dx_part, unsigned long long* __restrict__ skip_counter) {
+  constexpr int R = 32, C = 64;
+  using M = TileMap<T, R, C>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* Xs = reinterpret_cast<T*>(smem_raw);
+  T* Es = Xs + D * (R + 1);
+  T* Gs = Es + D * (C + 1);  // [R][C+1]
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * R;
+  const int64_t c_begin = static_cast<int64_t>(blockIdx.y) * chunk;
+  const int64_t c_end = min(v, c_begin + chunk);
+  stage_T<T, R>(Xs, X, r0, n, D);
+
+  T row_lse[M::RPT];
+  int64_t tgt[M::RPT];
+#pragma unroll
+  for (int i = 0; i < M::RPT; ++i) {
+    const int64_t row = r0 + M::row(i);
+    row_lse[i] = row < n ? static_cast<T>(lse[row]) : T(0);
+    tgt[i] = row < n ? targets[row] - v_offset : -1;
+  }
+  // dX accumulators: row = tid/8, dims (tid%8) + 8q.
+  const int arow = threadIdx.x / 8, adim = threadIdx.x % 8;
+  const int nq = (D - adim + 7) / 8;
+  T acc[32];
+#pragma unroll
+  for (int q = 0; q < 32; ++q) acc[q] = T(0);
+  unsigned skips = 0;
+
+  for (int64_t c0 = c_begin; c0 < c_end; c0 += C) {
+    __syncthreads();
+    stage_T<T, C>(Es, E, c0, c_end, D);
+    __syncthreads();
+    T o[M::RPT][M::CPT];
+    M::logits(Xs, Es, D, o);
+#pragma unroll
+    for (int i = 0; i < M::RPT; ++i)
+#pragma unroll
+      for (int q = 0; q < M::CPT; ++q) {
+        const int64_t col = c0 + M::col(q);
+        const bool valid = col < c_end && (r0 + M::row(i)) < n;
+        T g = T(0);
+        if (valid) g = coeff(o[i][q], row_lse[i], col == tgt[i], eps, scale, skips);
+        Gs[M::row(i) * (C + 1) + M::col(q)] = g;
+      }
+    __syncthreads();
+    const int cn = static_cast<int>((c_end - c0 < C ? c_end - c0 : C));
+    for (int j = 0; j < cn; ++j) {
+      const T gv = Gs[arow * (C + 1) + j];
+#pragma unroll
+      for (int q = 0; q < 32; ++q)
+        if (q < nq) acc[q] = fma_acc(acc[q], gv, Es[(adim + 8 * q) * (C + 1) + j]);
+    }
+  }
+  const int64_t row = r0 + arow;
+  if (row < n) {
+    T* out = dx_part + static_cast<int64_t>(blockIdx.y) * n * D + row * D;
+#pragma unroll
+    for (int q = 0; q < 32; ++q)
+      if (q < nq) out[adim + 8 * q] = acc[q];
+  }
+  if (skip_counter) {
+    for (int off = 16; off > 0; off >>= 1) skips += __shfl_xor_sync(0xffffffffu, skips, off);
+    if ((threadIdx.x & 31) == 0 && skips) atomicAdd(skip_counter, static_cast<unsigned long long>(skips));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Backward dE: block = 32 items, loops over all rows (ascending row tiles).
+// ---------------------------------------------------------------------------
+template <class T>
+__global__ void __launch_bounds__(kThreads) cce_simt_bwd_de(
+    const T* __restrict__ X, const T* __restrict__ E, const int64_t* __restrict__ targets,
+    const double* __restrict__ lse, int64_t n, int D, int64_t v, int64_t v_offset, T scale,
+    T eps, T* __restrict__ dE) {
+  constexpr int R = 64, C = 32;
+  using M = TileMap<T, R, C>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* Es = reinterpret_cast<T*>(smem_raw);
+  T* Xs = Es + D * (C + 1);
+  T* Gs = Xs + D * (R + 1);  // [R][C+1]
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * C;
+  stage_T<T, C>(Es, E, c0, v, D);
+  const int aitem = threadIdx.x / 8, adim = threadIdx.x % 8;
+  const int nq = (D - adim + 7) / 8;
+  T acc[32];
+#pragma unroll
+  for (int q = 0; q < 32; ++q) acc[q] = T(0);
+  unsigned skips = 0;
+
+  for (int64_t r0 = 0; r0 < n; r0 += R) {
+    __syncthreads();
+    stage_T<T, R>(Xs, X, r0, n, D);
+    __syncthreads();
+    T o[M::RPT][M::CPT];
+    M::logits(Xs, Es, D, o);
+#pragma unroll
+    for (int i = 0; i < M::RPT; ++i) {
+      const int64_t row = r0 + M::row(i);
+      const bool rvalid = row < n;
+      const T rl = rvalid ? static_cast<T>(lse[row]) : T(0);
+      const int64_t tg = rvalid ? targets[row] - v_offset : -1;
+#pragma unroll
+      for (int q = 0; q < M::CPT; ++q) {
+        const int64_t col = c0 + M::col(q);
+        T g = T(0);
+        if (rvalid && col < v) g = coeff(o[i][q], rl, col == tg, eps, scale, skips);
+        Gs[M::row(i) * (C + 1) + M::col(q)] = g;
+      }
+    }
+    __syncthreads();
+    const int rn = static_cast<int>((n - r0 < R ? n - r0 : R));
+    for (int i = 0; i < rn; ++i) {
+      const T gv = Gs[i * (C + 1) + aitem];
+#pragma unroll
+      for (int q = 0; q < 32; ++q)
+        if (q < nq) acc[q] = fma_acc(acc[q], gv, Xs[(adim + 8 * q) * (R + 1) + i]);
+    }
+  }
+  const int64_t item = c0 + aitem;
+  if (item < v) {
+#pragma unroll
+    for (int q = 0; q < 32; ++q)
+      if (q < nq) dE[item * D + adim + 8 * q] = acc[q];
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Combine / reduce (shared with the tensor-core path).
+// ---------------------------------------------------------------------------
+template <class T, bool LOG2>
+__global__ void combine_partials(const Partial<T>* __restrict__ part, int P, int64_t n,
+                                 double* __restrict__ lse, double* __restrict__ pos) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double M = -INFINITY;
+  for (int p = 0; p < P; ++p) M = fmax(M, static_cast<double>(part[p * n + i].m));
+  double S = 0.0, t = 0.0;
+  for (int p = 0; p < P; ++p) {
+    const Partial<T> q = part[p * n + i];
+    if (q.m != -INFINITY) S += static_cast<double>(q.s) * (LOG2 ? exp2(static_cast<double>(q.m) - M)
+                                                               : exp(static_cast<double>(q.m) - M));
+    if (q.has != T(0)) t = static_cast<double>(q.t);
+  }
+  lse[i] = LOG2 ? (M + log2(S)) * 0.6931471805599453 : M + log(S);
+  pos[i] = t;
+}
+
+// loss = mean(lse - pos), one block, fixed summation order (deterministic).
+__global__ void mean_loss(const double* __restrict__ lse, const double* __restrict__ pos,
+                          int64_t n, double* __restrict__ loss) {
+  __shared__ double red[1024];
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += lse[i] - pos[i];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *loss = red[0] / static_cast<double>(n);
+}
+
+template <class Tin, class Tout>
+__global__ void reduce_chunks(const Tin* __restrict__ part, int P, int64_t count,
+                              Tout* __restrict__ out) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    Tin acc = part[i];
+    for (int p = 1; p < P; ++p) acc += part[p * count + i];
+    out[i] = static_cast<Tout>(acc);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host launchers
+// ---------------------------------------------------------------------------
+int launch_combine_f32log2(const float* part, int P, int64_t n, double* lse, double* pos,
+                           double* loss, cudaStream_t st) {
+  if (n <= 0) return fail(LF_EINVAL, "combine: n must be >= 1");
+  combine_partials<float, true><<<ceil_div(n, 256), 256, 0, st>>>(
+      reinterpret_cast<const Partial<float>*>(part), P, n, lse, pos);
+  LF_LAUNCHED();
+  if (loss) {
+    mean_loss<<<1, 1024, 0, st>>>(lse, pos, n, loss);
+    LF_LAUNCHED();
+  }
+  return LF_OK;
+}
+
+template <class T>
+static size_t fwd_smem(int D) { return sizeof(T) * D * (32 + 1 + 64 + 1); }
+template <class T>
+static size_t dx_smem(int D) { return sizeof(T) * (D * (32 + 1 + 64 + 1) + 32 * (64 + 1)); }
+template <class T>
+static size_t de_smem(int D) { return sizeof(T) * (D * (32 + 1 + 64 + 1) + 64 * (32 + 1)); }
+
+static int64_t pick_chunks(int64_t row_tiles, int64_t v, int64_t min_cols) {
+  const int64_t want = 4 * num_sms();
+  int64_t chunks = ceil_div(want, row_tiles);
+  chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, ceil_div(v, min_cols)));
+  return chunks;
+}
+
+template <class T>
+int simt_cce_forward(const T* X, const T* E, const int64_t* targets, int64_t n, int D,
+                     int64_t v, int64_t v_offset, Partial<T>** part_out, int* P_out,
+                     Scratch& ws, cudaStream_t st) {
+  const size_t smem = fwd_smem<T>(D);
+  if (smem > 227 * 1024) return fail(LF_EUNSUPPORTED, "simt forward: d too large");
+  LF_CUDA(cudaFuncSetAttribute(cce_simt_fwd<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)));
+  const int64_t rt = ceil_div(n, 32);
+  const int64_t chunks = pick_chunks(rt, v, 256);
+  const int64_t chunk = ceil_div(ceil_div(v, chunks), 64) * 64;
+  const int64_t P = ceil_div(v, chunk);
+  int rc = ws.alloc(sizeof(Partial<T>) * P * n, st);
+  if (rc) return rc;
+  cce_simt_fwd<T><<<dim3(rt, P), kThreads, smem, st>>>(X, E, targets, n, D, v, v_offset, chunk,
+                                                      ws.as<Partial<T>>());
+  LF_LAUNCHED();
+  *part_out = ws.as<Partial<T>>();
+  *P_out = static_cast<int>(P);
+  return LF_OK;
+}
+
+template <class T>
+int simt_cce_forward_full(const T* X, const T* E, const int64_t* targets, int64_t n, int D,
+                          int64_t v, double* lse, double* pos, double* loss, cudaStream_t st) {
+  Scratch ws;
+  Partial<T>* part;
+  int P;
+  int rc = simt_cce_forward<T>(X, E, targets, n, D, v, 0, &part, &P, ws, st);
+  if (rc) return rc;
+  combine_partials<T, false><<<ceil_div(n, 256), 256, 0, st>>>(part, P, n, lse, pos);
+  LF_LAUNCHED();
+  if (loss) {
+    mean_loss<<<1, 1024, 0, st>>>(lse, pos, n, loss);
+    LF_LAUNCHED();
+  }
+  return LF_OK;
+}
+
+template <class T>
+int simt_cce_forward_partial_log2(const T* X, const T* E, const int64_t* targets, int64_t n,
+                                  int D, int64_t v, int64_t v_offset, float* out,
+                                  cudaStream_t st);
+
+template <class T>
+__global__ void partial_to_log2(const Partial<T>* __restrict__ part, int P, int64_t n,
+                                float4* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double M = -INFINITY;
+  for (int p = 0; p < P; ++p) M = fmax(M, static_cast<double>(part[p * n + i].m));
+  double S = 0.0, t = 0.0, h = 0.0;
+  for (int p = 0; p < P; ++p) {
+    const Partial<T> q = part[p * n + i];
+    if (q.m != -INFINITY) S += static_cast<double>(q.s) * exp(static_cast<double>(q.m) - M);
+    if (q.has != T(0)) { t = static_cast<double>(q.t); h = 1.0; }
+  }
+  out[i] = make_float4(static_cast<float>(M * 1.4426950408889634), static_cast<float>(S),
+                       static_cast<float>(t), static_cast<float>(h));
+}
+
+template <class T>
+int simt_cce_forward_partial_log2(const T* X, const T* E, const int64_t* targets, int64_t n,
+                                  int D, int64_t v, int64_t v_offset, float* out,
+                                  cudaStream_t st) {
+  Scratch ws;
+  Partial<T>* part;
+  int P;
+  int rc = simt_cce_forward<T>(X, E, targets, n, D, v, v_offset, &part, &P, ws, st);
+  if (rc) return rc;
+  partial_to_log2<T><<<ceil_div(n, 256), 256, 0, st>>>(part, P, n, reinterpret_cast<float4*>(out));
+  LF_LAUNCHED();
+  return LF_OK;
+}
+
+template <class T>
+int simt_cce_backward(const T* X, const T* E, const int64_t* targets, const double* lse, double scale,
+                      double eps, int64_t n, int D, int64_t v, int64_t v_offset, T* dX, T* dE,
+                      unsigned long long* skip_counter, cudaStream_t st) {
+  const size_t sdx = dx_smem<T>(D), sde = de_smem<T>(D);
+  if (sdx > 227 * 1024 || sde > 227 * 1024) return fail(LF_EUNSUPPORTED, "simt backward: d too large");
+  if (D > 256) return fail(LF_EUNSUPPORTED, "simt backward: d > 256");
+  LF_CUDA(cudaFuncSetAttribute(cce_simt_bwd_dx<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(sdx)));
+  LF_CUDA(cudaFuncSetAttribute(cce_simt_bwd_de<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(sde)));
+  const int64_t rt = ceil_div(n, 32);
+  int64_t chunks = std::min<int64_t>(pick_chunks(rt, v, 1024), 8);
+  const int64_t chunk = ceil_div(ceil_div(v, chunks), 64) * 64;
+  const int64_t P = ceil_div(v, chunk);
+  Scratch ws;
+  T* part = dX;
+  if (P > 1) {
+    int rc = ws.alloc(sizeof(T) * P * n * D, st);
+    if (rc) return rc;
+    part = ws.as<T>();
+  }
+  cce_simt_bwd_dx<T><<<dim3(rt, P), kThreads, sdx, st>>>(X, E, targets, lse, n, D, v, v_offset,
+                                                        chunk, T(scale), T(eps), part,
+                                                        skip_counter);
+  LF_LAUNCHED();
+  if (P > 1) {
+    reduce_chunks<T, T><<<std::min<int64_t>(ceil_div(n * D, 256), 4 * num_sms()), 256, 0, st>>>(
+        part, static_cast<int>(P), n * D, dX);
+    LF_LAUNCHED();
+  }
+  cce_simt_bwd_de<T><<<ceil_div(v, 32), kThreads, sde, st>>>(X, E, targets, lse, n, D, v,
+                                                           v_offset, T(scale), T(eps), dE);
+  LF_LAUNCHED();
+  return LF_OK;
+}
+
+template int simt_cce_forward_full<float>(const float*, const float*, const int64_t*, int64_t, int,
+                                          int64_t, double*, double*, double*, cudaStream_t);
+template int simt_cce_forward_full<double>(const double*, const double*, const int64_t*, int64_t,
+                                           int, int64_t, double*, double*, double*, cudaStream_t);
+template int simt_cce_forward_partial_log2<float>(const float*, const float*, const int64_t*,
+                                                  int64_t, int, int64_t, int64_t, float*,
+                                                  cudaStream_t);
+template int simt_cce_forward_partial_log2<double>(const double*, const double*, const int64_t*,
+                                                   int64_t, int, int64_t, int64_t, float*,
+                                                   cudaStream_t);
+template int simt_cce_backward<float>(const float*, const float*, const int64_t*, const double*,
+                                      double, double, int64_t, int, int64_t, int64_t, float*,
+                                      float*, unsigned long long*, cudaStream_t);
+template int simt_cce_backward<double>(const double*, const double*, const int64_t*,
+                                       const double*, double, double, int64_t, int, int64_t,
+                                       int64_t, double*, double*, unsigned long long*,
+                                       cudaStream_t);
+
+int launch_reduce_f32(const float* part, int P, int64_t count, float* out, cudaStream_t st) {
+  reduce_chunks<float, float><<<std::min<int64_t>(ceil_div(count, 256), 4 * num_sms()), 256, 0, st>>>(
+      part, P, count, out);
+  LF_LAUNCHED();
+  return LF_OK;
+}
+
+__global__ void fold_partials(const float4* __restrict__ part, int P, int64_t n,
+                              float4* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float M = -INFINITY;
+  for (int p = 0; p < P; ++p) M = fmaxf(M, part[p * n + i].x);
+  float S = 0.f, t = 0.f, h = 0.f;
+  for (int p = 0; p < P; ++p) {
+    const float4 q = part[p * n + i];
+    if (q.x != -INFINITY) S += q.y * exp2f(q.x - M);
+    if (q.w != 0.f) { t = q.z; h = 1.f; }
+  }
+  out[i] = make_float4(M, S, t, h);
+}
+
+__global__ void negate_kernel(float* __restrict__ x, int64_t count) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    x[i] = -x[i];
+}
+
+int launch_fold_partials(const float* part, int P, int64_t n, float* out, cudaStream_t st) {
+  fold_partials<<<ceil_div(n, 256), 256, 0, st>>>(reinterpret_cast<const float4*>(part), P, n,
+                                                  reinterpret_cast<float4*>(out));
+  LF_LAUNCHED();
+  return LF_OK;
+}
+
+int launch_negate(float* x, int64_t count, cudaStream_t st) {
+  negate_kernel<<<std::min<int64_t>(ceil_div(count, 256), 8 * num_sms()), 256, 0, st>>>(x, count);
+  LF_LAUNCHED();
+  return LF_OK;
+}
+
+int launch_mean_loss(const double* lse, const double* pos, int64_t n, double* loss, cudaStream_t st) {
+  mean_loss<<<1, 1024, 0, st>>>(lse, pos, n, loss);
+  LF_LAUNCHED();
+  return LF_OK;
+}
+
+}  // namespace lf

@@ -1,0 +1,677 @@
+// lf_tc.cu — tcgen05 / TMEM / TMA kernels for the bf16 CCE path (sm_100a).
+//
+// One warp-specialized persistent kernel, three modes:
+//   FWD       owner = 128 rows of X, stream = 128-item tiles of E.
+//             S = X_o E_t^T in TMEM; epilogue does the online LSE (log2
+//             domain) and the target-logit capture in registers; writes one
+//             float4 partial {m, s, t, has} per (V-chunk, row)
+//             (reference: cce_forward, cce.cpp:99-137).
+//   BWD_ROWS  owner = rows, stream = items: S -> G = softmax*scale (-scale at
+//             the target, 0 below the filter threshold) -> bf16 into TMEM ->
+//             TS-MMA dX_o += G E_t (E_t reused from smem as an MN-major B
+//             operand).  Pass 1 of cce_backward (cce.cpp:210-233).
+//   BWD_ITEMS owner = items, stream = rows: S^T -> G^T -> dE_o += G^T X_t.
+//             Pass 2 of cce_backward (cce.cpp:240-262).  No atomics: every
+//             output row has one owner CTA.
+//
+// Roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA
+// issuer (one elected lane), warps 2..9 = two epilogue warpgroups that take
+// alternate stream tiles (ping-pong), so the MUFU-bound epilogue of one tile
+// overlaps the MMA of the next.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+
+#include "lf_internal.cuh"
+#include "lf_kernels.cuh"
+#include "lf_ptx.cuh"
+
+namespace lf {
+
+namespace {
+
+constexpr int BM = 128;  // owner tile (TMEM lanes)
+constexpr int BN = 128;  // stream tile (S columns)
+constexpr int kThreads = 320;
+constexpr int kEpiThreads = 256;
+
+enum Mode : int { FWD = 0, BWD_ROWS = 1, BWD_ITEMS = 2 };
+
+struct TcParams {
+  int64_t n_owner;       // owner rows (n or v_shard)
+  int64_t n_stream;      // stream rows (v_shard or n)
+  int64_t owner_tiles;
+  int64_t chunk;         // stream rows per unit (multiple of BN)
+  int64_t n_chunks;
+  int64_t units;
+  const int32_t* tgt;    // FWD/BWD_ROWS: per owner row (local item or -1); BWD_ITEMS: per stream row
+  const float* lse2;     // lse*log2e - log2|scale| per row (padded; +inf pad)
+  float thr2;            // log2(eps) + log2|scale| (filter threshold), -inf = off
+  float abs_scale;
+  float4* part;          // FWD: [n_chunks][n_owner]
+  float* out;            // BWD_ROWS: [n_chunks][n_owner][D]; BWD_ITEMS: [n_owner][D]
+  unsigned long long* counters;  // [0] skipped elems, [1] skipped tiles, [2] total tiles
+};
+
+template <int D, int MODE>
+struct Cfg {
+  static constexpr int kAtoms = D / 64;               // 128-byte K atoms per row
+  static constexpr int kOwnerBytes = BM * D * 2;
+  static constexpr int kTileBytes = BN * D * 2;
+  static constexpr int kExtraBytes = MODE == BWD_ITEMS ? 2048 : 0;  // lse2[128] + hits[129]
+  static constexpr int kStageBytes = kTileBytes + kExtraBytes;
+  static constexpr int kStages = D == 64 ? 8 : (D == 128 ? 5 : (D == 192 ? 3 : 2));
+  static constexpr int kNB = MODE == FWD ? 4 : (512 - D) / BN;  // S buffers in TMEM
+  static constexpr int kAccCol = kNB * BN;
+  static constexpr int kSmem = 1024 /*align slack*/ + kOwnerBytes + kStages * kStageBytes +
+                               1024 /*barriers*/ + (MODE == FWD ? BM * 16 : 0);
+};
+
+__device__ __forceinline__ float fma_log2(float v, float sub) { return fmaf(v, kLog2e, -sub); }
+
+// Select r[idx] from a register array without dynamic indexing.
+template <int N>
+__device__ __forceinline__ float select_reg(const float (&r)[N], int idx) {
+  float out = 0.f;
+#pragma unroll
+  for (int j = 0; j < N; ++j) out = (j == idx) ? r[j] : out;
+  return out;
+}
+
+template <int D, int MODE>
+__global__ void __launch_bounds__(kThreads, 1)
+    cce_tc_kernel(const __grid_constant__ CUtensorMap map_owner,
+                  const __grid_constant__ CUtensorMap map_stream, const TcParams p) {
+  using C = Cfg<D, MODE>;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  unsigned char* owner_smem = base;
+  unsigned char* stage_smem = base + C::kOwnerBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage_smem + C::kStages * C::kStageBytes);
+  uint64_t* full = bars;                      // [kStages]
+  uint64_t* empty = full + C::kStages;        // [kStages]
+  uint64_t* s_full = empty + C::kStages;      // [kNB]
+  uint64_t* s_empty = s_full + C::kNB;        // [kNB]
+  uint64_t* g_ready = s_empty + C::kNB;       // [kNB]
+  uint64_t* owner_full = g_ready + C::kNB;
+  uint64_t* owner_empty = owner_full + 1;
+  uint64_t* acc_full = owner_empty + 1;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  float4* merge = reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(bars) + 1024);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::kStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < C::kNB; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], MODE == FWD ? 128 : 1);
+      mbar_init(&g_ready[i], 128);
+    }
+    mbar_init(owner_full, 1);
+    mbar_init(owner_empty, 1);
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, kEpiThreads);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_owner);
+    tma_prefetch_desc(&map_stream);
+  }
+  if (warp == 1) tmem_alloc(tmem_holder, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    // ============================ TMA producer ============================
+    const uint64_t pol = policy_evict_normal();
+    int64_t t = 0;
+    uint32_t j = 0;
+    for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
+      const int64_t chunk = u / p.owner_tiles, ot = u % p.owner_tiles;
+      const int64_t s_begin = chunk * p.chunk;
+      const int64_t s_end = min(p.n_stream, s_begin + p.chunk);
+      if (lane == 0) {
+        mbar_wait(owner_empty, (j & 1) ^ 1);
+        mbar_arrive_expect_tx(owner_full, C::kOwnerBytes);
+#pragma unroll
+        for (int a = 0; a < C::kAtoms; ++a)
+          tma_load_2d(owner_smem + a * BM * 128, &map_owner, owner_full, a * 64,
+                      static_cast<int32_t>(ot * BM), pol);
+      }
+      for (int64_t s0 = s_begin; s0 < s_end; s0 += BN, ++t) {
+        const int st = static_cast<int>(t % C::kStages);
+        const uint32_t ph = static_cast<uint32_t>((t / C::kStages) & 1);
+        unsigned char* stg = stage_smem + st * C::kStageBytes;
+        if (lane == 0) {
+          mbar_wait(&empty[st], ph ^ 1);
+          if (MODE == BWD_ITEMS) {
+            mbar_expect_tx(&full[st], C::kTileBytes + 512);
+          } else {
+            mbar_arrive_expect_tx(&full[st], C::kTileBytes);
+          }
+#pragma unroll
+          for (int a = 0; a < C::kAtoms; ++a)
+            tma_load_2d(stg + a * BN * 128, &map_stream, &full[st], a * 64,
+                        static_cast<int32_t>(s0), pol);
+          if (MODE == BWD_ITEMS) bulk_load(stg + C::kTileBytes, p.lse2 + s0, 512, &full[st]);
+        }
+        if (MODE == BWD_ITEMS) {
+          // Rows of this stream tile whose target lies in the owner item tile.
+          __syncwarp();
+          int* hits = reinterpret_cast<int*>(stg + C::kTileBytes + 512);
+          const int64_t o0 = ot * BM;
+          int nh = 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int jcol = q * 32 + lane;
+            const int tg = p.tgt[s0 + jcol];
+            const int li = tg - static_cast<int>(o0);
+            const bool hit = tg >= 0 && li >= 0 && li < BM;
+            const unsigned bal = __ballot_sync(0xffffffffu, hit);
+            if (hit) {
+              const int slot = nh + __popc(bal & ((1u << lane) - 1u));
+              hits[1 + slot] = (jcol << 8) | li;
+            }
+            nh += __popc(bal);
+          }
+          if (lane == 0) hits[0] = nh;
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full[st]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ============================= MMA issuer =============================
+    constexpr uint32_t idesc1 = idesc_bf16(BM, BN, 0, 0);
+    constexpr uint32_t idesc2 = idesc_bf16(BM, D, 0, 1);
+    const uint32_t owner_addr = smem_u32(owner_smem);
+    const uint32_t stage_addr = smem_u32(stage_smem);
+    int64_t t = 0;
+    uint32_t j = 0;
+    unsigned long long tiles_seen = 0;
+    auto mma2 = [&](int64_t tt, bool first) {
+      const int st = static_cast<int>(tt % C::kStages);
+      const int b = static_cast<int>(tt % C::kNB);
+      mbar_wait(&g_ready[b], static_cast<uint32_t>((tt / C::kNB) & 1));
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t sb = stage_addr + st * C::kStageBytes;
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk) {
+          // B = stream tile viewed K(stream rows) x N(D), MN-major SW128:
+          // 16 rows = 2048 B per K step; 64-col D atoms are BN*128 B apart.
+          const uint64_t bdesc = umma_desc_sw128(sb + kk * 2048, BN * 128, 1024);
+          mma_ts(tmem + C::kAccCol, tmem + b * BN + kk * 8, bdesc, idesc2,
+                 (first && kk == 0) ? 0u : 1u);
+        }
+        mma_commit(&empty[st]);
+        mma_commit(&s_empty[b]);
+      }
+      __syncwarp();
+    };
+    for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
+      const int64_t chunk = u / p.owner_tiles;
+      const int64_t s_begin = chunk * p.chunk;
+      const int64_t s_end = min(p.n_stream, s_begin + p.chunk);
+      const int64_t ntile = ceil_div(s_end - s_begin, BN);
+      mbar_wait(owner_full, j & 1);
+      if (MODE != FWD) mbar_wait(acc_empty, (j & 1) ^ 1);
+      tc_fence_after();
+      for (int64_t i = 0; i < ntile; ++i, ++t) {
+        const int st = static_cast<int>(t % C::kStages);
+        const int b = static_cast<int>(t % C::kNB);
+        mbar_wait(&full[st], static_cast<uint32_t>((t / C::kStages) & 1));
+        mbar_wait(&s_empty[b], static_cast<uint32_t>(((t / C::kNB) & 1) ^ 1));
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sb = stage_addr + st * C::kStageBytes;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t koff = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
+            const uint32_t koffb = (kk >> 2) * (BN * 128) + (kk & 3) * 32;
+            const uint64_t adesc = umma_desc_sw128(owner_addr + koff, 16, 1024);
+            const uint64_t bdesc = umma_desc_sw128(sb + koffb, 16, 1024);
+            mma_ss(tmem + b * BN, adesc, bdesc, idesc1, kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&s_full[b]);
+          if (MODE == FWD) mma_commit(&empty[st]);
+        }
+        __syncwarp();
+        if (MODE != FWD && i > 0) mma2(t - 1, i == 1);
+        ++tiles_seen;
+      }
+      if (MODE != FWD) {
+        mma2(t - 1, ntile == 1);
+        if (lane == 0) mma_commit(acc_full);
+        __syncwarp();
+      }
+      if (lane == 0) mma_commit(owner_empty);
+      __syncwarp();
+    }
+    if (lane == 0 && MODE == BWD_ROWS && p.counters) atomicAdd(&p.counters[2], tiles_seen);
+  } else {
+    // ============================== epilogue ==============================
+    const int wg = (warp - 2) >> 2;   // 0 or 1: takes tiles with t % 2 == wg
+    const int quad = warp & 3;        // TMEM lane quadrant this warp may access
+    const int lrow = quad * 32 + lane;  // owner row within the tile
+    const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
+    unsigned long long skipped = 0;
+    int64_t t = 0;
+    uint32_t j = 0;
+    for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
+      const int64_t chunk = u / p.owner_tiles, ot = u % p.owner_tiles;
+      const int64_t s_begin = chunk * p.chunk;
+      const int64_t s_end = min(p.n_stream, s_begin + p.chunk);
+      const int64_t ntile = ceil_div(s_end - s_begin, BN);
+      const int64_t orow = ot * BM + lrow;
+      int tgt = -1;
+      float lse2 = 0.f;
+      if (MODE != BWD_ITEMS) {
+        tgt = p.tgt[orow];  // padded to owner_tiles*BM
+        if (MODE == BWD_ROWS) lse2 = p.lse2[orow];
+      }
+      float m = -INFINITY, s = 0.f, tv = 0.f, has = 0.f;
+      for (int64_t i = 0; i < ntile; ++i, ++t) {
+        if ((t & 1) != wg) continue;
+        const int b = static_cast<int>(t % C::kNB);
+        const int64_t col0 = s_begin + i * BN;
+        const int nvalid = static_cast<int>((s_end - col0 < BN ? s_end - col0 : BN));
+        mbar_wait(&s_full[b], static_cast<uint32_t>((t / C::kNB) & 1));
+        tc_fence_after();
+        float v[BN];
+        {
+          uint32_t* r = reinterpret_cast<uint32_t*>(v);
+          const uint32_t ta = tmem + lane_base + b * BN;
+          LF_TMEM_LD32(ta + 0, (r + 0));
+          LF_TMEM_LD32(ta + 32, (r + 32));
+          LF_TMEM_LD32(ta + 64, (r + 64));
+          LF_TMEM_LD32(ta + 96, (r + 96));
+          tmem_ld_wait();
+        }
+        if (MODE == FWD) {
+          tc_fence_before();
+          mbar_arrive(&s_empty[b]);
+          if (nvalid < BN) {
+#pragma unroll
+            for (int c = 0; c < BN; ++c)
+              if (c >= nvalid) v[c] = -INFINITY;
+          }
+          const int lc = tgt - static_cast<int>(col0);
+          if (lc >= 0 && lc < BN) {
+            tv = select_reg(v, lc);
+            has = 1.f;
+          }
+          if (m == -INFINITY) {
+            float mx = v[0];
+#pragma unroll
+            for (int c = 1; c < BN; ++c) mx = fmaxf(mx, v[c]);
+            m = mx * kLog2e;
+          }
+          float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+          for (int c = 0; c < BN; c += 2) {
+            acc0 += ex2_approx(fma_log2(v[c], m));
+            acc1 += ex2_approx(fma_log2(v[c + 1], m));
+          }
+          float sum = acc0 + acc1;
+          if (!(sum <= 1.8446744e19f)) {  // > 2^64 or NaN: rebase on the true max
+            float mx = v[0];
+#pragma unroll
+            for (int c = 1; c < BN; ++c) mx = fmaxf(mx, v[c]);
+            const float nm = fmaxf(m, mx * kLog2e);
+            s *= ex2_approx(m - nm);
+            m = nm;
+            acc0 = 0.f;
+            acc1 = 0.f;
+#pragma unroll
+            for (int c = 0; c < BN; c += 2) {
+              acc0 += ex2_approx(fma_log2(v[c], m));
+              acc1 += ex2_approx(fma_log2(v[c + 1], m));
+            }
+            sum = acc0 + acc1;
+          }
+          s += sum;
+        } else {
+          // ---- backward: G = 2^(S log2e - lse2) with filter and target fix
+          uint32_t g2[BN / 2];
+          const float* lse2s = nullptr;
+          if (MODE == BWD_ITEMS) {
+            const int st = static_cast<int>(t % C::kStages);
+            lse2s = reinterpret_cast<const float*>(stage_smem + st * C::kStageBytes + C::kTileBytes);
+          }
+          const bool filt = p.thr2 > -INFINITY;
+          // raw logit of this row's target column (rare: one tile per row)
+          const int lc_t = MODE == BWD_ROWS ? tgt - static_cast<int>(col0) : -1;
+          float o_t = 0.f;
+          if (MODE == BWD_ROWS && lc_t >= 0 && lc_t < BN) o_t = select_reg(v, lc_t);
+#pragma unroll
+          for (int c = 0; c < BN; c += 4) {
+            float l[4] = {lse2, lse2, lse2, lse2};
+            if (MODE == BWD_ITEMS) {
+              const float4 lp = *reinterpret_cast<const float4*>(lse2s + c);
+              l[0] = lp.x;
+              l[1] = lp.y;
+              l[2] = lp.z;
+              l[3] = lp.w;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float a = fma_log2(v[c + q], l[q]);
+              float e = ex2_approx(a);
+              if (filt) {
+                const bool k = a < p.thr2;
+                e = k ? 0.f : e;
+                if (MODE == BWD_ROWS) skipped += (k && c + q < nvalid && orow < p.n_owner);
+              }
+              v[c + q] = e;
+            }
+          }
+          if (MODE == BWD_ROWS && lc_t >= 0 && lc_t < BN) {
+            // the target is never filtered: g = (s - 1) * |scale|  (cce.cpp:193-195)
+            const float a = fma_log2(o_t, lse2);
+            if (filt && a < p.thr2 && orow < p.n_owner) --skipped;
+            const float g = ex2_approx(a) - p.abs_scale;
+#pragma unroll
+            for (int c = 0; c < BN; ++c)
+              if (c == lc_t) v[c] = g;
+          }
+          if (MODE == BWD_ITEMS) {
+            const int* hits = reinterpret_cast<const int*>(lse2s + 128);  // [0]=count, [1..128]
+            const int nh = hits[0];
+            for (int h = 0; h < nh; ++h) {
+              const int e = hits[1 + h];
+              if ((e & 0xFF) == lrow) {
+                const int jc = e >> 8;
+#pragma unroll
+                for (int c = 0; c < BN; ++c)
+                  if (c == jc) v[c] -= p.abs_scale;
+              }
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < BN / 2; ++c) g2[c] = pack_bf16x2(v[2 * c], v[2 * c + 1]);
+          const uint32_t ta = tmem + lane_base + b * BN;
+          LF_TMEM_ST16(ta + 0, (g2 + 0));
+          LF_TMEM_ST16(ta + 16, (g2 + 16));
+          LF_TMEM_ST16(ta + 32, (g2 + 32));
+          LF_TMEM_ST16(ta + 48, (g2 + 48));
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(&g_ready[b]);
+        }
+      }
+      if (MODE == FWD) {
+        // merge the two warpgroups' running states for each row
+        if (wg == 1) merge[lrow] = make_float4(m, s, tv, has);
+        named_bar_sync(1, kEpiThreads);
+        if (wg == 0) {
+          const float4 o = merge[lrow];
+          if (o.x != -INFINITY) {
+            if (m == -INFINITY) {
+              m = o.x;
+              s = o.y;
+            } else {
+              const float nm = fmaxf(m, o.x);
+              s = s * ex2_approx(m - nm) + o.y * ex2_approx(o.x - nm);
+              m = nm;
+            }
+          }
+          if (o.w != 0.f) {
+            tv = o.z;
+            has = 1.f;
+          }
+          if (orow < p.n_owner) p.part[chunk * p.n_owner + orow] = make_float4(m, s, tv, has);
+        }
+        named_bar_sync(1, kEpiThreads);
+      } else {
+        // accumulator read-out: wg 0 takes columns [0, D/2), wg 1 [D/2, D)
+        mbar_wait(acc_full, j & 1);
+        tc_fence_after();
+        float* dst = MODE == BWD_ROWS ? p.out + (chunk * p.n_owner + orow) * D
+                                      : p.out + orow * D;
+        for (int c0 = wg * (D / 2); c0 < (wg + 1) * (D / 2); c0 += 32) {
+          uint32_t r[32];
+          LF_TMEM_LD32(tmem + lane_base + C::kAccCol + c0, r);
+          tmem_ld_wait();
+          if (orow < p.n_owner) {
+#pragma unroll
+            for (int c = 0; c < 32; c += 4)
+              *reinterpret_cast<float4*>(dst + c0 + c) =
+                  make_float4(__uint_as_float(r[c]), __uint_as_float(r[c + 1]),
+                              __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(acc_empty);
+      }
+    }
+    if (MODE == BWD_ROWS && p.counters) {
+      for (int off = 16; off > 0; off >>= 1) skipped += __shfl_xor_sync(0xffffffffu, skipped, off);
+      if (lane == 0 && skipped) atomicAdd(&p.counters[0], skipped);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+// -------------------------------------------------------------- host side --
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// rows x D bf16 row-major, box = 64 cols x box_rows rows, 128-byte swizzle.
+int make_map(CUtensorMap* map, const void* ptr, int64_t rows, int D, int box_rows) {
+  auto enc = get_encode();
+  if (!enc) return fail(LF_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  if (reinterpret_cast<uintptr_t>(ptr) % 16 != 0)
+    return fail(LF_EINVAL, "bf16 path: X/E base pointers must be 16-byte aligned");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(D) * 2};
+  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(LF_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return LF_OK;
+}
+
+__global__ void prep_rows(const int64_t* __restrict__ targets, const double* __restrict__ lse,
+                          int64_t n, int64_t n_pad, int64_t v_shard, int64_t v_offset,
+                          double log2_abs_scale, int32_t* __restrict__ tgt,
+                          float* __restrict__ lse2) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n_pad) return;
+  int32_t t = -1;
+  float l = INFINITY;
+  if (i < n) {
+    const int64_t x = targets[i] - v_offset;
+    t = (x >= 0 && x < v_shard) ? static_cast<int32_t>(x) : -1;
+    if (lse) l = static_cast<float>(lse[i] * 1.4426950408889634 - log2_abs_scale);
+  }
+  tgt[i] = t;
+  if (lse2) lse2[i] = l;
+}
+
+template <int D, int MODE>
+int launch_mode(const CUtensorMap& mo, const CUtensorMap& ms, const TcParams& p, cudaStream_t st) {
+  using C = Cfg<D, MODE>;
+  auto kern = cce_tc_kernel<D, MODE>;
+  LF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+  const int grid = static_cast<int>(std::min<int64_t>(p.units, num_sms()));
+  kern<<<grid, kThreads, C::kSmem, st>>>(mo, ms, p);
+  LF_LAUNCHED();
+  return LF_OK;
+}
+
+template <int MODE>
+int launch_d(int D, const CUtensorMap& mo, const CUtensorMap& ms, const TcParams& p,
+             cudaStream_t st) {
+  switch (D) {
+    case 64: return launch_mode<64, MODE>(mo, ms, p, st);
+    case 128: return launch_mode<128, MODE>(mo, ms, p, st);
+    case 192: return launch_mode<192, MODE>(mo, ms, p, st);
+    case 256: return launch_mode<256, MODE>(mo, ms, p, st);
+    default: return fail(LF_EUNSUPPORTED, "tc: d must be 64/128/192/256");
+  }
+}
+
+// Pick the number of stream chunks so units fill the SMs evenly.
+int64_t pick_chunks(int64_t owner_tiles, int64_t stream_tiles, int64_t max_chunks) {
+  const int64_t sms = num_sms();
+  int64_t best = 1;
+  double best_eff = 0.0;
+  for (int64_t c = 1; c <= std::min(max_chunks, stream_tiles); ++c) {
+    const int64_t tiles_per = ceil_div(stream_tiles, c);
+    const int64_t real_c = ceil_div(stream_tiles, tiles_per);
+    const int64_t units = owner_tiles * real_c;
+    const int64_t waves = ceil_div(units, sms);
+    const double eff = static_cast<double>(units) / static_cast<double>(waves * sms);
+    if (eff > best_eff + 0.02 || (eff > best_eff - 1e-9 && c < best && eff >= best_eff)) {
+      best_eff = eff;
+      best = c;
+    }
+    if (eff > 0.97) break;
+  }
+  return best;
+}
+
+}  // namespace
+
+// Both fold the per-chunk partials and run the forward.
+int tc_cce_forward_partials(const void* X, const void* E, const int64_t* targets, int64_t n,
+                            int D, int64_t v, int64_t v_offset, Scratch& ws, float** part_out,
+                            int* P_out, cudaStream_t st) {
+  const int64_t owner_tiles = ceil_div(n, BM);
+  const int64_t stream_tiles = ceil_div(v, BN);
+  const int64_t chunks = pick_chunks(owner_tiles, stream_tiles, 64);
+  const int64_t tiles_per = ceil_div(stream_tiles, chunks);
+  const int64_t P = ceil_div(stream_tiles, tiles_per);
+  const int64_t n_pad = owner_tiles * BM;
+  Scratch tgt;
+  int rc = tgt.alloc(sizeof(int32_t) * n_pad, st);
+  if (!rc) rc = ws.alloc(sizeof(float4) * P * n, st);
+  if (rc) return rc;
+  prep_rows<<<ceil_div(n_pad, 256), 256, 0, st>>>(targets, nullptr, n, n_pad, v, v_offset, 0.0,
+                                                 tgt.as<int32_t>(), nullptr);
+  LF_LAUNCHED();
+  CUtensorMap mo, ms;
+  rc = make_map(&mo, X, n, D, BM);
+  if (!rc) rc = make_map(&ms, E, v, D, BN);
+  if (rc) return rc;
+  TcParams p{};
+  p.n_owner = n;
+  p.n_stream = v;
+  p.owner_tiles = owner_tiles;
+  p.chunk = tiles_per * BN;
+  p.n_chunks = P;
+  p.units = owner_tiles * P;
+  p.tgt = tgt.as<int32_t>();
+  p.part = ws.as<float4>();
+  rc = launch_d<FWD>(D, mo, ms, p, st);
+  if (rc) return rc;
+  *part_out = ws.as<float>();
+  *P_out = static_cast<int>(P);
+  return LF_OK;
+}
+
+int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const double* lse,
+                    double scale, double eps, int64_t n, int D, int64_t v, int64_t v_offset,
+                    float* dX, float* dE, unsigned long long* counters, cudaStream_t st) {
+  if (scale == 0.0) {
+    LF_CUDA(cudaMemsetAsync(dX, 0, sizeof(float) * n * D, st));
+    LF_CUDA(cudaMemsetAsync(dE, 0, sizeof(float) * v * D, st));
+    return LF_OK;
+  }
+  const double abs_scale = std::fabs(scale);
+  const double l2s = std::log2(abs_scale);
+  const int64_t row_tiles = ceil_div(n, BM);
+  const int64_t item_tiles = ceil_div(v, BN);
+  const int64_t n_pad = std::max(row_tiles * BM, ceil_div(n, BN) * BN);
+  Scratch tgt, lse2;
+  int rc = tgt.alloc(sizeof(int32_t) * n_pad, st);
+  if (!rc) rc = lse2.alloc(sizeof(float) * n_pad, st);
+  if (rc) return rc;
+  prep_rows<<<ceil_div(n_pad, 256), 256, 0, st>>>(targets, lse, n, n_pad, v, v_offset, l2s,
+                                                 tgt.as<int32_t>(), lse2.as<float>());
+  LF_LAUNCHED();
+  CUtensorMap mx, me;
+  rc = make_map(&mx, X, n, D, 128);
+  if (!rc) rc = make_map(&me, E, v, D, 128);
+  if (rc) return rc;
+  const float thr2 = eps > 0.0 ? static_cast<float>(std::log2(eps) + l2s) : -INFINITY;
+
+  // ---- pass 1: dX (owner rows, stream items), V split into a few chunks ----
+  const int64_t chunks = pick_chunks(row_tiles, item_tiles, 8);
+  const int64_t tiles_per = ceil_div(item_tiles, chunks);
+  const int64_t P = ceil_div(item_tiles, tiles_per);
+  Scratch dxp;
+  float* dx_out = dX;
+  if (P > 1) {
+    rc = dxp.alloc(sizeof(float) * P * n * D, st);
+    if (rc) return rc;
+    dx_out = dxp.as<float>();
+  }
+  TcParams p{};
+  p.n_owner = n;
+  p.n_stream = v;
+  p.owner_tiles = row_tiles;
+  p.chunk = tiles_per * BN;
+  p.n_chunks = P;
+  p.units = row_tiles * P;
+  p.tgt = tgt.as<int32_t>();
+  p.lse2 = lse2.as<float>();
+  p.thr2 = thr2;
+  p.abs_scale = static_cast<float>(abs_scale);
+  p.out = dx_out;
+  p.counters = counters;
+  rc = launch_d<BWD_ROWS>(D, mx, me, p, st);
+  if (rc) return rc;
+  if (P > 1) {
+    rc = launch_reduce_f32(dx_out, static_cast<int>(P), n * D, dX, st);
+    if (rc) return rc;
+  }
+  // ---- pass 2: dE (owner items, stream rows) ----
+  TcParams q{};
+  q.n_owner = v;
+  q.n_stream = n;
+  q.owner_tiles = item_tiles;
+  q.chunk = ceil_div(n, BN) * BN;
+  q.n_chunks = 1;
+  q.units = item_tiles;
+  q.tgt = tgt.as<int32_t>();
+  q.lse2 = lse2.as<float>();
+  q.thr2 = thr2;
+  q.abs_scale = static_cast<float>(abs_scale);
+  q.out = dE;
+  q.counters = counters;
+  rc = launch_d<BWD_ITEMS>(D, me, mx, q, st);
+  if (rc) return rc;
+  if (scale < 0.0) {
+    rc = launch_negate(dX, n * D, st);
+    if (!rc) rc = launch_negate(dE, v * D, st);
+    if (rc) return rc;
+  }
+  return LF_OK;
+}
+
+}  // namespace lf
