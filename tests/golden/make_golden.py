@@ -1,0 +1,83 @@
+"""Generate tests/golden/*.npz from the REFERENCE implementation.
+
+Runs the unmodified reference hot-path sources compiled in place
+(oracle/_ref/liblseforge_ref.so, built by oracle/Makefile from
+/root/reference/proj/src) on small instances drawn with the reference's own
+fixtures (support.hpp make_instance / make_candidates, SplitMix64) and stores
+inputs + outputs.  The committed .npz files travel to the GPU box, where
+/root/reference does not exist; tests/test_oracle.py pins the C restatement to
+them and the GPU tests compare the CUDA path against them.
+
+    python tests/golden/make_golden.py
+"""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))
+import oracle_bind as ob  # noqa: E402
+
+
+def ref_instance(seed, n, d, v):
+    E = np.empty((n, d), np.float32)
+    C = np.empty((d, v), np.float32)
+    t = np.empty(n, np.int64)
+    ob.ref().ref_make_instance(seed, n, d, v, 1.0, E, C, t)
+    return E, C, t
+
+
+def ref_instance_cand(seed, n, d, v, ns):
+    E = np.empty((n, d), np.float32)
+    C = np.empty((d, v), np.float32)
+    t = np.empty(n, np.int64)
+    inds = np.empty((n, 1 + ns), np.int64)
+    ob.ref().ref_make_instance_candidates(seed, n, d, v, ns, E, C, t, inds)
+    return E, C, t, inds
+
+
+def main():
+    out = {}
+    # SplitMix64 streams (also pinned by test_core.cpp:21-52)
+    for seed in (0, 42, 0xDEADBEEF, 0xB2000002):
+        out[f"rng_{seed:x}"] = ob.ref_rng_stream(seed, 16)
+    np.savez_compressed(os.path.join(HERE, "rng_streams.npz"), **out)
+
+    # CCE: a spread of shapes incl. ragged tiles; eps 0 and 1e-3.
+    cases = [(1001, 17, 6, 37), (1002, 33, 16, 129), (1003, 5, 1, 2), (1004, 64, 64, 300),
+             (1005, 130, 64, 257), (1006, 40, 128, 200)]
+    cce = {}
+    for k, (seed, n, d, v) in enumerate(cases):
+        E, C, t = ref_instance(seed, n, d, v)
+        loss, pos, lse = ob.ref_cce_forward(E, C, t, rb=7, cb=13)
+        dE0, dC0, f0 = ob.ref_cce_backward(E, C, t, lse, 1.0, 0.0, rb=7, cb=13)
+        dE1, dC1, f1 = ob.ref_cce_backward(E, C, t, lse, 1.0, 1e-3, rb=7, cb=13)
+        cce.update({f"{k}_E": E, f"{k}_C": C, f"{k}_t": t, f"{k}_loss": np.float64(loss),
+                    f"{k}_pos": pos, f"{k}_lse": lse, f"{k}_dE": dE0, f"{k}_dC": dC0,
+                    f"{k}_dE_eps": dE1, f"{k}_dC_eps": dC1, f"{k}_frac": np.float64(f0),
+                    f"{k}_frac_eps": np.float64(f1)})
+    cce["count"] = np.int64(len(cases))
+    np.savez_compressed(os.path.join(HERE, "cce_ref.npz"), **cce)
+
+    # CCE-: sampled candidates (make_candidates) and sampler output.
+    ccases = [(2001, 13, 8, 40, 5), (2002, 41, 8, 67, 9), (2003, 6, 3, 16, 4), (2004, 64, 64, 500, 31),
+              (2005, 9, 5, 10, 0)]
+    ccem = {}
+    for k, (seed, n, d, v, ns) in enumerate(ccases):
+        E, C, t, inds = ref_instance_cand(seed, n, d, v, ns)
+        loss, pos, lse = ob.ref_ccem_forward(E, C, inds)
+        up = np.full(n, 1.0 / n)
+        dE, dC = ob.ref_ccem_backward_rows(E, C, inds, lse, up)
+        ccem.update({f"{k}_E": E, f"{k}_C": C, f"{k}_inds": inds, f"{k}_loss": np.float64(loss),
+                     f"{k}_pos": pos, f"{k}_lse": lse, f"{k}_dE": dE, f"{k}_dC": dC})
+    ccem["count"] = np.int64(len(ccases))
+    pos = np.arange(50, dtype=np.int64) % 97
+    ccem["sampler_pos"] = pos
+    ccem["sampler_inds"] = ob.ref_sample_uniform(pos, 12, 97, 0xB2000003)
+    np.savez_compressed(os.path.join(HERE, "ccem_ref.npz"), **ccem)
+    print("wrote", sorted(f for f in os.listdir(HERE) if f.endswith(".npz")))
+
+
+if __name__ == "__main__":
+    main()

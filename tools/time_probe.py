@@ -16,6 +16,7 @@ ap.add_argument("--v", type=int, default=1000000)
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--eps", type=float, default=0.0)
 ap.add_argument("--ccem", type=int, default=0)
+ap.add_argument("--once", type=int, default=0)
 a = ap.parse_args()
 
 g = torch.Generator(device="cuda").manual_seed(0)
@@ -47,6 +48,10 @@ if a.ccem:
     tba = timed(lambda: lf.ccem_backward(X, E, inds, out.lse, 1.0, cfg2, validate=False), a.iters)
     print(f"ccem n={a.n} d={a.d} v={a.v} K={a.ccem}: fwd {tf:.3f} ms  bwd(det) {tb:.3f} ms  "
           f"bwd(atomic) {tba:.3f} ms  pos/s={a.n/(tf+tb)*1e3:.3e}")
+elif a.once:
+    out = lf.cce_forward(X, E, x, cfg, validate=False)
+    lf.cce_backward(X, E, x, out.lse, 1.0, cfg, validate=False, stats=False)
+    torch.cuda.synchronize()
 else:
     out = lf.cce_forward(X, E, x, cfg, validate=False)
     print("loss", float(out.loss))
