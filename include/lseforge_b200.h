@@ -169,6 +169,25 @@ LF_API int lf_workspace_reset_peak(void);
 LF_API uint64_t lf_launch_count(void);
 LF_API void lf_launch_count_reset(void);
 
+/* ------------------------------------------------------------ tracing ---- */
+/* Per-kernel CUDA-event timing.  When enabled, the library brackets each of
+ * its main kernel launches with events recorded on the launching stream;
+ * lf_profile_read synchronizes those events and returns, for one kernel kind,
+ * the launch count and summed device milliseconds since the last reset. */
+enum lf_kernel_kind {
+  LF_K_CCE_FWD = 0,    /* tcgen05 forward (online LSE epilogue) */
+  LF_K_CCE_BWD_DX = 1, /* tcgen05 backward, row-owned dX pass */
+  LF_K_CCE_BWD_DE = 2, /* tcgen05 backward, item-owned dE pass */
+  LF_K_CCE_SIMT = 3,   /* fp32 / fp64 CUDA-core CCE kernels */
+  LF_K_CCEM_FWD = 4,   /* CCE- forward gather/dot/LSE */
+  LF_K_CCEM_BWD = 5,   /* CCE- backward (rows pass + sort + segment reduce) */
+  LF_K_AUX = 6,        /* combine / reduce / prep kernels */
+  LF_K_COUNT = 7
+};
+LF_API int lf_profile_enable(int on);
+LF_API int lf_profile_read(int32_t kind, uint64_t* launches, double* total_ms);
+LF_API void lf_profile_reset(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -22,7 +22,9 @@ EXPORTS = (
     "lf_cce_forward_partial", "lf_cce_combine", "lf_cce_backward_shard", "lf_ccem_forward",
     "lf_ccem_backward", "lf_validate_targets", "lf_validate_inds", "lf_estimate_flops",
     "lf_workspace_stats", "lf_workspace_reset_peak", "lf_launch_count", "lf_launch_count_reset",
+    "lf_profile_enable", "lf_profile_read", "lf_profile_reset",
 )
+KERNEL_KINDS = ("cce_fwd", "cce_bwd_dx", "cce_bwd_de", "cce_simt", "ccem_fwd", "ccem_bwd", "aux")
 
 
 class CceConfigC(C.Structure):
@@ -70,6 +72,10 @@ def lib():
                                         C.POINTER(C.c_uint64)]
         L.lf_workspace_stats.argtypes = [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         L.lf_launch_count.restype = C.c_uint64
+        L.lf_profile_enable.argtypes = [C.c_int]
+        L.lf_profile_enable.restype = C.c_int
+        L.lf_profile_read.argtypes = [C.c_int32, C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
+        L.lf_profile_read.restype = C.c_int
         for name in ("lf_cce_forward", "lf_cce_backward", "lf_cce_forward_partial",
                      "lf_cce_combine", "lf_cce_backward_shard", "lf_ccem_forward",
                      "lf_ccem_backward", "lf_validate_targets", "lf_validate_inds",

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "lf_internal.cuh"
 #include "lf_kernels.cuh"
@@ -31,6 +32,45 @@ int cuda_fail(cudaError_t e, const char* what) {
   return e == cudaErrorMemoryAllocation ? LF_ENOMEM : LF_ECUDA;
 }
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+namespace {
+std::atomic<int> g_prof_on{0};
+std::mutex g_prof_mu;
+struct ProfRec {
+  int kind;
+  cudaEvent_t a, b;
+};
+std::vector<ProfRec> g_prof_pending;
+uint64_t g_prof_launches[LF_K_COUNT] = {};
+double g_prof_ms[LF_K_COUNT] = {};
+}  // namespace
+
+ProfScope::ProfScope(int k, cudaStream_t s) : kind(k), st(s) {
+  if (g_prof_on.load() && cudaEventCreate(&start) == cudaSuccess) cudaEventRecord(start, st);
+}
+ProfScope::~ProfScope() {
+  if (!start) return;
+  cudaEvent_t end;
+  if (cudaEventCreate(&end) != cudaSuccess) return;
+  cudaEventRecord(end, st);
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_prof_pending.push_back({kind, start, end});
+}
+
+static void prof_drain() {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  for (auto& r : g_prof_pending) {
+    float ms = 0.f;
+    cudaEventSynchronize(r.b);
+    if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess && r.kind >= 0 && r.kind < LF_K_COUNT) {
+      g_prof_ms[r.kind] += ms;
+      g_prof_launches[r.kind] += 1;
+    }
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_prof_pending.clear();
+}
 
 int Scratch::alloc(size_t nbytes, cudaStream_t s) {
   if (ptr) return fail(LF_EINVAL, "internal: scratch reused");
@@ -316,6 +356,25 @@ int lf_workspace_reset_peak(void) {
   return LF_OK;
 }
 uint64_t lf_launch_count(void) { return g_launches.load(); }
+
+int lf_profile_enable(int on) {
+  g_prof_on.store(on ? 1 : 0);
+  return LF_OK;
+}
+int lf_profile_read(int32_t kind, uint64_t* launches, double* total_ms) {
+  if (kind < 0 || kind >= LF_K_COUNT) return fail(LF_EINVAL, "lf_profile_read: bad kind");
+  prof_drain();
+  if (launches) *launches = g_prof_launches[kind];
+  if (total_ms) *total_ms = g_prof_ms[kind];
+  return LF_OK;
+}
+void lf_profile_reset(void) {
+  prof_drain();
+  for (int k = 0; k < LF_K_COUNT; ++k) {
+    g_prof_launches[k] = 0;
+    g_prof_ms[k] = 0.0;
+  }
+}
 void lf_launch_count_reset(void) { g_launches.store(0); }
 
 }  // extern "C"

@@ -450,6 +450,7 @@ __global__ void __launch_bounds__(256) segment_reduce(const TX* __restrict__ X,
 int ccem_forward(int dtype, const void* X, const void* E, const int64_t* inds, int64_t n, int D,
                  int64_t v, int64_t w, double* lse, double* pos, double* loss, cudaStream_t st) {
   (void)v;
+  ProfScope prof(LF_K_CCEM_FWD, st);
   const dim3 grid(static_cast<unsigned>(ceil_div(n, 8)));
   if (dtype == LF_BF16 || (dtype == LF_F32 && D % 64 == 0 && D <= 256)) {
 #define LF_FWD_VEC(TE, DD)                                                                     \
@@ -531,6 +532,7 @@ int ccem_backward(int dtype, const void* X, const void* E, const int64_t* inds,
                   int D, int64_t v, int64_t w, bool atomic_de, void* dX, void* dE,
                   cudaStream_t st) {
   const double u_n = upstream / static_cast<double>(n);
+  ProfScope prof(LF_K_CCEM_BWD, st);
   const dim3 grid(static_cast<unsigned>(ceil_div(n, 8)));
   const int64_t count = n * w;
   const bool vec = dtype == LF_BF16 || (dtype == LF_F32 && D % 64 == 0 && D <= 256);

@@ -32,6 +32,15 @@ int cuda_fail(cudaError_t e, const char* what);
 
 void note_launch();
 
+// Event bracket around one kernel launch when profiling is on (lf_profile_*).
+struct ProfScope {
+  int kind;
+  cudaStream_t st;
+  cudaEvent_t start = nullptr;
+  ProfScope(int k, cudaStream_t s);
+  ~ProfScope();
+};
+
 // --------------------------------------------------- scratch allocator ------
 // Stream-ordered device scratch (cudaMallocAsync on the default mempool);
 // tracks current and peak bytes for the peak-HBM figure.

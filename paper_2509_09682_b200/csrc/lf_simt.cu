@@ -419,6 +419,7 @@ int simt_cce_forward(const T* X, const T* E, const int64_t* targets, int64_t n, 
   const int64_t P = ceil_div(v, chunk);
   int rc = ws.alloc(sizeof(Partial<T>) * P * n, st);
   if (rc) return rc;
+  ProfScope prof(LF_K_CCE_SIMT, st);
   cce_simt_fwd<T><<<dim3(rt, P), kThreads, smem, st>>>(X, E, targets, n, D, v, v_offset, chunk,
                                                       ws.as<Partial<T>>());
   LF_LAUNCHED();
@@ -502,6 +503,7 @@ int simt_cce_backward(const T* X, const T* E, const int64_t* targets, const doub
     if (rc) return rc;
     part = ws.as<T>();
   }
+  ProfScope prof(LF_K_CCE_SIMT, st);
   cce_simt_bwd_dx<T><<<dim3(rt, P), kThreads, sdx, st>>>(X, E, targets, lse, n, D, v, v_offset,
                                                         chunk, T(scale), T(eps), part,
                                                         skip_counter);

@@ -518,6 +518,7 @@ int launch_mode(const CUtensorMap& mo, const CUtensorMap& ms, const TcParams& p,
   auto kern = cce_tc_kernel<D, MODE>;
   LF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
   const int grid = static_cast<int>(std::min<int64_t>(p.units, num_sms()));
+  ProfScope prof(MODE == FWD ? LF_K_CCE_FWD : (MODE == BWD_ROWS ? LF_K_CCE_BWD_DX : LF_K_CCE_BWD_DE), st);
   kern<<<grid, kThreads, C::kSmem, st>>>(mo, ms, p);
   LF_LAUNCHED();
   return LF_OK;

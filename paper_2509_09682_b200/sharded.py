@@ -1,0 +1,132 @@
+"""Catalog-sharded CCE across the GPUs of one node (one process per GPU).
+
+Rank p owns the contiguous item slice [v_begin, v_end) of E (and of dE); X,
+targets and the per-row outputs are replicated.  The reference has no
+distributed layer (SPEC.md:243 lists vocabulary sharding as a non-goal); this
+is the exchange the north star specifies:
+
+  forward   each rank computes per-row partial triples (m, s, t) over its
+            slice (lf_cce_forward_partial) -> ONE all-gather of n x 16 bytes
+            -> every rank combines them (lf_cce_combine): lse = M + log sum_p
+            s_p 2^(m_p - M) (log2 units), pos = the t of the shard that owns
+            the target, loss = mean(lse - pos).
+  backward  dE rows of the local slice are complete; dX is a partial sum over
+            the local items -> ONE all-reduce(sum) of n x d fp32.  The skip
+            count is summed across ranks before dividing by n (v_total - 1)
+            (cce.cpp:264-268).
+
+The collectives go through torch.distributed (NCCL on GPUs, gloo in the CPU
+tests); the kernels behind ``kernels`` are the C-ABI (``DeviceKernels``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Tuple
+
+import torch
+import torch.distributed as dist
+
+from . import _capi
+from .cce import CceBackwardResult, CceConfig, _stream
+from .losses import GradPair, LossOutput, grad_dtype, lf_dtype
+
+
+def shard_bounds(v_total: int, P: int, p: int) -> Tuple[int, int]:
+    """Near-equal contiguous split of [0, v_total) into P slices; slice p."""
+    base, rem = divmod(v_total, P)
+    begin = p * base + min(p, rem)
+    return begin, begin + base + (1 if p < rem else 0)
+
+
+@dataclass
+class ShardStats:
+    skipped_elems: int
+    skipped_tiles: int
+    total_tiles: int
+
+
+class DeviceKernels:
+    """The C-ABI kernels of liblseforge_b200.so on CUDA tensors."""
+
+    def forward_partial(self, X, E_shard, targets, v_offset: int, cfg: CceConfig) -> torch.Tensor:
+        n, d = X.shape
+        part = torch.empty((n, 4), dtype=torch.float32, device=X.device)
+        c = cfg.to_c(lf_dtype(X))
+        _capi.check(_capi.lib().lf_cce_forward_partial(
+            X.data_ptr(), E_shard.data_ptr(), targets.data_ptr(), n, d, E_shard.shape[0], v_offset,
+            C.byref(c), part.data_ptr(), _stream(X)))
+        return part
+
+    def combine(self, parts: torch.Tensor) -> LossOutput:
+        P, n, _ = parts.shape
+        lse = torch.empty(n, dtype=torch.float64, device=parts.device)
+        pos = torch.empty(n, dtype=torch.float64, device=parts.device)
+        loss = torch.empty((), dtype=torch.float64, device=parts.device)
+        _capi.check(_capi.lib().lf_cce_combine(parts.data_ptr(), P, n, lse.data_ptr(),
+                                               pos.data_ptr(), loss.data_ptr(), _stream(parts)))
+        return LossOutput(loss, pos, lse)
+
+    def backward_shard(self, X, E_shard, targets, lse, upstream, v_offset, v_total, cfg,
+                       stats: bool):
+        n, d = X.shape
+        vs = E_shard.shape[0]
+        gd = grad_dtype(X)
+        dX = torch.empty((n, d), dtype=gd, device=X.device)
+        dE = torch.empty((vs, d), dtype=gd, device=X.device)
+        c = cfg.to_c(lf_dtype(X))
+        st = _capi.CceStatsC()
+        _capi.check(_capi.lib().lf_cce_backward_shard(
+            X.data_ptr(), E_shard.data_ptr(), targets.data_ptr(),
+            lse.to(torch.float64).contiguous().data_ptr(), float(upstream), n, d, vs, v_offset,
+            v_total, C.byref(c), dX.data_ptr(), dE.data_ptr(), C.byref(st) if stats else None,
+            _stream(X)))
+        s = ShardStats(int(st.skipped_elems), int(st.skipped_tiles), int(st.total_tiles)) if stats else None
+        return dX, dE, s
+
+
+class ShardedCce:
+    """Catalog-sharded cce_forward / cce_backward over a process group."""
+
+    def __init__(self, v_total: int, group=None, kernels=None):
+        self.group = group
+        self.P = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.v_total = v_total
+        self.v_begin, self.v_end = shard_bounds(v_total, self.P, self.rank)
+        self.kernels = kernels if kernels is not None else DeviceKernels()
+
+    @property
+    def v_shard(self) -> int:
+        return self.v_end - self.v_begin
+
+    def forward(self, X, E_shard, targets, cfg: CceConfig = CceConfig()) -> LossOutput:
+        if E_shard.shape[0] != self.v_shard:
+            raise ValueError(f"sharded cce: rank {self.rank} expects {self.v_shard} item rows, "
+                             f"got {E_shard.shape[0]}")
+        part = self.kernels.forward_partial(X, E_shard, targets, self.v_begin, cfg)
+        if self.P == 1:
+            return self.kernels.combine(part.unsqueeze(0))
+        n = part.shape[0]
+        flat = torch.empty((self.P * n,) + tuple(part.shape[1:]), dtype=part.dtype,
+                           device=part.device)
+        dist.all_gather_into_tensor(flat, part.contiguous(), group=self.group)
+        return self.kernels.combine(flat.view((self.P, n) + tuple(part.shape[1:])))
+
+    def backward(self, X, E_shard, targets, lse, upstream: float = 1.0,
+                 cfg: CceConfig = CceConfig(), stats: bool = True) -> CceBackwardResult:
+        dX, dE, st = self.kernels.backward_shard(X, E_shard, targets, lse, upstream, self.v_begin,
+                                                 self.v_total, cfg, stats)
+        if self.P > 1:
+            dist.all_reduce(dX, op=dist.ReduceOp.SUM, group=self.group)
+        res = CceBackwardResult(GradPair(dX, dE))
+        if stats:
+            cnt = torch.tensor([st.skipped_elems, st.skipped_tiles, st.total_tiles],
+                               dtype=torch.float64, device=dX.device)
+            if self.P > 1:
+                dist.all_reduce(cnt, op=dist.ReduceOp.SUM, group=self.group)
+            n = X.shape[0]
+            off = n * (self.v_total - 1)
+            res.skipped_fraction = float(cnt[0]) / off if off else 0.0
+            res.skipped_tiles, res.total_tiles = int(cnt[1]), int(cnt[2])
+        return res
