@@ -153,6 +153,27 @@ LF_API int lf_validate_targets(const int64_t* d_targets, int64_t n, int64_t v, v
 /* Replaces NegIndexMatrix::validate (neg_index.cpp:8-28). Synchronizes. */
 LF_API int lf_validate_inds(const int64_t* d_inds, int64_t n, int64_t w, int64_t v, void* stream);
 
+/* ------------------------------------------------------ boundary layouts -- */
+/* For callers holding the reference's host layouts (the C++ drop-in,
+ * paper_2509_09682_b200/shim/lseforge_shim.cpp).  Stream-ordered, no sync. */
+
+/* ref-C (float d x v row-major, cce.hpp:36 "C") -> E (v x d row-major) in
+ * `dtype` (exact for f32/f64, round-to-nearest-even for bf16). */
+LF_API int lf_classifier_to_items(const float* d_C, int64_t d, int64_t v, int32_t dtype, void* d_E,
+                                  void* stream);
+/* Element conversion of a float buffer (ref-E, the hidden rows) to `dtype`. */
+LF_API int lf_convert_rows(const float* d_src, int64_t count, int32_t dtype, void* d_dst,
+                           void* stream);
+/* dE (v x d, float for bf16/f32 inputs or double for f64 — the gradient type
+ * of `dtype`) -> d_classifier (double d x v, GradPair::d_classifier,
+ * losses.hpp:24-27). */
+LF_API int lf_items_grad_to_classifier(const void* d_dE, int32_t dtype, int64_t v, int64_t d,
+                                       double* d_dC, void* stream);
+/* Widen a gradient buffer of `dtype`'s gradient type to double (dX ->
+ * GradPair::d_embeddings). */
+LF_API int lf_widen_grad(const void* d_src, int32_t dtype, int64_t count, double* d_dst,
+                         void* stream);
+
 /* -------------------------------------------------------- accounting ----- */
 /* Replaces lseforge::estimate_flops (ccem.hpp:43-49, ccem.cpp:207-235):
  * backend 0 ce, 1 cem, 2 cce, 3 ccem, 4 bce (backend.hpp:10-16). */

@@ -22,7 +22,8 @@ EXPORTS = (
     "lf_cce_forward_partial", "lf_cce_combine", "lf_cce_backward_shard", "lf_ccem_forward",
     "lf_ccem_backward", "lf_validate_targets", "lf_validate_inds", "lf_estimate_flops",
     "lf_workspace_stats", "lf_workspace_reset_peak", "lf_launch_count", "lf_launch_count_reset",
-    "lf_profile_enable", "lf_profile_read", "lf_profile_reset",
+    "lf_profile_enable", "lf_profile_read", "lf_profile_reset", "lf_classifier_to_items",
+    "lf_convert_rows", "lf_items_grad_to_classifier", "lf_widen_grad",
 )
 KERNEL_KINDS = ("cce_fwd", "cce_bwd_dx", "cce_bwd_de", "cce_simt", "ccem_fwd", "ccem_bwd", "aux")
 

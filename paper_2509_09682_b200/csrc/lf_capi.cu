@@ -175,7 +175,7 @@ int backward_impl(const void* X, const void* E, const int64_t* targets, const do
       if (!rc)
         rc = tc_cce_backward(X, E, targets, lse, scale, cfg->filter_eps, n, static_cast<int>(d),
                              v_shard, v_offset, static_cast<float*>(dX), static_cast<float*>(dE),
-                             c.ptr(), st);
+                             stats ? c.ptr() : nullptr, st);
       break;
     case LF_F32:
       rc = simt_cce_backward<float>(static_cast<const float*>(X), static_cast<const float*>(E),
@@ -325,6 +325,29 @@ int lf_validate_targets(const int64_t* d_targets, int64_t n, int64_t v, void* st
 
 int lf_validate_inds(const int64_t* d_inds, int64_t n, int64_t w, int64_t v, void* stream) {
   return validate_inds(d_inds, n, w, v, as_stream(stream));
+}
+
+int lf_classifier_to_items(const float* d_C, int64_t d, int64_t v, int32_t dtype, void* d_E,
+                           void* stream) {
+  if (d < 0 || v < 0) return fail(LF_EINVAL, "lf_classifier_to_items: negative extent");
+  return layout_classifier_to_items(d_C, d, v, dtype, d_E, as_stream(stream));
+}
+
+int lf_convert_rows(const float* d_src, int64_t count, int32_t dtype, void* d_dst, void* stream) {
+  if (count < 0) return fail(LF_EINVAL, "lf_convert_rows: negative count");
+  return layout_convert_rows(d_src, count, dtype, d_dst, as_stream(stream));
+}
+
+int lf_items_grad_to_classifier(const void* d_dE, int32_t dtype, int64_t v, int64_t d,
+                                double* d_dC, void* stream) {
+  if (d < 0 || v < 0) return fail(LF_EINVAL, "lf_items_grad_to_classifier: negative extent");
+  return layout_items_grad_to_classifier(d_dE, dtype == LF_F64 ? LF_F64 : LF_F32, v, d, d_dC,
+                                         as_stream(stream));
+}
+
+int lf_widen_grad(const void* d_src, int32_t dtype, int64_t count, double* d_dst, void* stream) {
+  if (count < 0) return fail(LF_EINVAL, "lf_widen_grad: negative count");
+  return layout_widen(d_src, dtype == LF_F64 ? LF_F64 : LF_F32, count, d_dst, as_stream(stream));
 }
 
 int lf_estimate_flops(int64_t n, int64_t d, int64_t v, int64_t ns, int32_t backend,

@@ -59,4 +59,12 @@ int ccem_backward(int dtype, const void* X, const void* E, const int64_t* inds,
 int validate_targets(const int64_t* targets, int64_t n, int64_t v, cudaStream_t st);
 int validate_inds(const int64_t* inds, int64_t n, int64_t w, int64_t v, cudaStream_t st);
 
+// ---- boundary layouts (lf_layout.cu) ----
+int layout_classifier_to_items(const float* C, int64_t d, int64_t v, int dtype, void* E,
+                               cudaStream_t st);
+int layout_convert_rows(const float* src, int64_t count, int dtype, void* dst, cudaStream_t st);
+int layout_items_grad_to_classifier(const void* dE, int grad_dtype, int64_t v, int64_t d,
+                                    double* dC, cudaStream_t st);
+int layout_widen(const void* src, int grad_dtype, int64_t count, double* dst, cudaStream_t st);
+
 }  // namespace lf

@@ -37,6 +37,9 @@ constexpr int kThreads = 320;
 constexpr int kEpiThreads = 256;
 
 enum Mode : int { FWD = 0, BWD_ROWS = 1, BWD_ITEMS = 2 };
+// Backward variants: kFilt = filter_eps > 0 (flush below eps, sub-tile skip);
+// kCount = also count skipped elements / sub-tiles (only when stats are read).
+constexpr int kFilt = 1, kCount = 2;
 
 struct TcParams {
   int64_t n_owner;       // owner rows (n or v_shard)
@@ -47,8 +50,8 @@ struct TcParams {
   int64_t units;
   const int32_t* tgt;    // FWD/BWD_ROWS: per owner row (local item or -1); BWD_ITEMS: per stream row
   const float* lse2;     // lse*log2e - log2|scale| per row (padded; +inf pad)
-  float thr2;            // log2(eps) + log2|scale| (filter threshold), -inf = off
-  float abs_scale;
+  float abs_scale;       // |upstream / n| in the kernel's (possibly rescaled) G domain
+  float out_scale;       // multiplies the dX / dE accumulators on read-out
   float4* part;          // FWD: [n_chunks][n_owner]
   float* out;            // BWD_ROWS: [n_chunks][n_owner][D]; BWD_ITEMS: [n_owner][D]
   unsigned long long* counters;  // [0] skipped elems, [1] skipped tiles, [2] total tiles
@@ -59,7 +62,7 @@ struct Cfg {
   static constexpr int kAtoms = D / 64;               // 128-byte K atoms per row
   static constexpr int kOwnerBytes = BM * D * 2;
   static constexpr int kTileBytes = BN * D * 2;
-  static constexpr int kExtraBytes = MODE == BWD_ITEMS ? 2048 : 0;  // lse2[128] + hits[129]
+  static constexpr int kExtraBytes = MODE == BWD_ITEMS ? 1024 : 0;  // lse2[128] + tgt[128]
   static constexpr int kStageBytes = kTileBytes + kExtraBytes;
   static constexpr int kStages = D == 64 ? 8 : (D == 128 ? 5 : (D == 192 ? 3 : 2));
   static constexpr int kNB = MODE == FWD ? 4 : (512 - D) / BN;  // S buffers in TMEM
@@ -70,6 +73,13 @@ struct Cfg {
 
 __device__ __forceinline__ float fma_log2(float v, float sub) { return fmaf(v, kLog2e, -sub); }
 
+// Backward coefficient of a row's own target column (never filtered).
+template <int FLAGS>
+__device__ __forceinline__ float target_g(float e, uint32_t raw, float l, float t_scale) {
+  if (FLAGS & kFilt) return ex2_approx(fmaf(__uint_as_float(raw), kLog2e, -l) + 64.f) - t_scale;
+  return e - t_scale;
+}
+
 // Select r[idx] from a register array without dynamic indexing.
 template <int N>
 __device__ __forceinline__ float select_reg(const float (&r)[N], int idx) {
@@ -79,7 +89,7 @@ __device__ __forceinline__ float select_reg(const float (&r)[N], int idx) {
   return out;
 }
 
-template <int D, int MODE>
+template <int D, int MODE, int FLAGS>
 __global__ void __launch_bounds__(kThreads, 1)
     cce_tc_kernel(const __grid_constant__ CUtensorMap map_owner,
                   const __grid_constant__ CUtensorMap map_stream, const TcParams p) {
@@ -153,39 +163,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         unsigned char* stg = stage_smem + st * C::kStageBytes;
         if (lane == 0) {
           mbar_wait(&empty[st], ph ^ 1);
-          if (MODE == BWD_ITEMS) {
-            mbar_expect_tx(&full[st], C::kTileBytes + 512);
-          } else {
-            mbar_arrive_expect_tx(&full[st], C::kTileBytes);
-          }
+          // BWD_ITEMS also stages the stream rows' lse2 and local targets
+          // (512 B each) next to the X tile.
+          mbar_arrive_expect_tx(&full[st], C::kTileBytes + (MODE == BWD_ITEMS ? 1024 : 0));
 #pragma unroll
           for (int a = 0; a < C::kAtoms; ++a)
             tma_load_2d(stg + a * BN * 128, &map_stream, &full[st], a * 64,
                         static_cast<int32_t>(s0), pol);
-          if (MODE == BWD_ITEMS) bulk_load(stg + C::kTileBytes, p.lse2 + s0, 512, &full[st]);
-        }
-        if (MODE == BWD_ITEMS) {
-          // Rows of this stream tile whose target lies in the owner item tile.
-          __syncwarp();
-          int* hits = reinterpret_cast<int*>(stg + C::kTileBytes + 512);
-          const int64_t o0 = ot * BM;
-          int nh = 0;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int jcol = q * 32 + lane;
-            const int tg = p.tgt[s0 + jcol];
-            const int li = tg - static_cast<int>(o0);
-            const bool hit = tg >= 0 && li >= 0 && li < BM;
-            const unsigned bal = __ballot_sync(0xffffffffu, hit);
-            if (hit) {
-              const int slot = nh + __popc(bal & ((1u << lane) - 1u));
-              hits[1 + slot] = (jcol << 8) | li;
-            }
-            nh += __popc(bal);
+          if (MODE == BWD_ITEMS) {
+            bulk_load(stg + C::kTileBytes, p.lse2 + s0, 512, &full[st]);
+            bulk_load(stg + C::kTileBytes + 512, p.tgt + s0, 512, &full[st]);
           }
-          if (lane == 0) hits[0] = nh;
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&full[st]);
         }
       }
     }
@@ -246,10 +234,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (MODE == FWD) mma_commit(&empty[st]);
         }
         __syncwarp();
-        if (MODE != FWD && i > 0) mma2(t - 1, i == 1);
+        // Lookahead 2: S(i) is issued before waiting on G(i-2), so with two
+        // epilogue warpgroups the next S tile is always ready when one frees up.
+        if (MODE != FWD && i >= 2) mma2(t - 2, i == 2);
         ++tiles_seen;
       }
       if (MODE != FWD) {
+        if (ntile >= 2) mma2(t - 2, ntile == 2);
         mma2(t - 1, ntile == 1);
         if (lane == 0) mma_commit(acc_full);
         __syncwarp();
@@ -257,14 +248,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mma_commit(owner_empty);
       __syncwarp();
     }
-    if (lane == 0 && MODE == BWD_ROWS && p.counters) atomicAdd(&p.counters[2], tiles_seen);
+    // 16 sub-tiles (4 warps x 4 column chunks) per 128 x 128 tile
+    if (lane == 0 && MODE == BWD_ROWS && (FLAGS & kCount)) atomicAdd(&p.counters[2], 16 * tiles_seen);
   } else {
     // ============================== epilogue ==============================
     const int wg = (warp - 2) >> 2;   // 0 or 1: takes tiles with t % 2 == wg
     const int quad = warp & 3;        // TMEM lane quadrant this warp may access
     const int lrow = quad * 32 + lane;  // owner row within the tile
     const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
-    unsigned long long skipped = 0;
+    unsigned long long skipped = 0, skipped_sub = 0;
     int64_t t = 0;
     uint32_t j = 0;
     for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
@@ -287,17 +279,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int nvalid = static_cast<int>((s_end - col0 < BN ? s_end - col0 : BN));
         mbar_wait(&s_full[b], static_cast<uint32_t>((t / C::kNB) & 1));
         tc_fence_after();
-        float v[BN];
-        {
-          uint32_t* r = reinterpret_cast<uint32_t*>(v);
-          const uint32_t ta = tmem + lane_base + b * BN;
-          LF_TMEM_LD32(ta + 0, (r + 0));
-          LF_TMEM_LD32(ta + 32, (r + 32));
-          LF_TMEM_LD32(ta + 64, (r + 64));
-          LF_TMEM_LD32(ta + 96, (r + 96));
-          tmem_ld_wait();
-        }
         if (MODE == FWD) {
+          float v[BN];
+          {
+            uint32_t* r = reinterpret_cast<uint32_t*>(v);
+            const uint32_t ta = tmem + lane_base + b * BN;
+            LF_TMEM_LD32(ta + 0, (r + 0));
+            LF_TMEM_LD32(ta + 32, (r + 32));
+            LF_TMEM_LD32(ta + 64, (r + 64));
+            LF_TMEM_LD32(ta + 96, (r + 96));
+            tmem_ld_wait();
+          }
           tc_fence_before();
           mbar_arrive(&s_empty[b]);
           if (nvalid < BN) {
@@ -341,69 +333,118 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           s += sum;
         } else {
-          // ---- backward: G = 2^(S log2e - lse2) with filter and target fix
-          uint32_t g2[BN / 2];
+          // ---- backward: G = softmax * |scale| (target: minus |scale|), bf16, into TMEM.
+          // Processed in four 32-column chunks with the next chunk's tcgen05.ld in
+          // flight.  Filtering (FILT): lse2 carries the shift thr2 + 126, so
+          // a = S log2e - lse2 < -126 exactly when softmax < eps, and
+          // ex2.approx.ftz flushes those results (denormal) to +0 — no compare or
+          // select per element; the survivors are rescaled by 2^64 so every
+          // bf16 G and every MMA product stays normal, and out_scale undoes the
+          // 2^(64 - thr2 - 126) factor on the accumulator.  A 32x32 sub-tile
+          // whose largest a is below the threshold (and that holds no target)
+          // skips its exps entirely (warp vote).
+          (void)fma_log2;
           const float* lse2s = nullptr;
+          const int* tgts = nullptr;
           if (MODE == BWD_ITEMS) {
             const int st = static_cast<int>(t % C::kStages);
             lse2s = reinterpret_cast<const float*>(stage_smem + st * C::kStageBytes + C::kTileBytes);
+            tgts = reinterpret_cast<const int*>(lse2s + 128);
           }
-          const bool filt = p.thr2 > -INFINITY;
-          // raw logit of this row's target column (rare: one tile per row)
+          const int o0 = static_cast<int>(ot * BM);
           const int lc_t = MODE == BWD_ROWS ? tgt - static_cast<int>(col0) : -1;
-          float o_t = 0.f;
-          if (MODE == BWD_ROWS && lc_t >= 0 && lc_t < BN) o_t = select_reg(v, lc_t);
-#pragma unroll
-          for (int c = 0; c < BN; c += 4) {
-            float l[4] = {lse2, lse2, lse2, lse2};
-            if (MODE == BWD_ITEMS) {
-              const float4 lp = *reinterpret_cast<const float4*>(lse2s + c);
-              l[0] = lp.x;
-              l[1] = lp.y;
-              l[2] = lp.z;
-              l[3] = lp.w;
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const float a = fma_log2(v[c + q], l[q]);
-              float e = ex2_approx(a);
-              if (filt) {
-                const bool k = a < p.thr2;
-                e = k ? 0.f : e;
-                if (MODE == BWD_ROWS) skipped += (k && c + q < nvalid && orow < p.n_owner);
-              }
-              v[c + q] = e;
-            }
-          }
-          if (MODE == BWD_ROWS && lc_t >= 0 && lc_t < BN) {
-            // the target is never filtered: g = (s - 1) * |scale|  (cce.cpp:193-195)
-            const float a = fma_log2(o_t, lse2);
-            if (filt && a < p.thr2 && orow < p.n_owner) --skipped;
-            const float g = ex2_approx(a) - p.abs_scale;
-#pragma unroll
-            for (int c = 0; c < BN; ++c)
-              if (c == lc_t) v[c] = g;
-          }
-          if (MODE == BWD_ITEMS) {
-            const int* hits = reinterpret_cast<const int*>(lse2s + 128);  // [0]=count, [1..128]
-            const int nh = hits[0];
-            for (int h = 0; h < nh; ++h) {
-              const int e = hits[1 + h];
-              if ((e & 0xFF) == lrow) {
-                const int jc = e >> 8;
-#pragma unroll
-                for (int c = 0; c < BN; ++c)
-                  if (c == jc) v[c] -= p.abs_scale;
-              }
-            }
-          }
-#pragma unroll
-          for (int c = 0; c < BN / 2; ++c) g2[c] = pack_bf16x2(v[2 * c], v[2 * c + 1]);
           const uint32_t ta = tmem + lane_base + b * BN;
-          LF_TMEM_ST16(ta + 0, (g2 + 0));
-          LF_TMEM_ST16(ta + 16, (g2 + 16));
-          LF_TMEM_ST16(ta + 32, (g2 + 32));
-          LF_TMEM_ST16(ta + 48, (g2 + 48));
+          uint32_t ra[32], rb[32];
+          LF_TMEM_LD32(ta, ra);
+          tmem_ld_wait();
+#pragma unroll
+          for (int q = 0; q < BN / 32; ++q) {
+            uint32_t(&cur)[32] = (q & 1) ? rb : ra;
+            uint32_t(&nxt)[32] = (q & 1) ? ra : rb;
+            if (q + 1 < BN / 32) LF_TMEM_LD32(ta + (q + 1) * 32, nxt);
+            float e[32];
+#pragma unroll
+            for (int c = 0; c < 32; c += 4) {
+              float l[4] = {lse2, lse2, lse2, lse2};
+              if (MODE == BWD_ITEMS) {
+                const float4 lp = *reinterpret_cast<const float4*>(lse2s + q * 32 + c);
+                l[0] = lp.x;
+                l[1] = lp.y;
+                l[2] = lp.z;
+                l[3] = lp.w;
+              }
+#pragma unroll
+              for (int k = 0; k < 4; ++k) e[c + k] = fmaf(__uint_as_float(cur[c + k]), kLog2e, -l[k]);
+            }
+            // BWD_ITEMS: lane k checks stream row q*32+k; hm = rows of this chunk
+            // whose target item lies in the owner tile (warp-uniform, rare).
+            int tq = 0;
+            unsigned hm = 0;
+            if (MODE == BWD_ITEMS) {
+              tq = tgts[q * 32 + lane] - o0;
+              hm = __ballot_sync(0xffffffffu, static_cast<unsigned>(tq) < static_cast<unsigned>(BM));
+            }
+            const bool tgt_here =
+                MODE == BWD_ROWS ? static_cast<unsigned>(lc_t - q * 32) < 32u : hm != 0u;
+            bool skip = false;
+            if (FLAGS & kFilt) {
+              float mx = e[0];
+#pragma unroll
+              for (int c = 1; c < 32; c += 2) mx = fmaxf(mx, fmaxf(e[c], c + 1 < 32 ? e[c + 1] : e[c]));
+              skip = __all_sync(0xffffffffu, mx < -126.f && !tgt_here);
+              if ((FLAGS & kCount) && MODE == BWD_ROWS) {
+#pragma unroll
+                for (int c = 0; c < 32; ++c)
+                  skipped += (e[c] < -126.f && q * 32 + c < nvalid && orow < p.n_owner) ? 1 : 0;
+                if (tgt_here) {
+                  // the target is never filtered (cce.cpp:193-195): undo its count
+                  float et = 0.f;
+#pragma unroll
+                  for (int c = 0; c < 32; ++c) et = (c == lc_t - q * 32) ? e[c] : et;
+                  if (et < -126.f && orow < p.n_owner) --skipped;
+                }
+                if (skip) ++skipped_sub;
+              }
+            }
+            uint32_t g[16];
+            if (skip) {
+#pragma unroll
+              for (int c = 0; c < 16; ++c) g[c] = 0u;
+            } else {
+#pragma unroll
+              for (int c = 0; c < 32; ++c) {
+                float x = ex2_approx(e[c]);
+                if (FLAGS & kFilt) x *= 18446744073709551616.f;  // 2^64
+                e[c] = x;
+              }
+              // The target is never filtered: g = (s - 1) |scale| (cce.cpp:193-195).
+              // Under FILT its softmax is recomputed unflushed from the raw logit
+              // still in `cur`: s * 2^-62 / eps = 2^(a + 64).
+              if (MODE == BWD_ROWS && tgt_here) {
+                const int jc = lc_t - q * 32;
+#pragma unroll
+                for (int c = 0; c < 32; ++c)
+                  if (c == jc) e[c] = target_g<FLAGS>(e[c], cur[c], lse2, p.abs_scale);
+              }
+              if (MODE == BWD_ITEMS) {
+                while (hm) {  // warp-uniform loop over the hit columns
+                  const int jc = __ffs(hm) - 1;
+                  hm &= hm - 1u;
+                  const int li = __shfl_sync(0xffffffffu, tq, jc);
+                  if (li == lrow) {
+                    const float lj = lse2s[q * 32 + jc];
+#pragma unroll
+                    for (int c = 0; c < 32; ++c)
+                      if (c == jc) e[c] = target_g<FLAGS>(e[c], cur[c], lj, p.abs_scale);
+                  }
+                }
+              }
+#pragma unroll
+              for (int c = 0; c < 16; ++c) g[c] = pack_bf16x2(e[2 * c], e[2 * c + 1]);
+            }
+            LF_TMEM_ST16(ta + q * 16, g);
+            if (q + 1 < BN / 32) tmem_ld_wait();
+          }
           tmem_st_wait();
           tc_fence_before();
           mbar_arrive(&g_ready[b]);
@@ -443,20 +484,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           LF_TMEM_LD32(tmem + lane_base + C::kAccCol + c0, r);
           tmem_ld_wait();
           if (orow < p.n_owner) {
+            const float os = p.out_scale;
 #pragma unroll
             for (int c = 0; c < 32; c += 4)
               *reinterpret_cast<float4*>(dst + c0 + c) =
-                  make_float4(__uint_as_float(r[c]), __uint_as_float(r[c + 1]),
-                              __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
+                  make_float4(__uint_as_float(r[c]) * os, __uint_as_float(r[c + 1]) * os,
+                              __uint_as_float(r[c + 2]) * os, __uint_as_float(r[c + 3]) * os);
           }
         }
         tc_fence_before();
         mbar_arrive(acc_empty);
       }
     }
-    if (MODE == BWD_ROWS && p.counters) {
+    if ((FLAGS & kCount) && MODE == BWD_ROWS) {
       for (int off = 16; off > 0; off >>= 1) skipped += __shfl_xor_sync(0xffffffffu, skipped, off);
       if (lane == 0 && skipped) atomicAdd(&p.counters[0], skipped);
+      if (lane == 0 && skipped_sub) atomicAdd(&p.counters[1], skipped_sub);
     }
   }
   tc_fence_before();
@@ -497,7 +540,7 @@ int make_map(CUtensorMap* map, const void* ptr, int64_t rows, int D, int box_row
 
 __global__ void prep_rows(const int64_t* __restrict__ targets, const double* __restrict__ lse,
                           int64_t n, int64_t n_pad, int64_t v_shard, int64_t v_offset,
-                          double log2_abs_scale, int32_t* __restrict__ tgt,
+                          double lse_sub, int32_t* __restrict__ tgt,
                           float* __restrict__ lse2) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n_pad) return;
@@ -506,16 +549,16 @@ __global__ void prep_rows(const int64_t* __restrict__ targets, const double* __r
   if (i < n) {
     const int64_t x = targets[i] - v_offset;
     t = (x >= 0 && x < v_shard) ? static_cast<int32_t>(x) : -1;
-    if (lse) l = static_cast<float>(lse[i] * 1.4426950408889634 - log2_abs_scale);
+    if (lse) l = static_cast<float>(lse[i] * 1.4426950408889634 - lse_sub);
   }
   tgt[i] = t;
   if (lse2) lse2[i] = l;
 }
 
-template <int D, int MODE>
+template <int D, int MODE, int FLAGS>
 int launch_mode(const CUtensorMap& mo, const CUtensorMap& ms, const TcParams& p, cudaStream_t st) {
   using C = Cfg<D, MODE>;
-  auto kern = cce_tc_kernel<D, MODE>;
+  auto kern = cce_tc_kernel<D, MODE, FLAGS>;
   LF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
   const int grid = static_cast<int>(std::min<int64_t>(p.units, num_sms()));
   ProfScope prof(MODE == FWD ? LF_K_CCE_FWD : (MODE == BWD_ROWS ? LF_K_CCE_BWD_DX : LF_K_CCE_BWD_DE), st);
@@ -524,14 +567,25 @@ int launch_mode(const CUtensorMap& mo, const CUtensorMap& ms, const TcParams& p,
   return LF_OK;
 }
 
+template <int D, int MODE>
+int launch_flags(int flags, const CUtensorMap& mo, const CUtensorMap& ms, const TcParams& p,
+                 cudaStream_t st) {
+  if (MODE == FWD) return launch_mode<D, MODE, 0>(mo, ms, p, st);
+  switch (flags) {
+    case 0: return launch_mode<D, MODE, 0>(mo, ms, p, st);
+    case kFilt: return launch_mode<D, MODE, kFilt>(mo, ms, p, st);
+    default: return launch_mode<D, MODE, kFilt | kCount>(mo, ms, p, st);
+  }
+}
+
 template <int MODE>
-int launch_d(int D, const CUtensorMap& mo, const CUtensorMap& ms, const TcParams& p,
+int launch_d(int D, int flags, const CUtensorMap& mo, const CUtensorMap& ms, const TcParams& p,
              cudaStream_t st) {
   switch (D) {
-    case 64: return launch_mode<64, MODE>(mo, ms, p, st);
-    case 128: return launch_mode<128, MODE>(mo, ms, p, st);
-    case 192: return launch_mode<192, MODE>(mo, ms, p, st);
-    case 256: return launch_mode<256, MODE>(mo, ms, p, st);
+    case 64: return launch_flags<64, MODE>(flags, mo, ms, p, st);
+    case 128: return launch_flags<128, MODE>(flags, mo, ms, p, st);
+    case 192: return launch_flags<192, MODE>(flags, mo, ms, p, st);
+    case 256: return launch_flags<256, MODE>(flags, mo, ms, p, st);
     default: return fail(LF_EUNSUPPORTED, "tc: d must be 64/128/192/256");
   }
 }
@@ -588,7 +642,7 @@ int tc_cce_forward_partials(const void* X, const void* E, const int64_t* targets
   p.units = owner_tiles * P;
   p.tgt = tgt.as<int32_t>();
   p.part = ws.as<float4>();
-  rc = launch_d<FWD>(D, mo, ms, p, st);
+  rc = launch_d<FWD>(D, 0, mo, ms, p, st);
   if (rc) return rc;
   *part_out = ws.as<float>();
   *P_out = static_cast<int>(P);
@@ -603,8 +657,20 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
     LF_CUDA(cudaMemsetAsync(dE, 0, sizeof(float) * v * D, st));
     return LF_OK;
   }
-  const double abs_scale = std::fabs(scale);
-  const double l2s = std::log2(abs_scale);
+  // G domain.  No filter: G = softmax * |scale| (lse2 = lse log2e - log2|scale|).
+  // Filter (eps >= 2^-100): lse2 = lse log2e + log2(eps) + 126, so the exp
+  // argument is < -126 exactly when softmax < eps and ex2.approx.ftz flushes
+  // it; survivors are scaled by 2^64, i.e. G = softmax * 2^-62 / eps, and the
+  // read-out multiplies by scale * eps * 2^62 (sign included).  Below 2^-100
+  // the filtered entries are far under fp32 resolution of the accumulated
+  // gradient and the unfiltered kernel is used.
+  if (eps > 2.0) eps = 2.0;  // softmax <= 1: every eps > 1 filters every off-target entry
+  const bool filt = eps >= 0x1p-100;
+  const bool count = filt && counters != nullptr;
+  const int flags = filt ? (kFilt | (count ? kCount : 0)) : 0;
+  const double sub = filt ? -std::log2(eps) - 126.0 : std::log2(std::fabs(scale));
+  const double gscale = filt ? std::ldexp(1.0, -62) / eps : std::fabs(scale);
+  const double out_scale = filt ? scale * eps * std::ldexp(1.0, 62) : (scale < 0 ? -1.0 : 1.0);
   const int64_t row_tiles = ceil_div(n, BM);
   const int64_t item_tiles = ceil_div(v, BN);
   const int64_t n_pad = std::max(row_tiles * BM, ceil_div(n, BN) * BN);
@@ -612,14 +678,13 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
   int rc = tgt.alloc(sizeof(int32_t) * n_pad, st);
   if (!rc) rc = lse2.alloc(sizeof(float) * n_pad, st);
   if (rc) return rc;
-  prep_rows<<<ceil_div(n_pad, 256), 256, 0, st>>>(targets, lse, n, n_pad, v, v_offset, l2s,
+  prep_rows<<<ceil_div(n_pad, 256), 256, 0, st>>>(targets, lse, n, n_pad, v, v_offset, sub,
                                                  tgt.as<int32_t>(), lse2.as<float>());
   LF_LAUNCHED();
   CUtensorMap mx, me;
   rc = make_map(&mx, X, n, D, 128);
   if (!rc) rc = make_map(&me, E, v, D, 128);
   if (rc) return rc;
-  const float thr2 = eps > 0.0 ? static_cast<float>(std::log2(eps) + l2s) : -INFINITY;
 
   // ---- pass 1: dX (owner rows, stream items), V split into a few chunks ----
   const int64_t chunks = pick_chunks(row_tiles, item_tiles, 8);
@@ -641,11 +706,11 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
   p.units = row_tiles * P;
   p.tgt = tgt.as<int32_t>();
   p.lse2 = lse2.as<float>();
-  p.thr2 = thr2;
-  p.abs_scale = static_cast<float>(abs_scale);
+  p.abs_scale = static_cast<float>(gscale);
+  p.out_scale = static_cast<float>(out_scale);
   p.out = dx_out;
   p.counters = counters;
-  rc = launch_d<BWD_ROWS>(D, mx, me, p, st);
+  rc = launch_d<BWD_ROWS>(D, flags, mx, me, p, st);
   if (rc) return rc;
   if (P > 1) {
     rc = launch_reduce_f32(dx_out, static_cast<int>(P), n * D, dX, st);
@@ -661,18 +726,12 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
   q.units = item_tiles;
   q.tgt = tgt.as<int32_t>();
   q.lse2 = lse2.as<float>();
-  q.thr2 = thr2;
-  q.abs_scale = static_cast<float>(abs_scale);
+  q.abs_scale = static_cast<float>(gscale);
+  q.out_scale = static_cast<float>(out_scale);
   q.out = dE;
   q.counters = counters;
-  rc = launch_d<BWD_ITEMS>(D, me, mx, q, st);
-  if (rc) return rc;
-  if (scale < 0.0) {
-    rc = launch_negate(dX, n * D, st);
-    if (!rc) rc = launch_negate(dE, v * D, st);
-    if (rc) return rc;
-  }
-  return LF_OK;
+  rc = launch_d<BWD_ITEMS>(D, flags, me, mx, q, st);
+  return rc;
 }
 
 }  // namespace lf

@@ -1,0 +1,358 @@
+// lseforge_shim.cpp — the C++ drop-in for the reference's loss hot path.
+//
+// Defines, with the reference's exact signatures, the functions a maintainer
+// would otherwise get from proj/src/cce.cpp and proj/src/ccem.cpp:
+//
+//   lseforge::cce_forward          cce.hpp:36-38   (reference cce.cpp:65-145)
+//   lseforge::cce_backward         cce.hpp:51-54   (reference cce.cpp:147-272)
+//   lseforge::ccem_forward         ccem.hpp:19-20  (reference ccem.cpp:48-105)
+//   lseforge::ccem_backward        ccem.hpp:27-29  (reference ccem.cpp:196-205)
+//   lseforge::ccem_backward_rows   ccem.hpp:34-36  (reference ccem.cpp:107-194)
+//   lseforge::estimate_flops       ccem.hpp:48-49  (reference ccem.cpp:207-235)
+//
+// It is compiled against the reference's own headers (-I proj/include) and
+// linked in place of cce.cpp + ccem.cpp; everything else in liblseforge
+// (losses.cpp validation and oracles, neg_index.cpp, accountant.cpp, the
+// trainer) is unchanged.  Each call: validate on the host with the
+// reference's own functions and messages -> upload the host matrices ->
+// convert layouts on the device (ref-C D x V float -> E V x D) -> run the
+// B200 kernels through the C-ABI (include/lseforge_b200.h) -> convert the
+// gradients back (dE -> d_classifier D x V double) -> download.  Synchronous
+// and blocking, like the reference.  No CPU fallback: a missing GPU or a
+// kernel error throws.
+//
+// Element type of the device computation: environment LSEFORGE_B200_DTYPE =
+//   f64  (default) exact mode — fp64 kernels in the reference's operand order,
+//        pos_logits bitwise equal to the reference's double results;
+//   f32  fp32 FFMA kernels;
+//   bf16 tcgen05 tensor-core kernels (inputs rounded to bf16, d % 64 == 0).
+// CceConfig::row_block / col_block / workers are CPU tiling knobs: validated
+// exactly as the reference does, otherwise ignored (the device results never
+// depend on them, which is the reference's own worker-invariance contract,
+// README.md:149-153).
+//
+// Memory accounting: the "retained/..." tags are charged exactly as the
+// reference charges them (cce.cpp:79-84, ccem.cpp:64-69, ccem.cpp:132-137);
+// the "scratch/..." tags are charged with the library's real device scratch
+// high-water mark for the call, in 4-byte scalars, and released before
+// returning.  The reference's CPU tile-scratch closed form
+// (memory_model.cpp:46-60) does not describe the GPU and is not imitated.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "lseforge/accountant.hpp"
+#include "lseforge/backend.hpp"
+#include "lseforge/cce.hpp"
+#include "lseforge/ccem.hpp"
+#include "lseforge/losses.hpp"
+#include "lseforge/matrix.hpp"
+#include "lseforge/neg_index.hpp"
+#include "lseforge_b200.h"
+
+namespace lseforge {
+
+namespace {
+
+[[noreturn]] void throw_status(int rc, const char* what) {
+  const std::string msg = lf_last_error();
+  if (rc == LF_EINVAL) throw std::invalid_argument(msg);
+  throw std::runtime_error(std::string(what) + ": " + msg);
+}
+
+void check(int rc, const char* what) {
+  if (rc != LF_OK) throw_status(rc, what);
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw std::runtime_error(std::string("lseforge_b200 shim: ") + what + ": " + cudaGetErrorString(e));
+}
+
+int device_dtype() {
+  const char* s = std::getenv("LSEFORGE_B200_DTYPE");
+  if (!s || !*s || std::strcmp(s, "f64") == 0) return LF_F64;
+  if (std::strcmp(s, "f32") == 0) return LF_F32;
+  if (std::strcmp(s, "bf16") == 0) return LF_BF16;
+  throw std::invalid_argument(std::string("LSEFORGE_B200_DTYPE must be f64, f32 or bf16, got ") + s);
+}
+
+std::size_t elem_bytes(int dtype) { return dtype == LF_F64 ? 8 : (dtype == LF_F32 ? 4 : 2); }
+std::size_t grad_bytes(int dtype) { return dtype == LF_F64 ? 8 : 4; }
+
+// Device buffer owned for the duration of one call.
+struct Dev {
+  void* p = nullptr;
+  explicit Dev(std::size_t bytes) {
+    if (bytes) cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
+  }
+  ~Dev() {
+    if (p) cudaFree(p);
+  }
+  Dev(const Dev&) = delete;
+  Dev& operator=(const Dev&) = delete;
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+void upload(void* dst, const void* src, std::size_t bytes) {
+  if (bytes) cuda_check(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice), "upload");
+}
+void download(void* dst, const void* src, std::size_t bytes) {
+  if (bytes) cuda_check(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost), "download");
+}
+
+// The inputs of one loss call, resident on the device in kernel layout.
+struct DeviceInputs {
+  int dtype;
+  std::size_t n, d, v;
+  Dev X, E;
+  DeviceInputs(const DenseMatrix& Eh, const DenseMatrix& Ch, int dt)
+      : dtype(dt), n(Eh.rows()), d(Eh.cols()), v(Ch.cols()),
+        X(n * d * elem_bytes(dt)), E(v * d * elem_bytes(dt)) {
+    Dev stage(std::max(n * d, d * v) * sizeof(float));
+    upload(stage.p, Eh.data().data(), n * d * sizeof(float));
+    check(lf_convert_rows(stage.as<float>(), static_cast<int64_t>(n * d), dtype, X.p, nullptr),
+          "lf_convert_rows");
+    upload(stage.p, Ch.data().data(), d * v * sizeof(float));
+    check(lf_classifier_to_items(stage.as<float>(), static_cast<int64_t>(d), static_cast<int64_t>(v),
+                                 dtype, E.p, nullptr),
+          "lf_classifier_to_items");
+  }
+};
+
+lf_cce_config make_cfg(const CceConfig& cfg, int dtype) {
+  lf_cce_config c{};
+  c.filter_eps = cfg.filter_eps;
+  c.dtype = dtype;
+  c.flags = LF_FLAG_NONE;
+  return c;
+}
+
+// cce.cpp:17-27 (same messages).
+void validate_config(const CceConfig& cfg) {
+  if (cfg.row_block < 1 || cfg.col_block < 1) {
+    throw std::invalid_argument("CceConfig: block sizes must be >= 1 (row_block=" +
+                                std::to_string(cfg.row_block) + ", col_block=" +
+                                std::to_string(cfg.col_block) + ")");
+  }
+  if (!(cfg.filter_eps >= 0.0)) {
+    throw std::invalid_argument("CceConfig: filter_eps must be >= 0, got " +
+                                std::to_string(cfg.filter_eps));
+  }
+}
+
+// ccem.cpp:16-31 (same messages); index checks by NegIndexMatrix::validate.
+void validate_sampled_inputs(const DenseMatrix& E, const DenseMatrix& C,
+                             const NegIndexMatrix& inds) {
+  if (inds.rows() != E.rows()) {
+    throw std::invalid_argument("fused sampled loss: " + std::to_string(inds.rows()) +
+                                " candidate rows for " + std::to_string(E.rows()) +
+                                " embedding rows");
+  }
+  if (E.rows() == 0) {
+    throw std::invalid_argument("fused sampled loss: zero rows; the mean loss is undefined");
+  }
+  if (E.cols() != C.rows()) {
+    throw std::invalid_argument("fused sampled loss: embedding width " + std::to_string(E.cols()) +
+                                " does not match classifier height " + std::to_string(C.rows()));
+  }
+  inds.validate(C.cols());
+}
+
+// Charges the library's device scratch high-water of the enclosed calls.
+struct ScratchCharge {
+  MemAccountant* acct;
+  const char* tag;
+  uint64_t base = 0;
+  ScratchCharge(MemAccountant* a, const char* t) : acct(a), tag(t) {
+    if (!acct) return;
+    lf_workspace_reset_peak();
+    uint64_t cur = 0;
+    lf_workspace_stats(&cur, &base);
+  }
+  void settle() {
+    if (!acct) return;
+    uint64_t cur = 0, peak = 0;
+    lf_workspace_stats(&cur, &peak);
+    const std::size_t scalars = static_cast<std::size_t>((peak - base + 3) / 4);
+    if (scalars) {
+      acct->record_alloc(tag, scalars);
+      acct->record_free(tag, scalars);
+    }
+  }
+};
+
+LossOutput download_loss(const Dev& lse, const Dev& pos, const Dev& loss, std::size_t n) {
+  LossOutput out;
+  out.lse.resize(n);
+  out.pos_logits.resize(n);
+  download(out.lse.data(), lse.p, n * sizeof(double));
+  download(out.pos_logits.data(), pos.p, n * sizeof(double));
+  download(&out.loss, loss.p, sizeof(double));
+  return out;
+}
+
+GradPair download_grads(const Dev& dX, const Dev& dE, int dtype, std::size_t n, std::size_t d,
+                        std::size_t v) {
+  GradPair g{DenseMatrixD(n, d), DenseMatrixD(d, v)};
+  Dev wide(std::max(n * d, d * v) * sizeof(double));
+  check(lf_widen_grad(dX.p, dtype, static_cast<int64_t>(n * d), wide.as<double>(), nullptr),
+        "lf_widen_grad");
+  download(g.d_embeddings.data().data(), wide.p, n * d * sizeof(double));
+  check(lf_items_grad_to_classifier(dE.p, dtype, static_cast<int64_t>(v), static_cast<int64_t>(d),
+                                    wide.as<double>(), nullptr),
+        "lf_items_grad_to_classifier");
+  download(g.d_classifier.data().data(), wide.p, d * v * sizeof(double));
+  return g;
+}
+
+}  // namespace
+
+LossOutput cce_forward(const DenseMatrix& E, const DenseMatrix& C, std::span<const std::int64_t> x,
+                       const CceConfig& cfg, MemAccountant* acct) {
+  validate_loss_inputs(E, C, x);
+  validate_config(cfg);
+  const std::size_t n = E.rows();
+  if (acct) {
+    acct->record_ensure("retained/cce/pos_logits", n);
+    acct->record_ensure("retained/cce/lse", n);
+  }
+  ScratchCharge sc(acct, "scratch/cce/forward");
+  const int dt = device_dtype();
+  DeviceInputs in(E, C, dt);
+  Dev tg(n * sizeof(int64_t)), lse(n * sizeof(double)), pos(n * sizeof(double)), loss(sizeof(double));
+  upload(tg.p, x.data(), n * sizeof(int64_t));
+  const lf_cce_config c = make_cfg(cfg, dt);
+  check(lf_cce_forward(in.X.p, in.E.p, tg.as<int64_t>(), static_cast<int64_t>(n),
+                       static_cast<int64_t>(in.d), static_cast<int64_t>(in.v), &c, lse.as<double>(),
+                       pos.as<double>(), loss.as<double>(), nullptr),
+        "lf_cce_forward");
+  LossOutput out = download_loss(lse, pos, loss, n);
+  sc.settle();
+  return out;
+}
+
+CceBackwardResult cce_backward(const DenseMatrix& E, const DenseMatrix& C,
+                               std::span<const std::int64_t> x, std::span<const double> lse,
+                               double upstream, const CceConfig& cfg, MemAccountant* acct) {
+  validate_loss_inputs(E, C, x);
+  validate_config(cfg);
+  if (lse.size() != E.rows()) {
+    throw std::invalid_argument("cce_backward: LSE vector has " + std::to_string(lse.size()) +
+                                " entries for " + std::to_string(E.rows()) + " rows");
+  }
+  const std::size_t n = E.rows(), d = E.cols(), v = C.cols();
+  if (acct) acct->record_ensure("retained/cce/lse", n);
+  ScratchCharge sc(acct, "scratch/cce/backward");
+  const int dt = device_dtype();
+  DeviceInputs in(E, C, dt);
+  Dev tg(n * sizeof(int64_t)), dl(n * sizeof(double));
+  Dev dX(n * d * grad_bytes(dt)), dE(v * d * grad_bytes(dt));
+  upload(tg.p, x.data(), n * sizeof(int64_t));
+  upload(dl.p, lse.data(), n * sizeof(double));
+  const lf_cce_config c = make_cfg(cfg, dt);
+  lf_cce_stats st{};
+  check(lf_cce_backward(in.X.p, in.E.p, tg.as<int64_t>(), dl.as<double>(), upstream,
+                        static_cast<int64_t>(n), static_cast<int64_t>(d), static_cast<int64_t>(v),
+                        &c, dX.p, dE.p, &st, nullptr),
+        "lf_cce_backward");
+  CceBackwardResult out{download_grads(dX, dE, dt, n, d, v), st.skipped_fraction};
+  sc.settle();
+  return out;
+}
+
+LossOutput ccem_forward(const DenseMatrix& E, const DenseMatrix& C, const NegIndexMatrix& inds,
+                        const CceConfig& cfg, MemAccountant* acct) {
+  validate_sampled_inputs(E, C, inds);
+  if (cfg.row_block < 1) throw std::invalid_argument("CceConfig: row_block must be >= 1");
+  const std::size_t n = E.rows(), w = inds.width();
+  if (acct) {
+    acct->record_ensure("retained/ccem/pos_logits", n);
+    acct->record_ensure("retained/ccem/lse", n);
+    acct->record_ensure("retained/ccem/inds", n * w, ScalarKind::kIndex);
+  }
+  ScratchCharge sc(acct, "scratch/ccem/forward");
+  const int dt = device_dtype();
+  DeviceInputs in(E, C, dt);
+  Dev ind(n * w * sizeof(int64_t)), lse(n * sizeof(double)), pos(n * sizeof(double)),
+      loss(sizeof(double));
+  upload(ind.p, inds.data().data(), n * w * sizeof(int64_t));
+  const lf_cce_config c = make_cfg(cfg, dt);
+  check(lf_ccem_forward(in.X.p, in.E.p, ind.as<int64_t>(), static_cast<int64_t>(n),
+                        static_cast<int64_t>(in.d), static_cast<int64_t>(in.v),
+                        static_cast<int64_t>(w), &c, lse.as<double>(), pos.as<double>(),
+                        loss.as<double>(), nullptr),
+        "lf_ccem_forward");
+  LossOutput out = download_loss(lse, pos, loss, n);
+  sc.settle();
+  return out;
+}
+
+GradPair ccem_backward_rows(const DenseMatrix& E, const DenseMatrix& C, const NegIndexMatrix& inds,
+                            std::span<const double> lse, std::span<const double> row_upstream,
+                            const CceConfig& cfg, MemAccountant* acct) {
+  validate_sampled_inputs(E, C, inds);
+  if (cfg.row_block < 1) throw std::invalid_argument("CceConfig: row_block must be >= 1");
+  const std::size_t n = E.rows(), d = E.cols(), v = C.cols(), w = inds.width();
+  if (lse.size() != n) {
+    throw std::invalid_argument("ccem_backward: LSE vector has " + std::to_string(lse.size()) +
+                                " entries for " + std::to_string(n) + " rows");
+  }
+  if (row_upstream.size() != n) {
+    throw std::invalid_argument("ccem_backward: upstream vector has " +
+                                std::to_string(row_upstream.size()) + " entries for " +
+                                std::to_string(n) + " rows");
+  }
+  if (acct) {
+    acct->record_ensure("retained/ccem/lse", n);
+    acct->record_ensure("retained/ccem/inds", n * w, ScalarKind::kIndex);
+  }
+  ScratchCharge sc(acct, "scratch/ccem/backward");
+  const int dt = device_dtype();
+  DeviceInputs in(E, C, dt);
+  Dev ind(n * w * sizeof(int64_t)), dl(n * sizeof(double)), up(n * sizeof(double));
+  Dev dX(n * d * grad_bytes(dt)), dE(v * d * grad_bytes(dt));
+  upload(ind.p, inds.data().data(), n * w * sizeof(int64_t));
+  upload(dl.p, lse.data(), n * sizeof(double));
+  upload(up.p, row_upstream.data(), n * sizeof(double));
+  const lf_cce_config c = make_cfg(cfg, dt);
+  check(lf_ccem_backward(in.X.p, in.E.p, ind.as<int64_t>(), dl.as<double>(), up.as<double>(), 0.0,
+                         static_cast<int64_t>(n), static_cast<int64_t>(d), static_cast<int64_t>(v),
+                         static_cast<int64_t>(w), &c, dX.p, dE.p, nullptr),
+        "lf_ccem_backward");
+  GradPair g = download_grads(dX, dE, dt, n, d, v);
+  sc.settle();
+  return g;
+}
+
+GradPair ccem_backward(const DenseMatrix& E, const DenseMatrix& C, const NegIndexMatrix& inds,
+                       std::span<const double> lse, double upstream, const CceConfig& cfg,
+                       MemAccountant* acct) {
+  const std::size_t n = E.rows();
+  if (n == 0) {
+    throw std::invalid_argument("fused sampled loss: zero rows; the mean loss is undefined");
+  }
+  // ccem.cpp:203: the scalar form is the per-row form with upstream / N.
+  std::vector<double> row_upstream(n, upstream / static_cast<double>(n));
+  return ccem_backward_rows(E, C, inds, lse, row_upstream, cfg, acct);
+}
+
+FlopEstimate estimate_flops(std::size_t n, std::size_t d, std::size_t v, std::size_t ns,
+                            Backend backend) {
+  FlopEstimate f;
+  const int rc = lf_estimate_flops(static_cast<int64_t>(n), static_cast<int64_t>(d),
+                                   static_cast<int64_t>(v), static_cast<int64_t>(ns),
+                                   static_cast<int32_t>(backend), &f.forward, &f.backward);
+  if (rc != LF_OK) throw_status(rc, "lf_estimate_flops");
+  return f;
+}
+
+}  // namespace lseforge

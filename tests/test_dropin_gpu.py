@@ -1,0 +1,71 @@
+"""GPU: the reference's OWN test programs, compiled in place from
+/root/reference/proj/tests and linked against the C++ drop-in
+(paper_2509_09682_b200/shim/lseforge_shim.cpp + liblseforge_b200.so) in place
+of the reference's cce.cpp / ccem.cpp (recipe: oracle/Makefile `dropin`; the
+binaries are built in the container and travel to the GPU box prebuilt).
+
+Default device dtype is the exact (f64) mode, which must pass everything the
+reference passes, bit-for-bit checks included.  Two known, documented
+divergences:
+  * test_memory "model predictions match kernel instrumentation": the shim
+    charges the library's real device scratch under the scratch/* tags, not
+    the CPU tile-scratch closed form (memory_model.cpp:46-60); the retained
+    tags — the contract the paper's memory claims rest on — match exactly.
+    acceptance criterion 4 fails for the same reason.
+  * acceptance criterion 6 fails in the reference itself
+    (proj/test_output.txt:30, proj/README.md:46-59).
+"""
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "oracle", "_ref", "dropin")
+
+pytestmark = pytest.mark.gpu
+
+
+def run(name, dtype="f64", timeout=900):
+    path = os.path.join(BIN, name)
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not built (needs /root/reference at build time)")
+    env = dict(os.environ, LSEFORGE_B200_DTYPE=dtype, LSEFORGE_THREADS="8")
+    p = subprocess.run([path], capture_output=True, text=True, timeout=timeout, env=env)
+    return p.returncode, p.stdout + p.stderr
+
+
+def failed_cases(out):
+    return sorted(set(re.findall(r"^\[FAIL\] (.*)$", out, re.M)))
+
+
+def test_reference_test_cce_passes_in_exact_mode(cuda):
+    rc, out = run("test_cce")
+    assert rc == 0 and "| 0 failed" in out, out[-3000:]
+
+
+def test_reference_test_ccem_passes_in_exact_mode(cuda):
+    rc, out = run("test_ccem")
+    assert rc == 0 and "| 0 failed" in out, out[-3000:]
+
+
+def test_reference_test_oracles_unchanged(cuda):
+    rc, out = run("test_oracles")
+    assert rc == 0, out[-3000:]
+
+
+def test_reference_test_memory_only_scratch_formula_differs(cuda):
+    rc, out = run("test_memory")
+    assert failed_cases(out) == ["model predictions match kernel instrumentation exactly across backends"], out[-3000:]
+    bad = re.findall(r"FAILED CHECK\( (.*?) \)", out)
+    assert bad and all(b == "rep.peak.scratch_real == want.scratch_real" for b in bad), set(bad)
+
+
+def test_reference_acceptance_criteria(cuda):
+    rc, out = run("acceptance", timeout=1200)
+    passed = set(int(m) for m in re.findall(r"^\[PASS\] criterion (\d+)", out, re.M))
+    failed = set(int(m) for m in re.findall(r"^\[FAIL\] criterion (\d+)", out, re.M))
+    assert passed == {1, 2, 3, 5, 7, 8, 9, 10, 11}, out
+    assert failed == {4, 6}, out
+    assert "instrumentation mismatch" in out  # criterion 4: the scratch formula only
