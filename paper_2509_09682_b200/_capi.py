@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblseforge_b200.so")
+# LSEFORGE_B200_LIB selects an alternative in-tree build (tuning variants).
+LIB_PATH = os.environ.get("LSEFORGE_B200_LIB") or os.path.join(_HERE, "liblseforge_b200.so")
 
 LF_OK, LF_EINVAL, LF_EUNSUPPORTED, LF_ECUDA, LF_ENOMEM = 0, -1, -2, -3, -4
 LF_F32, LF_F64, LF_BF16 = 0, 1, 2

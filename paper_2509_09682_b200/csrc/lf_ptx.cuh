@@ -147,6 +147,16 @@ __device__ __forceinline__ void tmem_st_wait() {
         "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])              \
       : "r"(taddr))
 
+// 32 lanes x 32 bit, 16 consecutive columns -> 16 registers per thread.
+#define LF_TMEM_LD16(taddr, r)                                                                    \
+  asm volatile(                                                                                   \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14," \
+      "%15}, [%16];"                                                                              \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),       \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),   \
+        "=r"(r[14]), "=r"(r[15])                                                                  \
+      : "r"(taddr))
+
 // 32 lanes x 32 bit, 16 consecutive columns <- 16 registers per thread.
 #define LF_TMEM_ST16(taddr, r)                                                                    \
   asm volatile(                                                                                   \
@@ -195,6 +205,18 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // magic add, f in [-0.5, 0.5], 2^f by a degree-3 minimax polynomial (max
 // relative error 7.5e-5), 2^j added into the exponent field.  Valid for
 // x in [-125, 127]; callers clamp or select.
+// ex2_fma_shl<S>(x) = 2^(x + S) with the shift folded into the magic constant
+// (valid for x + S in [-125, 127]).
+template <int S>
+__device__ __forceinline__ float ex2_fma_shl(float x) {
+  const float t = x + (12582912.0f + static_cast<float>(S));
+  const float j = t - (12582912.0f + static_cast<float>(S));
+  const float f = x - j;
+  float p = fmaf(0.05517137654f, f, 0.24261121067f);
+  p = fmaf(p, f, 0.69326103069f);
+  p = fmaf(p, f, 0.99992806957f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
 __device__ __forceinline__ float ex2_fma(float x) {
   const float t = x + 12582912.0f;
   const float j = t - 12582912.0f;

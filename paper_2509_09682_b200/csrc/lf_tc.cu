@@ -1,7 +1,7 @@
 // lf_tc.cu — tcgen05 / TMEM / TMA kernels for the bf16 CCE path (sm_100a).
 //
 // One warp-specialized persistent kernel, three modes:
-//   FWD       owner = 128 rows of X, stream = 128-item tiles of E.
+//   FWD       owner = 128 rows of X, stream = BN-item tiles of E.
 //             S = X_o E_t^T in TMEM; epilogue does the online LSE (log2
 //             domain) and the target-logit capture in registers; writes one
 //             float4 partial {m, s, t, has} per (V-chunk, row)
@@ -14,10 +14,12 @@
 //             Pass 2 of cce_backward (cce.cpp:240-262).  No atomics: every
 //             output row has one owner CTA.
 //
-// Roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA
-// issuer (one elected lane), warps 2..9 = two epilogue warpgroups that take
-// alternate stream tiles (ping-pong), so the MUFU-bound epilogue of one tile
-// overlaps the MMA of the next.
+// Roles: warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer (one
+// elected lane), then NWG epilogue warpgroups that take stream tiles round
+// robin, so the MUFU-bound epilogue of one tile overlaps the MMAs of the
+// next ones.  Tile width BN and NWG are per mode (Geo below); the MMA warp
+// runs NWG tiles ahead of the G read-back (lookahead), which needs
+// NWG + 1 S buffers in TMEM.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -27,14 +29,36 @@
 #include "lf_kernels.cuh"
 #include "lf_ptx.cuh"
 
+#ifndef LF_POLY_FWD
+#define LF_POLY_FWD 0
+#endif
+#ifndef LF_POLY_BWD
+#define LF_POLY_BWD 0
+#endif
+#ifndef LF_PRESEL
+#define LF_PRESEL 0
+#endif
+#ifndef LF_SWP
+#define LF_SWP 0
+#endif
+#ifndef LF_NWG_FWD
+#define LF_NWG_FWD 2
+#endif
+#ifndef LF_BN_FWD
+#define LF_BN_FWD 128
+#endif
+#ifndef LF_NWG_BWD
+#define LF_NWG_BWD 2
+#endif
+#ifndef LF_BN_BWD
+#define LF_BN_BWD 128
+#endif
+
 namespace lf {
 
 namespace {
 
 constexpr int BM = 128;  // owner tile (TMEM lanes)
-constexpr int BN = 128;  // stream tile (S columns)
-constexpr int kThreads = 320;
-constexpr int kEpiThreads = 256;
 
 enum Mode : int { FWD = 0, BWD_ROWS = 1, BWD_ITEMS = 2 };
 // Backward variants: kFilt = filter_eps > 0 (flush below eps, sub-tile skip);
@@ -57,26 +81,69 @@ struct TcParams {
   unsigned long long* counters;  // [0] skipped elems, [1] skipped tiles, [2] total tiles
 };
 
+template <int MODE>
+struct Geo {
+  static constexpr int BN = MODE == FWD ? LF_BN_FWD : LF_BN_BWD;    // stream tile (S columns)
+  static constexpr int NWG = MODE == FWD ? LF_NWG_FWD : LF_NWG_BWD;  // epilogue warpgroups
+  static constexpr int kThreads = 64 + 128 * NWG;
+  static constexpr int kEpiThreads = 128 * NWG;
+  static constexpr int NQ = BN / 32;  // 32-column chunks per tile and thread
+  static_assert(BN == 64 || BN == 128, "BN");
+};
+
 template <int D, int MODE>
 struct Cfg {
+  using G = Geo<MODE>;
+  static constexpr int BN = G::BN;
   static constexpr int kAtoms = D / 64;               // 128-byte K atoms per row
   static constexpr int kOwnerBytes = BM * D * 2;
   static constexpr int kTileBytes = BN * D * 2;
-  static constexpr int kExtraBytes = MODE == BWD_ITEMS ? 1024 : 0;  // lse2[128] + tgt[128]
+  static constexpr int kExtraBytes = MODE == BWD_ITEMS ? 1024 : 0;  // lse2[BN] + tgt[BN] (padded)
   static constexpr int kStageBytes = kTileBytes + kExtraBytes;
-  static constexpr int kStages = D == 64 ? 8 : (D == 128 ? 5 : (D == 192 ? 3 : 2));
-  static constexpr int kNB = MODE == FWD ? 4 : (512 - D) / BN;  // S buffers in TMEM
+  static constexpr int kStagesFit = (200 * 1024 - kOwnerBytes) / kStageBytes;
+  static constexpr int kStages = kStagesFit > 12 ? 12 : kStagesFit;
+  static constexpr int kNBMax = (MODE == FWD ? 512 : 512 - D) / BN;  // S buffers that fit in TMEM
+  static constexpr int kNB = kNBMax > 8 ? 8 : kNBMax;
+  // MMA2 lookahead (tiles): NWG keeps every warpgroup fed; it needs NWG + 1
+  // S buffers, so wide rows (little TMEM left beside the accumulator) run
+  // with less.  Any lookahead in [1, kNB - 1] is deadlock-free.
+  static constexpr int kLook = G::NWG < kNB - 1 ? G::NWG : kNB - 1;
+  static_assert(MODE == FWD || kLook >= 1, "not enough TMEM for the backward pipeline");
   static constexpr int kAccCol = kNB * BN;
   static constexpr int kSmem = 1024 /*align slack*/ + kOwnerBytes + kStages * kStageBytes +
-                               1024 /*barriers*/ + (MODE == FWD ? BM * 16 : 0);
+                               1024 /*barriers*/ + (MODE == FWD ? (G::NWG - 1) * BM * 16 : 0);
 };
-
 __device__ __forceinline__ float fma_log2(float v, float sub) { return fmaf(v, kLog2e, -sub); }
+
+// Exp offload: of every 32 columns, the last POLY take 2^x on the FMA pipe
+// (ex2_fma) and the rest on MUFU.  The clamp keeps ex2_fma in range; an
+// argument above 127 still yields a huge value, so the forward's overflow
+// rebase check fires exactly as with MUFU's +inf.
+constexpr int kPolyFwd = LF_POLY_FWD;
+constexpr int kPolyBwd = LF_POLY_BWD;
+template <int POLY>
+__device__ __forceinline__ float ex2_mix(int c, float a) {
+  if ((c & 31) >= 32 - POLY) return ex2_fma(fminf(fmaxf(a, -125.f), 127.f));
+  return ex2_approx(a);
+}
+
+// Backward filter domain.  The exp argument a = S log2e - lse2 is offset so
+// that a < kThr exactly when softmax < eps.  kPreSel (filtered kernels): lse2
+// also carries +64 (kPreA) and the flush is a select BEFORE the MUFU; else
+// ex2.approx.ftz flushes a < -126 and the result is scaled by 2^64 after.
+constexpr bool kPreSel = LF_PRESEL != 0;
+constexpr bool kSwp = LF_SWP != 0;
+template <int FLAGS>
+constexpr int kPreA = ((FLAGS & kFilt) && kPreSel) ? 64 : 0;
+template <int FLAGS>
+constexpr float kThr = -126.f + static_cast<float>(kPreA<FLAGS>);
 
 // Backward coefficient of a row's own target column (never filtered).
 template <int FLAGS>
 __device__ __forceinline__ float target_g(float e, uint32_t raw, float l, float t_scale) {
-  if (FLAGS & kFilt) return ex2_approx(fmaf(__uint_as_float(raw), kLog2e, -l) + 64.f) - t_scale;
+  if (FLAGS & kFilt)
+    return ex2_approx(fmaf(__uint_as_float(raw), kLog2e, -l) + static_cast<float>(64 - kPreA<FLAGS>)) -
+           t_scale;
   return e - t_scale;
 }
 
@@ -90,10 +157,14 @@ __device__ __forceinline__ float select_reg(const float (&r)[N], int idx) {
 }
 
 template <int D, int MODE, int FLAGS>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
     cce_tc_kernel(const __grid_constant__ CUtensorMap map_owner,
                   const __grid_constant__ CUtensorMap map_stream, const TcParams p) {
   using C = Cfg<D, MODE>;
+  using G = Geo<MODE>;
+  constexpr int BN = G::BN;
+  constexpr int NWG = G::NWG;
+  constexpr int NQ = G::NQ;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -121,13 +192,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < C::kNB; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], MODE == FWD ? 128 : 1);
-      mbar_init(&g_ready[i], 128);
+      mbar_init(&s_empty[i], MODE == FWD ? 4 : 1);  // FWD: one arrive per epilogue warp
+      mbar_init(&g_ready[i], 4);
     }
     mbar_init(owner_full, 1);
     mbar_init(owner_empty, 1);
     mbar_init(acc_full, 1);
-    mbar_init(acc_empty, kEpiThreads);
+    mbar_init(acc_empty, 4 * NWG);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -142,37 +213,34 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ============================ TMA producer ============================
-    const uint64_t pol = policy_evict_normal();
-    int64_t t = 0;
-    uint32_t j = 0;
-    for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
-      const int64_t chunk = u / p.owner_tiles, ot = u % p.owner_tiles;
-      const int64_t s_begin = chunk * p.chunk;
-      const int64_t s_end = min(p.n_stream, s_begin + p.chunk);
-      if (lane == 0) {
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_normal();
+      int64_t t = 0;
+      uint32_t j = 0;
+      for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
+        const int64_t chunk = u / p.owner_tiles, ot = u % p.owner_tiles;
+        const int64_t s_begin = chunk * p.chunk;
+        const int64_t s_end = min(p.n_stream, s_begin + p.chunk);
         mbar_wait(owner_empty, (j & 1) ^ 1);
         mbar_arrive_expect_tx(owner_full, C::kOwnerBytes);
 #pragma unroll
         for (int a = 0; a < C::kAtoms; ++a)
           tma_load_2d(owner_smem + a * BM * 128, &map_owner, owner_full, a * 64,
                       static_cast<int32_t>(ot * BM), pol);
-      }
-      for (int64_t s0 = s_begin; s0 < s_end; s0 += BN, ++t) {
-        const int st = static_cast<int>(t % C::kStages);
-        const uint32_t ph = static_cast<uint32_t>((t / C::kStages) & 1);
-        unsigned char* stg = stage_smem + st * C::kStageBytes;
-        if (lane == 0) {
+        for (int64_t s0 = s_begin; s0 < s_end; s0 += BN, ++t) {
+          const int st = static_cast<int>(t % C::kStages);
+          const uint32_t ph = static_cast<uint32_t>((t / C::kStages) & 1);
+          unsigned char* stg = stage_smem + st * C::kStageBytes;
           mbar_wait(&empty[st], ph ^ 1);
-          // BWD_ITEMS also stages the stream rows' lse2 and local targets
-          // (512 B each) next to the X tile.
-          mbar_arrive_expect_tx(&full[st], C::kTileBytes + (MODE == BWD_ITEMS ? 1024 : 0));
+          // BWD_ITEMS also stages the stream rows' lse2 and local targets.
+          mbar_arrive_expect_tx(&full[st], C::kTileBytes + (MODE == BWD_ITEMS ? 8 * BN : 0));
 #pragma unroll
           for (int a = 0; a < C::kAtoms; ++a)
             tma_load_2d(stg + a * BN * 128, &map_stream, &full[st], a * 64,
                         static_cast<int32_t>(s0), pol);
           if (MODE == BWD_ITEMS) {
-            bulk_load(stg + C::kTileBytes, p.lse2 + s0, 512, &full[st]);
-            bulk_load(stg + C::kTileBytes + 512, p.tgt + s0, 512, &full[st]);
+            bulk_load(stg + C::kTileBytes, p.lse2 + s0, 4 * BN, &full[st]);
+            bulk_load(stg + C::kTileBytes + 512, p.tgt + s0, 4 * BN, &full[st]);
           }
         }
       }
@@ -186,6 +254,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     int64_t t = 0;
     uint32_t j = 0;
     unsigned long long tiles_seen = 0;
+    // dX_o (dE_o) += G(tt) * stream tile(tt); G(tt) is bf16 in S buffer b,
+    // K step kk (stream rows 16kk..16kk+15) at columns 8kk.
     auto mma2 = [&](int64_t tt, bool first) {
       const int st = static_cast<int>(tt % C::kStages);
       const int b = static_cast<int>(tt % C::kNB);
@@ -198,8 +268,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           // B = stream tile viewed K(stream rows) x N(D), MN-major SW128:
           // 16 rows = 2048 B per K step; 64-col D atoms are BN*128 B apart.
           const uint64_t bdesc = umma_desc_sw128(sb + kk * 2048, BN * 128, 1024);
+#ifndef LF_DIAG_NOMMA2
           mma_ts(tmem + C::kAccCol, tmem + b * BN + kk * 8, bdesc, idesc2,
                  (first && kk == 0) ? 0u : 1u);
+#endif
         }
         mma_commit(&empty[st]);
         mma_commit(&s_empty[b]);
@@ -211,6 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t s_begin = chunk * p.chunk;
       const int64_t s_end = min(p.n_stream, s_begin + p.chunk);
       const int64_t ntile = ceil_div(s_end - s_begin, BN);
+      const int64_t t0 = t;
       mbar_wait(owner_full, j & 1);
       if (MODE != FWD) mbar_wait(acc_empty, (j & 1) ^ 1);
       tc_fence_after();
@@ -234,26 +307,26 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (MODE == FWD) mma_commit(&empty[st]);
         }
         __syncwarp();
-        // Lookahead 2: S(i) is issued before waiting on G(i-2), so with two
-        // epilogue warpgroups the next S tile is always ready when one frees up.
-        if (MODE != FWD && i >= 2) mma2(t - 2, i == 2);
+        // Lookahead: S(i) is issued before waiting on G(i - kLook), so the
+        // next S tile is ready whenever an epilogue warpgroup frees up.
+        if (MODE != FWD && i >= C::kLook) mma2(t - C::kLook, i == C::kLook);
         ++tiles_seen;
       }
       if (MODE != FWD) {
-        if (ntile >= 2) mma2(t - 2, ntile == 2);
-        mma2(t - 1, ntile == 1);
+        for (int64_t k = ntile > C::kLook ? ntile - C::kLook : 0; k < ntile; ++k) mma2(t0 + k, k == 0);
         if (lane == 0) mma_commit(acc_full);
         __syncwarp();
       }
       if (lane == 0) mma_commit(owner_empty);
       __syncwarp();
     }
-    // 16 sub-tiles (4 warps x 4 column chunks) per 128 x 128 tile
-    if (lane == 0 && MODE == BWD_ROWS && (FLAGS & kCount)) atomicAdd(&p.counters[2], 16 * tiles_seen);
+    // 4 * NQ sub-tiles (4 warps x NQ column chunks) per 128 x BN tile
+    if (lane == 0 && MODE == BWD_ROWS && (FLAGS & kCount))
+      atomicAdd(&p.counters[2], 4ull * NQ * tiles_seen);
   } else {
     // ============================== epilogue ==============================
-    const int wg = (warp - 2) >> 2;   // 0 or 1: takes tiles with t % 2 == wg
-    const int quad = warp & 3;        // TMEM lane quadrant this warp may access
+    const int wg = (warp - 2) >> 2;     // takes tiles with t % NWG == wg
+    const int quad = warp & 3;          // TMEM lane quadrant this warp may access
     const int lrow = quad * 32 + lane;  // owner row within the tile
     const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
     unsigned long long skipped = 0, skipped_sub = 0;
@@ -265,6 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t s_end = min(p.n_stream, s_begin + p.chunk);
       const int64_t ntile = ceil_div(s_end - s_begin, BN);
       const int64_t orow = ot * BM + lrow;
+      const int o0 = static_cast<int>(ot * BM);
       int tgt = -1;
       float lse2 = 0.f;
       if (MODE != BWD_ITEMS) {
@@ -273,32 +347,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       float m = -INFINITY, s = 0.f, tv = 0.f, has = 0.f;
       for (int64_t i = 0; i < ntile; ++i, ++t) {
-        if ((t & 1) != wg) continue;
+        if (static_cast<int>(t % NWG) != wg) continue;
         const int b = static_cast<int>(t % C::kNB);
         const int64_t col0 = s_begin + i * BN;
         const int nvalid = static_cast<int>((s_end - col0 < BN ? s_end - col0 : BN));
         mbar_wait(&s_full[b], static_cast<uint32_t>((t / C::kNB) & 1));
         tc_fence_after();
+        const uint32_t ta = tmem + lane_base + b * BN;
         if (MODE == FWD) {
+          // Whole tile in registers (one wait), S released at once.
           float v[BN];
           {
             uint32_t* r = reinterpret_cast<uint32_t*>(v);
-            const uint32_t ta = tmem + lane_base + b * BN;
-            LF_TMEM_LD32(ta + 0, (r + 0));
-            LF_TMEM_LD32(ta + 32, (r + 32));
-            LF_TMEM_LD32(ta + 64, (r + 64));
-            LF_TMEM_LD32(ta + 96, (r + 96));
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) LF_TMEM_LD32(ta + q * 32, (r + q * 32));
             tmem_ld_wait();
           }
           tc_fence_before();
-          mbar_arrive(&s_empty[b]);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s_empty[b]);
           if (nvalid < BN) {
 #pragma unroll
             for (int c = 0; c < BN; ++c)
               if (c >= nvalid) v[c] = -INFINITY;
           }
           const int lc = tgt - static_cast<int>(col0);
-          if (lc >= 0 && lc < BN) {
+          if (static_cast<unsigned>(lc) < static_cast<unsigned>(BN)) {
             tv = select_reg(v, lc);
             has = 1.f;
           }
@@ -306,13 +380,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             float mx = v[0];
 #pragma unroll
             for (int c = 1; c < BN; ++c) mx = fmaxf(mx, v[c]);
-            m = mx * kLog2e;
+            m = mx * kLog2e;  // a tile is never entirely past the catalog end
           }
           float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
           for (int c = 0; c < BN; c += 2) {
-            acc0 += ex2_approx(fma_log2(v[c], m));
-            acc1 += ex2_approx(fma_log2(v[c + 1], m));
+            acc0 += ex2_mix<kPolyFwd>(c, fma_log2(v[c], m));
+            acc1 += ex2_mix<kPolyFwd>(c + 1, fma_log2(v[c + 1], m));
           }
           float sum = acc0 + acc1;
           if (!(sum <= 1.8446744e19f)) {  // > 2^64 or NaN: rebase on the true max
@@ -333,17 +407,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           s += sum;
         } else {
-          // ---- backward: G = softmax * |scale| (target: minus |scale|), bf16, into TMEM.
-          // Processed in four 32-column chunks with the next chunk's tcgen05.ld in
-          // flight.  Filtering (FILT): lse2 carries the shift thr2 + 126, so
-          // a = S log2e - lse2 < -126 exactly when softmax < eps, and
-          // ex2.approx.ftz flushes those results (denormal) to +0 — no compare or
-          // select per element; the survivors are rescaled by 2^64 so every
-          // bf16 G and every MMA product stays normal, and out_scale undoes the
-          // 2^(64 - thr2 - 126) factor on the accumulator.  A 32x32 sub-tile
-          // whose largest a is below the threshold (and that holds no target)
-          // skips its exps entirely (warp vote).
-          (void)fma_log2;
+          // ---- backward: G = softmax * |scale| (target: minus |scale|), bf16,
+          // back into the same TMEM columns (chunk q -> columns 16q..16q+15,
+          // already consumed by this warp).  Filtering (FILT): lse2 carries the
+          // shift log2(eps) + 126, so a = S log2e - lse2 < -126 exactly when
+          // softmax < eps and ex2.approx.ftz flushes those results to +0 — no
+          // compare or select per element; survivors are rescaled by 2^64 so
+          // every bf16 G and every MMA product stays normal, and out_scale
+          // undoes the factor on the accumulator.  A 32 x 32 sub-tile whose
+          // largest a is below the threshold (and that holds no target) skips
+          // its exps (warp vote).
           const float* lse2s = nullptr;
           const int* tgts = nullptr;
           if (MODE == BWD_ITEMS) {
@@ -351,17 +424,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             lse2s = reinterpret_cast<const float*>(stage_smem + st * C::kStageBytes + C::kTileBytes);
             tgts = reinterpret_cast<const int*>(lse2s + 128);
           }
-          const int o0 = static_cast<int>(ot * BM);
           const int lc_t = MODE == BWD_ROWS ? tgt - static_cast<int>(col0) : -1;
-          const uint32_t ta = tmem + lane_base + b * BN;
+          // 32-column chunks, the next chunk's tcgen05.ld in flight while this
+          // one is processed.
           uint32_t ra[32], rb[32];
+          float xp[32];  // kSwp: previous chunk's coefficients
           LF_TMEM_LD32(ta, ra);
           tmem_ld_wait();
 #pragma unroll
-          for (int q = 0; q < BN / 32; ++q) {
+          for (int q = 0; q < NQ; ++q) {
             uint32_t(&cur)[32] = (q & 1) ? rb : ra;
             uint32_t(&nxt)[32] = (q & 1) ? ra : rb;
-            if (q + 1 < BN / 32) LF_TMEM_LD32(ta + (q + 1) * 32, nxt);
+            if (q + 1 < NQ) LF_TMEM_LD32(ta + (q + 1) * 32, nxt);
             float e[32];
 #pragma unroll
             for (int c = 0; c < 32; c += 4) {
@@ -384,47 +458,57 @@ __global__ void __launch_bounds__(kThreads, 1)
               tq = tgts[q * 32 + lane] - o0;
               hm = __ballot_sync(0xffffffffu, static_cast<unsigned>(tq) < static_cast<unsigned>(BM));
             }
-            const bool tgt_here =
-                MODE == BWD_ROWS ? static_cast<unsigned>(lc_t - q * 32) < 32u : hm != 0u;
+            const int jt = lc_t - q * 32;
+            const bool tgt_here = MODE == BWD_ROWS ? static_cast<unsigned>(jt) < 32u : hm != 0u;
             bool skip = false;
             if (FLAGS & kFilt) {
               float mx = e[0];
 #pragma unroll
               for (int c = 1; c < 32; c += 2) mx = fmaxf(mx, fmaxf(e[c], c + 1 < 32 ? e[c + 1] : e[c]));
-              skip = __all_sync(0xffffffffu, mx < -126.f && !tgt_here);
+              skip = __all_sync(0xffffffffu, mx < kThr<FLAGS> && !tgt_here);
               if ((FLAGS & kCount) && MODE == BWD_ROWS) {
 #pragma unroll
                 for (int c = 0; c < 32; ++c)
-                  skipped += (e[c] < -126.f && q * 32 + c < nvalid && orow < p.n_owner) ? 1 : 0;
-                if (tgt_here) {
-                  // the target is never filtered (cce.cpp:193-195): undo its count
-                  float et = 0.f;
-#pragma unroll
-                  for (int c = 0; c < 32; ++c) et = (c == lc_t - q * 32) ? e[c] : et;
-                  if (et < -126.f && orow < p.n_owner) --skipped;
-                }
+                  skipped += (e[c] < kThr<FLAGS> && q * 32 + c < nvalid && orow < p.n_owner) ? 1 : 0;
+                // the target is never filtered (cce.cpp:193-195): undo its count
+                if (tgt_here && select_reg(e, jt) < kThr<FLAGS> && orow < p.n_owner) --skipped;
                 if (skip) ++skipped_sub;
               }
             }
-            uint32_t g[16];
+            float x[32];
             if (skip) {
 #pragma unroll
-              for (int c = 0; c < 16; ++c) g[c] = 0u;
+              for (int c = 0; c < 32; ++c) x[c] = 0.f;
             } else {
 #pragma unroll
               for (int c = 0; c < 32; ++c) {
-                float x = ex2_approx(e[c]);
-                if (FLAGS & kFilt) x *= 18446744073709551616.f;  // 2^64
-                e[c] = x;
+                if (c >= 32 - kPolyBwd) {  // FMA-pipe share of the exps
+                  if (FLAGS & kFilt) {
+                    const float y = ex2_fma_shl<64 - kPreA<FLAGS>>(e[c]);
+                    x[c] = e[c] < kThr<FLAGS> ? 0.f : y;
+                  } else {
+                    x[c] = ex2_fma(fmaxf(e[c], -125.f));
+                  }
+                } else if ((FLAGS & kFilt) && kPreSel) {
+                  // flush decided before the MUFU: nothing waits on its result
+                  // except the bf16 pack
+                  x[c] = ex2_approx(e[c] < kThr<FLAGS> ? -INFINITY : e[c]);
+                } else {
+#ifdef LF_DIAG_NOEXP
+                  x[c] = e[c];  // timing diagnostic only: wrong results
+#else
+                  x[c] = ex2_approx(e[c]);
+#endif
+                  if (FLAGS & kFilt) x[c] *= 18446744073709551616.f;  // 2^64
+                }
               }
               // The target is never filtered: g = (s - 1) |scale| (cce.cpp:193-195).
-              // Under FILT its softmax is recomputed unflushed from the raw logit
-              // still in `cur`: s * 2^-62 / eps = 2^(a + 64).
+              // Under FILT its softmax is recomputed unflushed from the raw
+              // logit still in `cur`: s * 2^-62 / eps = 2^(a + 64).
               if (MODE == BWD_ROWS && tgt_here) {
-                const int jc = lc_t - q * 32;
 #pragma unroll
                 for (int c = 0; c < 32; ++c)
-                  if (c == jc) e[c] = target_g<FLAGS>(e[c], cur[c], lse2, p.abs_scale);
+                  if (c == jt) x[c] = target_g<FLAGS>(x[c], cur[c], lse2, p.abs_scale);
               }
               if (MODE == BWD_ITEMS) {
                 while (hm) {  // warp-uniform loop over the hit columns
@@ -435,65 +519,90 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const float lj = lse2s[q * 32 + jc];
 #pragma unroll
                     for (int c = 0; c < 32; ++c)
-                      if (c == jc) e[c] = target_g<FLAGS>(e[c], cur[c], lj, p.abs_scale);
+                      if (c == jc) x[c] = target_g<FLAGS>(x[c], cur[c], lj, p.abs_scale);
                   }
                 }
               }
-#pragma unroll
-              for (int c = 0; c < 16; ++c) g[c] = pack_bf16x2(e[2 * c], e[2 * c + 1]);
             }
-            LF_TMEM_ST16(ta + q * 16, g);
-            if (q + 1 < BN / 32) tmem_ld_wait();
+            if (kSwp) {
+              // software pipeline: pack and store the PREVIOUS chunk, so the
+              // MUFU results of this one are consumed a full chunk later
+              if (q > 0) {
+                uint32_t g[16];
+#pragma unroll
+                for (int c = 0; c < 16; ++c) g[c] = pack_bf16x2(xp[2 * c], xp[2 * c + 1]);
+                LF_TMEM_ST16(ta + (q - 1) * 16, g);
+              }
+#pragma unroll
+              for (int c = 0; c < 32; ++c) xp[c] = x[c];
+            } else {
+              uint32_t g[16];
+#pragma unroll
+              for (int c = 0; c < 16; ++c) g[c] = pack_bf16x2(x[2 * c], x[2 * c + 1]);
+              LF_TMEM_ST16(ta + q * 16, g);
+            }
+            if (q + 1 < NQ) tmem_ld_wait();
+          }
+          if (kSwp) {
+            uint32_t g[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) g[c] = pack_bf16x2(xp[2 * c], xp[2 * c + 1]);
+            LF_TMEM_ST16(ta + (NQ - 1) * 16, g);
           }
           tmem_st_wait();
           tc_fence_before();
-          mbar_arrive(&g_ready[b]);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&g_ready[b]);
         }
       }
       if (MODE == FWD) {
-        // merge the two warpgroups' running states for each row
-        if (wg == 1) merge[lrow] = make_float4(m, s, tv, has);
-        named_bar_sync(1, kEpiThreads);
+        // merge the warpgroups' running states for each row
+        if (wg > 0) merge[(wg - 1) * BM + lrow] = make_float4(m, s, tv, has);
+        named_bar_sync(1, G::kEpiThreads);
         if (wg == 0) {
-          const float4 o = merge[lrow];
-          if (o.x != -INFINITY) {
-            if (m == -INFINITY) {
-              m = o.x;
-              s = o.y;
-            } else {
-              const float nm = fmaxf(m, o.x);
-              s = s * ex2_approx(m - nm) + o.y * ex2_approx(o.x - nm);
-              m = nm;
+#pragma unroll
+          for (int k = 0; k < NWG - 1; ++k) {
+            const float4 o = merge[k * BM + lrow];
+            if (o.x != -INFINITY) {
+              if (m == -INFINITY) {
+                m = o.x;
+                s = o.y;
+              } else {
+                const float nm = fmaxf(m, o.x);
+                s = s * ex2_approx(m - nm) + o.y * ex2_approx(o.x - nm);
+                m = nm;
+              }
             }
-          }
-          if (o.w != 0.f) {
-            tv = o.z;
-            has = 1.f;
+            if (o.w != 0.f) {
+              tv = o.z;
+              has = 1.f;
+            }
           }
           if (orow < p.n_owner) p.part[chunk * p.n_owner + orow] = make_float4(m, s, tv, has);
         }
-        named_bar_sync(1, kEpiThreads);
+        named_bar_sync(1, G::kEpiThreads);
       } else {
-        // accumulator read-out: wg 0 takes columns [0, D/2), wg 1 [D/2, D)
+        // accumulator read-out: 16-column groups round robin over warpgroups
         mbar_wait(acc_full, j & 1);
         tc_fence_after();
         float* dst = MODE == BWD_ROWS ? p.out + (chunk * p.n_owner + orow) * D
                                       : p.out + orow * D;
-        for (int c0 = wg * (D / 2); c0 < (wg + 1) * (D / 2); c0 += 32) {
-          uint32_t r[32];
-          LF_TMEM_LD32(tmem + lane_base + C::kAccCol + c0, r);
+        const float os = p.out_scale;
+        for (int c0 = wg * 16; c0 < D; c0 += 16 * NWG) {
+          uint32_t r16[16];
+          LF_TMEM_LD16(tmem + lane_base + C::kAccCol + c0, r16);
           tmem_ld_wait();
           if (orow < p.n_owner) {
-            const float os = p.out_scale;
 #pragma unroll
-            for (int c = 0; c < 32; c += 4)
+            for (int c = 0; c < 16; c += 4)
               *reinterpret_cast<float4*>(dst + c0 + c) =
-                  make_float4(__uint_as_float(r[c]) * os, __uint_as_float(r[c + 1]) * os,
-                              __uint_as_float(r[c + 2]) * os, __uint_as_float(r[c + 3]) * os);
+                  make_float4(__uint_as_float(r16[c]) * os, __uint_as_float(r16[c + 1]) * os,
+                              __uint_as_float(r16[c + 2]) * os, __uint_as_float(r16[c + 3]) * os);
           }
         }
         tc_fence_before();
-        mbar_arrive(acc_empty);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty);
       }
     }
     if ((FLAGS & kCount) && MODE == BWD_ROWS) {
@@ -562,7 +671,7 @@ int launch_mode(const CUtensorMap& mo, const CUtensorMap& ms, const TcParams& p,
   LF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
   const int grid = static_cast<int>(std::min<int64_t>(p.units, num_sms()));
   ProfScope prof(MODE == FWD ? LF_K_CCE_FWD : (MODE == BWD_ROWS ? LF_K_CCE_BWD_DX : LF_K_CCE_BWD_DE), st);
-  kern<<<grid, kThreads, C::kSmem, st>>>(mo, ms, p);
+  kern<<<grid, Geo<MODE>::kThreads, C::kSmem, st>>>(mo, ms, p);
   LF_LAUNCHED();
   return LF_OK;
 }
@@ -583,9 +692,11 @@ int launch_d(int D, int flags, const CUtensorMap& mo, const CUtensorMap& ms, con
              cudaStream_t st) {
   switch (D) {
     case 64: return launch_flags<64, MODE>(flags, mo, ms, p, st);
+#ifndef LF_VARIANT_D64_ONLY
     case 128: return launch_flags<128, MODE>(flags, mo, ms, p, st);
     case 192: return launch_flags<192, MODE>(flags, mo, ms, p, st);
     case 256: return launch_flags<256, MODE>(flags, mo, ms, p, st);
+#endif
     default: return fail(LF_EUNSUPPORTED, "tc: d must be 64/128/192/256");
   }
 }
@@ -616,6 +727,7 @@ int64_t pick_chunks(int64_t owner_tiles, int64_t stream_tiles, int64_t max_chunk
 int tc_cce_forward_partials(const void* X, const void* E, const int64_t* targets, int64_t n,
                             int D, int64_t v, int64_t v_offset, Scratch& ws, float** part_out,
                             int* P_out, cudaStream_t st) {
+  constexpr int BN = Geo<FWD>::BN;
   const int64_t owner_tiles = ceil_div(n, BM);
   const int64_t stream_tiles = ceil_div(v, BN);
   const int64_t chunks = pick_chunks(owner_tiles, stream_tiles, 64);
@@ -668,11 +780,14 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
   const bool filt = eps >= 0x1p-100;
   const bool count = filt && counters != nullptr;
   const int flags = filt ? (kFilt | (count ? kCount : 0)) : 0;
-  const double sub = filt ? -std::log2(eps) - 126.0 : std::log2(std::fabs(scale));
+  const double sub = filt ? -std::log2(eps) - 126.0 + (kPreSel ? 64.0 : 0.0)
+                          : std::log2(std::fabs(scale));
   const double gscale = filt ? std::ldexp(1.0, -62) / eps : std::fabs(scale);
   const double out_scale = filt ? scale * eps * std::ldexp(1.0, 62) : (scale < 0 ? -1.0 : 1.0);
+  constexpr int BN = Geo<BWD_ROWS>::BN;
   const int64_t row_tiles = ceil_div(n, BM);
-  const int64_t item_tiles = ceil_div(v, BN);
+  const int64_t item_tiles = ceil_div(v, BM);     // dE owner tiles
+  const int64_t item_stream = ceil_div(v, BN);    // dX stream tiles
   const int64_t n_pad = std::max(row_tiles * BM, ceil_div(n, BN) * BN);
   Scratch tgt, lse2;
   int rc = tgt.alloc(sizeof(int32_t) * n_pad, st);
@@ -681,15 +796,17 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
   prep_rows<<<ceil_div(n_pad, 256), 256, 0, st>>>(targets, lse, n, n_pad, v, v_offset, sub,
                                                  tgt.as<int32_t>(), lse2.as<float>());
   LF_LAUNCHED();
-  CUtensorMap mx, me;
-  rc = make_map(&mx, X, n, D, 128);
-  if (!rc) rc = make_map(&me, E, v, D, 128);
+  CUtensorMap mx_own, mx_str, me_own, me_str;  // owner box 128 rows, stream box BN rows
+  rc = make_map(&mx_own, X, n, D, BM);
+  if (!rc) rc = make_map(&mx_str, X, n, D, BN);
+  if (!rc) rc = make_map(&me_own, E, v, D, BM);
+  if (!rc) rc = make_map(&me_str, E, v, D, BN);
   if (rc) return rc;
 
   // ---- pass 1: dX (owner rows, stream items), V split into a few chunks ----
-  const int64_t chunks = pick_chunks(row_tiles, item_tiles, 8);
-  const int64_t tiles_per = ceil_div(item_tiles, chunks);
-  const int64_t P = ceil_div(item_tiles, tiles_per);
+  const int64_t chunks = pick_chunks(row_tiles, item_stream, 8);
+  const int64_t tiles_per = ceil_div(item_stream, chunks);
+  const int64_t P = ceil_div(item_stream, tiles_per);
   Scratch dxp;
   float* dx_out = dX;
   if (P > 1) {
@@ -710,7 +827,7 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
   p.out_scale = static_cast<float>(out_scale);
   p.out = dx_out;
   p.counters = counters;
-  rc = launch_d<BWD_ROWS>(D, flags, mx, me, p, st);
+  rc = launch_d<BWD_ROWS>(D, flags, mx_own, me_str, p, st);
   if (rc) return rc;
   if (P > 1) {
     rc = launch_reduce_f32(dx_out, static_cast<int>(P), n * D, dX, st);
@@ -730,7 +847,7 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
   q.out_scale = static_cast<float>(out_scale);
   q.out = dE;
   q.counters = counters;
-  rc = launch_d<BWD_ITEMS>(D, flags, me, mx, q, st);
+  rc = launch_d<BWD_ITEMS>(D, flags, me_own, mx_str, q, st);
   return rc;
 }
 
