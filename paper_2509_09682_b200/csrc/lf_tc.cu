@@ -81,14 +81,28 @@ struct TcParams {
   unsigned long long* counters;  // [0] skipped elems, [1] skipped tiles, [2] total tiles
 };
 
+// Position + phase in an N-slot mbarrier ring.
+template <int N>
+struct Ring {
+  uint32_t i = 0, ph = 0;
+  __device__ __forceinline__ void next() {
+    if (++i == N) {
+      i = 0;
+      ph ^= 1;
+    }
+  }
+};
+
 template <int MODE>
 struct Geo {
   static constexpr int BN = MODE == FWD ? LF_BN_FWD : LF_BN_BWD;    // stream tile (S columns)
   static constexpr int NWG = MODE == FWD ? LF_NWG_FWD : LF_NWG_BWD;  // epilogue warpgroups
-  static constexpr int kThreads = 64 + 128 * NWG;
+  // control warps: TMA producer, S-MMA issuer (+ the G-MMA issuer in the backward)
+  static constexpr int kCtrlWarps = MODE == FWD ? 2 : 3;
+  static constexpr int kThreads = 32 * kCtrlWarps + 128 * NWG;
   static constexpr int kEpiThreads = 128 * NWG;
   static constexpr int NQ = BN / 32;  // 32-column chunks per tile and thread
-  static_assert(BN == 64 || BN == 128, "BN");
+  static_assert(BN % 32 == 0 && BN >= 64 && BN <= 128, "BN");
 };
 
 template <int D, int MODE>
@@ -104,11 +118,7 @@ struct Cfg {
   static constexpr int kStages = kStagesFit > 12 ? 12 : kStagesFit;
   static constexpr int kNBMax = (MODE == FWD ? 512 : 512 - D) / BN;  // S buffers that fit in TMEM
   static constexpr int kNB = kNBMax > 8 ? 8 : kNBMax;
-  // MMA2 lookahead (tiles): NWG keeps every warpgroup fed; it needs NWG + 1
-  // S buffers, so wide rows (little TMEM left beside the accumulator) run
-  // with less.  Any lookahead in [1, kNB - 1] is deadlock-free.
-  static constexpr int kLook = G::NWG < kNB - 1 ? G::NWG : kNB - 1;
-  static_assert(MODE == FWD || kLook >= 1, "not enough TMEM for the backward pipeline");
+  static_assert(MODE == FWD || kNB >= 2, "not enough TMEM for the backward pipeline");
   static constexpr int kAccCol = kNB * BN;
   static constexpr int kSmem = 1024 /*align slack*/ + kOwnerBytes + kStages * kStageBytes +
                                1024 /*barriers*/ + (MODE == FWD ? (G::NWG - 1) * BM * 16 : 0);
@@ -215,7 +225,7 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
     // ============================ TMA producer ============================
     if (lane == 0) {
       const uint64_t pol = policy_evict_normal();
-      int64_t t = 0;
+      Ring<C::kStages> rs;
       uint32_t j = 0;
       for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
         const int64_t chunk = u / p.owner_tiles, ot = u % p.owner_tiles;
@@ -227,95 +237,62 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
         for (int a = 0; a < C::kAtoms; ++a)
           tma_load_2d(owner_smem + a * BM * 128, &map_owner, owner_full, a * 64,
                       static_cast<int32_t>(ot * BM), pol);
-        for (int64_t s0 = s_begin; s0 < s_end; s0 += BN, ++t) {
-          const int st = static_cast<int>(t % C::kStages);
-          const uint32_t ph = static_cast<uint32_t>((t / C::kStages) & 1);
-          unsigned char* stg = stage_smem + st * C::kStageBytes;
-          mbar_wait(&empty[st], ph ^ 1);
+        for (int64_t s0 = s_begin; s0 < s_end; s0 += BN, rs.next()) {
+          unsigned char* stg = stage_smem + rs.i * C::kStageBytes;
+          mbar_wait(&empty[rs.i], rs.ph ^ 1);
           // BWD_ITEMS also stages the stream rows' lse2 and local targets.
-          mbar_arrive_expect_tx(&full[st], C::kTileBytes + (MODE == BWD_ITEMS ? 8 * BN : 0));
+          mbar_arrive_expect_tx(&full[rs.i], C::kTileBytes + (MODE == BWD_ITEMS ? 8 * BN : 0));
 #pragma unroll
           for (int a = 0; a < C::kAtoms; ++a)
-            tma_load_2d(stg + a * BN * 128, &map_stream, &full[st], a * 64,
+            tma_load_2d(stg + a * BN * 128, &map_stream, &full[rs.i], a * 64,
                         static_cast<int32_t>(s0), pol);
           if (MODE == BWD_ITEMS) {
-            bulk_load(stg + C::kTileBytes, p.lse2 + s0, 4 * BN, &full[st]);
-            bulk_load(stg + C::kTileBytes + 512, p.tgt + s0, 4 * BN, &full[st]);
+            bulk_load(stg + C::kTileBytes, p.lse2 + s0, 4 * BN, &full[rs.i]);
+            bulk_load(stg + C::kTileBytes + 512, p.tgt + s0, 4 * BN, &full[rs.i]);
           }
         }
       }
     }
   } else if (warp == 1) {
-    // ============================= MMA issuer =============================
+    // =========================== MMA issuer: S ===========================
+    // S(t) = owner . stream(t)^T into S buffer b1.  Kept lean (ring cursors,
+    // split descriptors): this warp shares its SM sub-partition with
+    // epilogue warps.  In the backward the G.stream MMAs are issued by a
+    // second warp, so the commit that frees an S buffer never tracks the S
+    // MMA just issued here, and consecutive S MMAs never wait on each other.
     constexpr uint32_t idesc1 = idesc_bf16(BM, BN, 0, 0);
-    constexpr uint32_t idesc2 = idesc_bf16(BM, D, 0, 1);
-    const uint32_t owner_addr = smem_u32(owner_smem);
-    const uint32_t stage_addr = smem_u32(stage_smem);
-    int64_t t = 0;
+    constexpr uint32_t hi = umma_desc_hi_sw128(1024);
+    const uint32_t a_lo = umma_desc_lo(smem_u32(owner_smem), 16);
+    const uint32_t b_lo = umma_desc_lo(smem_u32(stage_smem), 16);
+    Ring<C::kStages> s1;
+    Ring<C::kNB> b1;
     uint32_t j = 0;
     unsigned long long tiles_seen = 0;
-    // dX_o (dE_o) += G(tt) * stream tile(tt); G(tt) is bf16 in S buffer b,
-    // K step kk (stream rows 16kk..16kk+15) at columns 8kk.
-    auto mma2 = [&](int64_t tt, bool first) {
-      const int st = static_cast<int>(tt % C::kStages);
-      const int b = static_cast<int>(tt % C::kNB);
-      mbar_wait(&g_ready[b], static_cast<uint32_t>((tt / C::kNB) & 1));
-      tc_fence_after();
-      if (lane == 0) {
-        const uint32_t sb = stage_addr + st * C::kStageBytes;
-#pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk) {
-          // B = stream tile viewed K(stream rows) x N(D), MN-major SW128:
-          // 16 rows = 2048 B per K step; 64-col D atoms are BN*128 B apart.
-          const uint64_t bdesc = umma_desc_sw128(sb + kk * 2048, BN * 128, 1024);
-#ifndef LF_DIAG_NOMMA2
-          mma_ts(tmem + C::kAccCol, tmem + b * BN + kk * 8, bdesc, idesc2,
-                 (first && kk == 0) ? 0u : 1u);
-#endif
-        }
-        mma_commit(&empty[st]);
-        mma_commit(&s_empty[b]);
-      }
-      __syncwarp();
-    };
     for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
       const int64_t chunk = u / p.owner_tiles;
       const int64_t s_begin = chunk * p.chunk;
       const int64_t s_end = min(p.n_stream, s_begin + p.chunk);
-      const int64_t ntile = ceil_div(s_end - s_begin, BN);
-      const int64_t t0 = t;
+      const int ntile = static_cast<int>(ceil_div(s_end - s_begin, BN));
       mbar_wait(owner_full, j & 1);
-      if (MODE != FWD) mbar_wait(acc_empty, (j & 1) ^ 1);
       tc_fence_after();
-      for (int64_t i = 0; i < ntile; ++i, ++t) {
-        const int st = static_cast<int>(t % C::kStages);
-        const int b = static_cast<int>(t % C::kNB);
-        mbar_wait(&full[st], static_cast<uint32_t>((t / C::kStages) & 1));
-        mbar_wait(&s_empty[b], static_cast<uint32_t>(((t / C::kNB) & 1) ^ 1));
+      for (int i = 0; i < ntile; ++i, s1.next(), b1.next()) {
+        mbar_wait(&full[s1.i], s1.ph);
+        mbar_wait(&s_empty[b1.i], b1.ph ^ 1);
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t sb = stage_addr + st * C::kStageBytes;
+          const uint32_t lo = b_lo + s1.i * (C::kStageBytes >> 4);
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
             const uint32_t koff = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
             const uint32_t koffb = (kk >> 2) * (BN * 128) + (kk & 3) * 32;
-            const uint64_t adesc = umma_desc_sw128(owner_addr + koff, 16, 1024);
-            const uint64_t bdesc = umma_desc_sw128(sb + koffb, 16, 1024);
-            mma_ss(tmem + b * BN, adesc, bdesc, idesc1, kk > 0 ? 1u : 0u);
+            mma_ss(tmem + b1.i * BN, umma_desc(a_lo + (koff >> 4), hi),
+                   umma_desc(lo + (koffb >> 4), hi), idesc1, kk > 0 ? 1u : 0u);
           }
-          mma_commit(&s_full[b]);
-          if (MODE == FWD) mma_commit(&empty[st]);
+          mma_commit(&s_full[b1.i]);
+          if (MODE == FWD) mma_commit(&empty[s1.i]);
         }
         __syncwarp();
-        // Lookahead: S(i) is issued before waiting on G(i - kLook), so the
-        // next S tile is ready whenever an epilogue warpgroup frees up.
-        if (MODE != FWD && i >= C::kLook) mma2(t - C::kLook, i == C::kLook);
         ++tiles_seen;
-      }
-      if (MODE != FWD) {
-        for (int64_t k = ntile > C::kLook ? ntile - C::kLook : 0; k < ntile; ++k) mma2(t0 + k, k == 0);
-        if (lane == 0) mma_commit(acc_full);
-        __syncwarp();
       }
       if (lane == 0) mma_commit(owner_empty);
       __syncwarp();
@@ -323,14 +300,54 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
     // 4 * NQ sub-tiles (4 warps x NQ column chunks) per 128 x BN tile
     if (lane == 0 && MODE == BWD_ROWS && (FLAGS & kCount))
       atomicAdd(&p.counters[2], 4ull * NQ * tiles_seen);
+  } else if (MODE != FWD && warp == 2) {
+    // ==================== MMA issuer: G . stream (backward) ====================
+    // acc (dX_o or dE_o) += G(t) . stream(t): G is bf16 in S buffer b2, K step
+    // kk (stream rows 16kk..16kk+15) at columns 8kk; B = the stream tile viewed
+    // K(stream rows) x N(D), MN-major SW128: 16 rows = 2048 B per K step, 64-col
+    // D atoms BN*128 B apart.  Its commits free the stage and the S buffer.
+    constexpr uint32_t idesc2 = idesc_bf16(BM, D, 0, 1);
+    constexpr uint32_t hi = umma_desc_hi_sw128(1024);
+    const uint32_t b2_lo = umma_desc_lo(smem_u32(stage_smem), BN * 128);
+    Ring<C::kStages> s2;
+    Ring<C::kNB> b2;
+    uint32_t j = 0;
+    for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
+      const int64_t chunk = u / p.owner_tiles;
+      const int64_t s_begin = chunk * p.chunk;
+      const int64_t s_end = min(p.n_stream, s_begin + p.chunk);
+      const int ntile = static_cast<int>(ceil_div(s_end - s_begin, BN));
+      mbar_wait(acc_empty, (j & 1) ^ 1);
+      for (int i = 0; i < ntile; ++i, s2.next(), b2.next()) {
+        mbar_wait(&g_ready[b2.i], b2.ph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t lo = b2_lo + s2.i * (C::kStageBytes >> 4);
+#pragma unroll
+          for (int kk = 0; kk < BN / 16; ++kk) {
+#ifndef LF_DIAG_NOMMA2
+            mma_ts(tmem + C::kAccCol, tmem + b2.i * BN + kk * 8, umma_desc(lo + kk * 128, hi), idesc2,
+                   (i == 0 && kk == 0) ? 0u : 1u);
+#endif
+          }
+          mma_commit(&empty[s2.i]);
+          mma_commit(&s_empty[b2.i]);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) mma_commit(acc_full);
+      __syncwarp();
+    }
   } else {
     // ============================== epilogue ==============================
-    const int wg = (warp - 2) >> 2;     // takes tiles with t % NWG == wg
+    const int wg = (warp - G::kCtrlWarps) >> 2;  // takes tiles with t % NWG == wg
     const int quad = warp & 3;          // TMEM lane quadrant this warp may access
     const int lrow = quad * 32 + lane;  // owner row within the tile
     const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
     unsigned long long skipped = 0, skipped_sub = 0;
-    int64_t t = 0;
+    Ring<C::kNB> rb;         // S buffer of the current tile
+    Ring<C::kStages> rst;    // its smem stage (BWD_ITEMS staging)
+    int tw = 0;              // current tile's warpgroup (t % NWG)
     uint32_t j = 0;
     for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
       const int64_t chunk = u / p.owner_tiles, ot = u % p.owner_tiles;
@@ -346,12 +363,12 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
         if (MODE == BWD_ROWS) lse2 = p.lse2[orow];
       }
       float m = -INFINITY, s = 0.f, tv = 0.f, has = 0.f;
-      for (int64_t i = 0; i < ntile; ++i, ++t) {
-        if (static_cast<int>(t % NWG) != wg) continue;
-        const int b = static_cast<int>(t % C::kNB);
+      for (int64_t i = 0; i < ntile; ++i, rb.next(), rst.next(), tw = (tw + 1 == NWG ? 0 : tw + 1)) {
+        if (tw != wg) continue;
+        const int b = static_cast<int>(rb.i);
         const int64_t col0 = s_begin + i * BN;
         const int nvalid = static_cast<int>((s_end - col0 < BN ? s_end - col0 : BN));
-        mbar_wait(&s_full[b], static_cast<uint32_t>((t / C::kNB) & 1));
+        mbar_wait(&s_full[b], rb.ph);
         tc_fence_after();
         const uint32_t ta = tmem + lane_base + b * BN;
         if (MODE == FWD) {
@@ -420,10 +437,27 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
           const float* lse2s = nullptr;
           const int* tgts = nullptr;
           if (MODE == BWD_ITEMS) {
-            const int st = static_cast<int>(t % C::kStages);
-            lse2s = reinterpret_cast<const float*>(stage_smem + st * C::kStageBytes + C::kTileBytes);
+            lse2s = reinterpret_cast<const float*>(stage_smem + rst.i * C::kStageBytes + C::kTileBytes);
             tgts = reinterpret_cast<const int*>(lse2s + 128);
           }
+#ifdef LF_DIAG_EPI
+          {  // timing diagnostic only (wrong results): 1 = no TMEM traffic, 2 = ld + st only
+            if (LF_DIAG_EPI == 2) {
+              uint32_t r0[32];
+#pragma unroll
+              for (int q = 0; q < NQ; ++q) {
+                LF_TMEM_LD32(ta + q * 32, r0);
+                tmem_ld_wait();
+                LF_TMEM_ST16(ta + q * 16, r0);
+              }
+              tmem_st_wait();
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&g_ready[b]);
+            continue;
+          }
+#endif
           const int lc_t = MODE == BWD_ROWS ? tgt - static_cast<int>(col0) : -1;
           // 32-column chunks, the next chunk's tcgen05.ld in flight while this
           // one is processed.
