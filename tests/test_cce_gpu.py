@@ -233,3 +233,20 @@ def test_invalid_inputs_name_the_row(lf):  # test_oracles.cpp:215-231, test_cce.
         lf.cce_forward(X, E, bad)
     with pytest.raises(ValueError, match="LSE vector has 3 entries for 4 rows"):
         lf.cce_backward(X, E, x, torch.zeros(3, dtype=torch.float64, device="cuda"))
+
+
+@pytest.mark.parametrize("gamma", [0.0, 1.0, 2.0])
+def test_bf16_filtered_backward_matches_filtered_oracle(lf, gamma):
+    """The headline configuration's filter (eps = kFp16MinPositive = 6e-8,
+    cce.hpp:26-30) on uniform (gamma = 0) and "trained-like" rows
+    X_i = U(-1,1)^D + gamma E_{x_i}: the bf16 gradients match
+    the oracle's FILTERED gradients at the bf16 tolerances, and the skip count
+    matches the oracle's (decisions differ only where softmax is within fp32
+    rounding of eps)."""
+    n, d, v = 384, 64, 40000
+    inst = ob.make_instance(ob.Rng(0xB2000002), n, d, v)
+    Eref = (inst.E + gamma * inst.C.T[inst.targets]).astype(np.float32)
+    X, E, Eh, Ch = prepare(Eref, inst.C, torch.bfloat16)
+    x = torch.from_numpy(inst.targets).cuda()
+    out, bwd = run(lf, X, E, x, eps=6e-8)
+    compare(out, bwd, Eh, Ch, inst.targets, torch.bfloat16, eps=6e-8, frac_tol=2e-3)
