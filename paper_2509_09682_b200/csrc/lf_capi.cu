@@ -72,9 +72,29 @@ static void prof_drain() {
   g_prof_pending.clear();
 }
 
+// The library's scratch comes from the device's default stream-ordered pool.
+// Its default release threshold (0) hands freed memory back to the driver at
+// every synchronization, so the next call would pay a full cudaMalloc again;
+// keep the pool's high-water mark resident instead (once per device).
+static void keep_pool_resident() {
+  static std::mutex mu;
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  std::lock_guard<std::mutex> g(mu);
+  if (done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done[dev] = true;
+}
+
 int Scratch::alloc(size_t nbytes, cudaStream_t s) {
   if (ptr) return fail(LF_EINVAL, "internal: scratch reused");
   if (nbytes == 0) nbytes = 16;
+  keep_pool_resident();
   cudaError_t e = cudaMallocAsync(&ptr, nbytes, s);
   if (e != cudaSuccess) {
     ptr = nullptr;

@@ -287,6 +287,10 @@ __global__ void __launch_bounds__(256) ccem_bwd_rows_generic(
 // ------------------------------------------------- stable radix sort --------
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
+// Radix digit width: 11 bits sorts any catalog below 2^22 items in two passes
+// (the per-warp digit counters, 8 x 2048 x 4 B = 64 KB, live in shared memory).
+constexpr int kDigitBits = 11;
+constexpr int kDigits = 1 << kDigitBits;
 constexpr int kPerWarp = 512;  // contiguous elements per warp
 constexpr int kSortTile = kSortWarps * kPerWarp;
 
@@ -299,16 +303,16 @@ __global__ void __launch_bounds__(kSortThreads) radix_hist(const int64_t* __rest
                                                            const uint32_t* __restrict__ keys,
                                                            int64_t count, int shift,
                                                            uint32_t* __restrict__ hist) {
-  __shared__ uint32_t h[256];
-  for (int i = threadIdx.x; i < 256; i += kSortThreads) h[i] = 0;
+  __shared__ uint32_t h[kDigits];
+  for (int i = threadIdx.x; i < kDigits; i += kSortThreads) h[i] = 0;
   __syncthreads();
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kSortTile;
   for (int j = threadIdx.x; j < kSortTile; j += kSortThreads) {
     const int64_t i = base + j;
-    if (i < count) atomicAdd(&h[(load_item(inds, keys, i) >> shift) & 0xFF], 1u);
+    if (i < count) atomicAdd(&h[(load_item(inds, keys, i) >> shift) & (kDigits - 1)], 1u);
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < 256; d += kSortThreads) hist[d * gridDim.x + blockIdx.x] = h[d];
+  for (int d = threadIdx.x; d < kDigits; d += kSortThreads) hist[d * gridDim.x + blockIdx.x] = h[d];
 }
 
 // Stable scatter: element order inside the tile = warp-major, then 32-wide
@@ -318,9 +322,10 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter(
     const uint32_t* __restrict__ vals_in, int64_t count, int shift,
     const uint32_t* __restrict__ offs, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out) {
-  __shared__ uint32_t wcnt[kSortWarps][256];
+  extern __shared__ uint32_t wcnt_raw[];  // [kSortWarps][kDigits]
+  uint32_t(*wcnt)[kDigits] = reinterpret_cast<uint32_t(*)[kDigits]>(wcnt_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < kSortWarps * 256; i += kSortThreads) (&wcnt[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < kSortWarps * kDigits; i += kSortThreads) wcnt_raw[i] = 0;
   __syncthreads();
   const int64_t wbase = static_cast<int64_t>(blockIdx.x) * kSortTile + warp * kPerWarp;
   const unsigned lt = (1u << lane) - 1u;
@@ -328,14 +333,14 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter(
   for (int st = 0; st < kPerWarp; st += 32) {
     const int64_t i = wbase + st + lane;
     const bool ok = i < count;
-    const uint32_t dg = ok ? (load_item(inds, keys_in, i) >> shift) & 0xFF : 256u + lane;
+    const uint32_t dg = ok ? (load_item(inds, keys_in, i) >> shift) & (kDigits - 1) : kDigits + lane;
     const unsigned peers = __match_any_sync(0xffffffffu, dg);
     if (ok && (peers & lt) == 0) wcnt[warp][dg] += __popc(peers);
     __syncwarp();
   }
   __syncthreads();
   // exclusive prefix over warps per digit, plus the block's global offset
-  for (int d = threadIdx.x; d < 256; d += kSortThreads) {
+  for (int d = threadIdx.x; d < kDigits; d += kSortThreads) {
     uint32_t run = offs[d * gridDim.x + blockIdx.x];
     for (int wi = 0; wi < kSortWarps; ++wi) {
       const uint32_t c = wcnt[wi][d];
@@ -349,7 +354,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter(
     const int64_t i = wbase + st + lane;
     const bool ok = i < count;
     const uint32_t key = ok ? load_item(inds, keys_in, i) : 0u;
-    const uint32_t dg = ok ? (key >> shift) & 0xFF : 256u + lane;
+    const uint32_t dg = ok ? (key >> shift) & (kDigits - 1) : kDigits + lane;
     const unsigned peers = __match_any_sync(0xffffffffu, dg);
     if (ok) {
       const uint32_t dst = wcnt[warp][dg] + __popc(peers & lt);
@@ -444,6 +449,50 @@ __global__ void __launch_bounds__(256) segment_reduce(const TX* __restrict__ X,
   }
 }
 
+// bf16 / f32 rows with D % 64 == 0: warp per item, lane = 8g + c; group g
+// takes the item's entries g, g+4, g+8, ... (four X rows in flight, each a
+// coalesced 2D-byte row, 16 B per lane), then the four partial sums are
+// combined in a fixed order — deterministic run to run.
+template <class TX, int D>
+__global__ void __launch_bounds__(256) segment_reduce_vec(const TX* __restrict__ X,
+                                                          const float* __restrict__ coeff,
+                                                          const uint32_t* __restrict__ sorted_vals,
+                                                          const uint32_t* __restrict__ item_off,
+                                                          int64_t v, int64_t w,
+                                                          float* __restrict__ dE) {
+  constexpr int DPL = D / 8;
+  const int lane = threadIdx.x & 31, g = lane >> 3, c = lane & 7;
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (item >= v) return;
+  const uint32_t b = item_off[item], e = item_off[item + 1];
+  float acc[DPL];
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) acc[i] = 0.f;
+  for (uint32_t p = b + g; p < e; p += 4) {
+    const uint32_t key = __ldg(sorted_vals + p);
+    const float gk = __ldg(coeff + key);
+    const TX* xr = X + static_cast<int64_t>(key / w) * D + c * DPL;
+#pragma unroll
+    for (int k = 0; k < DPL / 8; ++k) {
+      float f[8];
+      Vec8<TX>::load(xr + 8 * k, f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[8 * k + i] = fmaf(gk, f[i], acc[8 * k + i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) {
+    acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 8);
+    acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 16);
+  }
+  if (g == 0) {
+#pragma unroll
+    for (int i = 0; i < DPL; i += 4)
+      *reinterpret_cast<float4*>(dE + item * D + c * DPL + i) =
+          make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+  }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -452,7 +501,7 @@ int ccem_forward(int dtype, const void* X, const void* E, const int64_t* inds, i
   (void)v;
   ProfScope prof(LF_K_CCEM_FWD, st);
   const dim3 grid(static_cast<unsigned>(ceil_div(n, 8)));
-  if (dtype == LF_BF16 || (dtype == LF_F32 && D % 64 == 0 && D <= 256)) {
+  if (dtype == LF_BF16 || (dtype == LF_F32 && (D == 64 || D == 128 || D == 256))) {
 #define LF_FWD_VEC(TE, DD)                                                                     \
   ccem_fwd_vec<TE, DD><<<grid, 256, 0, st>>>(static_cast<const TE*>(X),                        \
                                             static_cast<const TE*>(E), inds, n, w, lse, pos)
@@ -492,12 +541,15 @@ static int sort_by_item(const int64_t* inds, int64_t count, int64_t v, Scratch& 
   if (!rc) rc = v1.alloc(sizeof(uint32_t) * count, st);
   if (!rc) rc = sorted_vals.alloc(sizeof(uint32_t) * count, st);
   const int64_t blocks = ceil_div(count, kSortTile);
-  if (!rc) rc = hist.alloc(sizeof(uint32_t) * 256 * blocks, st);
-  if (!rc) rc = offs.alloc(sizeof(uint32_t) * 256 * blocks, st);
+  if (!rc) rc = hist.alloc(sizeof(uint32_t) * kDigits * blocks, st);
+  if (!rc) rc = offs.alloc(sizeof(uint32_t) * kDigits * blocks, st);
   if (!rc) rc = item_off.alloc(sizeof(uint32_t) * (v + 1), st);
   if (rc) return rc;
   int passes = 1;
-  while (passes < 4 && ((static_cast<uint64_t>(v - 1) >> (8 * passes)) != 0)) ++passes;
+  while (passes < 3 && ((static_cast<uint64_t>(v - 1) >> (kDigitBits * passes)) != 0)) ++passes;
+  constexpr int kScatterSmem = kSortWarps * kDigits * sizeof(uint32_t);
+  LF_CUDA(cudaFuncSetAttribute(radix_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               kScatterSmem));
   // ping-pong so the final pass lands in sorted_vals (pass p writes S when
   // passes-1-p is even, else the spare buffer); keys alternate k0/k1.
   uint32_t* kin = nullptr;
@@ -506,12 +558,12 @@ static int sort_by_item(const int64_t* inds, int64_t count, int64_t v, Scratch& 
     const bool even_from_end = ((passes - 1 - p) % 2) == 0;
     uint32_t* kout = even_from_end ? k0.as<uint32_t>() : k1.as<uint32_t>();
     uint32_t* vout = even_from_end ? sorted_vals.as<uint32_t>() : v1.as<uint32_t>();
-    radix_hist<<<blocks, kSortThreads, 0, st>>>(inds, kin, count, 8 * p, hist.as<uint32_t>());
+    radix_hist<<<blocks, kSortThreads, 0, st>>>(inds, kin, count, kDigitBits * p, hist.as<uint32_t>());
     LF_LAUNCHED();
-    rc = exclusive_scan(hist.as<uint32_t>(), offs.as<uint32_t>(), 256 * blocks, st);
+    rc = exclusive_scan(hist.as<uint32_t>(), offs.as<uint32_t>(), kDigits * blocks, st);
     if (rc) return rc;
-    radix_scatter<<<blocks, kSortThreads, 0, st>>>(inds, kin, vin, count, 8 * p,
-                                                   offs.as<uint32_t>(), kout, vout);
+    radix_scatter<<<blocks, kSortThreads, kScatterSmem, st>>>(
+        inds, kin, vin, count, kDigitBits * p, offs.as<uint32_t>(), kout, vout);
     LF_LAUNCHED();
     kin = kout;
     vin = vout;
@@ -535,7 +587,7 @@ int ccem_backward(int dtype, const void* X, const void* E, const int64_t* inds,
   ProfScope prof(LF_K_CCEM_BWD, st);
   const dim3 grid(static_cast<unsigned>(ceil_div(n, 8)));
   const int64_t count = n * w;
-  const bool vec = dtype == LF_BF16 || (dtype == LF_F32 && D % 64 == 0 && D <= 256);
+  const bool vec = dtype == LF_BF16 || (dtype == LF_F32 && (D == 64 || D == 128 || D == 256));
   if (dtype == LF_BF16 && !(D == 64 || D == 128 || D == 256))
     return fail(LF_EUNSUPPORTED, "ccem bf16: d must be 64, 128 or 256");
   if (dtype == LF_F64) atomic_de = false;  // exact mode is always ordered
@@ -580,10 +632,22 @@ int ccem_backward(int dtype, const void* X, const void* E, const int64_t* inds,
   int rc = sort_by_item(inds, count, v, sorted_vals, item_off, st);
   if (rc) return rc;
   const dim3 sgrid(static_cast<unsigned>(ceil_div(v, 8)));
-  if (dtype == LF_BF16) {
-    segment_reduce<__nv_bfloat16, float, float><<<sgrid, 256, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(X), coeff.as<float>(), sorted_vals.as<uint32_t>(),
-        item_off.as<uint32_t>(), v, D, w, static_cast<float*>(dE));
+  if (vec) {
+#define LF_SEG(TX, DD)                                                                          \
+  segment_reduce_vec<TX, DD><<<sgrid, 256, 0, st>>>(static_cast<const TX*>(X), coeff.as<float>(), \
+                                                    sorted_vals.as<uint32_t>(),                \
+                                                    item_off.as<uint32_t>(), v, w,             \
+                                                    static_cast<float*>(dE))
+    if (dtype == LF_BF16) {
+      if (D == 64) LF_SEG(__nv_bfloat16, 64);
+      else if (D == 128) LF_SEG(__nv_bfloat16, 128);
+      else LF_SEG(__nv_bfloat16, 256);
+    } else {
+      if (D == 64) LF_SEG(float, 64);
+      else if (D == 128) LF_SEG(float, 128);
+      else LF_SEG(float, 256);
+    }
+#undef LF_SEG
   } else if (dtype == LF_F32) {
     segment_reduce<float, float, float><<<sgrid, 256, 0, st>>>(
         static_cast<const float*>(X), coeff.as<float>(), sorted_vals.as<uint32_t>(),
