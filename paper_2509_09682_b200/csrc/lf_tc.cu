@@ -24,6 +24,7 @@
 #include <cudaTypedefs.h>
 
 #include <cmath>
+#include <type_traits>
 
 #include "lf_internal.cuh"
 #include "lf_kernels.cuh"
@@ -155,6 +156,19 @@ __device__ __forceinline__ float target_g(float e, uint32_t raw, float l, float 
     return ex2_approx(fmaf(__uint_as_float(raw), kLog2e, -l) + static_cast<float>(64 - kPreA<FLAGS>)) -
            t_scale;
   return e - t_scale;
+}
+
+// Tree max of 32 registers, depth 4 with 3-input max (FMNMX3).
+__device__ __forceinline__ float max32(const float (&e)[32]) {
+  float a[11];
+#pragma unroll
+  for (int i = 0; i < 10; ++i) a[i] = fmaxf(e[3 * i], fmaxf(e[3 * i + 1], e[3 * i + 2]));
+  a[10] = fmaxf(e[30], e[31]);
+  float b[4];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) b[i] = fmaxf(a[3 * i], fmaxf(a[3 * i + 1], a[3 * i + 2]));
+  b[3] = fmaxf(a[9], a[10]);
+  return fmaxf(fmaxf(b[0], b[1]), fmaxf(b[2], b[3]));
 }
 
 // Select r[idx] from a register array without dynamic indexing.
@@ -345,6 +359,7 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
     const int lrow = quad * 32 + lane;  // owner row within the tile
     const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
     unsigned long long skipped = 0, skipped_sub = 0;
+    bool skip_on = true;  // backward: run the skipping variant on the next tile (warp-uniform)
     Ring<C::kNB> rb;         // S buffer of the current tile
     Ring<C::kStages> rst;    // its smem stage (BWD_ITEMS staging)
     int tw = 0;              // current tile's warpgroup (t % NWG)
@@ -462,11 +477,26 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
 #endif
           const int lc_t = MODE == BWD_ROWS ? tgt - static_cast<int>(col0) : -1;
           // 32-column chunks, the next chunk's tcgen05.ld in flight while this
-          // one is processed.
+          // one is processed.  Two instantiations: TEST = false is straight-line
+          // code across all chunks (no branch in front of the exps) and only
+          // notes, off the critical path, whether some sub-tile was entirely
+          // below the filter threshold; TEST = true also skips those sub-tiles'
+          // exps (warp vote + branch).  The next tile uses TEST = true only
+          // while skippable sub-tiles keep appearing (uniform logits — the
+          // headline case — never have one).  Either way the result is exact:
+          // the ftz flush zeroes every entry below eps.
+          auto process = [&](auto test_tag) -> bool {
+          constexpr bool TEST = decltype(test_tag)::value;
+          bool any_below = false;
           uint32_t ra[32], rb[32];
           float xp[32];  // kSwp: previous chunk's coefficients
           LF_TMEM_LD32(ta, ra);
           tmem_ld_wait();
+#ifdef LF_DIAG_EARLY  // timing diagnostic only (wrong results): hand G over before computing it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&g_ready[b]);
+#endif
 #pragma unroll
           for (int q = 0; q < NQ; ++q) {
             uint32_t(&cur)[32] = (q & 1) ? rb : ra;
@@ -497,11 +527,12 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
             const int jt = lc_t - q * 32;
             const bool tgt_here = MODE == BWD_ROWS ? static_cast<unsigned>(jt) < 32u : hm != 0u;
             bool skip = false;
-            if (FLAGS & kFilt) {
-              float mx = e[0];
-#pragma unroll
-              for (int c = 1; c < 32; c += 2) mx = fmaxf(mx, fmaxf(e[c], c + 1 < 32 ? e[c + 1] : e[c]));
-              skip = __all_sync(0xffffffffu, mx < kThr<FLAGS> && !tgt_here);
+            // (TEST = false samples only the first chunk of the tile)
+            if ((FLAGS & kFilt) && (TEST || q == 0 || (FLAGS & kCount))) {
+              const float mx = max32(e);  // log-depth (FMNMX3 tree)
+              const bool below = __all_sync(0xffffffffu, mx < kThr<FLAGS> && !tgt_here);
+              any_below |= below;
+              if (TEST) skip = below;
               if ((FLAGS & kCount) && MODE == BWD_ROWS) {
 #pragma unroll
                 for (int c = 0; c < 32; ++c)
@@ -585,10 +616,15 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
             for (int c = 0; c < 16; ++c) g[c] = pack_bf16x2(xp[2 * c], xp[2 * c + 1]);
             LF_TMEM_ST16(ta + (NQ - 1) * 16, g);
           }
+          return any_below;
+          };
+          skip_on = skip_on ? process(std::true_type{}) : process(std::false_type{});
           tmem_st_wait();
+#ifndef LF_DIAG_EARLY
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&g_ready[b]);
+#endif
         }
       }
       if (MODE == FWD) {
