@@ -532,7 +532,7 @@ int ccem_forward(int dtype, const void* X, const void* E, const int64_t* inds, i
 
 // Sort (item, key) pairs stably by item; returns sorted keys (slot ids) and
 // per-item offsets (v+1).
-static int sort_by_item(const int64_t* inds, int64_t count, int64_t v, Scratch& sorted_vals,
+int sort_by_item(const int64_t* inds, int64_t count, int64_t v, Scratch& sorted_vals,
                         Scratch& item_off, cudaStream_t st) {
   if (count >= (int64_t(1) << 32)) return fail(LF_EUNSUPPORTED, "ccem: n*w must be < 2^32");
   Scratch k0, k1, v1, hist, offs;

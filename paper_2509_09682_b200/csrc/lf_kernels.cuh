@@ -55,6 +55,12 @@ int ccem_backward(int dtype, const void* X, const void* E, const int64_t* inds,
                   int D, int64_t v, int64_t w, bool atomic_de, void* dX, void* dE,
                   cudaStream_t st);
 
+// Stable counting-by-radix sort of `count` entries by item (inds[i] in
+// [0, v)): sorted_vals = entry indices grouped by item in index order,
+// item_off[v + 1] = segment offsets (lf_ccem.cu).
+int sort_by_item(const int64_t* inds, int64_t count, int64_t v, Scratch& sorted_vals,
+                 Scratch& item_off, cudaStream_t st);
+
 // ---- validation (lf_ccem.cu) ----
 int validate_targets(const int64_t* targets, int64_t n, int64_t v, cudaStream_t st);
 int validate_inds(const int64_t* inds, int64_t n, int64_t w, int64_t v, cudaStream_t st);

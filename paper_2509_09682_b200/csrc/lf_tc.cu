@@ -64,7 +64,14 @@ constexpr int BM = 128;  // owner tile (TMEM lanes)
 enum Mode : int { FWD = 0, BWD_ROWS = 1, BWD_ITEMS = 2 };
 // Backward variants: kFilt = filter_eps > 0 (flush below eps, sub-tile skip);
 // kCount = also count skipped elements / sub-tiles (only when stats are read).
-constexpr int kFilt = 1, kCount = 2;
+// kTgtIn = handle each row's own target inside the tile loop (exact for any
+// eps, needed for the skip statistics); without it the target column is an
+// ordinary softmax entry and the "-1" of softmax - onehot is applied at the
+// accumulator read-out (dX_i -= scale E_{x_i}; dE_v -= scale sum_{x_i = v} X_i),
+// which keeps the tile loop free of per-row branches.  The two differ only
+// when the target's own softmax is below eps (then < eps relative), so the
+// read-out form is used for eps < 2^-12 without stats.
+constexpr int kFilt = 1, kCount = 2, kTgtIn = 4;
 
 struct TcParams {
   int64_t n_owner;       // owner rows (n or v_shard)
@@ -77,6 +84,10 @@ struct TcParams {
   const float* lse2;     // lse*log2e - log2|scale| per row (padded; +inf pad)
   float abs_scale;       // |upstream / n| in the kernel's (possibly rescaled) G domain
   float out_scale;       // multiplies the dX / dE accumulators on read-out
+  const __nv_bfloat16* fix_rows;  // !kTgtIn read-out: BWD_ROWS E, BWD_ITEMS X (bf16)
+  float fix_scale;               // scale = upstream / n (signed, real units)
+  const uint32_t* fix_off;       // BWD_ITEMS: [v + 2] offsets into fix_list per local item
+  const uint32_t* fix_list;      // BWD_ITEMS: rows sorted by local target
   float4* part;          // FWD: [n_chunks][n_owner]
   float* out;            // BWD_ROWS: [n_chunks][n_owner][D]; BWD_ITEMS: [n_owner][D]
   unsigned long long* counters;  // [0] skipped elems, [1] skipped tiles, [2] total tiles
@@ -520,12 +531,20 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
             // whose target item lies in the owner tile (warp-uniform, rare).
             int tq = 0;
             unsigned hm = 0;
-            if (MODE == BWD_ITEMS) {
+#ifndef LF_DIAG_NOTGT
+            if (MODE == BWD_ITEMS && (FLAGS & kTgtIn)) {
               tq = lds_i32(lse2_sa + 512 + 4 * (q * 32 + lane)) - o0;
               hm = __ballot_sync(0xffffffffu, static_cast<unsigned>(tq) < static_cast<unsigned>(BM));
             }
+#endif
             const int jt = lc_t - q * 32;
-            const bool tgt_here = MODE == BWD_ROWS ? static_cast<unsigned>(jt) < 32u : hm != 0u;
+#ifdef LF_DIAG_NOTGT  // timing diagnostic only (wrong results): no target handling
+            const bool tgt_here = false;
+            hm = 0;
+#else
+            const bool tgt_here = !(FLAGS & kTgtIn) ? false
+                                  : MODE == BWD_ROWS ? static_cast<unsigned>(jt) < 32u : hm != 0u;
+#endif
             bool skip = false;
             // (TEST = false samples only the first chunk of the tile)
             if ((FLAGS & kFilt) && (TEST || q == 0 || (FLAGS & kCount))) {
@@ -572,12 +591,12 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
               // The target is never filtered: g = (s - 1) |scale| (cce.cpp:193-195).
               // Under FILT its softmax is recomputed unflushed from the raw
               // logit still in `cur`: s * 2^-62 / eps = 2^(a + 64).
-              if (MODE == BWD_ROWS && tgt_here) {
+              if (MODE == BWD_ROWS && (FLAGS & kTgtIn) && tgt_here) {
 #pragma unroll
                 for (int c = 0; c < 32; ++c)
                   if (c == jt) x[c] = target_g<FLAGS>(x[c], cur[c], lse2, p.abs_scale);
               }
-              if (MODE == BWD_ITEMS) {
+              if (MODE == BWD_ITEMS && (FLAGS & kTgtIn)) {
                 while (hm) {  // warp-uniform loop over the hit columns
                   const int jc = __ffs(hm) - 1;
                   hm &= hm - 1u;
@@ -660,16 +679,45 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
         float* dst = MODE == BWD_ROWS ? p.out + (chunk * p.n_owner + orow) * D
                                       : p.out + orow * D;
         const float os = p.out_scale;
+        // !kTgtIn: the onehot part of softmax - onehot, -scale x (the target's
+        // item row | the rows targeting this item, in sorted = row order)
+        uint32_t fb = 0, fe = 0;
+        const __nv_bfloat16* frow = nullptr;
+        if (!(FLAGS & kTgtIn) && orow < p.n_owner) {
+          if (MODE == BWD_ROWS) {
+            if (tgt >= s_begin && tgt < s_end) {
+              frow = p.fix_rows + static_cast<int64_t>(tgt) * D;
+              fe = 1;
+            }
+          } else {
+            fb = p.fix_off[orow];
+            fe = p.fix_off[orow + 1];
+          }
+        }
         for (int c0 = wg * 16; c0 < D; c0 += 16 * NWG) {
           uint32_t r16[16];
           LF_TMEM_LD16(tmem + lane_base + C::kAccCol + c0, r16);
           tmem_ld_wait();
           if (orow < p.n_owner) {
+            float o[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) o[c] = __uint_as_float(r16[c]) * os;
+            if (!(FLAGS & kTgtIn)) {
+              float fx[16];
+#pragma unroll
+              for (int c = 0; c < 16; ++c) fx[c] = 0.f;
+              for (uint32_t k = fb; k < fe; ++k) {
+                const __nv_bfloat16* xr =
+                    MODE == BWD_ROWS ? frow : p.fix_rows + static_cast<int64_t>(p.fix_list[k]) * D;
+#pragma unroll
+                for (int c = 0; c < 16; ++c) fx[c] += __bfloat162float(xr[c0 + c]);
+              }
+#pragma unroll
+              for (int c = 0; c < 16; ++c) o[c] = fmaf(-p.fix_scale, fx[c], o[c]);
+            }
 #pragma unroll
             for (int c = 0; c < 16; c += 4)
-              *reinterpret_cast<float4*>(dst + c0 + c) =
-                  make_float4(__uint_as_float(r16[c]) * os, __uint_as_float(r16[c + 1]) * os,
-                              __uint_as_float(r16[c + 2]) * os, __uint_as_float(r16[c + 3]) * os);
+              *reinterpret_cast<float4*>(dst + c0 + c) = make_float4(o[c], o[c + 1], o[c + 2], o[c + 3]);
           }
         }
         tc_fence_before();
@@ -736,6 +784,12 @@ __global__ void prep_rows(const int64_t* __restrict__ targets, const double* __r
   if (lse2) lse2[i] = l;
 }
 
+__global__ void target_keys(const int32_t* __restrict__ tgt, int64_t n, int64_t v,
+                            int64_t* __restrict__ keys) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) keys[i] = tgt[i] >= 0 ? tgt[i] : v;
+}
+
 template <int D, int MODE, int FLAGS>
 int launch_mode(const CUtensorMap& mo, const CUtensorMap& ms, const TcParams& p, cudaStream_t st) {
   using C = Cfg<D, MODE>;
@@ -755,7 +809,8 @@ int launch_flags(int flags, const CUtensorMap& mo, const CUtensorMap& ms, const 
   switch (flags) {
     case 0: return launch_mode<D, MODE, 0>(mo, ms, p, st);
     case kFilt: return launch_mode<D, MODE, kFilt>(mo, ms, p, st);
-    default: return launch_mode<D, MODE, kFilt | kCount>(mo, ms, p, st);
+    case kFilt | kTgtIn: return launch_mode<D, MODE, kFilt | kTgtIn>(mo, ms, p, st);
+    default: return launch_mode<D, MODE, kFilt | kCount | kTgtIn>(mo, ms, p, st);
   }
 }
 
@@ -851,7 +906,8 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
   if (eps > 2.0) eps = 2.0;  // softmax <= 1: every eps > 1 filters every off-target entry
   const bool filt = eps >= 0x1p-100;
   const bool count = filt && counters != nullptr;
-  const int flags = filt ? (kFilt | (count ? kCount : 0)) : 0;
+  const bool tgt_in = filt && (count || eps >= 0x1p-12);
+  const int flags = filt ? (kFilt | (count ? kCount : 0) | (tgt_in ? kTgtIn : 0)) : 0;
   const double sub = filt ? -std::log2(eps) - 126.0 + (kPreSel ? 64.0 : 0.0)
                           : std::log2(std::fabs(scale));
   const double gscale = filt ? std::ldexp(1.0, -62) / eps : std::fabs(scale);
@@ -899,6 +955,8 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
   p.out_scale = static_cast<float>(out_scale);
   p.out = dx_out;
   p.counters = counters;
+  p.fix_rows = static_cast<const __nv_bfloat16*>(E);
+  p.fix_scale = static_cast<float>(scale);
   rc = launch_d<BWD_ROWS>(D, flags, mx_own, me_str, p, st);
   if (rc) return rc;
   if (P > 1) {
@@ -919,6 +977,21 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
   q.out_scale = static_cast<float>(out_scale);
   q.out = dE;
   q.counters = counters;
+  q.fix_rows = static_cast<const __nv_bfloat16*>(X);
+  q.fix_scale = static_cast<float>(scale);
+  Scratch keys, fix_list, fix_off;
+  if (!tgt_in) {
+    // rows grouped by local target item (stable, so each item's rows are
+    // summed in row order at the dE read-out); out-of-shard targets -> item v
+    rc = keys.alloc(sizeof(int64_t) * n, st);
+    if (rc) return rc;
+    target_keys<<<ceil_div(n, 256), 256, 0, st>>>(tgt.as<int32_t>(), n, v, keys.as<int64_t>());
+    LF_LAUNCHED();
+    rc = sort_by_item(keys.as<int64_t>(), n, v + 1, fix_list, fix_off, st);
+    if (rc) return rc;
+    q.fix_off = fix_off.as<uint32_t>();
+    q.fix_list = fix_list.as<uint32_t>();
+  }
   rc = launch_d<BWD_ITEMS>(D, flags, me_own, mx_str, q, st);
   return rc;
 }
