@@ -201,8 +201,10 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
   constexpr int NWG = G::NWG;
   constexpr int NQ = G::NQ;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* base = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  // 1 KB alignment by plain pointer arithmetic on the __shared__ array, so
+  // every pointer derived from `base` stays in the shared address space
+  // (ordinary loads through it compile to LDS, not generic LD).
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   unsigned char* owner_smem = base;
   unsigned char* stage_smem = base + C::kOwnerBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(stage_smem + C::kStages * C::kStageBytes);
@@ -462,10 +464,8 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
           // its exps (warp vote).
           const float* lse2s = nullptr;
           const int* tgts = nullptr;
-          uint32_t lse2_sa = 0;  // shared-window address of the staged lse2[], tgt[] (ld.shared)
           if (MODE == BWD_ITEMS) {
             lse2s = reinterpret_cast<const float*>(stage_smem + rst.i * C::kStageBytes + C::kTileBytes);
-            lse2_sa = smem_u32(lse2s);
             tgts = reinterpret_cast<const int*>(lse2s + 128);
           }
 #ifdef LF_DIAG_EPI
@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
             for (int c = 0; c < 32; c += 4) {
               float l[4] = {lse2, lse2, lse2, lse2};
               if (MODE == BWD_ITEMS) {
-                const float4 lp = lds_f4(lse2_sa + 4 * (q * 32 + c));
+                const float4 lp = *reinterpret_cast<const float4*>(lse2s + q * 32 + c);
                 l[0] = lp.x;
                 l[1] = lp.y;
                 l[2] = lp.z;
@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
             unsigned hm = 0;
 #ifndef LF_DIAG_NOTGT
             if (MODE == BWD_ITEMS && (FLAGS & kTgtIn)) {
-              tq = lds_i32(lse2_sa + 512 + 4 * (q * 32 + lane)) - o0;
+              tq = tgts[q * 32 + lane] - o0;
               hm = __ballot_sync(0xffffffffu, static_cast<unsigned>(tq) < static_cast<unsigned>(BM));
             }
 #endif
@@ -602,7 +602,7 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
                   hm &= hm - 1u;
                   const int li = __shfl_sync(0xffffffffu, tq, jc);
                   if (li == lrow) {
-                    const float lj = __int_as_float(lds_i32(lse2_sa + 4 * (q * 32 + jc)));
+                    const float lj = lse2s[q * 32 + jc];
 #pragma unroll
                     for (int c = 0; c < 32; ++c)
                       if (c == jc) x[c] = target_g<FLAGS>(x[c], cur[c], lj, p.abs_scale);

@@ -263,3 +263,27 @@ def test_bf16_filtered_backward_matches_filtered_oracle(lf, gamma):
     ge = bwd.grads.d_classifier.double().cpu().numpy()
     assert np.linalg.norm(gx - dX) <= 0.1 * np.linalg.norm(dX)
     assert np.linalg.norm(ge - dC.T) <= 0.1 * np.linalg.norm(dC)
+
+
+@pytest.mark.parametrize("gamma", [0.0, 1.0])
+def test_bf16_filtered_backward_without_stats(lf, gamma):
+    """stats=False selects the production kernels (no skip counters): with
+    eps < 2^-12 the onehot part of softmax - onehot is applied at the
+    accumulator read-out instead of inside the tile loop.  Same gradients as
+    the filtered oracle at the bf16 tolerances."""
+    n, d, v = 384, 64, 40000
+    inst = ob.make_instance(ob.Rng(0xB2000003), n, d, v)
+    Eref = (inst.E + gamma * inst.C.T[inst.targets]).astype(np.float32)
+    X, E, Eh, Ch = prepare(Eref, inst.C, torch.bfloat16)
+    x = torch.from_numpy(inst.targets).cuda()
+    cfg = lf.CceConfig(filter_eps=6e-8)
+    out = lf.cce_forward(X, E, x, cfg)
+    bwd = lf.cce_backward(X, E, x, out.lse, 1.0, cfg, stats=False)
+    loss, pos, lse = ob.cce_forward(Eh, Ch, inst.targets)
+    dX, dC, _, _ = ob.cce_backward(Eh, Ch, inst.targets, lse, 1.0, 6e-8)
+    check_grad(bwd.grads.d_embeddings, dX, torch.bfloat16, "dX")
+    check_grad(bwd.grads.d_classifier, dC.T, torch.bfloat16, "dE")
+    # negative upstream flips the sign of both gradients exactly
+    neg = lf.cce_backward(X, E, x, out.lse, -1.0, cfg, stats=False)
+    assert torch.equal(neg.grads.d_embeddings, -bwd.grads.d_embeddings)
+    assert torch.equal(neg.grads.d_classifier, -bwd.grads.d_classifier)
