@@ -501,6 +501,17 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
           bool any_below = false;
           uint32_t ra[32], rb[32];
           float xp[32];  // kSwp: previous chunk's coefficients
+          float lcur[32], lnext[32];  // BWD_ITEMS: per-column lse2 (chunk q, q + 1)
+          if (MODE == BWD_ITEMS) {
+#pragma unroll
+            for (int c = 0; c < 32; c += 4) {
+              const float4 lp = *reinterpret_cast<const float4*>(lse2s + c);
+              lcur[c] = lp.x;
+              lcur[c + 1] = lp.y;
+              lcur[c + 2] = lp.z;
+              lcur[c + 3] = lp.w;
+            }
+          }
           LF_TMEM_LD32(ta, ra);
           tmem_ld_wait();
 #ifdef LF_DIAG_EARLY  // timing diagnostic only (wrong results): hand G over before computing it
@@ -513,19 +524,26 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
             uint32_t(&cur)[32] = (q & 1) ? rb : ra;
             uint32_t(&nxt)[32] = (q & 1) ? ra : rb;
             if (q + 1 < NQ) LF_TMEM_LD32(ta + (q + 1) * 32, nxt);
+            // BWD_ITEMS: the stream rows' lse2 of this chunk were loaded one
+            // chunk ahead (lcur), the next chunk's are fetched now (lnext), so
+            // the shared-memory latency never sits in front of the FFMAs.
+            if (MODE == BWD_ITEMS && q + 1 < NQ) {
+#pragma unroll
+              for (int c = 0; c < 32; c += 4) {
+                const float4 lp = *reinterpret_cast<const float4*>(lse2s + (q + 1) * 32 + c);
+                lnext[c] = lp.x;
+                lnext[c + 1] = lp.y;
+                lnext[c + 2] = lp.z;
+                lnext[c + 3] = lp.w;
+              }
+            }
             float e[32];
 #pragma unroll
-            for (int c = 0; c < 32; c += 4) {
-              float l[4] = {lse2, lse2, lse2, lse2};
-              if (MODE == BWD_ITEMS) {
-                const float4 lp = *reinterpret_cast<const float4*>(lse2s + q * 32 + c);
-                l[0] = lp.x;
-                l[1] = lp.y;
-                l[2] = lp.z;
-                l[3] = lp.w;
-              }
+            for (int c = 0; c < 32; ++c)
+              e[c] = fmaf(__uint_as_float(cur[c]), kLog2e, MODE == BWD_ITEMS ? -lcur[c] : -lse2);
+            if (MODE == BWD_ITEMS) {
 #pragma unroll
-              for (int k = 0; k < 4; ++k) e[c + k] = fmaf(__uint_as_float(cur[c + k]), kLog2e, -l[k]);
+              for (int c = 0; c < 32; ++c) lcur[c] = lnext[c];
             }
             // BWD_ITEMS: lane k checks stream row q*32+k; hm = rows of this chunk
             // whose target item lies in the owner tile (warp-uniform, rare).
