@@ -54,7 +54,8 @@ enum lf_status {
   LF_EINVAL = -1,      /* bad argument (shape, range, config) */
   LF_EUNSUPPORTED = -2, /* valid request this build cannot serve (e.g. bf16 with d % 64) */
   LF_ECUDA = -3,       /* CUDA runtime / driver error */
-  LF_ENOMEM = -4
+  LF_ENOMEM = -4,
+  LF_ERUNTIME = -5     /* the reference's std::runtime_error cases (e.g. sampler retry cap) */
 };
 
 enum lf_dtype { LF_F32 = 0, LF_F64 = 1, LF_BF16 = 2 };
@@ -144,6 +145,18 @@ LF_API int lf_ccem_backward(const void* d_X, const void* d_E, const int64_t* d_i
                      const double* d_row_upstream, double upstream, int64_t n, int64_t d,
                      int64_t v, int64_t w, const lf_cce_config* cfg, void* d_dX, void* d_dE,
                      void* stream);
+
+/* ------------------------------------------------------- negative sampler -- */
+/* Replaces lseforge::sample_uniform (sampler.hpp, sampler.cpp:44-75) with a
+ * device restatement that produces the SAME indices: row i draws from
+ * SplitMix64(seed).derived(i) (rng.hpp:46-48; only the generator's
+ * construction seed matters), slot 0 = positives[i], slots 1..ns = the next
+ * in-catalog draws that differ from the positive; retry_cap consecutive
+ * positive draws in one slot -> LF_ERUNTIME with the reference's message.
+ * Writes d_inds[n x (1 + ns)] (int64, the NegIndexMatrix layout CCE- takes).
+ * Synchronizes `stream` (validation and the retry-cap status). */
+LF_API int lf_sample_uniform(const int64_t* d_positives, int64_t n, int64_t ns, int64_t catalog,
+                             uint64_t seed, int32_t retry_cap, int64_t* d_inds, void* stream);
 
 /* ----------------------------------------------------------- validation --- */
 /* Replaces validate_loss_inputs' index scan (losses.cpp:58-67) for device

@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # LSEFORGE_B200_LIB selects an alternative in-tree build (tuning variants).
 LIB_PATH = os.environ.get("LSEFORGE_B200_LIB") or os.path.join(_HERE, "liblseforge_b200.so")
 
-LF_OK, LF_EINVAL, LF_EUNSUPPORTED, LF_ECUDA, LF_ENOMEM = 0, -1, -2, -3, -4
+LF_OK, LF_EINVAL, LF_EUNSUPPORTED, LF_ECUDA, LF_ENOMEM, LF_ERUNTIME = 0, -1, -2, -3, -4, -5
 LF_F32, LF_F64, LF_BF16 = 0, 1, 2
 LF_FLAG_NONE, LF_FLAG_ATOMIC_DE = 0, 1
 
@@ -24,7 +24,7 @@ EXPORTS = (
     "lf_ccem_backward", "lf_validate_targets", "lf_validate_inds", "lf_estimate_flops",
     "lf_workspace_stats", "lf_workspace_reset_peak", "lf_launch_count", "lf_launch_count_reset",
     "lf_profile_enable", "lf_profile_read", "lf_profile_reset", "lf_classifier_to_items",
-    "lf_convert_rows", "lf_items_grad_to_classifier", "lf_widen_grad",
+    "lf_convert_rows", "lf_items_grad_to_classifier", "lf_widen_grad", "lf_sample_uniform",
 )
 KERNEL_KINDS = ("cce_fwd", "cce_bwd_dx", "cce_bwd_de", "cce_simt", "ccem_fwd", "ccem_bwd", "aux")
 
@@ -73,6 +73,11 @@ def lib():
         L.lf_estimate_flops.argtypes = [i64, i64, i64, i64, C.c_int32, C.POINTER(C.c_uint64),
                                         C.POINTER(C.c_uint64)]
         L.lf_workspace_stats.argtypes = [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        L.lf_sample_uniform.argtypes = [vp, i64, i64, i64, C.c_uint64, C.c_int32, vp, vp]
+        L.lf_classifier_to_items.argtypes = [vp, i64, i64, C.c_int32, vp, vp]
+        L.lf_convert_rows.argtypes = [vp, i64, C.c_int32, vp, vp]
+        L.lf_items_grad_to_classifier.argtypes = [vp, C.c_int32, i64, i64, vp, vp]
+        L.lf_widen_grad.argtypes = [vp, C.c_int32, i64, vp, vp]
         L.lf_launch_count.restype = C.c_uint64
         L.lf_profile_enable.argtypes = [C.c_int]
         L.lf_profile_enable.restype = C.c_int
@@ -81,7 +86,9 @@ def lib():
         for name in ("lf_cce_forward", "lf_cce_backward", "lf_cce_forward_partial",
                      "lf_cce_combine", "lf_cce_backward_shard", "lf_ccem_forward",
                      "lf_ccem_backward", "lf_validate_targets", "lf_validate_inds",
-                     "lf_estimate_flops", "lf_workspace_stats", "lf_workspace_reset_peak"):
+                     "lf_estimate_flops", "lf_workspace_stats", "lf_workspace_reset_peak",
+                     "lf_sample_uniform", "lf_classifier_to_items", "lf_convert_rows",
+                     "lf_items_grad_to_classifier", "lf_widen_grad"):
             getattr(L, name).restype = C.c_int
         if L.lf_abi_version() != 1:
             raise ImportError("liblseforge_b200.so ABI mismatch")
@@ -97,4 +104,6 @@ def check(rc: int) -> None:
     msg = lib().lf_last_error().decode()
     if rc == LF_EINVAL:
         raise ValueError(msg)
+    if rc == LF_ERUNTIME:  # the reference's std::runtime_error cases
+        raise RuntimeError(msg)
     raise LfError(f"[status {rc}] {msg}")

@@ -370,6 +370,12 @@ int lf_widen_grad(const void* d_src, int32_t dtype, int64_t count, double* d_dst
   return layout_widen(d_src, dtype == LF_F64 ? LF_F64 : LF_F32, count, d_dst, as_stream(stream));
 }
 
+int lf_sample_uniform(const int64_t* d_positives, int64_t n, int64_t ns, int64_t catalog,
+                      uint64_t seed, int32_t retry_cap, int64_t* d_inds, void* stream) {
+  if (retry_cap < 1) return fail(LF_EINVAL, "sample_uniform: retry_cap must be >= 1");
+  return sample_uniform(d_positives, n, ns, catalog, seed, retry_cap, d_inds, as_stream(stream));
+}
+
 int lf_estimate_flops(int64_t n, int64_t d, int64_t v, int64_t ns, int32_t backend,
                       uint64_t* forward, uint64_t* backward) {
   // ccem.cpp:207-235
