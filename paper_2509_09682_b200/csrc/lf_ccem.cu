@@ -302,7 +302,9 @@ __device__ __forceinline__ uint32_t load_item(const int64_t* inds, const uint32_
 __global__ void __launch_bounds__(kSortThreads) radix_hist(const int64_t* __restrict__ inds,
                                                            const uint32_t* __restrict__ keys,
                                                            int64_t count, int shift,
-                                                           uint32_t* __restrict__ hist) {
+                                                           uint32_t* __restrict__ hist,
+                                                           const uint32_t* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   __shared__ uint32_t h[kDigits];
   for (int i = threadIdx.x; i < kDigits; i += kSortThreads) h[i] = 0;
   __syncthreads();
@@ -321,7 +323,8 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter(
     const int64_t* __restrict__ inds, const uint32_t* __restrict__ keys_in,
     const uint32_t* __restrict__ vals_in, int64_t count, int shift,
     const uint32_t* __restrict__ offs, uint32_t* __restrict__ keys_out,
-    uint32_t* __restrict__ vals_out) {
+    uint32_t* __restrict__ vals_out, const uint32_t* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   extern __shared__ uint32_t wcnt_raw[];  // [kSortWarps][kDigits]
   uint32_t(*wcnt)[kDigits] = reinterpret_cast<uint32_t(*)[kDigits]>(wcnt_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -368,8 +371,12 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter(
 }
 
 // Exclusive scan of uint32 (3-level: tiles of 2048 -> block sums -> add).
+// `gate` (optional): device flag; 0 = this launch is a no-op (used to run the
+// radix fallback of the CCE- grouping without a host round trip).
 __global__ void scan_tiles(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
-                           int64_t count, uint32_t* __restrict__ sums) {
+                           int64_t count, uint32_t* __restrict__ sums,
+                           const uint32_t* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   __shared__ uint32_t s[1024];
   const int64_t base = static_cast<int64_t>(blockIdx.x) * 2048;
   const int64_t i0 = base + 2 * threadIdx.x;
@@ -389,15 +396,17 @@ __global__ void scan_tiles(const uint32_t* __restrict__ in, uint32_t* __restrict
   if (threadIdx.x == 1023 && sums) sums[blockIdx.x] = s[1023];
 }
 __global__ void scan_add(uint32_t* __restrict__ out, int64_t count,
-                         const uint32_t* __restrict__ sums_scanned) {
+                         const uint32_t* __restrict__ sums_scanned, const uint32_t* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < count) out[i] += sums_scanned[i / 2048];
 }
 
-int exclusive_scan(const uint32_t* in, uint32_t* out, int64_t count, cudaStream_t st) {
+int exclusive_scan(const uint32_t* in, uint32_t* out, int64_t count, cudaStream_t st,
+                   const uint32_t* gate = nullptr) {
   const int64_t tiles = ceil_div(count, 2048);
   if (tiles == 1) {
-    scan_tiles<<<1, 1024, 0, st>>>(in, out, count, nullptr);
+    scan_tiles<<<1, 1024, 0, st>>>(in, out, count, nullptr, gate);
     LF_LAUNCHED();
     return LF_OK;
   }
@@ -405,11 +414,11 @@ int exclusive_scan(const uint32_t* in, uint32_t* out, int64_t count, cudaStream_
   int rc = sums.alloc(sizeof(uint32_t) * tiles, st);
   if (!rc) rc = sums_scan.alloc(sizeof(uint32_t) * tiles, st);
   if (rc) return rc;
-  scan_tiles<<<tiles, 1024, 0, st>>>(in, out, count, sums.as<uint32_t>());
+  scan_tiles<<<tiles, 1024, 0, st>>>(in, out, count, sums.as<uint32_t>(), gate);
   LF_LAUNCHED();
-  rc = exclusive_scan(sums.as<uint32_t>(), sums_scan.as<uint32_t>(), tiles, st);
+  rc = exclusive_scan(sums.as<uint32_t>(), sums_scan.as<uint32_t>(), tiles, st, gate);
   if (rc) return rc;
-  scan_add<<<ceil_div(count, 256), 256, 0, st>>>(out, count, sums_scan.as<uint32_t>());
+  scan_add<<<ceil_div(count, 256), 256, 0, st>>>(out, count, sums_scan.as<uint32_t>(), gate);
   LF_LAUNCHED();
   return LF_OK;
 }
@@ -459,12 +468,15 @@ __global__ void __launch_bounds__(256) segment_reduce_vec(const TX* __restrict__
                                                           const uint32_t* __restrict__ sorted_vals,
                                                           const uint32_t* __restrict__ item_off,
                                                           int64_t v, int64_t w,
-                                                          float* __restrict__ dE) {
+                                                          float* __restrict__ dE, uint32_t min_len,
+                                                          const uint32_t* __restrict__ gate) {
   constexpr int DPL = D / 8;
+  if (gate && *gate == 0) return;
   const int lane = threadIdx.x & 31, g = lane >> 3, c = lane & 7;
   const int64_t item = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   if (item >= v) return;
   const uint32_t b = item_off[item], e = item_off[item + 1];
+  if (e - b <= min_len) return;  // written by segment_reduce_sorted
   float acc[DPL];
 #pragma unroll
   for (int i = 0; i < DPL; ++i) acc[i] = 0.f;
@@ -532,8 +544,24 @@ int ccem_forward(int dtype, const void* X, const void* E, const int64_t* inds, i
 
 // Sort (item, key) pairs stably by item; returns sorted keys (slot ids) and
 // per-item offsets (v+1).
-int sort_by_item(const int64_t* inds, int64_t count, int64_t v, Scratch& sorted_vals,
-                        Scratch& item_off, cudaStream_t st) {
+// Segment offsets of the entries grouped by item: item_off[v + 1].
+static int group_offsets(const int64_t* inds, int64_t count, int64_t v, Scratch& item_off,
+                         cudaStream_t st) {
+  Scratch counts;
+  int rc = counts.alloc(sizeof(uint32_t) * (v + 1), st);
+  if (!rc) rc = item_off.alloc(sizeof(uint32_t) * (v + 1), st);
+  if (rc) return rc;
+  LF_CUDA(cudaMemsetAsync(counts.ptr, 0, sizeof(uint32_t) * (v + 1), st));
+  item_hist<<<std::min<int64_t>(ceil_div(count, 256), 8 * num_sms()), 256, 0, st>>>(
+      inds, count, counts.as<uint32_t>());
+  LF_LAUNCHED();
+  return exclusive_scan(counts.as<uint32_t>(), item_off.as<uint32_t>(), v + 1, st);
+}
+
+// Entry indices stably grouped by item (LSD radix, kDigitBits per pass).
+// With `gate`, every launch is a device-side no-op unless *gate != 0.
+static int radix_group(const int64_t* inds, int64_t count, int64_t v, Scratch& sorted_vals,
+                       cudaStream_t st, const uint32_t* gate) {
   if (count >= (int64_t(1) << 32)) return fail(LF_EUNSUPPORTED, "ccem: n*w must be < 2^32");
   Scratch k0, k1, v1, hist, offs;
   int rc = k0.alloc(sizeof(uint32_t) * count, st);
@@ -543,7 +571,6 @@ int sort_by_item(const int64_t* inds, int64_t count, int64_t v, Scratch& sorted_
   const int64_t blocks = ceil_div(count, kSortTile);
   if (!rc) rc = hist.alloc(sizeof(uint32_t) * kDigits * blocks, st);
   if (!rc) rc = offs.alloc(sizeof(uint32_t) * kDigits * blocks, st);
-  if (!rc) rc = item_off.alloc(sizeof(uint32_t) * (v + 1), st);
   if (rc) return rc;
   int passes = 1;
   while (passes < 3 && ((static_cast<uint64_t>(v - 1) >> (kDigitBits * passes)) != 0)) ++passes;
@@ -558,25 +585,113 @@ int sort_by_item(const int64_t* inds, int64_t count, int64_t v, Scratch& sorted_
     const bool even_from_end = ((passes - 1 - p) % 2) == 0;
     uint32_t* kout = even_from_end ? k0.as<uint32_t>() : k1.as<uint32_t>();
     uint32_t* vout = even_from_end ? sorted_vals.as<uint32_t>() : v1.as<uint32_t>();
-    radix_hist<<<blocks, kSortThreads, 0, st>>>(inds, kin, count, kDigitBits * p, hist.as<uint32_t>());
+    radix_hist<<<blocks, kSortThreads, 0, st>>>(inds, kin, count, kDigitBits * p, hist.as<uint32_t>(),
+                                                gate);
     LF_LAUNCHED();
-    rc = exclusive_scan(hist.as<uint32_t>(), offs.as<uint32_t>(), kDigits * blocks, st);
+    rc = exclusive_scan(hist.as<uint32_t>(), offs.as<uint32_t>(), kDigits * blocks, st, gate);
     if (rc) return rc;
     radix_scatter<<<blocks, kSortThreads, kScatterSmem, st>>>(
-        inds, kin, vin, count, kDigitBits * p, offs.as<uint32_t>(), kout, vout);
+        inds, kin, vin, count, kDigitBits * p, offs.as<uint32_t>(), kout, vout, gate);
     LF_LAUNCHED();
     kin = kout;
     vin = vout;
   }
-  // item offsets
-  Scratch counts;
-  rc = counts.alloc(sizeof(uint32_t) * (v + 1), st);
-  if (rc) return rc;
-  LF_CUDA(cudaMemsetAsync(counts.ptr, 0, sizeof(uint32_t) * (v + 1), st));
-  item_hist<<<std::min<int64_t>(ceil_div(count, 256), 8 * num_sms()), 256, 0, st>>>(
-      inds, count, counts.as<uint32_t>());
-  LF_LAUNCHED();
-  return exclusive_scan(counts.as<uint32_t>(), item_off.as<uint32_t>(), v + 1, st);
+  return LF_OK;
+}
+
+int sort_by_item(const int64_t* inds, int64_t count, int64_t v, Scratch& sorted_vals,
+                 Scratch& item_off, cudaStream_t st, const uint32_t* gate) {
+  int rc = radix_group(inds, count, v, sorted_vals, st, gate);
+  if (!rc) rc = group_offsets(inds, count, v, item_off, st);
+  return rc;
+}
+
+// Unstable grouping: each entry claims the next free position of its item's
+// segment (cursor[v] starts at item_off[v]).  Order inside a segment is
+// arbitrary; segment_reduce_sorted restores index order.
+__global__ void scatter_by_item(const int64_t* __restrict__ inds, int64_t count,
+                                uint32_t* __restrict__ cursor, uint32_t* __restrict__ grouped) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    grouped[atomicAdd(&cursor[inds[i]], 1u)] = static_cast<uint32_t>(i);
+}
+
+// Ascending bitonic sort of 64 keys held as k[r] at index r*32 + lane.
+__device__ __forceinline__ void warp_sort64(uint32_t (&k)[2]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int size = 2; size <= 64; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride == 32) {
+        const uint32_t lo = min(k[0], k[1]), hi = max(k[0], k[1]);
+        k[0] = lo;
+        k[1] = hi;
+      } else {
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int idx = r * 32 + lane;
+          const uint32_t other = __shfl_xor_sync(0xffffffffu, k[r], stride);
+          const bool up = (idx & size) == 0;
+          const bool lower = (idx & stride) == 0;
+          k[r] = (lower == up) ? min(k[r], other) : max(k[r], other);
+        }
+      }
+    }
+  }
+}
+
+// dE for items with at most 64 entries, in entry-index order (the unstable
+// grouping sorted back per segment), four X rows in flight, partial sums
+// combined in a fixed order.  Longer segments set *long_flag and are left to
+// segment_reduce_long (radix-grouped).
+template <class TX, int D>
+__global__ void __launch_bounds__(256) segment_reduce_sorted(
+    const TX* __restrict__ X, const float* __restrict__ coeff, const uint32_t* __restrict__ grouped,
+    const uint32_t* __restrict__ item_off, int64_t v, int64_t w, float* __restrict__ dE,
+    uint32_t* __restrict__ long_flag) {
+  constexpr int DPL = D / 8;
+  const int lane = threadIdx.x & 31, g = lane >> 3, c = lane & 7;
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (item >= v) return;
+  const uint32_t b = item_off[item], L = item_off[item + 1] - b;
+  if (L > 64) {
+    if (lane == 0) *long_flag = 1u;
+    return;
+  }
+  uint32_t k[2];
+  k[0] = lane < static_cast<int>(L) ? grouped[b + lane] : 0xffffffffu;
+  k[1] = lane + 32 < static_cast<int>(L) ? grouped[b + 32 + lane] : 0xffffffffu;
+  if (L > 1) warp_sort64(k);
+  float acc[DPL];
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) acc[i] = 0.f;
+  for (uint32_t j0 = 0; j0 < L; j0 += 4) {
+    const uint32_t j = j0 + g;
+    const uint32_t key = __shfl_sync(0xffffffffu, j0 < 32 ? k[0] : k[1], static_cast<int>(j & 31));
+    if (j < L) {
+      const float gk = __ldg(coeff + key);
+      const TX* xr = X + static_cast<int64_t>(key / w) * D + c * DPL;
+#pragma unroll
+      for (int q = 0; q < DPL / 8; ++q) {
+        float f[8];
+        Vec8<TX>::load(xr + 8 * q, f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[8 * q + i] = fmaf(gk, f[i], acc[8 * q + i]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) {
+    acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 8);
+    acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 16);
+  }
+  if (g == 0) {
+#pragma unroll
+    for (int i = 0; i < DPL; i += 4)
+      *reinterpret_cast<float4*>(dE + item * D + c * DPL + i) =
+          make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+  }
 }
 
 int ccem_backward(int dtype, const void* X, const void* E, const int64_t* inds,
@@ -628,16 +743,49 @@ int ccem_backward(int dtype, const void* X, const void* E, const int64_t* inds,
         row_upstream, u_n, static_cast<double*>(dX), coeff.as<double>());
     LF_LAUNCHED();
   }
-  Scratch sorted_vals, item_off;
-  int rc = sort_by_item(inds, count, v, sorted_vals, item_off, st);
-  if (rc) return rc;
   const dim3 sgrid(static_cast<unsigned>(ceil_div(v, 8)));
   if (vec) {
+    // Deterministic dE without a full sort when segments are short (uniform
+    // negatives: ~26 entries per item at cfg3): segment offsets, an unstable
+    // atomic grouping, then one warp per item sorts its <= 64 entry indices
+    // back into index order and reduces.  Items with longer segments raise a
+    // device flag; only then do the (gated, otherwise no-op) radix grouping
+    // and the long-segment reduce run — no host round trip either way.
+    if (count >= (int64_t(1) << 32)) return fail(LF_EUNSUPPORTED, "ccem: n*w must be < 2^32");
+    Scratch item_off, cursor, grouped, flag, sorted_vals;
+    int rc = group_offsets(inds, count, v, item_off, st);
+    if (!rc) rc = cursor.alloc(sizeof(uint32_t) * v, st);
+    if (!rc) rc = grouped.alloc(sizeof(uint32_t) * count, st);
+    if (!rc) rc = flag.alloc(sizeof(uint32_t), st);
+    if (rc) return rc;
+    LF_CUDA(cudaMemcpyAsync(cursor.ptr, item_off.ptr, sizeof(uint32_t) * v, cudaMemcpyDeviceToDevice, st));
+    LF_CUDA(cudaMemsetAsync(flag.ptr, 0, sizeof(uint32_t), st));
+    scatter_by_item<<<std::min<int64_t>(ceil_div(count, 256), 16 * num_sms()), 256, 0, st>>>(
+        inds, count, cursor.as<uint32_t>(), grouped.as<uint32_t>());
+    LF_LAUNCHED();
+#define LF_SEG2(TX, DD)                                                                           \
+  segment_reduce_sorted<TX, DD><<<sgrid, 256, 0, st>>>(                                          \
+      static_cast<const TX*>(X), coeff.as<float>(), grouped.as<uint32_t>(), item_off.as<uint32_t>(), \
+      v, w, static_cast<float*>(dE), flag.as<uint32_t>())
+    if (dtype == LF_BF16) {
+      if (D == 64) LF_SEG2(__nv_bfloat16, 64);
+      else if (D == 128) LF_SEG2(__nv_bfloat16, 128);
+      else LF_SEG2(__nv_bfloat16, 256);
+    } else {
+      if (D == 64) LF_SEG2(float, 64);
+      else if (D == 128) LF_SEG2(float, 128);
+      else LF_SEG2(float, 256);
+    }
+#undef LF_SEG2
+    LF_LAUNCHED();
+    rc = radix_group(inds, count, v, sorted_vals, st, flag.as<uint32_t>());
+    if (rc) return rc;
 #define LF_SEG(TX, DD)                                                                          \
   segment_reduce_vec<TX, DD><<<sgrid, 256, 0, st>>>(static_cast<const TX*>(X), coeff.as<float>(), \
                                                     sorted_vals.as<uint32_t>(),                \
                                                     item_off.as<uint32_t>(), v, w,             \
-                                                    static_cast<float*>(dE))
+                                                    static_cast<float*>(dE), 64u,              \
+                                                    flag.as<uint32_t>())
     if (dtype == LF_BF16) {
       if (D == 64) LF_SEG(__nv_bfloat16, 64);
       else if (D == 128) LF_SEG(__nv_bfloat16, 128);
@@ -648,7 +796,13 @@ int ccem_backward(int dtype, const void* X, const void* E, const int64_t* inds,
       else LF_SEG(float, 256);
     }
 #undef LF_SEG
-  } else if (dtype == LF_F32) {
+    LF_LAUNCHED();
+    return LF_OK;
+  }
+  Scratch sorted_vals, item_off;
+  int rc = sort_by_item(inds, count, v, sorted_vals, item_off, st);
+  if (rc) return rc;
+  if (dtype == LF_F32) {
     segment_reduce<float, float, float><<<sgrid, 256, 0, st>>>(
         static_cast<const float*>(X), coeff.as<float>(), sorted_vals.as<uint32_t>(),
         item_off.as<uint32_t>(), v, D, w, static_cast<float*>(dE));

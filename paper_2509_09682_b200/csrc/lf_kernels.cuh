@@ -59,7 +59,7 @@ int ccem_backward(int dtype, const void* X, const void* E, const int64_t* inds,
 // [0, v)): sorted_vals = entry indices grouped by item in index order,
 // item_off[v + 1] = segment offsets (lf_ccem.cu).
 int sort_by_item(const int64_t* inds, int64_t count, int64_t v, Scratch& sorted_vals,
-                 Scratch& item_off, cudaStream_t st);
+                 Scratch& item_off, cudaStream_t st, const uint32_t* gate = nullptr);
 
 // ---- negative sampler (lf_sampler.cu) ----
 int sample_uniform(const int64_t* positives, int64_t n, int64_t ns, int64_t catalog,
