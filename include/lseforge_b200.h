@@ -146,6 +146,19 @@ LF_API int lf_ccem_backward(const void* d_X, const void* d_E, const int64_t* d_i
                      int64_t v, int64_t w, const lf_cce_config* cfg, void* d_dX, void* d_dE,
                      void* stream);
 
+/* ------------------------------------------- materialising CE baseline ---- */
+/* Replace lseforge::ce_full_forward / ce_full_backward (losses.cpp:71-140):
+ * the baseline CCE is measured against.  The n x v logit matrix IS written
+ * to device memory (fp32; fp64 for LF_F64) by a cuBLAS GEMM, plus a n x v
+ * coefficient matrix in the backward — peak scratch ~6 n v bytes for bf16.
+ * Same outputs and layouts as lf_cce_forward / lf_cce_backward (no filter). */
+LF_API int lf_ce_forward(const void* d_X, const void* d_E, const int64_t* d_targets, int64_t n,
+                         int64_t d, int64_t v, const lf_cce_config* cfg, double* d_lse,
+                         double* d_pos, double* d_loss, void* stream);
+LF_API int lf_ce_backward(const void* d_X, const void* d_E, const int64_t* d_targets,
+                          double upstream, int64_t n, int64_t d, int64_t v,
+                          const lf_cce_config* cfg, void* d_dX, void* d_dE, void* stream);
+
 /* ------------------------------------------------------- negative sampler -- */
 /* Replaces lseforge::sample_uniform (sampler.hpp, sampler.cpp:44-75) with a
  * device restatement that produces the SAME indices: row i draws from

@@ -11,14 +11,15 @@ from .accountant import MemAccountant, Report, ScalarKind
 from .cce import CceBackwardResult, CceConfig, cce_backward, cce_forward, kFp16MinPositive
 from .ccem import (Backend, FlopEstimate, backend_is_sampled, ccem_backward, ccem_backward_rows,
                    ccem_forward, estimate_flops)
-from .losses import GradPair, LossOutput, validate_loss_inputs
+from .losses import GradPair, LossOutput, ce_full_backward, ce_full_forward, validate_loss_inputs
 from .sampler import sample_uniform
 
 __all__ = [
     "CceConfig", "CceBackwardResult", "cce_forward", "cce_backward", "kFp16MinPositive",
     "ccem_forward", "ccem_backward", "ccem_backward_rows", "estimate_flops", "FlopEstimate",
     "Backend", "backend_is_sampled", "LossOutput", "GradPair", "validate_loss_inputs",
-    "MemAccountant", "Report", "ScalarKind", "sample_uniform", "lib",
+    "MemAccountant", "Report", "ScalarKind", "sample_uniform", "ce_full_forward",
+    "ce_full_backward", "lib",
 ]
 
 

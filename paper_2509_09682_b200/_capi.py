@@ -25,6 +25,7 @@ EXPORTS = (
     "lf_workspace_stats", "lf_workspace_reset_peak", "lf_launch_count", "lf_launch_count_reset",
     "lf_profile_enable", "lf_profile_read", "lf_profile_reset", "lf_classifier_to_items",
     "lf_convert_rows", "lf_items_grad_to_classifier", "lf_widen_grad", "lf_sample_uniform",
+    "lf_ce_forward", "lf_ce_backward",
 )
 KERNEL_KINDS = ("cce_fwd", "cce_bwd_dx", "cce_bwd_de", "cce_simt", "ccem_fwd", "ccem_bwd", "aux")
 
@@ -74,6 +75,8 @@ def lib():
                                         C.POINTER(C.c_uint64)]
         L.lf_workspace_stats.argtypes = [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         L.lf_sample_uniform.argtypes = [vp, i64, i64, i64, C.c_uint64, C.c_int32, vp, vp]
+        L.lf_ce_forward.argtypes = [vp, vp, vp, i64, i64, i64, cfgp, dp, dp, dp, vp]
+        L.lf_ce_backward.argtypes = [vp, vp, vp, C.c_double, i64, i64, i64, cfgp, vp, vp, vp]
         L.lf_classifier_to_items.argtypes = [vp, i64, i64, C.c_int32, vp, vp]
         L.lf_convert_rows.argtypes = [vp, i64, C.c_int32, vp, vp]
         L.lf_items_grad_to_classifier.argtypes = [vp, C.c_int32, i64, i64, vp, vp]
@@ -88,7 +91,8 @@ def lib():
                      "lf_ccem_backward", "lf_validate_targets", "lf_validate_inds",
                      "lf_estimate_flops", "lf_workspace_stats", "lf_workspace_reset_peak",
                      "lf_sample_uniform", "lf_classifier_to_items", "lf_convert_rows",
-                     "lf_items_grad_to_classifier", "lf_widen_grad"):
+                     "lf_items_grad_to_classifier", "lf_widen_grad", "lf_ce_forward",
+                     "lf_ce_backward"):
             getattr(L, name).restype = C.c_int
         if L.lf_abi_version() != 1:
             raise ImportError("liblseforge_b200.so ABI mismatch")

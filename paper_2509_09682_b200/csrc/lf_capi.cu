@@ -370,6 +370,26 @@ int lf_widen_grad(const void* d_src, int32_t dtype, int64_t count, double* d_dst
   return layout_widen(d_src, dtype == LF_F64 ? LF_F64 : LF_F32, count, d_dst, as_stream(stream));
 }
 
+int lf_ce_forward(const void* d_X, const void* d_E, const int64_t* d_targets, int64_t n,
+                  int64_t d, int64_t v, const lf_cce_config* cfg, double* d_lse, double* d_pos,
+                  double* d_loss, void* stream) {
+  int rc = check_cfg(cfg);
+  if (!rc) rc = check_shapes(n, d, v);
+  if (rc) return rc;
+  return ce_forward(cfg->dtype, d_X, d_E, d_targets, n, static_cast<int>(d), v, d_lse, d_pos,
+                    d_loss, as_stream(stream));
+}
+
+int lf_ce_backward(const void* d_X, const void* d_E, const int64_t* d_targets, double upstream,
+                   int64_t n, int64_t d, int64_t v, const lf_cce_config* cfg, void* d_dX,
+                   void* d_dE, void* stream) {
+  int rc = check_cfg(cfg);
+  if (!rc) rc = check_shapes(n, d, v);
+  if (rc) return rc;
+  return ce_backward(cfg->dtype, d_X, d_E, d_targets, upstream, n, static_cast<int>(d), v, d_dX,
+                     d_dE, as_stream(stream));
+}
+
 int lf_sample_uniform(const int64_t* d_positives, int64_t n, int64_t ns, int64_t catalog,
                       uint64_t seed, int32_t retry_cap, int64_t* d_inds, void* stream) {
   if (retry_cap < 1) return fail(LF_EINVAL, "sample_uniform: retry_cap must be >= 1");

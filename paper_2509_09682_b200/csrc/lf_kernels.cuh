@@ -61,6 +61,12 @@ int ccem_backward(int dtype, const void* X, const void* E, const int64_t* inds,
 int sort_by_item(const int64_t* inds, int64_t count, int64_t v, Scratch& sorted_vals,
                  Scratch& item_off, cudaStream_t st, const uint32_t* gate = nullptr);
 
+// ---- materialising CE baseline (lf_ce.cu; cuBLAS GEMMs) ----
+int ce_forward(int dtype, const void* X, const void* E, const int64_t* targets, int64_t n, int D,
+               int64_t v, double* lse, double* pos, double* loss, cudaStream_t st);
+int ce_backward(int dtype, const void* X, const void* E, const int64_t* targets, double upstream,
+                int64_t n, int D, int64_t v, void* dX, void* dE, cudaStream_t st);
+
 // ---- negative sampler (lf_sampler.cu) ----
 int sample_uniform(const int64_t* positives, int64_t n, int64_t ns, int64_t catalog,
                    uint64_t seed, int retry_cap, int64_t* inds, cudaStream_t st);

@@ -77,3 +77,43 @@ def validate_loss_inputs(X: torch.Tensor, E: torch.Tensor, x: torch.Tensor,
     if check_range:
         st = torch.cuda.current_stream(X.device).cuda_stream if stream is None else stream
         _capi.check(_capi.lib().lf_validate_targets(x.data_ptr(), X.shape[0], E.shape[0], st))
+
+
+def _stream(t: torch.Tensor) -> int:
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def ce_full_forward(X: torch.Tensor, E: torch.Tensor, x: torch.Tensor,
+                    validate: bool = True) -> LossOutput:
+    """losses.cpp:71-96 — the MATERIALISING baseline: the n x v logit matrix is
+    written to device memory (cuBLAS GEMM) before the row log-sum-exp."""
+    import ctypes as C
+    validate_loss_inputs(X, E, x, check_range=validate)
+    n, d = X.shape
+    v = E.shape[0]
+    lse = torch.empty(n, dtype=torch.float64, device=X.device)
+    pos = torch.empty(n, dtype=torch.float64, device=X.device)
+    loss = torch.empty((), dtype=torch.float64, device=X.device)
+    c = _capi.CceConfigC(0.0, lf_dtype(X), 0)
+    _capi.check(_capi.lib().lf_ce_forward(X.data_ptr(), E.data_ptr(), x.data_ptr(), n, d, v,
+                                          C.byref(c), lse.data_ptr(), pos.data_ptr(),
+                                          loss.data_ptr(), _stream(X)))
+    return LossOutput(loss, pos, lse)
+
+
+def ce_full_backward(X: torch.Tensor, E: torch.Tensor, x: torch.Tensor, upstream: float = 1.0,
+                     validate: bool = True) -> GradPair:
+    """losses.cpp:98-140 — recomputes and materialises the logits and an n x v
+    coefficient matrix, then two cuBLAS GEMMs for dX and dE."""
+    import ctypes as C
+    validate_loss_inputs(X, E, x, check_range=validate)
+    n, d = X.shape
+    v = E.shape[0]
+    gd = grad_dtype(X)
+    dX = torch.empty((n, d), dtype=gd, device=X.device)
+    dE = torch.empty((v, d), dtype=gd, device=X.device)
+    c = _capi.CceConfigC(0.0, lf_dtype(X), 0)
+    _capi.check(_capi.lib().lf_ce_backward(X.data_ptr(), E.data_ptr(), x.data_ptr(),
+                                           float(upstream), n, d, v, C.byref(c), dX.data_ptr(),
+                                           dE.data_ptr(), _stream(X)))
+    return GradPair(dX, dE)
