@@ -36,12 +36,6 @@
 #ifndef LF_POLY_BWD
 #define LF_POLY_BWD 0
 #endif
-#ifndef LF_PRESEL
-#define LF_PRESEL 0
-#endif
-#ifndef LF_SWP
-#define LF_SWP 0
-#endif
 #ifndef LF_NWG_FWD
 #define LF_NWG_FWD 2
 #endif
@@ -149,22 +143,17 @@ __device__ __forceinline__ float ex2_mix(int c, float a) {
   return ex2_approx(a);
 }
 
-// Backward filter domain.  The exp argument a = S log2e - lse2 is offset so
-// that a < kThr exactly when softmax < eps.  kPreSel (filtered kernels): lse2
-// also carries +64 (kPreA) and the flush is a select BEFORE the MUFU; else
-// ex2.approx.ftz flushes a < -126 and the result is scaled by 2^64 after.
-constexpr bool kPreSel = LF_PRESEL != 0;
-constexpr bool kSwp = LF_SWP != 0;
+// Backward filter domain: the exp argument a = S log2e - lse2 is offset so
+// that a < kThr (= -126) exactly when softmax < eps; ex2.approx.ftz flushes
+// those results and the survivors are scaled by 2^64 after the MUFU.
 template <int FLAGS>
-constexpr int kPreA = ((FLAGS & kFilt) && kPreSel) ? 64 : 0;
-template <int FLAGS>
-constexpr float kThr = -126.f + static_cast<float>(kPreA<FLAGS>);
+constexpr float kThr = -126.f;
 
 // Backward coefficient of a row's own target column (never filtered).
 template <int FLAGS>
 __device__ __forceinline__ float target_g(float e, uint32_t raw, float l, float t_scale) {
   if (FLAGS & kFilt)
-    return ex2_approx(fmaf(__uint_as_float(raw), kLog2e, -l) + static_cast<float>(64 - kPreA<FLAGS>)) -
+    return ex2_approx(fmaf(__uint_as_float(raw), kLog2e, -l) + 64.f) -
            t_scale;
   return e - t_scale;
 }
@@ -500,7 +489,6 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
           constexpr bool TEST = decltype(test_tag)::value;
           bool any_below = false;
           uint32_t ra[32], rb[32];
-          float xp[32];  // kSwp: previous chunk's coefficients
           float lcur[32], lnext[32];  // BWD_ITEMS: per-column lse2 (chunk q, q + 1)
           if (MODE == BWD_ITEMS) {
 #pragma unroll
@@ -588,15 +576,11 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
               for (int c = 0; c < 32; ++c) {
                 if (c >= 32 - kPolyBwd) {  // FMA-pipe share of the exps
                   if (FLAGS & kFilt) {
-                    const float y = ex2_fma_shl<64 - kPreA<FLAGS>>(e[c]);
+                    const float y = ex2_fma_shl<64>(e[c]);
                     x[c] = e[c] < kThr<FLAGS> ? 0.f : y;
                   } else {
                     x[c] = ex2_fma(fmaxf(e[c], -125.f));
                   }
-                } else if ((FLAGS & kFilt) && kPreSel) {
-                  // flush decided before the MUFU: nothing waits on its result
-                  // except the bf16 pack
-                  x[c] = ex2_approx(e[c] < kThr<FLAGS> ? -INFINITY : e[c]);
                 } else {
 #ifdef LF_DIAG_NOEXP
                   x[c] = e[c];  // timing diagnostic only: wrong results
@@ -628,30 +612,13 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
                 }
               }
             }
-            if (kSwp) {
-              // software pipeline: pack and store the PREVIOUS chunk, so the
-              // MUFU results of this one are consumed a full chunk later
-              if (q > 0) {
-                uint32_t g[16];
-#pragma unroll
-                for (int c = 0; c < 16; ++c) g[c] = pack_bf16x2(xp[2 * c], xp[2 * c + 1]);
-                LF_TMEM_ST16(ta + (q - 1) * 16, g);
-              }
-#pragma unroll
-              for (int c = 0; c < 32; ++c) xp[c] = x[c];
-            } else {
+            {
               uint32_t g[16];
 #pragma unroll
               for (int c = 0; c < 16; ++c) g[c] = pack_bf16x2(x[2 * c], x[2 * c + 1]);
               LF_TMEM_ST16(ta + q * 16, g);
             }
             if (q + 1 < NQ) tmem_ld_wait();
-          }
-          if (kSwp) {
-            uint32_t g[16];
-#pragma unroll
-            for (int c = 0; c < 16; ++c) g[c] = pack_bf16x2(xp[2 * c], xp[2 * c + 1]);
-            LF_TMEM_ST16(ta + (NQ - 1) * 16, g);
           }
           return any_below;
           };
@@ -929,8 +896,7 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
   const bool count = filt && counters != nullptr;
   const bool tgt_in = filt && (count || eps >= 0x1p-12);
   const int flags = filt ? (kFilt | (count ? kCount : 0) | (tgt_in ? kTgtIn : 0)) : 0;
-  const double sub = filt ? -std::log2(eps) - 126.0 + (kPreSel ? 64.0 : 0.0)
-                          : std::log2(std::fabs(scale));
+  const double sub = filt ? -std::log2(eps) - 126.0 : std::log2(std::fabs(scale));
   const double gscale = filt ? std::ldexp(1.0, -62) / eps : std::fabs(scale);
   const double out_scale = filt ? scale * eps * std::ldexp(1.0, 62) : (scale < 0 ? -1.0 : 1.0);
   constexpr int BN = Geo<BWD_ROWS>::BN;
