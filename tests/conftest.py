@@ -13,10 +13,14 @@ def pytest_configure(config):
 
 
 def _ensure_built():
-    """Build the CPU checkers if they are missing (here only; the GPU box gets
-    the prebuilt files with the snapshot)."""
+    """Build what the tests load if it is missing (a fresh checkout: built
+    files are git-ignored): the CPU checkers and the CUDA library (nvcc
+    cross-compiles for sm_100a without a GPU).  The GPU box gets the prebuilt
+    files with the snapshot."""
     if not os.path.exists(os.path.join(ROOT, "oracle", "liboracle.so")):
         os.system(f"make -s -C {os.path.join(ROOT, 'oracle')} {os.path.join(ROOT, 'oracle', 'liboracle.so')}")
+    if not os.path.exists(os.path.join(ROOT, "paper_2509_09682_b200", "liblseforge_b200.so")):
+        os.system(f"make -s -j8 -C {os.path.join(ROOT, 'paper_2509_09682_b200')}")
 
 
 _ensure_built()
