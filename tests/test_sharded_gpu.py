@@ -42,3 +42,30 @@ def test_sharded_equals_unsharded(cuda, dtype, d, P):
     check_grad(dE, dC_o.T, dtype, "dE")
     tol = 0.0 if dtype == torch.float64 else 2e-3
     assert abs(skipped / (n * (v - 1)) - frac) <= tol
+
+
+@pytest.mark.parametrize("d,P,v,n", [(128, 8, 262144, 512), (256, 8, 131072, 256)])
+def test_sharded_config_shapes_reduced_catalog(cuda, d, P, v, n):
+    """cfg4 (D=128) and cfg5 (D=256) geometry through the 8-way sharded code
+    path at a reduced catalog (parity at reduced V), bf16,
+    eps = 6e-8, production kernels (no stats): loss, lse and both gradients
+    against the filtered oracle."""
+    import paper_2509_09682_b200 as lf
+    from paper_2509_09682_b200.sharded import DeviceKernels, shard_bounds
+    X, E, x, Eh, Ch, t = instance(0xC0F4 + d, n, d, v, torch.bfloat16)
+    cfg = lf.CceConfig(filter_eps=6e-8)
+    K = DeviceKernels()
+    bounds = [shard_bounds(v, P, p) for p in range(P)]
+    parts = torch.stack([K.forward_partial(X, E[b:e], x, b, cfg) for b, e in bounds])
+    out = K.combine(parts)
+    loss, pos, lse = ob.cce_forward(Eh, Ch, t)
+    assert ob.rel_err(float(out.loss), loss) < 1e-2
+    assert ob.rel_err(out.lse.cpu().numpy(), lse).max() < 1e-3
+    dX, dE = None, []
+    for b, e in bounds:
+        dx, de, _ = K.backward_shard(X, E[b:e], x, out.lse, 1.0, b, v, cfg, False)
+        dX = dx if dX is None else dX + dx
+        dE.append(de)
+    dX_o, dC_o, _, _ = ob.cce_backward(Eh, Ch, t, lse, 1.0, 6e-8)
+    check_grad(dX, dX_o, torch.bfloat16, "dX")
+    check_grad(torch.cat(dE), dC_o.T, torch.bfloat16, "dE")
