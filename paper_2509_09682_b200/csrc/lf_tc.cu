@@ -118,15 +118,21 @@ struct Cfg {
   static constexpr int kAtoms = D / 64;               // 128-byte K atoms per row
   static constexpr int kOwnerBytes = BM * D * 2;
   static constexpr int kTileBytes = BN * D * 2;
-  static constexpr int kExtraBytes = MODE == BWD_ITEMS ? 1024 : 0;  // lse2[BN] + tgt[BN] (padded)
+  // BWD_ITEMS stage extras: lse2[BN] + tgt[BN] (1 KB, padded), then the
+  // stream rows' bias columns (BN rows x 16 bf16 = 32 B, SWIZZLE_32B) that
+  // fold -lse2 into the S MMA as a fifth K=16 step.
+  static constexpr int kBiasOff = kTileBytes + 1024;
+  static constexpr int kBiasBytes = BN * 32;
+  static constexpr int kExtraBytes = MODE == BWD_ITEMS ? 1024 + kBiasBytes : 0;
   static constexpr int kStageBytes = kTileBytes + kExtraBytes;
-  static constexpr int kStagesFit = (200 * 1024 - kOwnerBytes) / kStageBytes;
+  static constexpr int kOnesBytes = MODE == BWD_ITEMS ? BM * 32 : 0;  // constant A bias columns
+  static constexpr int kStagesFit = (200 * 1024 - kOwnerBytes - kOnesBytes) / kStageBytes;
   static constexpr int kStages = kStagesFit > 12 ? 12 : kStagesFit;
   static constexpr int kNBMax = (MODE == FWD ? 512 : 512 - D) / BN;  // S buffers that fit in TMEM
   static constexpr int kNB = kNBMax > 8 ? 8 : kNBMax;
   static_assert(MODE == FWD || kNB >= 2, "not enough TMEM for the backward pipeline");
   static constexpr int kAccCol = kNB * BN;
-  static constexpr int kSmem = 1024 /*align slack*/ + kOwnerBytes + kStages * kStageBytes +
+  static constexpr int kSmem = 1024 /*align slack*/ + kOwnerBytes + kOnesBytes + kStages * kStageBytes +
                                1024 /*barriers*/ + (MODE == FWD ? (G::NWG - 1) * BM * 16 : 0);
 };
 __device__ __forceinline__ float fma_log2(float v, float sub) { return fmaf(v, kLog2e, -sub); }
@@ -183,7 +189,9 @@ __device__ __forceinline__ float select_reg(const float (&r)[N], int idx) {
 template <int D, int MODE, int FLAGS>
 __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
     cce_tc_kernel(const __grid_constant__ CUtensorMap map_owner,
-                  const __grid_constant__ CUtensorMap map_stream, const TcParams p) {
+                  const __grid_constant__ CUtensorMap map_stream,
+                  const __grid_constant__ CUtensorMap map_lsex,
+                  const __grid_constant__ CUtensorMap map_ones, const TcParams p) {
   using C = Cfg<D, MODE>;
   using G = Geo<MODE>;
   constexpr int BN = G::BN;
@@ -195,7 +203,8 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
   // (ordinary loads through it compile to LDS, not generic LD).
   unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   unsigned char* owner_smem = base;
-  unsigned char* stage_smem = base + C::kOwnerBytes;
+  unsigned char* ones_smem = base + C::kOwnerBytes;  // BWD_ITEMS: [1,1,1,0..] per owner row
+  unsigned char* stage_smem = base + C::kOwnerBytes + C::kOnesBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(stage_smem + C::kStages * C::kStageBytes);
   uint64_t* full = bars;                      // [kStages]
   uint64_t* empty = full + C::kStages;        // [kStages]
@@ -248,21 +257,24 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
         const int64_t s_begin = chunk * p.chunk;
         const int64_t s_end = min(p.n_stream, s_begin + p.chunk);
         mbar_wait(owner_empty, (j & 1) ^ 1);
-        mbar_arrive_expect_tx(owner_full, C::kOwnerBytes);
+        mbar_arrive_expect_tx(owner_full, C::kOwnerBytes + C::kOnesBytes);
 #pragma unroll
         for (int a = 0; a < C::kAtoms; ++a)
           tma_load_2d(owner_smem + a * BM * 128, &map_owner, owner_full, a * 64,
                       static_cast<int32_t>(ot * BM), pol);
+        if (MODE == BWD_ITEMS) tma_load_2d(ones_smem, &map_ones, owner_full, 0, 0, pol);
         for (int64_t s0 = s_begin; s0 < s_end; s0 += BN, rs.next()) {
           unsigned char* stg = stage_smem + rs.i * C::kStageBytes;
           mbar_wait(&empty[rs.i], rs.ph ^ 1);
           // BWD_ITEMS also stages the stream rows' lse2 and local targets.
-          mbar_arrive_expect_tx(&full[rs.i], C::kTileBytes + (MODE == BWD_ITEMS ? 8 * BN : 0));
+          mbar_arrive_expect_tx(&full[rs.i],
+                                C::kTileBytes + (MODE == BWD_ITEMS ? 8 * BN + C::kBiasBytes : 0));
 #pragma unroll
           for (int a = 0; a < C::kAtoms; ++a)
             tma_load_2d(stg + a * BN * 128, &map_stream, &full[rs.i], a * 64,
                         static_cast<int32_t>(s0), pol);
           if (MODE == BWD_ITEMS) {
+            tma_load_2d(stg + C::kBiasOff, &map_lsex, &full[rs.i], 0, static_cast<int32_t>(s0), pol);
             bulk_load(stg + C::kTileBytes, p.lse2 + s0, 4 * BN, &full[rs.i]);
             bulk_load(stg + C::kTileBytes + 512, p.tgt + s0, 4 * BN, &full[rs.i]);
           }
@@ -280,6 +292,10 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
     constexpr uint32_t hi = umma_desc_hi_sw128(1024);
     const uint32_t a_lo = umma_desc_lo(smem_u32(owner_smem), 16);
     const uint32_t b_lo = umma_desc_lo(smem_u32(stage_smem), 16);
+    // SWIZZLE_32B K-major operands of the bias step: rows of 32 B, 8-row
+    // groups 256 B apart
+    constexpr uint32_t hi32 = umma_desc_hi_sw32(256);
+    const uint32_t ones_lo = umma_desc_lo(smem_u32(ones_smem), 16);
     Ring<C::kStages> s1;
     Ring<C::kNB> b1;
     uint32_t j = 0;
@@ -303,6 +319,12 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
             const uint32_t koffb = (kk >> 2) * (BN * 128) + (kk & 3) * 32;
             mma_ss(tmem + b1.i * BN, umma_desc(a_lo + (koff >> 4), hi),
                    umma_desc(lo + (koffb >> 4), hi), idesc1, kk > 0 ? 1u : 0u);
+          }
+          if (MODE == BWD_ITEMS) {
+            // fifth K = 16 step: [1, 1, 1, 0..] (owner) x [c1, c2, c3, 0..] (stream
+            // row), c1 + c2 + c3 = -lse2 ln 2 in three bf16 parts: S' = S - lse2 ln 2
+            mma_ss(tmem + b1.i * BN, umma_desc(ones_lo, hi32), umma_desc(lo + (C::kBiasOff >> 4), hi32),
+                   idesc1, 1u);
           }
           mma_commit(&s_full[b1.i]);
           if (MODE == FWD) mma_commit(&empty[s1.i]);
@@ -489,17 +511,6 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
           constexpr bool TEST = decltype(test_tag)::value;
           bool any_below = false;
           uint32_t ra[32], rb[32];
-          float lcur[32], lnext[32];  // BWD_ITEMS: per-column lse2 (chunk q, q + 1)
-          if (MODE == BWD_ITEMS) {
-#pragma unroll
-            for (int c = 0; c < 32; c += 4) {
-              const float4 lp = *reinterpret_cast<const float4*>(lse2s + c);
-              lcur[c] = lp.x;
-              lcur[c + 1] = lp.y;
-              lcur[c + 2] = lp.z;
-              lcur[c + 3] = lp.w;
-            }
-          }
           LF_TMEM_LD32(ta, ra);
           tmem_ld_wait();
 #ifdef LF_DIAG_EARLY  // timing diagnostic only (wrong results): hand G over before computing it
@@ -512,27 +523,12 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
             uint32_t(&cur)[32] = (q & 1) ? rb : ra;
             uint32_t(&nxt)[32] = (q & 1) ? ra : rb;
             if (q + 1 < NQ) LF_TMEM_LD32(ta + (q + 1) * 32, nxt);
-            // BWD_ITEMS: the stream rows' lse2 of this chunk were loaded one
-            // chunk ahead (lcur), the next chunk's are fetched now (lnext), so
-            // the shared-memory latency never sits in front of the FFMAs.
-            if (MODE == BWD_ITEMS && q + 1 < NQ) {
-#pragma unroll
-              for (int c = 0; c < 32; c += 4) {
-                const float4 lp = *reinterpret_cast<const float4*>(lse2s + (q + 1) * 32 + c);
-                lnext[c] = lp.x;
-                lnext[c + 1] = lp.y;
-                lnext[c + 2] = lp.z;
-                lnext[c + 3] = lp.w;
-              }
-            }
             float e[32];
 #pragma unroll
             for (int c = 0; c < 32; ++c)
-              e[c] = fmaf(__uint_as_float(cur[c]), kLog2e, MODE == BWD_ITEMS ? -lcur[c] : -lse2);
-            if (MODE == BWD_ITEMS) {
-#pragma unroll
-              for (int c = 0; c < 32; ++c) lcur[c] = lnext[c];
-            }
+              e[c] = MODE == BWD_ITEMS ? __uint_as_float(cur[c]) * kLog2e
+                                       : fmaf(__uint_as_float(cur[c]), kLog2e, -lse2);
+
             // BWD_ITEMS: lane k checks stream row q*32+k; hm = rows of this chunk
             // whose target item lies in the owner tile (warp-uniform, rare).
             int tq = 0;
@@ -604,7 +600,7 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
                   hm &= hm - 1u;
                   const int li = __shfl_sync(0xffffffffu, tq, jc);
                   if (li == lrow) {
-                    const float lj = lse2s[q * 32 + jc];
+                    const float lj = 0.f;  // S' already carries -lse2 ln 2
 #pragma unroll
                     for (int c = 0; c < 32; ++c)
                       if (c == jc) x[c] = target_g<FLAGS>(x[c], cur[c], lj, p.abs_scale);
@@ -752,6 +748,50 @@ int make_map(CUtensorMap* map, const void* ptr, int64_t rows, int D, int box_row
   return LF_OK;
 }
 
+// rows x 16 bf16 (32 B rows), box = 16 x box_rows, SWIZZLE_32B: the bias
+// columns of the BWD_ITEMS S MMA.
+int make_map_k16(CUtensorMap* map, const void* ptr, int64_t rows, int box_rows) {
+  auto enc = get_encode();
+  if (!enc) return fail(LF_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {16, static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {32};
+  cuuint32_t box[2] = {16, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(LF_ECUDA, "cuTensorMapEncodeTiled (k16) failed: " + std::to_string(r));
+  return LF_OK;
+}
+
+// Bias columns: stream row i -> [c1, c2, c3, 0 x 13] with c1 + c2 + c3 =
+// -lse2_i ln 2 to ~2^-24 relative (three bf16 parts); rows past n carry a
+// huge negative bias (their softmax is 0).  The owner side multiplies by the
+// constant [1, 1, 1, 0 x 13] rows (`ones`, 128 rows).
+__global__ void bias_columns(const double* __restrict__ lse, int64_t n, int64_t n_pad,
+                             double lse_sub, __nv_bfloat16* __restrict__ bias,
+                             __nv_bfloat16* __restrict__ ones) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < 128 && ones) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) ones[i * 16 + k] = __float2bfloat16_rn(k < 3 ? 1.f : 0.f);
+  }
+  if (i >= n_pad) return;
+  float c[3] = {-1e30f, 0.f, 0.f};
+  if (i < n) {
+    const double lse2 = lse[i] * 1.4426950408889634 - lse_sub;
+    double r = -lse2 * 0.6931471805599453;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const __nv_bfloat16 h = __double2bfloat16(r);
+      c[k] = __bfloat162float(h);
+      r -= static_cast<double>(c[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 16; ++k) bias[i * 16 + k] = __float2bfloat16_rn(k < 3 ? c[k] : 0.f);
+}
+
 __global__ void prep_rows(const int64_t* __restrict__ targets, const double* __restrict__ lse,
                           int64_t n, int64_t n_pad, int64_t v_shard, int64_t v_offset,
                           double lse_sub, int32_t* __restrict__ tgt,
@@ -776,38 +816,39 @@ __global__ void target_keys(const int32_t* __restrict__ tgt, int64_t n, int64_t 
 }
 
 template <int D, int MODE, int FLAGS>
-int launch_mode(const CUtensorMap& mo, const CUtensorMap& ms, const TcParams& p, cudaStream_t st) {
+int launch_mode(const CUtensorMap& mo, const CUtensorMap& ms, const CUtensorMap& mb,
+                const CUtensorMap& m1, const TcParams& p, cudaStream_t st) {
   using C = Cfg<D, MODE>;
   auto kern = cce_tc_kernel<D, MODE, FLAGS>;
   LF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
   const int grid = static_cast<int>(std::min<int64_t>(p.units, num_sms()));
   ProfScope prof(MODE == FWD ? LF_K_CCE_FWD : (MODE == BWD_ROWS ? LF_K_CCE_BWD_DX : LF_K_CCE_BWD_DE), st);
-  kern<<<grid, Geo<MODE>::kThreads, C::kSmem, st>>>(mo, ms, p);
+  kern<<<grid, Geo<MODE>::kThreads, C::kSmem, st>>>(mo, ms, mb, m1, p);
   LF_LAUNCHED();
   return LF_OK;
 }
 
 template <int D, int MODE>
-int launch_flags(int flags, const CUtensorMap& mo, const CUtensorMap& ms, const TcParams& p,
-                 cudaStream_t st) {
-  if (MODE == FWD) return launch_mode<D, MODE, 0>(mo, ms, p, st);
+int launch_flags(int flags, const CUtensorMap& mo, const CUtensorMap& ms, const CUtensorMap& mb,
+                 const CUtensorMap& m1, const TcParams& p, cudaStream_t st) {
+  if (MODE == FWD) return launch_mode<D, MODE, 0>(mo, ms, mb, m1, p, st);
   switch (flags) {
-    case 0: return launch_mode<D, MODE, 0>(mo, ms, p, st);
-    case kFilt: return launch_mode<D, MODE, kFilt>(mo, ms, p, st);
-    case kFilt | kTgtIn: return launch_mode<D, MODE, kFilt | kTgtIn>(mo, ms, p, st);
-    default: return launch_mode<D, MODE, kFilt | kCount | kTgtIn>(mo, ms, p, st);
+    case 0: return launch_mode<D, MODE, 0>(mo, ms, mb, m1, p, st);
+    case kFilt: return launch_mode<D, MODE, kFilt>(mo, ms, mb, m1, p, st);
+    case kFilt | kTgtIn: return launch_mode<D, MODE, kFilt | kTgtIn>(mo, ms, mb, m1, p, st);
+    default: return launch_mode<D, MODE, kFilt | kCount | kTgtIn>(mo, ms, mb, m1, p, st);
   }
 }
 
 template <int MODE>
-int launch_d(int D, int flags, const CUtensorMap& mo, const CUtensorMap& ms, const TcParams& p,
-             cudaStream_t st) {
+int launch_d(int D, int flags, const CUtensorMap& mo, const CUtensorMap& ms, const CUtensorMap& mb,
+             const CUtensorMap& m1, const TcParams& p, cudaStream_t st) {
   switch (D) {
-    case 64: return launch_flags<64, MODE>(flags, mo, ms, p, st);
+    case 64: return launch_flags<64, MODE>(flags, mo, ms, mb, m1, p, st);
 #ifndef LF_VARIANT_D64_ONLY
-    case 128: return launch_flags<128, MODE>(flags, mo, ms, p, st);
-    case 192: return launch_flags<192, MODE>(flags, mo, ms, p, st);
-    case 256: return launch_flags<256, MODE>(flags, mo, ms, p, st);
+    case 128: return launch_flags<128, MODE>(flags, mo, ms, mb, m1, p, st);
+    case 192: return launch_flags<192, MODE>(flags, mo, ms, mb, m1, p, st);
+    case 256: return launch_flags<256, MODE>(flags, mo, ms, mb, m1, p, st);
 #endif
     default: return fail(LF_EUNSUPPORTED, "tc: d must be 64/128/192/256");
   }
@@ -869,7 +910,7 @@ int tc_cce_forward_partials(const void* X, const void* E, const int64_t* targets
   p.units = owner_tiles * P;
   p.tgt = tgt.as<int32_t>();
   p.part = ws.as<float4>();
-  rc = launch_d<FWD>(D, 0, mo, ms, p, st);
+  rc = launch_d<FWD>(D, 0, mo, ms, mo, mo, p, st);
   if (rc) return rc;
   *part_out = ws.as<float>();
   *P_out = static_cast<int>(P);
@@ -944,7 +985,7 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
   p.counters = counters;
   p.fix_rows = static_cast<const __nv_bfloat16*>(E);
   p.fix_scale = static_cast<float>(scale);
-  rc = launch_d<BWD_ROWS>(D, flags, mx_own, me_str, p, st);
+  rc = launch_d<BWD_ROWS>(D, flags, mx_own, me_str, mx_own, mx_own, p, st);
   if (rc) return rc;
   if (P > 1) {
     rc = launch_reduce_f32(dx_out, static_cast<int>(P), n * D, dX, st);
@@ -979,7 +1020,19 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
     q.fix_off = fix_off.as<uint32_t>();
     q.fix_list = fix_list.as<uint32_t>();
   }
-  rc = launch_d<BWD_ITEMS>(D, flags, me_own, mx_str, q, st);
+  // bias columns folding -lse2 into the dE pass's S MMA (see bias_columns)
+  Scratch bias, ones;
+  rc = bias.alloc(sizeof(__nv_bfloat16) * 16 * n_pad, st);
+  if (!rc) rc = ones.alloc(sizeof(__nv_bfloat16) * 16 * BM, st);
+  if (rc) return rc;
+  bias_columns<<<ceil_div(n_pad, 256), 256, 0, st>>>(lse, n, n_pad, sub, bias.as<__nv_bfloat16>(),
+                                                     ones.as<__nv_bfloat16>());
+  LF_LAUNCHED();
+  CUtensorMap mbias, mones;
+  rc = make_map_k16(&mbias, bias.ptr, n_pad, BN);
+  if (!rc) rc = make_map_k16(&mones, ones.ptr, BM, BM);
+  if (rc) return rc;
+  rc = launch_d<BWD_ITEMS>(D, flags, me_own, mx_str, mbias, mones, q, st);
   return rc;
 }
 
