@@ -108,7 +108,7 @@ struct Geo {
   static constexpr int kThreads = 32 * kCtrlWarps + 128 * NWG;
   static constexpr int kEpiThreads = 128 * NWG;
   static constexpr int NQ = BN / 32;  // 32-column chunks per tile and thread
-  static_assert(BN % 32 == 0 && BN >= 64 && BN <= 128, "BN");
+  static_assert(BN % 32 == 0 && BN >= 64 && (BN <= 128 || (MODE == FWD && BN == 256)), "BN");
 };
 
 template <int D, int MODE>
@@ -411,36 +411,43 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
         tc_fence_after();
         const uint32_t ta = tmem + lane_base + b * BN;
         if (MODE == FWD) {
-          // Whole tile in registers (one wait), S released at once.
-          float v[BN];
+          // The tile in 128-column slabs, each entirely in registers (one
+          // wait per slab); S goes back once the last slab is loaded.
+          constexpr int SL = BN < 128 ? BN : 128;
+          const int lc = tgt - static_cast<int>(col0);
+#pragma unroll
+          for (int h = 0; h < BN / SL; ++h) {
+          float v[SL];
           {
             uint32_t* r = reinterpret_cast<uint32_t*>(v);
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) LF_TMEM_LD32(ta + q * 32, (r + q * 32));
+            for (int q = 0; q < SL / 32; ++q) LF_TMEM_LD32(ta + h * SL + q * 32, (r + q * 32));
             tmem_ld_wait();
           }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&s_empty[b]);
+          if (h + 1 == BN / SL) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[b]);
+          }
           if (nvalid < BN) {
 #pragma unroll
-            for (int c = 0; c < BN; ++c)
-              if (c >= nvalid) v[c] = -INFINITY;
+            for (int c = 0; c < SL; ++c)
+              if (h * SL + c >= nvalid) v[c] = -INFINITY;
           }
-          const int lc = tgt - static_cast<int>(col0);
-          if (static_cast<unsigned>(lc) < static_cast<unsigned>(BN)) {
-            tv = select_reg(v, lc);
+          if (static_cast<unsigned>(lc - h * SL) < static_cast<unsigned>(SL)) {
+            tv = select_reg(v, lc - h * SL);
             has = 1.f;
           }
           if (m == -INFINITY) {
             float mx = v[0];
 #pragma unroll
-            for (int c = 1; c < BN; ++c) mx = fmaxf(mx, v[c]);
-            m = mx * kLog2e;  // a tile is never entirely past the catalog end
+            for (int c = 1; c < SL; ++c) mx = fmaxf(mx, v[c]);
+            if (mx == -INFINITY) continue;  // slab entirely past the catalog end
+            m = mx * kLog2e;
           }
           float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
-          for (int c = 0; c < BN; c += 2) {
+          for (int c = 0; c < SL; c += 2) {
             acc0 += ex2_mix<kPolyFwd>(c, fma_log2(v[c], m));
             acc1 += ex2_mix<kPolyFwd>(c + 1, fma_log2(v[c + 1], m));
           }
@@ -448,20 +455,21 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
           if (!(sum <= 1.8446744e19f)) {  // > 2^64 or NaN: rebase on the true max
             float mx = v[0];
 #pragma unroll
-            for (int c = 1; c < BN; ++c) mx = fmaxf(mx, v[c]);
+            for (int c = 1; c < SL; ++c) mx = fmaxf(mx, v[c]);
             const float nm = fmaxf(m, mx * kLog2e);
             s *= ex2_approx(m - nm);
             m = nm;
             acc0 = 0.f;
             acc1 = 0.f;
 #pragma unroll
-            for (int c = 0; c < BN; c += 2) {
+            for (int c = 0; c < SL; c += 2) {
               acc0 += ex2_approx(fma_log2(v[c], m));
               acc1 += ex2_approx(fma_log2(v[c + 1], m));
             }
             sum = acc0 + acc1;
           }
           s += sum;
+          }
         } else {
           // ---- backward: G = softmax * |scale| (target: minus |scale|), bf16,
           // back into the same TMEM columns (chunk q -> columns 16q..16q+15,
