@@ -36,6 +36,9 @@
 #ifndef LF_POLY_BWD
 #define LF_POLY_BWD 0
 #endif
+#ifndef LF_NOSCALE
+#define LF_NOSCALE 1
+#endif
 #ifndef LF_NWG_FWD
 #define LF_NWG_FWD 2
 #endif
@@ -142,6 +145,14 @@ __device__ __forceinline__ float fma_log2(float v, float sub) { return fmaf(v, k
 // argument above 127 still yields a huge value, so the forward's overflow
 // rebase check fires exactly as with MUFU's +inf.
 constexpr int kPolyFwd = LF_POLY_FWD;
+// G domain of the filtered kernels.  Fast path (no kTgtIn): survivors of the
+// ftz flush are >= 2^-126 and stay as they are (the tensor cores keep the
+// tiny products exact enough: dX/dE errors are unchanged vs. the scaled
+// domain, tools/filter_accuracy.py); the target's -1 is applied at read-out
+// in real units.  kTgtIn puts (softmax - 1) x 2^-126 / eps into G, which for
+// coarse eps is subnormal, so those kernels scale survivors by 2^64.
+template <int FLAGS>
+constexpr bool kNoScale = LF_NOSCALE != 0 && !(FLAGS & kTgtIn);
 constexpr int kPolyBwd = LF_POLY_BWD;
 template <int POLY>
 __device__ __forceinline__ float ex2_mix(int c, float a) {
@@ -151,7 +162,7 @@ __device__ __forceinline__ float ex2_mix(int c, float a) {
 
 // Backward filter domain: the exp argument a = S log2e - lse2 is offset so
 // that a < kThr (= -126) exactly when softmax < eps; ex2.approx.ftz flushes
-// those results and the survivors are scaled by 2^64 after the MUFU.
+// those results; the kTgtIn kernels then scale the survivors by 2^64 (kNoScale).
 template <int FLAGS>
 constexpr float kThr = -126.f;
 
@@ -159,8 +170,7 @@ constexpr float kThr = -126.f;
 template <int FLAGS>
 __device__ __forceinline__ float target_g(float e, uint32_t raw, float l, float t_scale) {
   if (FLAGS & kFilt)
-    return ex2_approx(fmaf(__uint_as_float(raw), kLog2e, -l) + 64.f) -
-           t_scale;
+    return ex2_approx(fmaf(__uint_as_float(raw), kLog2e, -l) + (kNoScale<FLAGS> ? 0.f : 64.f)) - t_scale;
   return e - t_scale;
 }
 
@@ -476,7 +486,7 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
           // already consumed by this warp).  Filtering (FILT): lse2 carries the
           // shift log2(eps) + 126, so a = S log2e - lse2 < -126 exactly when
           // softmax < eps and ex2.approx.ftz flushes those results to +0 — no
-          // compare or select per element; survivors are rescaled by 2^64 so
+          // compare or select per element; (kTgtIn kernels) survivors are rescaled by 2^64 so
           // every bf16 G and every MMA product stays normal, and out_scale
           // undoes the factor on the accumulator.  A 32 x 32 sub-tile whose
           // largest a is below the threshold (and that holds no target) skips
@@ -591,7 +601,7 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
 #else
                   x[c] = ex2_approx(e[c]);
 #endif
-                  if (FLAGS & kFilt) x[c] *= 18446744073709551616.f;  // 2^64
+                  if ((FLAGS & kFilt) && !kNoScale<FLAGS>) x[c] *= 18446744073709551616.f;  // 2^64
                 }
               }
               // The target is never filtered: g = (s - 1) |scale| (cce.cpp:193-195).
@@ -946,8 +956,10 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
   const bool tgt_in = filt && (count || eps >= 0x1p-12);
   const int flags = filt ? (kFilt | (count ? kCount : 0) | (tgt_in ? kTgtIn : 0)) : 0;
   const double sub = filt ? -std::log2(eps) - 126.0 : std::log2(std::fabs(scale));
-  const double gscale = filt ? std::ldexp(1.0, -62) / eps : std::fabs(scale);
-  const double out_scale = filt ? scale * eps * std::ldexp(1.0, 62) : (scale < 0 ? -1.0 : 1.0);
+  const bool noscale = LF_NOSCALE != 0 && !tgt_in;
+  const double gscale = filt ? std::ldexp(1.0, noscale ? -126 : -62) / eps : std::fabs(scale);
+  const double out_scale =
+      filt ? scale * eps * std::ldexp(1.0, noscale ? 126 : 62) : (scale < 0 ? -1.0 : 1.0);
   constexpr int BN = Geo<BWD_ROWS>::BN;
   const int64_t row_tiles = ceil_div(n, BM);
   const int64_t item_tiles = ceil_div(v, BM);     // dE owner tiles
