@@ -79,8 +79,10 @@ typedef struct {
  * only when the caller passes a non-NULL pointer; that forces a stream sync). */
 typedef struct {
   uint64_t skipped_elems;  /* off-target (row,item) pairs with softmax < eps (cce.cpp:197-200) */
-  uint64_t skipped_tiles;  /* 128x128 tiles whose MMA+exp work was skipped entirely */
-  uint64_t total_tiles;    /* tiles visited by the dX pass */
+  uint64_t skipped_tiles;  /* bf16: 32-row x 32-item sub-tiles of the dX pass whose exps were
+                              skipped (every entry below eps; only tested while such
+                              sub-tiles keep appearing — see DESIGN.md) */
+  uint64_t total_tiles;    /* bf16: 32 x 32 sub-tiles visited by the dX pass */
   double skipped_fraction; /* skipped_elems / (n * (v_total - 1)), cce.cpp:264-268 */
 } lf_cce_stats;
 
