@@ -173,6 +173,49 @@ LF_API int lf_ce_backward(const void* d_X, const void* d_E, const int64_t* d_tar
 LF_API int lf_sample_uniform(const int64_t* d_positives, int64_t n, int64_t ns, int64_t catalog,
                              uint64_t seed, int32_t retry_cap, int64_t* d_inds, void* stream);
 
+/* ------------------------------------------- full-catalog evaluation ---- */
+/* The scoring and ranking of lseforge::evaluate (metrics.hpp:18-24,
+ * metrics.cpp:13-103) on the device; the encoder that produces h
+ * (metrics.cpp:46) is the caller's, d_X holds the encoded rows.  Scores
+ * s_ij = X_i . E_j are never materialised.
+ *
+ * lf_eval_rank_topk: over the catalog shard E [v_shard x d] holding items
+ * [v_offset, v_offset + v_shard), d_targets GLOBAL item ids:
+ *   d_ahead[i]            = #{shard items j : s_ij > s_it, or s_ij == s_it and
+ *                           j < t} (metrics.cpp:56-60; rank = 1 + the sum over shards)
+ *   d_top_idx[i*k + e]    = the shard's top-k items by (score desc, id asc)
+ *                           (metrics.cpp:63-72), global ids, -1 past the shard size
+ *   d_top_score[i*k + e]  = their scores (double).
+ * The target score s_it is computed on the same arithmetic path as the
+ * scores it is compared with: from d_target_rows [n x d] (the rows' target
+ * item rows, in dtype) when given — needed when a target lives in another
+ * shard — else gathered from E (every target must then be in the shard;
+ * LF_EINVAL otherwise, after a stream sync).  f64 reproduces the reference's
+ * double scores bit for bit (k ascending, metrics.cpp:49-54), so ranks and
+ * lists are identical; bf16 runs on the tensor cores (fp32 scores).
+ * k <= 16 (bf16) / 32 (f32, f64), else LF_EUNSUPPORTED. */
+LF_API int lf_eval_rank_topk(const void* d_X, const void* d_E, const int64_t* d_targets,
+                             const void* d_target_rows, int64_t n, int64_t d, int64_t v_shard,
+                             int64_t v_offset, int32_t k, int32_t dtype, int64_t* d_ahead,
+                             int64_t* d_top_idx, double* d_top_score, void* stream);
+/* Merge P shards' outputs (P consecutive blocks of n / n*k): d_rank = 1 +
+ * sum of ahead, merged global top-k. */
+LF_API int lf_eval_merge(const int64_t* d_ahead, const int64_t* d_top_idx, const double* d_top_score,
+                         int32_t P, int64_t n, int32_t k, int64_t* d_rank, int64_t* d_top_idx_out,
+                         double* d_top_score_out, void* stream);
+/* Aggregation of metrics.cpp:26-33, 62, 74-103 from 1-based ranks and the
+ * top-k lists (k = k_eff): out3 (HOST) = {ndcg, coverage, surprisal}.
+ * d_popularity: v_total training counts.  Synchronizes `stream`; LF_EINVAL
+ * with the reference's messages for a negative count / fewer than 2 events. */
+LF_API int lf_eval_summary(const int64_t* d_rank, const int64_t* d_top_idx, int64_t n, int32_t k,
+                           const int64_t* d_popularity, int64_t v_total, double* out3,
+                           void* stream);
+/* lseforge::evaluate for an unsharded catalog: k_eff = min(k, v), rank/top-k,
+ * then the summary into out3 (HOST). */
+LF_API int lf_evaluate(const void* d_X, const void* d_E, const int64_t* d_targets, int64_t n,
+                       int64_t d, int64_t v, int32_t k, int32_t dtype, const int64_t* d_popularity,
+                       double* out3, void* stream);
+
 /* ----------------------------------------------------------- validation --- */
 /* Replaces validate_loss_inputs' index scan (losses.cpp:58-67) for device
  * targets.  Synchronizes `stream`.  On failure returns LF_EINVAL with the
@@ -231,7 +274,8 @@ enum lf_kernel_kind {
   LF_K_CCEM_FWD = 4,   /* CCE- forward gather/dot/LSE */
   LF_K_CCEM_BWD = 5,   /* CCE- backward (rows pass + sort + segment reduce) */
   LF_K_AUX = 6,        /* combine / reduce / prep kernels */
-  LF_K_COUNT = 7
+  LF_K_EVAL = 7,       /* full-catalog ranking (rank + top-K) */
+  LF_K_COUNT = 8
 };
 LF_API int lf_profile_enable(int on);
 LF_API int lf_profile_read(int32_t kind, uint64_t* launches, double* total_ms);

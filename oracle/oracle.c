@@ -423,3 +423,81 @@ void orc_estimate_flops(size_t n, size_t d, size_t v, size_t ns, int backend, ui
   *fwd = (uint64_t)n * d * scored;
   *bwd = factor * *fwd;
 }
+
+/* ---- full-catalog evaluation (metrics.cpp:13-103) ------------------------- */
+static void eval_scores(const double* h, const float* C, size_t d, size_t v, double* scores) {
+  for (size_t j = 0; j < v; ++j) scores[j] = 0.0;
+  for (size_t kk = 0; kk < d; ++kk) { /* metrics.cpp:49-54 */
+    const double hk = h[kk];
+    const float* crow = C + kk * v;
+    for (size_t j = 0; j < v; ++j) scores[j] += hk * (double)crow[j];
+  }
+}
+
+void orc_eval_rank_topk(const double* H, const float* C, const int64_t* targets, size_t n,
+                        size_t d, size_t v, size_t v0, size_t v1, size_t k, int64_t* ahead,
+                        int64_t* top_idx, double* top_score) {
+#pragma omp parallel
+  {
+    double* scores = (double*)malloc(sizeof(double) * (v ? v : 1));
+#pragma omp for schedule(dynamic)
+    for (size_t i = 0; i < n; ++i) {
+      eval_scores(H + i * d, C, d, v, scores);
+      const size_t t = (size_t)targets[i];
+      const double st = scores[t];
+      int64_t a = 0;
+      for (size_t j = v0; j < v1; ++j) /* metrics.cpp:57-60 */
+        if (scores[j] > st || (scores[j] == st && j < t)) ++a;
+      ahead[i] = a;
+      /* top-k by (score desc, index asc): insertion into a sorted list */
+      int64_t* ti = top_idx + i * k;
+      double* tv = top_score + i * k;
+      size_t filled = 0;
+      for (size_t j = v0; j < v1; ++j) {
+        const double s = scores[j];
+        if (filled == k && !(s > tv[k - 1])) continue; /* ascending j: ties never displace */
+        size_t pos = filled < k ? filled : k - 1;
+        while (pos > 0 && s > tv[pos - 1]) {
+          if (pos < k) { tv[pos] = tv[pos - 1]; ti[pos] = ti[pos - 1]; }
+          --pos;
+        }
+        tv[pos] = s;
+        ti[pos] = (int64_t)j;
+        if (filled < k) ++filled;
+      }
+      for (size_t e = filled; e < k; ++e) { ti[e] = -1; tv[e] = -INFINITY; }
+    }
+    free(scores);
+  }
+}
+
+int orc_eval_summary(const int64_t* rank, const int64_t* top_idx, size_t n, size_t k,
+                     const int64_t* counts, size_t v, double* out3) {
+  double total = 0.0;
+  for (size_t j = 0; j < v; ++j) { /* metrics.cpp:26-33 */
+    if (counts[j] < 0) return 1;
+    total += (double)counts[j];
+  }
+  if (total < 2.0) return 2;
+  const double log2_total = log2(total);
+  double ndcg_sum = 0.0, surp_sum = 0.0;
+  size_t distinct = 0;
+  char* seen = (char*)calloc(v ? v : 1, 1);
+  for (size_t i = 0; i < n; ++i) {
+    const int64_t r = rank[i]; /* metrics.cpp:61 */
+    ndcg_sum += r <= (int64_t)k ? 1.0 / log2((double)r + 1.0) : 0.0;
+    double acc = 0.0; /* metrics.cpp:74-80 */
+    for (size_t e = 0; e < k; ++e) {
+      const int64_t item = top_idx[i * k + e];
+      const double c = (double)(counts[item] > 1 ? counts[item] : 1);
+      acc += -log2(c / total) / log2_total;
+      if (!seen[item]) { seen[item] = 1; ++distinct; } /* metrics.cpp:90-97 */
+    }
+    surp_sum += acc / (double)k;
+  }
+  free(seen);
+  out3[0] = ndcg_sum / (double)n;
+  out3[1] = (double)distinct / (double)v;
+  out3[2] = surp_sum / (double)n;
+  return 0;
+}

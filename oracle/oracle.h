@@ -97,6 +97,22 @@ int64_t orc_validate_inds(const int64_t* inds, size_t n, size_t w, size_t v);
 void orc_estimate_flops(size_t n, size_t d, size_t v, size_t ns, int backend, uint64_t* fwd,
                         uint64_t* bwd);
 
+/* ---- full-catalog evaluation (metrics.cpp:13-103, minus the encoder) ------
+ * H : n x d double (encode() output, metrics.cpp:46); C : d x v float.
+ * Scores s_j = sum_k H[k] * (double)C[k][j], k ascending (metrics.cpp:49-54).
+ * Over the item range [v0, v1): ahead[i] = #{j : s_j > s_t, or == and j < t}
+ * (metrics.cpp:56-60; rank = 1 + ahead over the whole catalog), top_idx /
+ * top_score = the first k items by (score desc, index asc) (metrics.cpp:63-72),
+ * -1 / -inf past the range size.  The target score comes from the full C. */
+void orc_eval_rank_topk(const double* H, const float* C, const int64_t* targets, size_t n,
+                        size_t d, size_t v, size_t v0, size_t v1, size_t k, int64_t* ahead,
+                        int64_t* top_idx, double* top_score);
+/* metrics.cpp:26-33, 62, 74-103: out3 = {ndcg, coverage, surprisal} from
+ * 1-based ranks and top-k lists (k = k_eff).  Returns 0, or 1 for a negative
+ * count, 2 for fewer than 2 training events (the reference's invalid_argument). */
+int orc_eval_summary(const int64_t* rank, const int64_t* top_idx, size_t n, size_t k,
+                     const int64_t* counts, size_t v, double* out3);
+
 #ifdef __cplusplus
 }
 #endif

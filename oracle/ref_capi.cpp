@@ -7,6 +7,7 @@
 // reference CPU timing.  The product library never links this.
 //
 // Layouts are the reference's own: E n×d float, C d×v float, outputs double.
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -19,7 +20,9 @@
 #include "lseforge/cce.hpp"
 #include "lseforge/ccem.hpp"
 #include "lseforge/losses.hpp"
+#include "lseforge/encoder.hpp"
 #include "lseforge/memory_model.hpp"
+#include "lseforge/metrics.hpp"
 #include "lseforge/neg_index.hpp"
 #include "lseforge/rng.hpp"
 #include "lseforge/sampler.hpp"
@@ -222,6 +225,45 @@ void ref_estimate_flops(std::size_t n, std::size_t d, std::size_t v, std::size_t
   FlopEstimate f = estimate_flops(n, d, v, ns, static_cast<Backend>(backend));
   *fwd = f.forward;
   *bwd = f.backward;
+}
+
+// ---- metrics.cpp -----------------------------------------------------------
+// One evaluation instance through the reference's own evaluate(): params =
+// ToyEncoderParams::Init(catalog, hidden, SplitMix64(seed)), pairs with
+// prefixes [n x L] and targets.  Returns the summary (out3 = ndcg, coverage,
+// surprisal), the encoded rows H [n x hidden] (encode(), what evaluate()
+// scores with), the classifier C [hidden x catalog], and per-row ranks
+// recovered from single-pair evaluate() calls at k = catalog
+// (ndcg = 1 / log2(rank + 1)).
+int ref_eval_instance(std::size_t catalog, std::size_t hidden, uint64_t seed, std::size_t n,
+                      std::size_t L, const int64_t* prefixes, const int64_t* targets, std::size_t k,
+                      const int64_t* counts, int workers, double* out3, double* H, float* C,
+                      int64_t* ranks) {
+  return guard([&] {
+    const ToyEncoderParams p = ToyEncoderParams::Init(catalog, hidden, SplitMix64(seed));
+    std::vector<EvalPair> pairs(n);
+    for (std::size_t i = 0; i < n; ++i) {
+      pairs[i].user = static_cast<int64_t>(i);
+      pairs[i].prefix.assign(prefixes + i * L, prefixes + (i + 1) * L);
+      pairs[i].target = targets[i];
+    }
+    const std::vector<int64_t> cnt(counts, counts + catalog);
+    const EvalSummary sum = evaluate(p, pairs, k, cnt, workers);
+    out3[0] = sum.ndcg;
+    out3[1] = sum.coverage;
+    out3[2] = sum.surprisal;
+    if (C) std::memcpy(C, p.c.data().data(), sizeof(float) * hidden * catalog);
+    for (std::size_t i = 0; i < n; ++i) {
+      if (H) {
+        const std::vector<double> h = encode(p, pairs[i].prefix);
+        std::memcpy(H + i * hidden, h.data(), sizeof(double) * hidden);
+      }
+      if (ranks) {
+        const EvalSummary one = evaluate(p, std::span<const EvalPair>(&pairs[i], 1), catalog, cnt, 1);
+        ranks[i] = static_cast<int64_t>(std::llround(std::exp2(1.0 / one.ndcg) - 1.0));
+      }
+    }
+  });
 }
 
 }  // extern "C"

@@ -4,6 +4,7 @@
 // (losses.cpp:48-69, cce.cpp:17-27, ccem.cpp:16-31) with the same messages;
 // the index scans themselves are separate calls (lf_validate_*) because they
 // need a device->host sync.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <mutex>
@@ -394,6 +395,50 @@ int lf_sample_uniform(const int64_t* d_positives, int64_t n, int64_t ns, int64_t
                       uint64_t seed, int32_t retry_cap, int64_t* d_inds, void* stream) {
   if (retry_cap < 1) return fail(LF_EINVAL, "sample_uniform: retry_cap must be >= 1");
   return sample_uniform(d_positives, n, ns, catalog, seed, retry_cap, d_inds, as_stream(stream));
+}
+
+int lf_eval_rank_topk(const void* d_X, const void* d_E, const int64_t* d_targets,
+                      const void* d_target_rows, int64_t n, int64_t d, int64_t v_shard,
+                      int64_t v_offset, int32_t k, int32_t dtype, int64_t* d_ahead,
+                      int64_t* d_top_idx, double* d_top_score, void* stream) {
+  if (dtype != LF_F32 && dtype != LF_F64 && dtype != LF_BF16)
+    return fail(LF_EINVAL, "eval: unknown dtype " + std::to_string(dtype));
+  if (d < 1 || d > 4096) return fail(LF_EINVAL, "eval: d must be in [1, 4096]");
+  return eval_rank_topk(dtype, d_X, d_E, d_targets, d_target_rows, n, static_cast<int>(d), v_shard,
+                        v_offset, k, d_ahead, d_top_idx, d_top_score, as_stream(stream));
+}
+
+int lf_eval_merge(const int64_t* d_ahead, const int64_t* d_top_idx, const double* d_top_score,
+                  int32_t P, int64_t n, int32_t k, int64_t* d_rank, int64_t* d_top_idx_out,
+                  double* d_top_score_out, void* stream) {
+  return eval_merge(d_ahead, d_top_idx, d_top_score, P, n, k, d_rank, d_top_idx_out,
+                    d_top_score_out, as_stream(stream));
+}
+
+int lf_eval_summary(const int64_t* d_rank, const int64_t* d_top_idx, int64_t n, int32_t k,
+                    const int64_t* d_popularity, int64_t v_total, double* out3, void* stream) {
+  return eval_summary(d_rank, d_top_idx, n, k, d_popularity, v_total, out3, as_stream(stream));
+}
+
+int lf_evaluate(const void* d_X, const void* d_E, const int64_t* d_targets, int64_t n, int64_t d,
+                int64_t v, int32_t k, int32_t dtype, const int64_t* d_popularity, double* out3,
+                void* stream) {
+  // metrics.cpp:16-33 argument checks, then k_eff = min(k, v) (metrics.cpp:34)
+  if (n <= 0) return fail(LF_EINVAL, "evaluate: no eval pairs");
+  if (k < 1) return fail(LF_EINVAL, "evaluate: k must be >= 1");
+  if (v < 1) return fail(LF_EINVAL, "evaluate: empty catalog");
+  const int32_t k_eff = static_cast<int32_t>(std::min<int64_t>(k, v));
+  cudaStream_t st = as_stream(stream);
+  Scratch rank, top, score;
+  int rc = rank.alloc(sizeof(int64_t) * n, st);
+  if (!rc) rc = top.alloc(sizeof(int64_t) * n * k_eff, st);
+  if (!rc) rc = score.alloc(sizeof(double) * n * k_eff, st);
+  if (!rc)
+    rc = lf_eval_rank_topk(d_X, d_E, d_targets, nullptr, n, d, v, 0, k_eff, dtype, rank.as<int64_t>(),
+                           top.as<int64_t>(), score.as<double>(), stream);
+  if (!rc) rc = launch_add_one(rank.as<int64_t>(), n, st);
+  if (!rc) rc = eval_summary(rank.as<int64_t>(), top.as<int64_t>(), n, k_eff, d_popularity, v, out3, st);
+  return rc;
 }
 
 int lf_estimate_flops(int64_t n, int64_t d, int64_t v, int64_t ns, int32_t backend,

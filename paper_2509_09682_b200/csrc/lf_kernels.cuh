@@ -47,6 +47,29 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
                     double scale, double eps, int64_t n, int D, int64_t v, int64_t v_offset,
                     float* dX, float* dE, unsigned long long* counters, cudaStream_t st);
 
+// EVAL-mode partials over the shard (bf16): Et = the rows' target item rows
+// (ceil(n/128)*128 rows), tl = clamped local target index; per (chunk, row)
+// count (uint32), top-16 values (float) and local indices (int32).
+int tc_eval_partials(const void* X, const void* E, const void* Et, const int32_t* tl, int64_t n,
+                     int D, int64_t v, Scratch& cnt, Scratch& val, Scratch& idx, int* P_out,
+                     cudaStream_t st);
+// Same for fp32 / fp64 (lf_simt.cu), top-K per chunk with K = k.
+template <class T>
+int simt_eval_partials(const T* X, const T* E, const T* Et, const int32_t* tl, int64_t n, int D,
+                       int64_t v, int K, Scratch& cnt, Scratch& val, Scratch& idx, int* P_out,
+                       cudaStream_t st);
+
+// ---- full-catalog evaluation (lf_eval.cu) ----
+int eval_rank_topk(int dtype, const void* X, const void* E, const int64_t* targets,
+                   const void* target_rows, int64_t n, int D, int64_t v, int64_t v_offset, int k,
+                   int64_t* ahead, int64_t* top_idx, double* top_score, cudaStream_t st);
+int eval_merge(const int64_t* ahead, const int64_t* top_idx, const double* top_score, int P,
+               int64_t n, int k, int64_t* rank, int64_t* top_idx_out, double* top_score_out,
+               cudaStream_t st);
+int launch_add_one(int64_t* x, int64_t n, cudaStream_t st);
+int eval_summary(const int64_t* rank, const int64_t* top_idx, int64_t n, int k, const int64_t* pop,
+                 int64_t v, double* out3_host, cudaStream_t st);
+
 // ---- CCE- (lf_ccem.cu) ----
 int ccem_forward(int dtype, const void* X, const void* E, const int64_t* inds, int64_t n, int D,
                  int64_t v, int64_t w, double* lse, double* pos, double* loss, cudaStream_t st);

@@ -519,6 +519,159 @@ int simt_cce_backward(const T* X, const T* E, const int64_t* targets, const doub
   return LF_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Full-catalog ranking, fp32 / fp64 (metrics.cpp:46-78).  Block = 32 rows x
+// one V chunk; the 32 x 64 score tile is staged in shared memory and each
+// warp walks 4 rows: lanes count the items ranked ahead of the target (score
+// higher, or equal with a smaller item index) and the row's top-K (K <= 32)
+// lives across the warp's lanes, lane e holding entry e (descending score,
+// ties to the smaller index).  Scores use the k-ascending operand order of
+// the reference (exact in fp64), and st is computed by eval_target_scores in
+// the same order, so a score compares equal to st exactly when it would in
+// the reference.
+// ---------------------------------------------------------------------------
+template <class T>
+__global__ void eval_target_scores(const T* __restrict__ X, const T* __restrict__ Et, int64_t n,
+                                   int D, T* __restrict__ st) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  T acc = T(0);
+  for (int k = 0; k < D; ++k) acc = fma_acc(acc, X[i * D + k], Et[i * D + k]);
+  st[i] = acc;
+}
+
+template <class T>
+__global__ void __launch_bounds__(kThreads) eval_simt(const T* __restrict__ X,
+                                                      const T* __restrict__ E,
+                                                      const T* __restrict__ st_in,
+                                                      const int32_t* __restrict__ tl, int64_t n,
+                                                      int D, int64_t v, int64_t chunk, int K,
+                                                      uint32_t* __restrict__ cnt_out,
+                                                      T* __restrict__ val_out,
+                                                      int32_t* __restrict__ idx_out) {
+  constexpr int R = 32, C = 64, RW = 4;  // rows per warp
+  using M = TileMap<T, R, C>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* Xs = reinterpret_cast<T*>(smem_raw);
+  T* Es = Xs + D * (R + 1);
+  T* Ss = Es + D * (C + 1);  // [R][C + 1]
+  const unsigned full = 0xffffffffu;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * R;
+  const int64_t c_begin = static_cast<int64_t>(blockIdx.y) * chunk;
+  const int64_t c_end = min(v, c_begin + chunk);
+  stage_T<T, R>(Xs, X, r0, n, D);
+  T stv[RW], kv[RW];
+  int64_t tlv[RW];
+  int ki[RW];
+  uint32_t cnt[RW];
+#pragma unroll
+  for (int rr = 0; rr < RW; ++rr) {
+    const int64_t row = r0 + warp * RW + rr;
+    stv[rr] = row < n ? st_in[row] : T(0);
+    tlv[rr] = row < n ? tl[row] : -1;
+    kv[rr] = neg_inf<T>();
+    ki[rr] = 0x7fffffff;
+    cnt[rr] = 0;
+  }
+  for (int64_t c0 = c_begin; c0 < c_end; c0 += C) {
+    __syncthreads();
+    stage_T<T, C>(Es, E, c0, c_end, D);
+    __syncthreads();
+    {
+      T o[M::RPT][M::CPT];
+      M::logits(Xs, Es, D, o);
+#pragma unroll
+      for (int i = 0; i < M::RPT; ++i)
+#pragma unroll
+        for (int q = 0; q < M::CPT; ++q) Ss[M::row(i) * (C + 1) + M::col(q)] = o[i][q];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int rr = 0; rr < RW; ++rr) {
+      const int r = warp * RW + rr;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int cl = half * 32 + lane;
+        const int64_t col = c0 + cl;
+        const bool valid = col < c_end;
+        const T val = Ss[r * (C + 1) + cl];
+        if (valid) cnt[rr] += col < tlv[rr] ? (val >= stv[rr]) : (col > tlv[rr] ? (val > stv[rr]) : 0);
+        // columns arrive in ascending order, so an equal score never displaces
+        const T kth = __shfl_sync(full, kv[rr], K - 1);
+        unsigned bm = __ballot_sync(full, valid && val > kth);
+        while (bm) {
+          const int src = __ffs(bm) - 1;
+          bm &= bm - 1u;
+          const T cv = __shfl_sync(full, val, src);
+          const int ci = static_cast<int>(c0 + half * 32 + src);
+          const bool ahead = lane < K && (kv[rr] > cv || (kv[rr] == cv && ki[rr] < ci));
+          const int pos = __popc(__ballot_sync(full, ahead));
+          const T upv = __shfl_up_sync(full, kv[rr], 1);
+          const int upi = __shfl_up_sync(full, ki[rr], 1);
+          if (lane == pos) {
+            kv[rr] = cv;
+            ki[rr] = ci;
+          } else if (lane > pos && lane < K) {
+            kv[rr] = upv;
+            ki[rr] = upi;
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int rr = 0; rr < RW; ++rr) {
+    uint32_t c = cnt[rr];
+    for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(full, c, off);
+    const int64_t row = r0 + warp * RW + rr;
+    if (row < n) {
+      const int64_t rp = static_cast<int64_t>(blockIdx.y) * n + row;
+      if (lane == 0) cnt_out[rp] = c;
+      if (lane < K) {
+        val_out[rp * K + lane] = kv[rr];
+        idx_out[rp * K + lane] = ki[rr];
+      }
+    }
+  }
+}
+
+template <class T>
+int simt_eval_partials(const T* X, const T* E, const T* Et, const int32_t* tl, int64_t n, int D,
+                       int64_t v, int K, Scratch& cnt, Scratch& val, Scratch& idx, int* P_out,
+                       cudaStream_t st) {
+  const size_t smem = sizeof(T) * (D * (32 + 1 + 64 + 1) + 32 * (64 + 1));
+  if (smem > 227 * 1024) return fail(LF_EUNSUPPORTED, "simt eval: d too large");
+  LF_CUDA(cudaFuncSetAttribute(eval_simt<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)));
+  const int64_t rt = ceil_div(n, 32);
+  const int64_t chunks = pick_chunks(rt, v, 256);
+  const int64_t chunk = ceil_div(ceil_div(v, chunks), 64) * 64;
+  const int64_t P = ceil_div(v, chunk);
+  Scratch stv;
+  int rc = stv.alloc(sizeof(T) * n, st);
+  if (!rc) rc = cnt.alloc(sizeof(uint32_t) * P * n, st);
+  if (!rc) rc = val.alloc(sizeof(T) * P * n * K, st);
+  if (!rc) rc = idx.alloc(sizeof(int32_t) * P * n * K, st);
+  if (rc) return rc;
+  ProfScope prof(LF_K_EVAL, st);
+  eval_target_scores<T><<<ceil_div(n, 128), 128, 0, st>>>(X, Et, n, D, stv.as<T>());
+  LF_LAUNCHED();
+  eval_simt<T><<<dim3(rt, P), kThreads, smem, st>>>(X, E, stv.as<T>(), tl, n, D, v, chunk, K,
+                                                    cnt.as<uint32_t>(), val.as<T>(),
+                                                    idx.as<int32_t>());
+  LF_LAUNCHED();
+  *P_out = static_cast<int>(P);
+  return LF_OK;
+}
+
+template int simt_eval_partials<float>(const float*, const float*, const float*, const int32_t*,
+                                       int64_t, int, int64_t, int, Scratch&, Scratch&, Scratch&,
+                                       int*, cudaStream_t);
+template int simt_eval_partials<double>(const double*, const double*, const double*,
+                                        const int32_t*, int64_t, int, int64_t, int, Scratch&,
+                                        Scratch&, Scratch&, int*, cudaStream_t);
+
 template int simt_cce_forward_full<float>(const float*, const float*, const int64_t*, int64_t, int,
                                           int64_t, double*, double*, double*, cudaStream_t);
 template int simt_cce_forward_full<double>(const double*, const double*, const int64_t*, int64_t,

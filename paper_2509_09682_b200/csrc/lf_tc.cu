@@ -13,6 +13,11 @@
 //   BWD_ITEMS owner = items, stream = rows: S^T -> G^T -> dE_o += G^T X_t.
 //             Pass 2 of cce_backward (cce.cpp:240-262).  No atomics: every
 //             output row has one owner CTA.
+//   EVAL      full-catalog ranking (metrics.cpp:46-78): owner = rows, stream =
+//             items; each unit first multiplies the owner rows by their own
+//             target items' rows (gathered) to get the target scores on the
+//             same MMA datapath, then counts per row the items ranked ahead
+//             of the target and keeps a per-row top-16 in registers.
 //
 // Roles: warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer (one
 // elected lane), then NWG epilogue warpgroups that take stream tiles round
@@ -58,7 +63,8 @@ namespace {
 
 constexpr int BM = 128;  // owner tile (TMEM lanes)
 
-enum Mode : int { FWD = 0, BWD_ROWS = 1, BWD_ITEMS = 2 };
+enum Mode : int { FWD = 0, BWD_ROWS = 1, BWD_ITEMS = 2, EVAL = 3 };
+constexpr int kEvalK = 16;  // per-row top-K kept by the EVAL epilogue
 // Backward variants: kFilt = filter_eps > 0 (flush below eps, sub-tile skip);
 // kCount = also count skipped elements / sub-tiles (only when stats are read).
 // kTgtIn = handle each row's own target inside the tile loop (exact for any
@@ -88,6 +94,11 @@ struct TcParams {
   float4* part;          // FWD: [n_chunks][n_owner]
   float* out;            // BWD_ROWS: [n_chunks][n_owner][D]; BWD_ITEMS: [n_owner][D]
   unsigned long long* counters;  // [0] skipped elems, [1] skipped tiles, [2] total tiles
+  // EVAL (tgt = the target's local index clamped to [-1, n_stream]: -1 = before
+  // the shard, n_stream = after it)
+  uint32_t* ev_count;    // [n_chunks][n_owner] items of the chunk ranked ahead of the target
+  float* ev_val;         // [n_chunks][n_owner][kEvalK] top scores, descending
+  int32_t* ev_idx;       // same, local item index (INT32_MAX = empty)
 };
 
 // Position + phase in an N-slot mbarrier ring.
@@ -104,10 +115,10 @@ struct Ring {
 
 template <int MODE>
 struct Geo {
-  static constexpr int BN = MODE == FWD ? LF_BN_FWD : LF_BN_BWD;    // stream tile (S columns)
-  static constexpr int NWG = MODE == FWD ? LF_NWG_FWD : LF_NWG_BWD;  // epilogue warpgroups
+  static constexpr int BN = MODE == FWD ? LF_BN_FWD : (MODE == EVAL ? 128 : LF_BN_BWD);  // stream tile
+  static constexpr int NWG = MODE == FWD ? LF_NWG_FWD : (MODE == EVAL ? 2 : LF_NWG_BWD);  // epilogue WGs
   // control warps: TMA producer, S-MMA issuer (+ the G-MMA issuer in the backward)
-  static constexpr int kCtrlWarps = MODE == FWD ? 2 : 3;
+  static constexpr int kCtrlWarps = MODE == FWD || MODE == EVAL ? 2 : 3;
   static constexpr int kThreads = 32 * kCtrlWarps + 128 * NWG;
   static constexpr int kEpiThreads = 128 * NWG;
   static constexpr int NQ = BN / 32;  // 32-column chunks per tile and thread
@@ -131,12 +142,17 @@ struct Cfg {
   static constexpr int kOnesBytes = MODE == BWD_ITEMS ? BM * 32 : 0;  // constant A bias columns
   static constexpr int kStagesFit = (200 * 1024 - kOwnerBytes - kOnesBytes) / kStageBytes;
   static constexpr int kStages = kStagesFit > 12 ? 12 : kStagesFit;
-  static constexpr int kNBMax = (MODE == FWD ? 512 : 512 - D) / BN;  // S buffers that fit in TMEM
+  static constexpr int kNBMax = (MODE == FWD || MODE == EVAL ? 512 : 512 - D) / BN;  // S buffers in TMEM
   static constexpr int kNB = kNBMax > 8 ? 8 : kNBMax;
-  static_assert(MODE == FWD || kNB >= 2, "not enough TMEM for the backward pipeline");
+  static_assert(MODE == FWD || MODE == EVAL || kNB >= 2, "not enough TMEM for the backward pipeline");
+  // EVAL: per-row merge records {count, K values, K indices} (stride 2K + 1
+  // words: conflict-free) of the other warpgroups + the shared target scores
+  static constexpr int kEvalStride = 2 * kEvalK + 1;
+  static constexpr int kEvalMerge = MODE == EVAL ? ((G::NWG - 1) * BM * kEvalStride + BM) * 4 : 0;
   static constexpr int kAccCol = kNB * BN;
   static constexpr int kSmem = 1024 /*align slack*/ + kOwnerBytes + kOnesBytes + kStages * kStageBytes +
-                               1024 /*barriers*/ + (MODE == FWD ? (G::NWG - 1) * BM * 16 : 0);
+                               1024 /*barriers*/ + (MODE == FWD ? (G::NWG - 1) * BM * 16 : 0) +
+                               kEvalMerge;
 };
 __device__ __forceinline__ float fma_log2(float v, float sub) { return fmaf(v, kLog2e, -sub); }
 
@@ -196,6 +212,50 @@ __device__ __forceinline__ float select_reg(const float (&r)[N], int idx) {
   return out;
 }
 
+// Work units (chunk, owner tile).  FWD / backward: round robin over the
+// grid, chunk-major.  EVAL: each CTA takes a contiguous range of units in
+// owner-tile-major order, so consecutive units usually share the owner rows
+// and the per-row top-k state carries over (see the EVAL epilogue).
+template <int MODE>
+struct Units {
+  int64_t begin, end, step, P, OT;
+  __device__ Units(const TcParams& p) : P(p.n_chunks), OT(p.owner_tiles) {
+    if (MODE == EVAL) {
+      begin = blockIdx.x * p.units / gridDim.x;
+      end = (blockIdx.x + 1) * p.units / gridDim.x;
+      step = 1;
+    } else {
+      begin = blockIdx.x;
+      end = p.units;
+      step = gridDim.x;
+    }
+  }
+  __device__ int64_t chunk(int64_t u) const { return MODE == EVAL ? u % P : u / OT; }
+  __device__ int64_t owner(int64_t u) const { return MODE == EVAL ? u / P : u % OT; }
+};
+
+// Largest float below x (finite x): "score >= x" == "score > next_down(x)".
+__device__ __forceinline__ float next_down(float x) {
+  if (x == 0.f) return __int_as_float(0x80000001);
+  const int b = __float_as_int(x);
+  return __int_as_float(x > 0.f ? b - 1 : b + 1);
+}
+
+// Insert (cv, ci) into a descending top-K list, ties to the smaller index
+// (metrics.cpp:64-71 order); a no-op when it ranks below the K-th entry.
+__device__ __forceinline__ void topk_insert(float (&kv)[kEvalK], int (&ki)[kEvalK], float cv, int ci) {
+#pragma unroll
+  for (int k = 0; k < kEvalK; ++k) {
+    const bool bt = cv > kv[k] || (cv == kv[k] && ci < ki[k]);
+    const float t = kv[k];
+    const int u = ki[k];
+    kv[k] = bt ? cv : t;
+    ki[k] = bt ? ci : u;
+    cv = bt ? t : cv;
+    ci = bt ? u : ci;
+  }
+}
+
 template <int D, int MODE, int FLAGS>
 __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
     cce_tc_kernel(const __grid_constant__ CUtensorMap map_owner,
@@ -237,7 +297,7 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
     }
     for (int i = 0; i < C::kNB; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], MODE == FWD ? 4 : 1);  // FWD: one arrive per epilogue warp
+      mbar_init(&s_empty[i], MODE == FWD || MODE == EVAL ? 4 : 1);  // one arrive per epilogue warp
       mbar_init(&g_ready[i], 4);
     }
     mbar_init(owner_full, 1);
@@ -262,8 +322,9 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
       const uint64_t pol = policy_evict_normal();
       Ring<C::kStages> rs;
       uint32_t j = 0;
-      for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
-        const int64_t chunk = u / p.owner_tiles, ot = u % p.owner_tiles;
+      const Units<MODE> U(p);
+      for (int64_t u = U.begin; u < U.end; u += U.step, ++j) {
+        const int64_t chunk = U.chunk(u), ot = U.owner(u);
         const int64_t s_begin = chunk * p.chunk;
         const int64_t s_end = min(p.n_stream, s_begin + p.chunk);
         mbar_wait(owner_empty, (j & 1) ^ 1);
@@ -273,6 +334,16 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
           tma_load_2d(owner_smem + a * BM * 128, &map_owner, owner_full, a * 64,
                       static_cast<int32_t>(ot * BM), pol);
         if (MODE == BWD_ITEMS) tma_load_2d(ones_smem, &map_ones, owner_full, 0, 0, pol);
+        if (MODE == EVAL) {
+          // the owner rows' own target items (gathered, row-aligned with the owner tile)
+          unsigned char* stg = stage_smem + rs.i * C::kStageBytes;
+          mbar_wait(&empty[rs.i], rs.ph ^ 1);
+          mbar_arrive_expect_tx(&full[rs.i], C::kTileBytes);
+#pragma unroll
+          for (int a = 0; a < C::kAtoms; ++a)
+            tma_load_2d(stg + a * BN * 128, &map_lsex, &full[rs.i], a * 64, static_cast<int32_t>(ot * BM), pol);
+          rs.next();
+        }
         for (int64_t s0 = s_begin; s0 < s_end; s0 += BN, rs.next()) {
           unsigned char* stg = stage_smem + rs.i * C::kStageBytes;
           mbar_wait(&empty[rs.i], rs.ph ^ 1);
@@ -310,11 +381,12 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
     Ring<C::kNB> b1;
     uint32_t j = 0;
     unsigned long long tiles_seen = 0;
-    for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
-      const int64_t chunk = u / p.owner_tiles;
+    const Units<MODE> U(p);
+    for (int64_t u = U.begin; u < U.end; u += U.step, ++j) {
+      const int64_t chunk = U.chunk(u);
       const int64_t s_begin = chunk * p.chunk;
       const int64_t s_end = min(p.n_stream, s_begin + p.chunk);
-      const int ntile = static_cast<int>(ceil_div(s_end - s_begin, BN));
+      const int ntile = static_cast<int>(ceil_div(s_end - s_begin, BN)) + (MODE == EVAL ? 1 : 0);
       mbar_wait(owner_full, j & 1);
       tc_fence_after();
       for (int i = 0; i < ntile; ++i, s1.next(), b1.next()) {
@@ -337,7 +409,7 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
                    idesc1, 1u);
           }
           mma_commit(&s_full[b1.i]);
-          if (MODE == FWD) mma_commit(&empty[s1.i]);
+          if (MODE == FWD || MODE == EVAL) mma_commit(&empty[s1.i]);
         }
         __syncwarp();
         ++tiles_seen;
@@ -348,7 +420,7 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
     // 4 * NQ sub-tiles (4 warps x NQ column chunks) per 128 x BN tile
     if (lane == 0 && MODE == BWD_ROWS && (FLAGS & kCount))
       atomicAdd(&p.counters[2], 4ull * NQ * tiles_seen);
-  } else if (MODE != FWD && warp == 2) {
+  } else if (G::kCtrlWarps == 3 && warp == 2) {
     // ==================== MMA issuer: G . stream (backward) ====================
     // acc (dX_o or dE_o) += G(t) . stream(t): G is bf16 in S buffer b2, K step
     // kk (stream rows 16kk..16kk+15) at columns 8kk; B = the stream tile viewed
@@ -360,8 +432,9 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
     Ring<C::kStages> s2;
     Ring<C::kNB> b2;
     uint32_t j = 0;
-    for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
-      const int64_t chunk = u / p.owner_tiles;
+    const Units<MODE> U(p);
+    for (int64_t u = U.begin; u < U.end; u += U.step, ++j) {
+      const int64_t chunk = U.chunk(u);
       const int64_t s_begin = chunk * p.chunk;
       const int64_t s_end = min(p.n_stream, s_begin + p.chunk);
       const int ntile = static_cast<int>(ceil_div(s_end - s_begin, BN));
@@ -398,8 +471,16 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
     Ring<C::kStages> rst;    // its smem stage (BWD_ITEMS staging)
     int tw = 0;              // current tile's warpgroup (t % NWG)
     uint32_t j = 0;
-    for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
-      const int64_t chunk = u / p.owner_tiles, ot = u % p.owner_tiles;
+    const Units<MODE> U(p);
+    // EVAL state, carried across the consecutive units of one owner tile:
+    // items ranked ahead of the target, running top-k
+    uint32_t ecnt = 0;
+    float kv[kEvalK];
+    int ki[kEvalK];
+    for (int64_t u = U.begin; u < U.end; u += U.step, ++j) {
+      const int64_t chunk = U.chunk(u), ot = U.owner(u);
+      const bool run_first = u == U.begin || U.owner(u - 1) != ot;
+      const bool run_last = u + 1 == U.end || U.owner(u + 1) != ot;
       const int64_t s_begin = chunk * p.chunk;
       const int64_t s_end = min(p.n_stream, s_begin + p.chunk);
       const int64_t ntile = ceil_div(s_end - s_begin, BN);
@@ -412,10 +493,46 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
         if (MODE == BWD_ROWS) lse2 = p.lse2[orow];
       }
       float m = -INFINITY, s = 0.f, tv = 0.f, has = 0.f;
-      for (int64_t i = 0; i < ntile; ++i, rb.next(), rst.next(), tw = (tw + 1 == NWG ? 0 : tw + 1)) {
+      float st = 0.f, st_dn = 0.f;  // EVAL: the row's target score
+      if (MODE == EVAL && run_first) {
+        ecnt = 0;
+#pragma unroll
+        for (int k = 0; k < kEvalK; ++k) {
+          kv[k] = -INFINITY;
+          ki[k] = 0x7fffffff;
+        }
+      }
+      constexpr int kPre = MODE == EVAL ? 1 : 0;  // EVAL: the target-rows tile comes first
+      for (int64_t i = 0; i < ntile + kPre; ++i, rb.next(), rst.next(), tw = (tw + 1 == NWG ? 0 : tw + 1)) {
+        if (MODE == EVAL && i == 0) {
+          // S = owner rows x their target rows: the diagonal is each row's
+          // target score, from the same MMA as the scores it is compared with.
+          // The warpgroup that owns this tile publishes it to the other.
+          static_assert(MODE != EVAL || NWG == 2, "EVAL hands the target scores between 2 warpgroups");
+          float* st_sh = reinterpret_cast<float*>(merge) + (NWG - 1) * BM * C::kEvalStride;
+          if (tw == wg) {
+            const int b = static_cast<int>(rb.i);
+            mbar_wait(&s_full[b], rb.ph);
+            tc_fence_after();
+            float d[32];
+            LF_TMEM_LD32(tmem + lane_base + b * BN + quad * 32, reinterpret_cast<uint32_t*>(d));
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[b]);
+            st = select_reg(d, lane);
+            st_sh[lrow] = st;
+            named_bar_arrive(2, G::kEpiThreads);
+          } else {
+            named_bar_sync(2, G::kEpiThreads);
+            st = st_sh[lrow];
+          }
+          st_dn = next_down(st);
+          continue;
+        }
         if (tw != wg) continue;
         const int b = static_cast<int>(rb.i);
-        const int64_t col0 = s_begin + i * BN;
+        const int64_t col0 = s_begin + (i - kPre) * BN;
         const int nvalid = static_cast<int>((s_end - col0 < BN ? s_end - col0 : BN));
         mbar_wait(&s_full[b], rb.ph);
         tc_fence_after();
@@ -479,6 +596,81 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
             sum = acc0 + acc1;
           }
           s += sum;
+          }
+        } else if (MODE == EVAL) {
+          // ---- ranking (metrics.cpp:56-78).  An item ranks ahead of the
+          // target if its score is higher, or equal with a smaller index: a
+          // 64-column slab wholly before the target counts score >= st (as
+          // > next_down(st)), one wholly after counts score > st, and the slab
+          // holding the target compares per element.  The top-k list only
+          // sees slabs whose max beats its k-th entry (rare after warm-up).
+          // The slab loop stays rolled: the epilogue must fit the i-cache.
+          const int lc = tgt - static_cast<int>(col0);
+#pragma unroll 1
+          for (int h = 0; h < BN / 64; ++h) {
+            float w[2][32];
+            LF_TMEM_LD32(ta + h * 64, reinterpret_cast<uint32_t*>(w[0]));
+            LF_TMEM_LD32(ta + h * 64 + 32, reinterpret_cast<uint32_t*>(w[1]));
+            tmem_ld_wait();
+            if (h + 1 == BN / 64) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&s_empty[b]);
+            }
+            if (nvalid - h * 64 < 64) {
+#pragma unroll
+              for (int g = 0; g < 2; ++g)
+#pragma unroll
+                for (int c = 0; c < 32; ++c)
+                  if (h * 64 + g * 32 + c >= nvalid) w[g][c] = -INFINITY;
+            }
+            const int l = lc - h * 64;
+            if (static_cast<unsigned>(l) < 64u) {
+#pragma unroll
+              for (int g = 0; g < 2; ++g)
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                  const int cc = g * 32 + c;
+                  ecnt -= cc < l ? set_ge(w[g][c], st) : (cc > l ? set_gt(w[g][c], st) : 0u);
+                }
+            } else {
+              // 1.0f / 0.0f per compare (FSET.BF, ALU pipe) summed on the FMA
+              // pipe: exact (<= 64), one ALU op per item
+              const float thr = l >= 64 ? st_dn : st;
+              float f[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+              for (int g = 0; g < 2; ++g)
+#pragma unroll
+                for (int c = 0; c < 32; ++c) f[c & 3] += fset_gt(w[g][c], thr);
+              ecnt += static_cast<uint32_t>((f[0] + f[1]) + (f[2] + f[3]));
+            }
+#ifndef LF_DIAG_NOTOPK
+            const float g0 = max32(w[0]), g1 = max32(w[1]);
+            if (fmaxf(g0, g1) > kv[kEvalK - 1]) {  // divergent, rare once the list has filled
+              const float kth = kv[kEvalK - 1];
+              uint32_t m0 = 0, m1 = 0;
+              if (g0 > kth) {
+#pragma unroll
+                for (int c = 0; c < 32; ++c) m0 |= (w[0][c] > kth ? 1u : 0u) << c;
+              }
+              if (g1 > kth) {
+#pragma unroll
+                for (int c = 0; c < 32; ++c) m1 |= (w[1][c] > kth ? 1u : 0u) << c;
+              }
+              unsigned long long msk = (static_cast<unsigned long long>(m1) << 32) | m0;
+              const int base = static_cast<int>(col0) + h * 64;
+              if ((msk & (msk - 1ull)) == 0ull) {  // the slab max is the only candidate
+                topk_insert(kv, ki, fmaxf(g0, g1), base + __ffsll(static_cast<long long>(msk)) - 1);
+              } else {
+                do {
+                  const int c = __ffsll(static_cast<long long>(msk)) - 1;
+                  msk &= msk - 1ull;
+                  const float cv = c < 32 ? select_reg(w[0], c) : select_reg(w[1], c - 32);
+                  if (cv > kv[kEvalK - 1]) topk_insert(kv, ki, cv, base + c);
+                } while (msk);
+              }
+            }
+#endif
           }
         } else {
           // ---- backward: G = softmax * |scale| (target: minus |scale|), bf16,
@@ -671,6 +863,54 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
           if (orow < p.n_owner) p.part[chunk * p.n_owner + orow] = make_float4(m, s, tv, has);
         }
         named_bar_sync(1, G::kEpiThreads);
+      } else if (MODE == EVAL && !run_last) {
+        // the owner rows continue in this CTA's next unit: keep the state, and
+        // leave this chunk's slot empty (the run's totals go to its last slot)
+        if (wg == 0 && orow < p.n_owner) {
+          const int64_t rowp = chunk * p.n_owner + orow;
+          p.ev_count[rowp] = 0;
+          int4* di = reinterpret_cast<int4*>(p.ev_idx + rowp * kEvalK);
+#pragma unroll
+          for (int k = 0; k < kEvalK; k += 4) di[k / 4] = make_int4(0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff);
+        }
+      } else if (MODE == EVAL) {
+        // end of the run: merge the warpgroups' counts and top-k lists, one
+        // record per row
+        uint32_t* rec = reinterpret_cast<uint32_t*>(merge);
+        if (wg > 0) {
+          uint32_t* r = rec + ((wg - 1) * BM + lrow) * C::kEvalStride;
+          r[0] = ecnt;
+#pragma unroll
+          for (int k = 0; k < kEvalK; ++k) {
+            r[1 + k] = __float_as_uint(kv[k]);
+            r[1 + kEvalK + k] = static_cast<uint32_t>(ki[k]);
+          }
+        }
+        named_bar_sync(1, G::kEpiThreads);
+        if (wg == 0) {
+          for (int o = 0; o < NWG - 1; ++o) {
+            const uint32_t* r = rec + (o * BM + lrow) * C::kEvalStride;
+            ecnt += r[0];
+            for (int k = 0; k < kEvalK; ++k) {  // descending: stop at the first that does not fit
+              const float cv = __uint_as_float(r[1 + k]);
+              const int ci = static_cast<int>(r[1 + kEvalK + k]);
+              if (!(cv > kv[kEvalK - 1] || (cv == kv[kEvalK - 1] && ci < ki[kEvalK - 1]))) break;
+              topk_insert(kv, ki, cv, ci);
+            }
+          }
+          if (orow < p.n_owner) {
+            const int64_t rowp = chunk * p.n_owner + orow;
+            p.ev_count[rowp] = ecnt;
+            float4* dv = reinterpret_cast<float4*>(p.ev_val + rowp * kEvalK);
+            int4* di = reinterpret_cast<int4*>(p.ev_idx + rowp * kEvalK);
+#pragma unroll
+            for (int k = 0; k < kEvalK; k += 4) {
+              dv[k / 4] = make_float4(kv[k], kv[k + 1], kv[k + 2], kv[k + 3]);
+              di[k / 4] = make_int4(ki[k], ki[k + 1], ki[k + 2], ki[k + 3]);
+            }
+          }
+        }
+        named_bar_sync(1, G::kEpiThreads);
       } else {
         // accumulator read-out: 16-column groups round robin over warpgroups
         mbar_wait(acc_full, j & 1);
@@ -840,7 +1080,10 @@ int launch_mode(const CUtensorMap& mo, const CUtensorMap& ms, const CUtensorMap&
   auto kern = cce_tc_kernel<D, MODE, FLAGS>;
   LF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
   const int grid = static_cast<int>(std::min<int64_t>(p.units, num_sms()));
-  ProfScope prof(MODE == FWD ? LF_K_CCE_FWD : (MODE == BWD_ROWS ? LF_K_CCE_BWD_DX : LF_K_CCE_BWD_DE), st);
+  ProfScope prof(MODE == FWD    ? LF_K_CCE_FWD
+                 : MODE == EVAL ? LF_K_EVAL
+                 : (MODE == BWD_ROWS ? LF_K_CCE_BWD_DX : LF_K_CCE_BWD_DE),
+                 st);
   kern<<<grid, Geo<MODE>::kThreads, C::kSmem, st>>>(mo, ms, mb, m1, p);
   LF_LAUNCHED();
   return LF_OK;
@@ -849,12 +1092,15 @@ int launch_mode(const CUtensorMap& mo, const CUtensorMap& ms, const CUtensorMap&
 template <int D, int MODE>
 int launch_flags(int flags, const CUtensorMap& mo, const CUtensorMap& ms, const CUtensorMap& mb,
                  const CUtensorMap& m1, const TcParams& p, cudaStream_t st) {
-  if (MODE == FWD) return launch_mode<D, MODE, 0>(mo, ms, mb, m1, p, st);
-  switch (flags) {
-    case 0: return launch_mode<D, MODE, 0>(mo, ms, mb, m1, p, st);
-    case kFilt: return launch_mode<D, MODE, kFilt>(mo, ms, mb, m1, p, st);
-    case kFilt | kTgtIn: return launch_mode<D, MODE, kFilt | kTgtIn>(mo, ms, mb, m1, p, st);
-    default: return launch_mode<D, MODE, kFilt | kCount | kTgtIn>(mo, ms, mb, m1, p, st);
+  if constexpr (MODE == FWD || MODE == EVAL) {
+    return launch_mode<D, MODE, 0>(mo, ms, mb, m1, p, st);
+  } else {
+    switch (flags) {
+      case 0: return launch_mode<D, MODE, 0>(mo, ms, mb, m1, p, st);
+      case kFilt: return launch_mode<D, MODE, kFilt>(mo, ms, mb, m1, p, st);
+      case kFilt | kTgtIn: return launch_mode<D, MODE, kFilt | kTgtIn>(mo, ms, mb, m1, p, st);
+      default: return launch_mode<D, MODE, kFilt | kCount | kTgtIn>(mo, ms, mb, m1, p, st);
+    }
   }
 }
 
@@ -931,6 +1177,44 @@ int tc_cce_forward_partials(const void* X, const void* E, const int64_t* targets
   rc = launch_d<FWD>(D, 0, mo, ms, mo, mo, p, st);
   if (rc) return rc;
   *part_out = ws.as<float>();
+  *P_out = static_cast<int>(P);
+  return LF_OK;
+}
+
+int tc_eval_partials(const void* X, const void* E, const void* Et, const int32_t* tl, int64_t n,
+                     int D, int64_t v, Scratch& cnt, Scratch& val, Scratch& idx, int* P_out,
+                     cudaStream_t st) {
+  constexpr int BN = Geo<EVAL>::BN;
+  const int64_t owner_tiles = ceil_div(n, BM);
+  const int64_t stream_tiles = ceil_div(v, BN);
+#ifndef LF_EVAL_CHUNKS
+#define LF_EVAL_CHUNKS 64
+#endif
+  const int64_t chunks = pick_chunks(owner_tiles, stream_tiles, LF_EVAL_CHUNKS);
+  const int64_t tiles_per = ceil_div(stream_tiles, chunks);
+  const int64_t P = ceil_div(stream_tiles, tiles_per);
+  int rc = cnt.alloc(sizeof(uint32_t) * P * n, st);
+  if (!rc) rc = val.alloc(sizeof(float) * P * n * kEvalK, st);
+  if (!rc) rc = idx.alloc(sizeof(int32_t) * P * n * kEvalK, st);
+  if (rc) return rc;
+  CUtensorMap mo, ms, mt;
+  rc = make_map(&mo, X, n, D, BM);
+  if (!rc) rc = make_map(&ms, E, v, D, BN);
+  if (!rc) rc = make_map(&mt, Et, owner_tiles * BM, D, BM);
+  if (rc) return rc;
+  TcParams p{};
+  p.n_owner = n;
+  p.n_stream = v;
+  p.owner_tiles = owner_tiles;
+  p.chunk = tiles_per * BN;
+  p.n_chunks = P;
+  p.units = owner_tiles * P;
+  p.tgt = tl;
+  p.ev_count = cnt.as<uint32_t>();
+  p.ev_val = val.as<float>();
+  p.ev_idx = idx.as<int32_t>();
+  rc = launch_d<EVAL>(D, 0, mo, ms, mt, mo, p, st);
+  if (rc) return rc;
   *P_out = static_cast<int>(P);
   return LF_OK;
 }

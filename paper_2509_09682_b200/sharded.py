@@ -85,6 +85,76 @@ class DeviceKernels:
         return dX, dE, s
 
 
+class DeviceEvalKernels:
+    """The C-ABI evaluation kernels (metrics.py) on CUDA tensors."""
+
+    def rank_topk(self, X, E_shard, targets, k, v_offset, target_rows):
+        from .metrics import rank_topk
+        return rank_topk(X, E_shard, targets, k, v_offset, target_rows)
+
+    def merge(self, ahead, top_idx, top_score):
+        from .metrics import merge_shards
+        return merge_shards(ahead, top_idx, top_score)
+
+    def summarize(self, rank, top_idx, popularity):
+        from .metrics import summarize
+        return summarize(rank, top_idx, popularity)
+
+
+class ShardedEval:
+    """Catalog-sharded evaluate() (metrics.cpp:13-103): every rank ranks the
+    replicated rows against its item slice.  Exchanges: one all-reduce of the
+    rows' target item rows (n x d; each target's owner contributes it, so
+    every rank scores the target on the same arithmetic path), then one
+    all-gather of the per-shard (ahead, top-k ids, top-k scores); ranks add,
+    lists merge, and every rank aggregates the same summary."""
+
+    def __init__(self, v_total: int, group=None, kernels=None):
+        self.group = group
+        self.P = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.v_total = v_total
+        self.v_begin, self.v_end = shard_bounds(v_total, self.P, self.rank)
+        self.kernels = kernels if kernels is not None else DeviceEvalKernels()
+
+    def target_rows(self, E_shard: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
+        local = targets.to(torch.int64) - self.v_begin
+        mine = (local >= 0) & (local < E_shard.shape[0])
+        wire = torch.float64 if E_shard.dtype == torch.float64 else torch.float32
+        rows = torch.zeros((targets.numel(), E_shard.shape[1]), dtype=wire, device=E_shard.device)
+        rows[mine] = E_shard[local[mine]].to(wire)
+        if self.P > 1:
+            dist.all_reduce(rows, op=dist.ReduceOp.SUM, group=self.group)
+        return rows.to(E_shard.dtype)
+
+    def _gather(self, t: torch.Tensor) -> torch.Tensor:
+        if self.P == 1:
+            return t.unsqueeze(0)
+        flat = torch.empty((self.P * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        dist.all_gather_into_tensor(flat, t.contiguous(), group=self.group)
+        return flat.view((self.P,) + tuple(t.shape))
+
+    def rank_topk(self, X, E_shard, targets, k: int):
+        """(1-based rank [n], global top-k ids [n, k], scores [n, k])."""
+        if E_shard.shape[0] != self.v_end - self.v_begin:
+            raise ValueError(f"sharded eval: rank {self.rank} expects {self.v_end - self.v_begin} "
+                             f"item rows, got {E_shard.shape[0]}")
+        rows = self.target_rows(E_shard, targets)
+        ahead, top, score = self.kernels.rank_topk(X, E_shard, targets, k, self.v_begin, rows)
+        return self.kernels.merge(self._gather(ahead), self._gather(top), self._gather(score))
+
+    def evaluate(self, X, E_shard, targets, k: int, popularity):
+        if X.shape[0] == 0:
+            raise ValueError("evaluate: no eval pairs")
+        if k < 1:
+            raise ValueError("evaluate: k must be >= 1")
+        if popularity.numel() != self.v_total:
+            raise ValueError("evaluate: popularity table size does not match the catalog")
+        k_eff = min(k, self.v_total)
+        rank, top, _ = self.rank_topk(X, E_shard, targets, k_eff)
+        return self.kernels.summarize(rank, top, popularity)
+
+
 class ShardedCce:
     """Catalog-sharded cce_forward / cce_backward over a process group."""
 

@@ -76,8 +76,30 @@ def main():
     ccem["sampler_pos"] = pos
     ccem["sampler_inds"] = ob.ref_sample_uniform(pos, 12, 97, 0xB2000003)
     np.savez_compressed(os.path.join(HERE, "ccem_ref.npz"), **ccem)
+    eval_fixtures()
     print("wrote", sorted(f for f in os.listdir(HERE) if f.endswith(".npz")))
 
 
+def eval_fixtures():
+    """evaluate() (metrics.cpp:13-103) on ToyEncoderParams::Init instances:
+    summary, encoded rows H, classifier C and per-row ranks (eval_ref.npz)."""
+    cases = [(300, 16, 11, 40, 3, 10), (1000, 64, 12, 100, 5, 16), (9, 4, 0xE1, 5, 2, 9),
+             (129, 8, 13, 33, 1, 1), (2000, 32, 14, 64, 4, 32)]
+    ev = {}
+    for c, (cat, hid, seed, n, L, k) in enumerate(cases):
+        g = np.random.default_rng(seed)
+        pre = g.integers(0, cat, (n, L))
+        tg = g.integers(0, cat, n)
+        counts = g.integers(0, 40, cat)
+        out3, H, Cm, ranks = ob.ref_eval_instance(cat, hid, seed, pre, tg, k, counts)
+        ev.update({f"{c}_H": H, f"{c}_C": Cm, f"{c}_t": tg, f"{c}_counts": counts,
+                   f"{c}_k": np.int64(k), f"{c}_out3": np.array(out3), f"{c}_ranks": ranks})
+    ev["count"] = np.int64(len(cases))
+    np.savez_compressed(os.path.join(HERE, "eval_ref.npz"), **ev)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["eval"]:
+        eval_fixtures()
+    else:
+        main()

@@ -74,6 +74,10 @@ def orc():
         L.orc_validate_inds.restype = C.c_int64
         L.orc_estimate_flops.argtypes = [_sz, _sz, _sz, _sz, C.c_int, C.POINTER(C.c_uint64),
                                          C.POINTER(C.c_uint64)]
+        L.orc_eval_rank_topk.argtypes = [_f64p, _f32p, _i64p, _sz, _sz, _sz, _sz, _sz, _sz,
+                                         _i64p, _i64p, _f64p]
+        L.orc_eval_summary.argtypes = [_i64p, _i64p, _sz, _sz, _i64p, _sz, _f64p]
+        L.orc_eval_summary.restype = C.c_int
         _orc = L
     return _orc
 
@@ -112,6 +116,8 @@ def ref():
         L.ref_validate_inds.argtypes = [_i64p, _sz, _sz, _sz]
         L.ref_estimate_flops.argtypes = [_sz, _sz, _sz, _sz, C.c_int, C.POINTER(C.c_uint64),
                                          C.POINTER(C.c_uint64)]
+        L.ref_eval_instance.argtypes = [_sz, _sz, C.c_uint64, _sz, _sz, _i64p, _i64p, _sz, _i64p,
+                                        C.c_int, _f64p, _f64p, _f32p, _i64p]
         _ref = L
     return _ref
 
@@ -241,6 +247,40 @@ def estimate_flops(n, d, v, ns, backend: int):
     return f.value, b.value
 
 
+def eval_rank_topk(H, Cm, targets, k, v0=0, v1=None):
+    """metrics.cpp:46-72 over items [v0, v1): (ahead, top_idx, top_score)."""
+    n, d = H.shape
+    v = Cm.shape[1]
+    v1 = v if v1 is None else v1
+    ahead = np.empty(n, np.int64)
+    top = np.empty((n, k), np.int64)
+    score = np.empty((n, k))
+    orc().orc_eval_rank_topk(np.ascontiguousarray(H, np.float64), np.ascontiguousarray(Cm, np.float32),
+                             np.ascontiguousarray(targets, np.int64), n, d, v, v0, v1, k, ahead,
+                             top, score)
+    return ahead, top, score
+
+
+def eval_summary(rank, top, counts):
+    """metrics.cpp:26-33, 62, 74-103 -> (ndcg, coverage, surprisal)."""
+    n, k = top.shape
+    out = np.empty(3)
+    rc = orc().orc_eval_summary(np.ascontiguousarray(rank, np.int64), np.ascontiguousarray(top, np.int64),
+                                n, k, np.ascontiguousarray(counts, np.int64), len(counts), out)
+    if rc == 1:
+        raise ValueError("evaluate: negative popularity count")
+    if rc == 2:
+        raise ValueError("evaluate: popularity table needs at least 2 training events")
+    return tuple(out)
+
+
+def evaluate(H, Cm, targets, k, counts):
+    """evaluate() minus the encoder: k_eff = min(k, v) (metrics.cpp:34)."""
+    k_eff = min(k, Cm.shape[1])
+    ahead, top, _ = eval_rank_topk(H, Cm, targets, k_eff)
+    return eval_summary(ahead + 1, top, counts)
+
+
 # ---------------------------------------------------------------------------
 # Reference (oracle/_ref) wrappers
 # ---------------------------------------------------------------------------
@@ -343,3 +383,19 @@ def rel_err(got, want):
     got = np.asarray(got, np.float64)
     want = np.asarray(want, np.float64)
     return np.abs(got - want) / np.maximum(1.0, np.abs(want))
+
+
+def ref_eval_instance(catalog, hidden, seed, prefixes, targets, k, counts, workers=1):
+    """The reference's evaluate() on ToyEncoderParams::Init(catalog, hidden,
+    SplitMix64(seed)): (out3, H, C, ranks) — see oracle/ref_capi.cpp."""
+    L = ref()
+    prefixes = np.ascontiguousarray(prefixes, np.int64)
+    n, Lp = prefixes.shape
+    out = np.empty(3)
+    H = np.empty((n, hidden))
+    Cm = np.empty((hidden, catalog), np.float32)
+    ranks = np.empty(n, np.int64)
+    _chk(L.ref_eval_instance(catalog, hidden, seed, n, Lp, prefixes,
+                             np.ascontiguousarray(targets, np.int64), k,
+                             np.ascontiguousarray(counts, np.int64), workers, out, H, Cm, ranks), L)
+    return tuple(out), H, Cm, ranks

@@ -1,0 +1,189 @@
+"""GPU: full-catalog evaluation (metrics.cpp:13-103) through the C-ABI
+(lf_eval_rank_topk / lf_eval_merge / lf_eval_summary / lf_evaluate).
+
+* f64 reproduces the reference: ranks and top-k lists bitwise, summary to
+  1e-14 (device log2 vs glibc), against golden fixtures made by running the
+  reference's own evaluate() (tests/golden/eval_ref.npz) and the C oracle.
+* f32 / bf16 (tcgen05 EVAL kernel): scores are rounded (fp32 accumulate), so
+  ranks are checked against exact fp64 scores of the same rounded inputs
+  within the score tolerance delta: every item the GPU counts ahead must be
+  ahead up to delta, and vice versa; top-k scores within delta of the exact
+  top-k.  Tolerances: delta = 1e-6 sum_k |x_k e_k| (f32 and bf16: products of
+  bf16 / fp32 inputs accumulated in fp32).
+* Ties (identical item rows, test_harness.cpp:795-815) are exact in every dtype.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle_bind as ob
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.fixture(scope="module")
+def lf(cuda):
+    import paper_2509_09682_b200 as lf
+    return lf
+
+
+@pytest.fixture(scope="module")
+def M(cuda):
+    from paper_2509_09682_b200 import metrics
+    return metrics
+
+
+def _golden():
+    return np.load(os.path.join(GOLDEN, "eval_ref.npz"))
+
+
+def test_f64_matches_reference_golden(lf, M):
+    g = _golden()
+    for c in range(int(g["count"])):
+        H, Cm, t, counts, k = g[f"{c}_H"], g[f"{c}_C"], g[f"{c}_t"], g[f"{c}_counts"], int(g[f"{c}_k"])
+        X = torch.from_numpy(H).cuda()
+        E = torch.from_numpy(np.ascontiguousarray(Cm.T).astype(np.float64)).cuda()
+        tg = torch.from_numpy(t).cuda()
+        k_eff = min(k, Cm.shape[1])
+        ahead, top, score = M.rank_topk(X, E, tg, k_eff)
+        assert np.array_equal(ahead.cpu().numpy() + 1, g[f"{c}_ranks"])
+        o_ahead, o_top, o_score = ob.eval_rank_topk(H, Cm, t, k_eff)
+        assert np.array_equal(top.cpu().numpy(), o_top)
+        assert np.array_equal(score.cpu().numpy(), o_score)
+        s = lf.evaluate(X, E, tg, k, torch.from_numpy(counts))
+        want = g[f"{c}_out3"]
+        assert s.ndcg == pytest.approx(want[0], rel=1e-14, abs=1e-15)
+        assert s.coverage == want[1]
+        assert s.surprisal == pytest.approx(want[2], rel=1e-14, abs=1e-15)
+
+
+def _check_rounded(X, E, tg, ahead, top, score, k):
+    """Rank / top-k of rounded-arithmetic scores vs exact fp64 scores of the
+    same inputs, within delta."""
+    Xd, Ed = X.double(), E.double()
+    S = Xd @ Ed.T                                      # exact enough (fp64)
+    A = Xd.abs() @ Ed.abs().T
+    v = S.shape[1]
+    n = S.shape[0]
+    rows = torch.arange(n, device=S.device)
+    st = S[rows, tg]
+    delta = 1e-6 * A[rows, tg].clamp_min(1e-30)
+    lo = (S > (st + 2 * delta)[:, None]).sum(1)
+    hi = (S >= (st - 2 * delta)[:, None]).sum(1) - 1     # minus the target itself
+    a = ahead
+    assert bool(((a >= lo) & (a <= hi)).all()), (a - lo).min().item()
+    # top-k: scores within delta of the exact k best, ids distinct and valid
+    kk = min(k, v)
+    best = torch.topk(S, kk, dim=1).values
+    dk = 2e-6 * A.max(1).values[:, None]
+    assert bool(((score[:, :kk] - best).abs() <= dk).all())
+    got = S.gather(1, top[:, :kk])
+    assert bool(((got - score[:, :kk]).abs() <= dk).all())
+    srt = torch.sort(top[:, :kk], dim=1).values
+    assert bool((srt[:, 1:] != srt[:, :-1]).all())
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("n,d,v,k", [(1, 64, 1000, 10), (300, 64, 5000, 16), (129, 128, 777, 5),
+                                     (257, 64, 130, 16), (64, 256, 3000, 10), (200, 192, 1500, 8)])
+def test_rounded_dtypes_rank_within_tolerance(M, dtype, n, d, v, k):
+    g = torch.Generator(device="cpu").manual_seed(n * 31 + v)
+    X = (torch.randn(n, d, generator=g) * 0.5).to(dtype).cuda()
+    E = (torch.randn(v, d, generator=g) * 0.5).to(dtype).cuda()
+    tg = torch.randint(0, v, (n,), generator=g).cuda()
+    ahead, top, score = M.rank_topk(X, E, tg, k)
+    _check_rounded(X, E, tg, ahead, top, score, k)
+
+
+def test_bf16_large_catalog(M):
+    n, d, v, k = 512, 64, 200_000, 10
+    g = torch.Generator(device="cpu").manual_seed(7)
+    X = (torch.randn(n, d, generator=g) * 0.3).to(torch.bfloat16).cuda()
+    E = (torch.randn(v, d, generator=g) * 0.3).to(torch.bfloat16).cuda()
+    tg = torch.randint(0, v, (n,), generator=g).cuda()
+    # plant a few well-ranked targets: the target row = the query row
+    E[tg[:32]] = X[:32]
+    ahead, top, score = M.rank_topk(X, E, tg, k)
+    _check_rounded(X, E, tg, ahead, top, score, k)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32, torch.bfloat16])
+def test_ties_break_to_smaller_id(M, dtype):
+    # test_harness.cpp:795-815: identical scores everywhere -> rank = t + 1,
+    # top-k = 0 .. k-1 (also across V chunks and 128-item tiles)
+    n, d, v, k = 200, 64, 3000, 16 if dtype == torch.bfloat16 else 20
+    row = torch.randn(1, d).to(dtype)
+    E = row.expand(v, d).contiguous().cuda()
+    X = torch.randn(n, d).to(dtype).cuda()
+    tg = torch.randint(0, v, (n,)).cuda()
+    ahead, top, _ = M.rank_topk(X, E, tg, k)
+    assert torch.equal(ahead, tg)
+    assert torch.equal(top, torch.arange(k, device="cuda").expand(n, k))
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.bfloat16])
+def test_shards_merge_to_full(M, dtype):
+    n, d, v, k = 150, 64, 4000, 12
+    g = torch.Generator(device="cpu").manual_seed(11)
+    X = torch.randn(n, d, generator=g).to(dtype).cuda()
+    E = torch.randn(v, d, generator=g).to(dtype).cuda()
+    tg = torch.randint(0, v, (n,), generator=g).cuda()
+    a_full, t_full, s_full = M.rank_topk(X, E, tg, k)
+    bounds = [0, 1337, 1338, 4000]
+    parts = [M.rank_topk(X, E[b:e], tg, k, v_offset=b, target_rows=E[tg])
+             for b, e in zip(bounds[:-1], bounds[1:])]
+    rank, top, score = M.merge_shards(torch.stack([p[0] for p in parts]),
+                                      torch.stack([p[1] for p in parts]),
+                                      torch.stack([p[2] for p in parts]))
+    assert torch.equal(rank, a_full + 1)
+    assert torch.equal(top, t_full)
+    assert torch.equal(score, s_full)
+    # a shard smaller than k pads with -1
+    assert int((parts[1][1] >= 0).sum(1).max()) == 1
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_target_score_matches_stream_scores(M, dtype):
+    # The target score (bf16: the diagonal of an MMA over the gathered target
+    # rows) must equal bitwise the score the same item gets in the stream:
+    # with the catalog duplicated, moving the target to the second copy adds
+    # exactly its own first-copy duplicate (plus exact ties) to `ahead`.
+    n, d, v = 256, 64, 2048
+    g = torch.Generator(device="cpu").manual_seed(3)
+    X = torch.randn(n, d, generator=g).to(dtype).cuda()
+    E = torch.randn(v, d, generator=g).to(dtype).cuda()
+    tg = torch.randint(0, v, (n,), generator=g).cuda()
+    E2 = torch.cat([E, E], 0)
+    a1, _, _ = M.rank_topk(X, E, tg, 8)          # gt + ties before t
+    a2, _, _ = M.rank_topk(X, E2, tg, 8)         # + gt of the second copy
+    a3, _, _ = M.rank_topk(X, E2, tg + v, 8)     # gt + all ties (incl. itself) + a1
+    eq_all = a3 - a2
+    assert bool((eq_all >= 1).all())
+    assert float((eq_all == 1).double().mean()) > 0.98
+    assert bool((a1 - (a2 - a1) >= 0).all())     # ties before t
+
+
+def test_errors(lf, M):
+    X = torch.randn(4, 64, device="cuda", dtype=torch.bfloat16)
+    E = torch.randn(100, 64, device="cuda", dtype=torch.bfloat16)
+    tg = torch.tensor([1, 2, 3, 99], device="cuda")
+    pop = torch.ones(100, dtype=torch.int64)
+    with pytest.raises(ValueError, match="k must be >= 1"):
+        lf.evaluate(X, E, tg, 0, pop)
+    with pytest.raises(ValueError, match="negative popularity"):
+        lf.evaluate(X, E, tg, 5, torch.cat([pop[:99], torch.tensor([-1])]))
+    with pytest.raises(ValueError, match="at least 2"):
+        lf.evaluate(X, E, tg, 5, torch.cat([torch.ones(1, dtype=torch.int64), torch.zeros(99, dtype=torch.int64)]))
+    with pytest.raises(ValueError, match="size does not match"):
+        lf.evaluate(X, E, tg, 5, pop[:50])
+    from paper_2509_09682_b200._capi import LfError
+    with pytest.raises(LfError, match="top-k"):
+        M.rank_topk(X, E, tg, 17)
+    with pytest.raises(ValueError, match="outside this catalog shard"):
+        M.rank_topk(X, E[:50], tg, 5)
+    s = lf.evaluate(X.double()[:, :8], E.double()[:20, :8], tg % 20, 200, pop[:20])  # k_eff = v
+    assert s.coverage == 1.0

@@ -120,3 +120,72 @@ def test_shard_bounds_cover_catalog():
             assert b[0][0] == 0 and b[-1][1] == v
             assert all(b[i][1] == b[i + 1][0] for i in range(P - 1))
             assert max(e - s for s, e in b) - min(e - s for s, e in b) <= 1
+
+
+class OracleEvalKernels:
+    """Test backend for ShardedEval: per-shard ranking from oracle/oracle.c on
+    the full instance (H n x d double, C d x v float); checks that the
+    exchanged target rows are the targets' item rows."""
+
+    def __init__(self, H, Cm, t):
+        self.H, self.Cm, self.t = H, Cm, t
+
+    def rank_topk(self, X, E_shard, targets, k, v_offset, target_rows):
+        want = np.ascontiguousarray(self.Cm.T[self.t]).astype(np.float64)
+        assert np.array_equal(target_rows.numpy(), want)
+        a, top, sc = ob.eval_rank_topk(self.H, self.Cm, self.t, k, v_offset,
+                                       v_offset + E_shard.shape[0])
+        return torch.from_numpy(a), torch.from_numpy(top), torch.from_numpy(sc)
+
+    def merge(self, ahead, top_idx, top_score):
+        P, n, k = top_idx.shape
+        rank = ahead.sum(0) + 1
+        top = np.empty((n, k), np.int64)
+        sc = np.empty((n, k))
+        for i in range(n):
+            cand = sorted((-float(top_score[p, i, e]), int(top_idx[p, i, e]))
+                          for p in range(P) for e in range(k) if top_idx[p, i, e] >= 0)[:k]
+            top[i] = [c[1] for c in cand]
+            sc[i] = [-c[0] for c in cand]
+        return rank, torch.from_numpy(top), torch.from_numpy(sc)
+
+    def summarize(self, rank, top_idx, popularity):
+        from paper_2509_09682_b200.metrics import EvalSummary
+        return EvalSummary(*ob.eval_summary(rank.numpy(), top_idx.numpy(), popularity.numpy()))
+
+
+def _eval_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2509_09682_b200.sharded import ShardedEval
+        g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "eval_ref.npz"))
+        H, Cm, t, counts, k = g["0_H"], g["0_C"], g["0_t"], g["0_counts"], int(g["0_k"])
+        se = ShardedEval(Cm.shape[1], kernels=OracleEvalKernels(H, Cm, t))
+        E_shard = torch.from_numpy(np.ascontiguousarray(Cm.T[se.v_begin:se.v_end]).astype(np.float64))
+        s = se.evaluate(torch.from_numpy(H), E_shard, torch.from_numpy(t), k, torch.from_numpy(counts))
+        r, top, _ = se.rank_topk(torch.from_numpy(H), E_shard, torch.from_numpy(t), k)
+        q.put((rank, (s.ndcg, s.coverage, s.surprisal), r.numpy(), top.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_sharded_evaluate_matches_reference():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_eval_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "eval_ref.npz"))
+    _, top_full, _ = ob.eval_rank_topk(g["0_H"], g["0_C"], g["0_t"], int(g["0_k"]))
+    for _, out3, r, top in results:
+        assert out3 == tuple(g["0_out3"])            # the reference's evaluate(), bitwise
+        assert np.array_equal(r, g["0_ranks"])
+        assert np.array_equal(top, top_full)
