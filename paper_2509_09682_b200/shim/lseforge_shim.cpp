@@ -9,9 +9,10 @@
 //   lseforge::ccem_backward        ccem.hpp:27-29  (reference ccem.cpp:196-205)
 //   lseforge::ccem_backward_rows   ccem.hpp:34-36  (reference ccem.cpp:107-194)
 //   lseforge::estimate_flops       ccem.hpp:48-49  (reference ccem.cpp:207-235)
+//   lseforge::evaluate             metrics.hpp:18-24 (reference metrics.cpp:13-103)
 //
 // It is compiled against the reference's own headers (-I proj/include) and
-// linked in place of cce.cpp + ccem.cpp; everything else in liblseforge
+// linked in place of cce.cpp + ccem.cpp + metrics.cpp; everything else in liblseforge
 // (losses.cpp validation and oracles, neg_index.cpp, accountant.cpp, the
 // trainer) is unchanged.  Each call: validate on the host with the
 // reference's own functions and messages -> upload the host matrices ->
@@ -39,6 +40,7 @@
 // (memory_model.cpp:46-60) does not describe the GPU and is not imitated.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -53,8 +55,12 @@
 #include "lseforge/cce.hpp"
 #include "lseforge/ccem.hpp"
 #include "lseforge/losses.hpp"
+#include "lseforge/encoder.hpp"
 #include "lseforge/matrix.hpp"
+#include "lseforge/metrics.hpp"
 #include "lseforge/neg_index.hpp"
+#include "lseforge/split.hpp"
+#include "lseforge/threads.hpp"
 #include "lseforge_b200.h"
 
 namespace lseforge {
@@ -353,6 +359,58 @@ FlopEstimate estimate_flops(std::size_t n, std::size_t d, std::size_t v, std::si
                                    static_cast<int32_t>(backend), &f.forward, &f.backward);
   if (rc != LF_OK) throw_status(rc, "lf_estimate_flops");
   return f;
+}
+
+EvalSummary evaluate(const ToyEncoderParams& params, std::span<const EvalPair> pairs, std::size_t k,
+                     const std::vector<std::int64_t>& popularity_counts, int workers) {
+  // argument checks in the reference's order (metrics.cpp:16-25); the
+  // popularity-table checks (metrics.cpp:26-33) run on the device with the
+  // same messages
+  if (pairs.empty()) throw std::invalid_argument("evaluate: no eval pairs");
+  if (k == 0) throw std::invalid_argument("evaluate: k must be >= 1");
+  const std::size_t v = params.catalog();
+  if (popularity_counts.size() != v)
+    throw std::invalid_argument("evaluate: popularity table size does not match the catalog");
+  const std::size_t n = pairs.size(), d = params.hidden();
+  // the encoder stays on the host (metrics.cpp:46): h for every pair
+  std::vector<double> H(n * d);
+  parallel_blocks(n, resolve_worker_count(workers), [&](std::size_t, std::size_t i) {
+    const std::vector<double> h = encode(params, pairs[i].prefix);
+    std::memcpy(H.data() + i * d, h.data(), sizeof(double) * d);
+  });
+  std::vector<std::int64_t> targets(n);
+  for (std::size_t i = 0; i < n; ++i) targets[i] = pairs[i].target;
+
+  const int dtype = device_dtype();
+  Dev X(n * d * elem_bytes(dtype)), E(v * d * elem_bytes(dtype)), tg(n * 8), pop(v * 8);
+  if (dtype == LF_F64) {
+    upload(X.p, H.data(), n * d * sizeof(double));  // exact: the reference scores in double
+  } else {
+    std::vector<float> Hf(H.begin(), H.end());
+    Dev stage(n * d * sizeof(float));
+    upload(stage.p, Hf.data(), n * d * sizeof(float));
+    check(lf_convert_rows(stage.as<float>(), static_cast<int64_t>(n * d), dtype, X.p, nullptr),
+          "lf_convert_rows");
+  }
+  {
+    Dev stage(d * v * sizeof(float));
+    upload(stage.p, params.c.data().data(), d * v * sizeof(float));
+    check(lf_classifier_to_items(stage.as<float>(), static_cast<int64_t>(d), static_cast<int64_t>(v),
+                                 dtype, E.p, nullptr),
+          "lf_classifier_to_items");
+  }
+  upload(tg.p, targets.data(), n * 8);
+  upload(pop.p, popularity_counts.data(), v * 8);
+  double out3[3];
+  check(lf_evaluate(X.p, E.p, tg.as<int64_t>(), static_cast<int64_t>(n), static_cast<int64_t>(d),
+                    static_cast<int64_t>(v), static_cast<int32_t>(std::min<std::size_t>(k, 1u << 30)),
+                    dtype, pop.as<int64_t>(), out3, nullptr),
+        "lf_evaluate");
+  EvalSummary out;
+  out.ndcg = out3[0];
+  out.coverage = out3[1];
+  out.surprisal = out3[2];
+  return out;
 }
 
 }  // namespace lseforge

@@ -9,7 +9,9 @@
 //
 // Supported surface (exactly what those suites use): TEST_CASE, CHECK,
 // REQUIRE, CHECK_NOTHROW, CHECK_THROWS_AS, CHECK_THROWS_WITH_AS with
-// doctest::Contains, CAPTURE, doctest::Approx(v).epsilon(e).scale(s), and
+// doctest::Contains, CAPTURE, CHECK_FALSE, FAIL, SUBCASE (one nesting level, with doctest's
+// re-run semantics: the test case runs once per subcase, entering exactly one
+// not-yet-run subcase each time), doctest::Approx(v).epsilon(e).scale(s), and
 // DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN.  Approx follows doctest's rule:
 // |a - b| < eps * (scale + max(|a|, |b|)), eps defaulting to 100 * FLT_EPSILON.
 // The runner prints one line per failed assertion and a summary; its exit
@@ -23,6 +25,7 @@
 #include <cstdio>
 #include <exception>
 #include <functional>
+#include <set>
 #include <sstream>
 #include <string>
 #include <type_traits>
@@ -145,12 +148,32 @@ struct State {
   int failed_assertions = 0;
   bool case_failed = false;
   std::vector<std::pair<std::string, std::string>> captures;
+  std::set<std::string> sub_done;  // subcases already run in this test case
+  bool sub_entered = false;        // a subcase was entered in this pass
+  bool sub_pending = false;        // a not-yet-run subcase was skipped in this pass
 };
 inline State& state() {
   static State s;
   return s;
 }
 struct RequireAbort {};
+
+struct Subcase {
+  bool active = false;
+  Subcase(const char* file, int line) {
+    State& s = state();
+    const std::string key = std::string(file) + ":" + std::to_string(line);
+    const bool done = s.sub_done.count(key) != 0;
+    if (s.sub_entered || done) {
+      if (!done) s.sub_pending = true;
+    } else {
+      s.sub_entered = true;
+      s.sub_done.insert(key);
+      active = true;
+    }
+  }
+  explicit operator bool() const { return active; }
+};
 
 struct Capture {
   template <class T>
@@ -182,16 +205,21 @@ inline int run(int argc, char** argv) {
     State& s = state();
     s.case_failed = false;
     s.captures.clear();
-    try {
-      tc.fn();
-    } catch (const RequireAbort&) {
-    } catch (const std::exception& e) {
-      std::fprintf(stderr, "%s:%d: test case threw: %s\n", tc.file, tc.line, e.what());
-      s.case_failed = true;
-    } catch (...) {
-      std::fprintf(stderr, "%s:%d: test case threw a non-std exception\n", tc.file, tc.line);
-      s.case_failed = true;
-    }
+    s.sub_done.clear();
+    do {
+      s.sub_entered = false;
+      s.sub_pending = false;
+      try {
+        tc.fn();
+      } catch (const RequireAbort&) {
+      } catch (const std::exception& e) {
+        std::fprintf(stderr, "%s:%d: test case threw: %s\n", tc.file, tc.line, e.what());
+        s.case_failed = true;
+      } catch (...) {
+        std::fprintf(stderr, "%s:%d: test case threw a non-std exception\n", tc.file, tc.line);
+        s.case_failed = true;
+      }
+    } while (s.sub_pending);
     if (s.case_failed) {
       ++failed;
       std::fprintf(stderr, "[FAIL] %s\n", tc.name);
@@ -222,8 +250,14 @@ inline int run(int argc, char** argv) {
     ::doctest::detail::report(lf_dt_r.ok, kind, #__VA_ARGS__, lf_dt_r.text, __FILE__,    \
                               __LINE__, require);                                        \
   } while (0)
+#define SUBCASE(name) \
+  if (const ::doctest::detail::Subcase LF_DT_CAT(lf_dt_sub_, __COUNTER__){__FILE__, __LINE__})
 #define CHECK(...) LF_DT_ASSERT("CHECK", false, __VA_ARGS__)
 #define REQUIRE(...) LF_DT_ASSERT("REQUIRE", true, __VA_ARGS__)
+#define CHECK_FALSE(...) \
+  ::doctest::detail::report(!static_cast<bool>(__VA_ARGS__), "CHECK_FALSE", #__VA_ARGS__, "", __FILE__, __LINE__, false)
+#define FAIL(msg) \
+  ::doctest::detail::report(false, "FAIL", "", ::doctest::detail::str(msg), __FILE__, __LINE__, true)
 
 #define CHECK_NOTHROW(...)                                                               \
   do {                                                                                   \
