@@ -148,7 +148,7 @@ struct Cfg {
   // EVAL: per-row merge records {count, K values, K indices} (stride 2K + 1
   // words: conflict-free) of the other warpgroups + the shared target scores
   static constexpr int kEvalStride = 2 * kEvalK + 1;
-  static constexpr int kEvalMerge = MODE == EVAL ? ((G::NWG - 1) * BM * kEvalStride + BM) * 4 : 0;
+  static constexpr int kEvalMerge = MODE == EVAL ? ((G::NWG - 1) * BM * kEvalStride + 2 * BM) * 4 : 0;
   static constexpr int kAccCol = kNB * BN;
   static constexpr int kSmem = 1024 /*align slack*/ + kOwnerBytes + kOnesBytes + kStages * kStageBytes +
                                1024 /*barriers*/ + (MODE == FWD ? (G::NWG - 1) * BM * 16 : 0) +
@@ -507,9 +507,10 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
         if (MODE == EVAL && i == 0) {
           // S = owner rows x their target rows: the diagonal is each row's
           // target score, from the same MMA as the scores it is compared with.
-          // The warpgroup that owns this tile publishes it to the other.
-          static_assert(MODE != EVAL || NWG == 2, "EVAL hands the target scores between 2 warpgroups");
-          float* st_sh = reinterpret_cast<float*>(merge) + (NWG - 1) * BM * C::kEvalStride;
+          // The warpgroup that owns this tile publishes it to the others
+          // (double-buffered by unit parity: a buffer is rewritten only after
+          // every warpgroup has passed the next unit's handoff).
+          float* st_sh = reinterpret_cast<float*>(merge) + (NWG - 1) * BM * C::kEvalStride + (j & 1) * BM;
           if (tw == wg) {
             const int b = static_cast<int>(rb.i);
             mbar_wait(&s_full[b], rb.ph);
