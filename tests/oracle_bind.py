@@ -117,7 +117,7 @@ def ref():
         L.ref_estimate_flops.argtypes = [_sz, _sz, _sz, _sz, C.c_int, C.POINTER(C.c_uint64),
                                          C.POINTER(C.c_uint64)]
         L.ref_eval_instance.argtypes = [_sz, _sz, C.c_uint64, _sz, _sz, _i64p, _i64p, _sz, _i64p,
-                                        C.c_int, _f64p, _f64p, _f32p, _i64p]
+                                        C.c_int, _f64p, C.c_void_p, C.c_void_p, C.c_void_p]
         _ref = L
     return _ref
 
@@ -385,17 +385,20 @@ def rel_err(got, want):
     return np.abs(got - want) / np.maximum(1.0, np.abs(want))
 
 
-def ref_eval_instance(catalog, hidden, seed, prefixes, targets, k, counts, workers=1):
+def ref_eval_instance(catalog, hidden, seed, prefixes, targets, k, counts, workers=1, extras=True):
     """The reference's evaluate() on ToyEncoderParams::Init(catalog, hidden,
-    SplitMix64(seed)): (out3, H, C, ranks) — see oracle/ref_capi.cpp."""
+    SplitMix64(seed)): (out3, H, C, ranks) — see oracle/ref_capi.cpp.  With
+    extras=False only evaluate() itself runs (timing) and H, C, ranks are None."""
     L = ref()
     prefixes = np.ascontiguousarray(prefixes, np.int64)
     n, Lp = prefixes.shape
     out = np.empty(3)
-    H = np.empty((n, hidden))
-    Cm = np.empty((hidden, catalog), np.float32)
-    ranks = np.empty(n, np.int64)
+    H = np.empty((n, hidden)) if extras else None
+    Cm = np.empty((hidden, catalog), np.float32) if extras else None
+    ranks = np.empty(n, np.int64) if extras else None
+    ptr = lambda a: a.ctypes.data if a is not None else None  # noqa: E731
     _chk(L.ref_eval_instance(catalog, hidden, seed, n, Lp, prefixes,
                              np.ascontiguousarray(targets, np.int64), k,
-                             np.ascontiguousarray(counts, np.int64), workers, out, H, Cm, ranks), L)
+                             np.ascontiguousarray(counts, np.int64), workers, out, ptr(H), ptr(Cm),
+                             ptr(ranks)), L)
     return tuple(out), H, Cm, ranks
