@@ -45,10 +45,13 @@
 #define LF_NOSCALE 1
 #endif
 #ifndef LF_NWG_FWD
-#define LF_NWG_FWD 2
+#define LF_NWG_FWD 3
 #endif
 #ifndef LF_BN_FWD
 #define LF_BN_FWD 128
+#endif
+#ifndef LF_SL_FWD
+#define LF_SL_FWD 64  // forward epilogue slab (columns held in registers at once)
 #endif
 #ifndef LF_NWG_BWD
 #define LF_NWG_BWD 2
@@ -541,7 +544,7 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
         if (MODE == FWD) {
           // The tile in 128-column slabs, each entirely in registers (one
           // wait per slab); S goes back once the last slab is loaded.
-          constexpr int SL = BN < 128 ? BN : 128;
+          constexpr int SL = BN < LF_SL_FWD ? BN : LF_SL_FWD;
           const int lc = tgt - static_cast<int>(col0);
 #pragma unroll
           for (int h = 0; h < BN / SL; ++h) {
