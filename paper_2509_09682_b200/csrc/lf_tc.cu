@@ -53,6 +53,9 @@
 #ifndef LF_SL_FWD
 #define LF_SL_FWD 64  // forward epilogue slab (columns held in registers at once)
 #endif
+#ifndef LF_BWD_PREFETCH
+#define LF_BWD_PREFETCH 1  // backward epilogue: double-buffered 32-column TMEM loads
+#endif
 #ifndef LF_NWG_BWD
 #define LF_NWG_BWD 2
 #endif
@@ -724,7 +727,11 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
           auto process = [&](auto test_tag) -> bool {
           constexpr bool TEST = decltype(test_tag)::value;
           bool any_below = false;
+#if LF_BWD_PREFETCH
           uint32_t ra[32], rb[32];
+#else
+          uint32_t ra[32];
+#endif
           LF_TMEM_LD32(ta, ra);
           tmem_ld_wait();
 #ifdef LF_DIAG_EARLY  // timing diagnostic only (wrong results): hand G over before computing it
@@ -734,9 +741,18 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
 #endif
 #pragma unroll
           for (int q = 0; q < NQ; ++q) {
+#if LF_BWD_PREFETCH
+            // the next chunk's tcgen05.ld in flight while this one is processed
             uint32_t(&cur)[32] = (q & 1) ? rb : ra;
             uint32_t(&nxt)[32] = (q & 1) ? ra : rb;
             if (q + 1 < NQ) LF_TMEM_LD32(ta + (q + 1) * 32, nxt);
+#else
+            uint32_t(&cur)[32] = ra;
+            if (q > 0) {
+              LF_TMEM_LD32(ta + q * 32, ra);
+              tmem_ld_wait();
+            }
+#endif
             float e[32];
 #pragma unroll
             for (int c = 0; c < 32; ++c)
@@ -828,7 +844,9 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
               for (int c = 0; c < 16; ++c) g[c] = pack_bf16x2(x[2 * c], x[2 * c + 1]);
               LF_TMEM_ST16(ta + q * 16, g);
             }
+#if LF_BWD_PREFETCH
             if (q + 1 < NQ) tmem_ld_wait();
+#endif
           }
           return any_below;
           };
