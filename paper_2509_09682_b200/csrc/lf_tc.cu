@@ -53,6 +53,9 @@
 #ifndef LF_SL_FWD
 #define LF_SL_FWD 64  // forward epilogue slab (columns held in registers at once)
 #endif
+#ifndef LF_NWG_EVAL
+#define LF_NWG_EVAL 2
+#endif
 #ifndef LF_BWD_PREFETCH
 #define LF_BWD_PREFETCH 1  // backward epilogue: double-buffered 32-column TMEM loads
 #endif
@@ -122,7 +125,7 @@ struct Ring {
 template <int MODE>
 struct Geo {
   static constexpr int BN = MODE == FWD ? LF_BN_FWD : (MODE == EVAL ? 128 : LF_BN_BWD);  // stream tile
-  static constexpr int NWG = MODE == FWD ? LF_NWG_FWD : (MODE == EVAL ? 2 : LF_NWG_BWD);  // epilogue WGs
+  static constexpr int NWG = MODE == FWD ? LF_NWG_FWD : (MODE == EVAL ? LF_NWG_EVAL : LF_NWG_BWD);  // epilogue WGs
   // control warps: TMA producer, S-MMA issuer (+ the G-MMA issuer in the backward)
   static constexpr int kCtrlWarps = MODE == FWD || MODE == EVAL ? 2 : 3;
   static constexpr int kThreads = 32 * kCtrlWarps + 128 * NWG;
@@ -146,15 +149,15 @@ struct Cfg {
   static constexpr int kExtraBytes = MODE == BWD_ITEMS ? 1024 + kBiasBytes : 0;
   static constexpr int kStageBytes = kTileBytes + kExtraBytes;
   static constexpr int kOnesBytes = MODE == BWD_ITEMS ? BM * 32 : 0;  // constant A bias columns
-  static constexpr int kStagesFit = (200 * 1024 - kOwnerBytes - kOnesBytes) / kStageBytes;
-  static constexpr int kStages = kStagesFit > 12 ? 12 : kStagesFit;
-  static constexpr int kNBMax = (MODE == FWD || MODE == EVAL ? 512 : 512 - D) / BN;  // S buffers in TMEM
-  static constexpr int kNB = kNBMax > 8 ? 8 : kNBMax;
-  static_assert(MODE == FWD || MODE == EVAL || kNB >= 2, "not enough TMEM for the backward pipeline");
   // EVAL: per-row merge records {count, K values, K indices} (stride 2K + 1
   // words: conflict-free) of the other warpgroups + the shared target scores
   static constexpr int kEvalStride = 2 * kEvalK + 1;
   static constexpr int kEvalMerge = MODE == EVAL ? ((G::NWG - 1) * BM * kEvalStride + 2 * BM) * 4 : 0;
+  static constexpr int kStagesFit = (200 * 1024 - kOwnerBytes - kOnesBytes - kEvalMerge) / kStageBytes;
+  static constexpr int kStages = kStagesFit > 12 ? 12 : kStagesFit;
+  static constexpr int kNBMax = (MODE == FWD || MODE == EVAL ? 512 : 512 - D) / BN;  // S buffers in TMEM
+  static constexpr int kNB = kNBMax > 8 ? 8 : kNBMax;
+  static_assert(MODE == FWD || MODE == EVAL || kNB >= 2, "not enough TMEM for the backward pipeline");
   static constexpr int kAccCol = kNB * BN;
   static constexpr int kSmem = 1024 /*align slack*/ + kOwnerBytes + kOnesBytes + kStages * kStageBytes +
                                1024 /*barriers*/ + (MODE == FWD ? (G::NWG - 1) * BM * 16 : 0) +
