@@ -216,6 +216,21 @@ LF_API int lf_evaluate(const void* d_X, const void* d_E, const int64_t* d_target
                        int64_t d, int64_t v, int32_t k, int32_t dtype, const int64_t* d_popularity,
                        double* out3, void* stream);
 
+/* -------------------------------------------------------------- optimizer -- */
+/* One step of AdamState::apply (adam.hpp:18-49, adam.cpp:22-36) over `count`
+ * float parameters with double moments d_m / d_v (zero before step 1), the
+ * gradient in f32 or f64 (grad_dtype), t = the 1-based step number (the
+ * reference's t_ after its increment; bias corrections 1 - beta^t as in
+ * adam.cpp:46-47).  Bitwise equal to the reference's parameters and moments.
+ * Optionally also writes the new parameters to d_shadow in shadow_dtype
+ * (LF_BF16 or LF_F32; pass NULL for none) — e.g. the bf16 E the next CCE
+ * step reads — in the same pass.  Layout-agnostic (elementwise): apply it to
+ * E [v x d] with dE [v x d] in the B200 layout.  LF_EINVAL with the
+ * reference's messages for bad betas / eps. */
+LF_API int lf_adam_step(float* d_param, const void* d_grad, int32_t grad_dtype, double* d_m,
+                        double* d_v, int64_t count, double lr, double beta1, double beta2,
+                        double eps, int64_t t, void* d_shadow, int32_t shadow_dtype, void* stream);
+
 /* ----------------------------------------------------------- validation --- */
 /* Replaces validate_loss_inputs' index scan (losses.cpp:58-67) for device
  * targets.  Synchronizes `stream`.  On failure returns LF_EINVAL with the

@@ -501,3 +501,19 @@ int orc_eval_summary(const int64_t* rank, const int64_t* top_idx, size_t n, size
   out3[2] = surp_sum / (double)n;
   return 0;
 }
+
+/* ---- optimizer (adam.cpp:22-36) ------------------------------------------- */
+void orc_adam_apply(float* param, const double* grad, double* m, double* v, size_t n, double lr,
+                    double b1, double b2, double eps, uint64_t t) {
+  const double corr1 = 1.0 - pow(b1, (double)t); /* adam.cpp:46-47 */
+  const double corr2 = 1.0 - pow(b2, (double)t);
+  for (size_t i = 0; i < n; ++i) { /* adam.cpp:27-35 */
+    const double g = grad[i];
+    m[i] = b1 * m[i] + (1.0 - b1) * g;
+    v[i] = b2 * v[i] + (1.0 - b2) * g * g;
+    const double mhat = m[i] / corr1;
+    const double vhat = v[i] / corr2;
+    const double p = (double)param[i] - lr * mhat / (sqrt(vhat) + eps);
+    param[i] = (float)p;
+  }
+}

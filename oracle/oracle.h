@@ -113,6 +113,12 @@ void orc_eval_rank_topk(const double* H, const float* C, const int64_t* targets,
 int orc_eval_summary(const int64_t* rank, const int64_t* top_idx, size_t n, size_t k,
                      const int64_t* counts, size_t v, double* out3);
 
+/* ---- optimizer (adam.cpp:22-36, 38-55) ------------------------------------
+ * One AdamState::apply over n float params with double grads and moments;
+ * corr1/2 = 1 - beta^t computed as the reference does (adam.cpp:46-47). */
+void orc_adam_apply(float* param, const double* grad, double* m, double* v, size_t n, double lr,
+                    double b1, double b2, double eps, uint64_t t);
+
 #ifdef __cplusplus
 }
 #endif

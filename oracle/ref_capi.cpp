@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "lseforge/accountant.hpp"
+#include "lseforge/adam.hpp"
 #include "lseforge/backend.hpp"
 #include "lseforge/cce.hpp"
 #include "lseforge/ccem.hpp"
@@ -263,6 +264,52 @@ int ref_eval_instance(std::size_t catalog, std::size_t hidden, uint64_t seed, st
         ranks[i] = static_cast<int64_t>(std::llround(std::exp2(1.0 / one.ndcg) - 1.0));
       }
     }
+  });
+}
+
+// ---- adam.cpp -------------------------------------------------------------
+// `steps` AdamState::step calls on ToyEncoderParams::Init(catalog, hidden,
+// SplitMix64(seed)) with the caller's gradients (grads: steps blocks of
+// [d_emb (catalog*hidden) | d_w (hidden^2) | d_b (hidden) | d_classifier
+// (hidden*catalog)] doubles); writes the final parameters in the same
+// concatenated order (floats).
+int ref_adam_steps(std::size_t catalog, std::size_t hidden, uint64_t seed, double lr, double b1,
+                   double b2, double eps, int steps, const double* grads, float* params_out) {
+  return guard([&] {
+    ToyEncoderParams p = ToyEncoderParams::Init(catalog, hidden, SplitMix64(seed));
+    AdamConfig cfg;
+    cfg.lr = lr;
+    cfg.beta1 = b1;
+    cfg.beta2 = b2;
+    cfg.eps = eps;
+    AdamState adam(catalog, hidden, cfg);
+    const std::size_t ne = catalog * hidden, nw = hidden * hidden, nb = hidden, nc = hidden * catalog;
+    const std::size_t block = ne + nw + nb + nc;
+    for (int s = 0; s < steps; ++s) {
+      EncoderGrads g(catalog, hidden);
+      const double* src = grads + static_cast<std::size_t>(s) * block;
+      std::memcpy(g.d_emb.data().data(), src, sizeof(double) * ne);
+      std::memcpy(g.d_w.data().data(), src + ne, sizeof(double) * nw);
+      std::memcpy(g.d_b.data(), src + ne + nw, sizeof(double) * nb);
+      std::memcpy(g.d_classifier.data().data(), src + ne + nw + nb, sizeof(double) * nc);
+      adam.step(p, g);
+    }
+    std::memcpy(params_out, p.emb.data().data(), sizeof(float) * ne);
+    std::memcpy(params_out + ne, p.w.data().data(), sizeof(float) * nw);
+    std::memcpy(params_out + ne + nw, p.b.data(), sizeof(float) * nb);
+    std::memcpy(params_out + ne + nw + nb, p.c.data().data(), sizeof(float) * nc);
+  });
+}
+
+// The initial parameters of ToyEncoderParams::Init in the same concatenated order.
+int ref_encoder_init(std::size_t catalog, std::size_t hidden, uint64_t seed, float* params_out) {
+  return guard([&] {
+    const ToyEncoderParams p = ToyEncoderParams::Init(catalog, hidden, SplitMix64(seed));
+    const std::size_t ne = catalog * hidden, nw = hidden * hidden, nb = hidden;
+    std::memcpy(params_out, p.emb.data().data(), sizeof(float) * ne);
+    std::memcpy(params_out + ne, p.w.data().data(), sizeof(float) * nw);
+    std::memcpy(params_out + ne + nw, p.b.data(), sizeof(float) * nb);
+    std::memcpy(params_out + ne + nw + nb, p.c.data().data(), sizeof(float) * hidden * catalog);
   });
 }
 

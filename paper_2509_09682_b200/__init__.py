@@ -12,6 +12,7 @@ from .cce import CceBackwardResult, CceConfig, cce_backward, cce_forward, kFp16M
 from .ccem import (Backend, FlopEstimate, backend_is_sampled, ccem_backward, ccem_backward_rows,
                    ccem_forward, estimate_flops)
 from .losses import GradPair, LossOutput, ce_full_backward, ce_full_forward, validate_loss_inputs
+from .adam import AdamConfig, DeviceAdam
 from .metrics import EvalSummary, evaluate
 from .sampler import sample_uniform
 
@@ -20,7 +21,7 @@ __all__ = [
     "ccem_forward", "ccem_backward", "ccem_backward_rows", "estimate_flops", "FlopEstimate",
     "Backend", "backend_is_sampled", "LossOutput", "GradPair", "validate_loss_inputs",
     "MemAccountant", "Report", "ScalarKind", "sample_uniform", "ce_full_forward",
-    "ce_full_backward", "EvalSummary", "evaluate", "lib",
+    "ce_full_backward", "EvalSummary", "evaluate", "AdamConfig", "DeviceAdam", "lib",
 ]
 
 

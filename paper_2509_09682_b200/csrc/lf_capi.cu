@@ -441,6 +441,13 @@ int lf_evaluate(const void* d_X, const void* d_E, const int64_t* d_targets, int6
   return rc;
 }
 
+int lf_adam_step(float* d_param, const void* d_grad, int32_t grad_dtype, double* d_m, double* d_v,
+                 int64_t count, double lr, double beta1, double beta2, double eps, int64_t t,
+                 void* d_shadow, int32_t shadow_dtype, void* stream) {
+  return adam_step(d_param, d_grad, grad_dtype, d_m, d_v, count, lr, beta1, beta2, eps, t, d_shadow,
+                   shadow_dtype, as_stream(stream));
+}
+
 int lf_estimate_flops(int64_t n, int64_t d, int64_t v, int64_t ns, int32_t backend,
                       uint64_t* forward, uint64_t* backward) {
   // ccem.cpp:207-235

@@ -70,6 +70,11 @@ int launch_add_one(int64_t* x, int64_t n, cudaStream_t st);
 int eval_summary(const int64_t* rank, const int64_t* top_idx, int64_t n, int k, const int64_t* pop,
                  int64_t v, double* out3_host, cudaStream_t st);
 
+// ---- optimizer (lf_adam.cu) ----
+int adam_step(float* param, const void* grad, int grad_dtype, double* m, double* v, int64_t n,
+              double lr, double b1, double b2, double eps, int64_t t, void* shadow, int shadow_dtype,
+              cudaStream_t st);
+
 // ---- CCE- (lf_ccem.cu) ----
 int ccem_forward(int dtype, const void* X, const void* E, const int64_t* inds, int64_t n, int D,
                  int64_t v, int64_t w, double* lse, double* pos, double* loss, cudaStream_t st);

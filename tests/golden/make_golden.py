@@ -77,6 +77,7 @@ def main():
     ccem["sampler_inds"] = ob.ref_sample_uniform(pos, 12, 97, 0xB2000003)
     np.savez_compressed(os.path.join(HERE, "ccem_ref.npz"), **ccem)
     eval_fixtures()
+    adam_fixtures()
     print("wrote", sorted(f for f in os.listdir(HERE) if f.endswith(".npz")))
 
 
@@ -98,8 +99,23 @@ def eval_fixtures():
     np.savez_compressed(os.path.join(HERE, "eval_ref.npz"), **ev)
 
 
+def adam_fixtures():
+    """AdamState::step (adam.cpp:22-55) on ToyEncoderParams::Init: initial
+    params, per-step gradients (spanning 1e-8 .. 10) and final params."""
+    cat, hid, seed, steps = 60, 4, 21, 4
+    lr, b1, b2, eps = 1e-2, 0.9, 0.999, 1e-8
+    p0 = ob.ref_encoder_init(cat, hid, seed)
+    g = np.random.default_rng(seed)
+    grads = [g.standard_normal(p0.size) * 10.0 ** g.integers(-8, 2, p0.size) for _ in range(steps)]
+    want = ob.ref_adam_steps(cat, hid, seed, lr, b1, b2, eps, grads)
+    np.savez_compressed(os.path.join(HERE, "adam_ref.npz"), p0=p0, grads=np.stack(grads), want=want,
+                        hp=np.array([lr, b1, b2, eps]))
+
+
 if __name__ == "__main__":
-    if sys.argv[1:] == ["eval"]:
+    if sys.argv[1:] == ["adam"]:
+        adam_fixtures()
+    elif sys.argv[1:] == ["eval"]:
         eval_fixtures()
     else:
         main()

@@ -78,6 +78,8 @@ def orc():
                                          _i64p, _i64p, _f64p]
         L.orc_eval_summary.argtypes = [_i64p, _i64p, _sz, _sz, _i64p, _sz, _f64p]
         L.orc_eval_summary.restype = C.c_int
+        L.orc_adam_apply.argtypes = [_f32p, _f64p, _f64p, _f64p, _sz, C.c_double, C.c_double,
+                                     C.c_double, C.c_double, C.c_uint64]
         _orc = L
     return _orc
 
@@ -118,6 +120,9 @@ def ref():
                                          C.POINTER(C.c_uint64)]
         L.ref_eval_instance.argtypes = [_sz, _sz, C.c_uint64, _sz, _sz, _i64p, _i64p, _sz, _i64p,
                                         C.c_int, _f64p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.ref_adam_steps.argtypes = [_sz, _sz, C.c_uint64, C.c_double, C.c_double, C.c_double,
+                                     C.c_double, C.c_int, _f64p, _f32p]
+        L.ref_encoder_init.argtypes = [_sz, _sz, C.c_uint64, _f32p]
         _ref = L
     return _ref
 
@@ -281,6 +286,12 @@ def evaluate(H, Cm, targets, k, counts):
     return eval_summary(ahead + 1, top, counts)
 
 
+def adam_apply(param, grad, m, v, lr, b1, b2, eps, t):
+    """adam.cpp:22-36 in place on float32 param / float64 m, v (numpy)."""
+    orc().orc_adam_apply(param, np.ascontiguousarray(grad, np.float64), m, v, param.size, lr, b1, b2,
+                         eps, t)
+
+
 # ---------------------------------------------------------------------------
 # Reference (oracle/_ref) wrappers
 # ---------------------------------------------------------------------------
@@ -402,3 +413,21 @@ def ref_eval_instance(catalog, hidden, seed, prefixes, targets, k, counts, worke
                              np.ascontiguousarray(counts, np.int64), workers, out, ptr(H), ptr(Cm),
                              ptr(ranks)), L)
     return tuple(out), H, Cm, ranks
+
+
+def ref_adam_steps(catalog, hidden, seed, lr, b1, b2, eps, grads):
+    """AdamState::step x len(grads) on ToyEncoderParams::Init; grads[s] is the
+    concatenated [d_emb | d_w | d_b | d_classifier] doubles -> final params
+    (float32, same order)."""
+    L = ref()
+    g = np.ascontiguousarray(np.stack(grads), np.float64)
+    out = np.empty(g.shape[1], np.float32)
+    _chk(L.ref_adam_steps(catalog, hidden, seed, lr, b1, b2, eps, len(grads), g.reshape(-1), out), L)
+    return out
+
+
+def ref_encoder_init(catalog, hidden, seed):
+    L = ref()
+    out = np.empty(catalog * hidden * 2 + hidden * hidden + hidden, np.float32)
+    _chk(L.ref_encoder_init(catalog, hidden, seed, out), L)
+    return out
