@@ -216,6 +216,32 @@ LF_API int lf_evaluate(const void* d_X, const void* d_E, const int64_t* d_target
                        int64_t d, int64_t v, int32_t k, int32_t dtype, const int64_t* d_popularity,
                        double* out3, void* stream);
 
+/* ----------------------------------------------------------------- encoder -- */
+/* encode_batch (encoder.hpp:46-60, encoder.cpp:64-116) on the device.  Windows
+ * as a CSR: d_items[d_win_off[w] .. d_win_off[w+1]) is window w (every window
+ * >= 2 items); rows = sum (len - 1), enumerated window by window, position
+ * t = 1 .. len-1.  Params in the reference layout: d_emb [catalog x d],
+ * d_W [d x d], d_b [d] (float).  Outputs: d_X [rows x d] = EncodedBatch::e
+ * (float(h)) converted to x_dtype (the loss input), d_a / d_h [rows x d]
+ * double (pooled means — bitwise the reference's — and tanh outputs), d_targets,
+ * d_row_window, d_row_pos [rows].  Synchronizes (validation); LF_EINVAL with
+ * the reference's messages. */
+LF_API int lf_encode_batch(const int64_t* d_items, const int64_t* d_win_off, int64_t n_windows,
+                           const float* d_emb, const float* d_W, const float* d_b, int64_t catalog,
+                           int64_t d, int64_t rows, int32_t x_dtype, void* d_X, double* d_a,
+                           double* d_h, int64_t* d_targets, int64_t* d_row_window,
+                           int64_t* d_row_pos, void* stream);
+/* encoder_backward (encoder.hpp:62-66, encoder.cpp:118-173): from d_h = the
+ * loss's dX [rows x d] (f32 or f64) to d_emb [catalog x d], d_W [d x d],
+ * d_b [d] (double, OVERWRITTEN — the reference accumulates into a fresh
+ * EncoderGrads per batch, trainer.cpp:222-223), summed in the reference's
+ * order. */
+LF_API int lf_encoder_backward(const int64_t* d_items, const int64_t* d_win_off, int64_t n_windows,
+                               const float* d_W, int64_t catalog, int64_t d, const double* d_a,
+                               const double* d_h, const int64_t* d_row_pos, int64_t rows,
+                               const void* d_dh, int32_t dh_dtype, double* d_demb, double* d_dW,
+                               double* d_db, void* stream);
+
 /* -------------------------------------------------------------- optimizer -- */
 /* One step of AdamState::apply (adam.hpp:18-49, adam.cpp:22-36) over `count`
  * float parameters with double moments d_m / d_v (zero before step 1), the

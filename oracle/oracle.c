@@ -517,3 +517,79 @@ void orc_adam_apply(float* param, const double* grad, double* m, double* v, size
     param[i] = (float)p;
   }
 }
+
+/* ---- encoder (encoder.cpp:64-173) ----------------------------------------- */
+void orc_encode_batch(const int64_t* items, const int64_t* win_off, size_t n_windows,
+                      const float* emb, const float* W, const float* b, size_t d, double* a,
+                      double* h, float* e, int64_t* targets, int64_t* row_pos) {
+  double* sum = (double*)malloc(sizeof(double) * d);
+  size_t r = 0;
+  for (size_t wi = 0; wi < n_windows; ++wi) { /* encoder.cpp:88-112 */
+    const int64_t* win = items + win_off[wi];
+    const size_t len = (size_t)(win_off[wi + 1] - win_off[wi]);
+    for (size_t k = 0; k < d; ++k) sum[k] = 0.0;
+    for (size_t t = 1; t < len; ++t, ++r) {
+      const float* erow = emb + (size_t)win[t - 1] * d;
+      for (size_t k = 0; k < d; ++k) sum[k] += (double)erow[k];
+      const double inv = 1.0 / (double)t;
+      double* arow = a + r * d;
+      for (size_t j = 0; j < d; ++j) arow[j] = sum[j] * inv;
+      for (size_t j = 0; j < d; ++j) {
+        double z = (double)b[j];
+        const float* wrow = W + j * d;
+        for (size_t k = 0; k < d; ++k) z += (double)wrow[k] * arow[k];
+        h[r * d + j] = tanh(z);
+        e[r * d + j] = (float)h[r * d + j];
+      }
+      targets[r] = win[t];
+      row_pos[r] = (int64_t)t;
+    }
+  }
+  free(sum);
+}
+
+void orc_encoder_backward(const int64_t* items, const int64_t* win_off, size_t n_windows,
+                          const float* W, size_t catalog, size_t d, const double* a, const double* h,
+                          const int64_t* row_pos, size_t rows, const double* dh, double* d_emb,
+                          double* d_W, double* d_b) {
+  memset(d_emb, 0, sizeof(double) * catalog * d);
+  memset(d_W, 0, sizeof(double) * d * d);
+  memset(d_b, 0, sizeof(double) * d);
+  double* g = (double*)malloc(sizeof(double) * d);
+  double* u = (double*)malloc(sizeof(double) * d);
+  double* suffix = (double*)malloc(sizeof(double) * d);
+  /* row offsets of each window */
+  size_t r_end = rows;
+  for (size_t wi = n_windows; wi-- > 0;) { /* encoder.cpp:137-170, windows last to first */
+    const int64_t* win = items + win_off[wi];
+    const size_t len = (size_t)(win_off[wi + 1] - win_off[wi]);
+    const size_t r_begin = r_end - (len - 1);
+    for (size_t k = 0; k < d; ++k) suffix[k] = 0.0;
+    for (size_t r = r_end; r-- > r_begin;) {
+      const size_t t = (size_t)row_pos[r];
+      const double* hrow = h + r * d;
+      const double* dhr = dh + r * d;
+      for (size_t j = 0; j < d; ++j) g[j] = (1.0 - hrow[j] * hrow[j]) * dhr[j];
+      const double* arow = a + r * d;
+      for (size_t j = 0; j < d; ++j) {
+        double* dwrow = d_W + j * d;
+        for (size_t k = 0; k < d; ++k) dwrow[k] += g[j] * arow[k];
+        d_b[j] += g[j];
+      }
+      const double inv = 1.0 / (double)t;
+      for (size_t k = 0; k < d; ++k) {
+        double acc = 0.0;
+        for (size_t j = 0; j < d; ++j) acc += (double)W[j * d + k] * g[j];
+        u[k] = acc * inv;
+      }
+      for (size_t k = 0; k < d; ++k) suffix[k] += u[k];
+      double* derow = d_emb + (size_t)win[t - 1] * d;
+      for (size_t k = 0; k < d; ++k) derow[k] += suffix[k];
+    }
+    r_end = r_begin;
+  }
+  (void)catalog;
+  free(g);
+  free(u);
+  free(suffix);
+}

@@ -113,6 +113,19 @@ void orc_eval_rank_topk(const double* H, const float* C, const int64_t* targets,
 int orc_eval_summary(const int64_t* rank, const int64_t* top_idx, size_t n, size_t k,
                      const int64_t* counts, size_t v, double* out3);
 
+/* ---- encoder (encoder.cpp:64-173) -----------------------------------------
+ * Windows as a CSR (items, win_off[n_windows + 1]); emb [catalog x d],
+ * W [d x d], b [d] float.  encode: rows = sum(len - 1) outputs a, h (double),
+ * e (float), targets, row_pos.  backward: from d_h (double) to d_emb, d_W,
+ * d_b (double, overwritten). */
+void orc_encode_batch(const int64_t* items, const int64_t* win_off, size_t n_windows,
+                      const float* emb, const float* W, const float* b, size_t d, double* a,
+                      double* h, float* e, int64_t* targets, int64_t* row_pos);
+void orc_encoder_backward(const int64_t* items, const int64_t* win_off, size_t n_windows,
+                          const float* W, size_t catalog, size_t d, const double* a, const double* h,
+                          const int64_t* row_pos, size_t rows, const double* dh, double* d_emb,
+                          double* d_W, double* d_b);
+
 /* ---- optimizer (adam.cpp:22-36, 38-55) ------------------------------------
  * One AdamState::apply over n float params with double grads and moments;
  * corr1/2 = 1 - beta^t computed as the reference does (adam.cpp:46-47). */

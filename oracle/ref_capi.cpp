@@ -301,6 +301,36 @@ int ref_adam_steps(std::size_t catalog, std::size_t hidden, uint64_t seed, doubl
   });
 }
 
+// encode_batch + encoder_backward (encoder.cpp:64-173) on caller-supplied
+// parameters and windows (CSR), with d_h supplied; outputs as oracle.h.
+int ref_encoder(std::size_t catalog, std::size_t hidden, const float* emb, const float* W,
+                const float* b, const int64_t* items, const int64_t* win_off, std::size_t n_windows,
+                const double* dh, double* a, double* h, float* e, int64_t* targets, double* d_emb,
+                double* d_W, double* d_b) {
+  return guard([&] {
+    ToyEncoderParams p;
+    p.emb = to_matrix(emb, catalog, hidden);
+    p.w = to_matrix(W, hidden, hidden);
+    p.b.assign(b, b + hidden);
+    p.c = DenseMatrix(hidden, catalog);
+    std::vector<std::vector<int64_t>> windows(n_windows);
+    for (std::size_t w = 0; w < n_windows; ++w) windows[w].assign(items + win_off[w], items + win_off[w + 1]);
+    const EncodedBatch enc = encode_batch(p, windows);
+    const std::size_t rows = enc.e.rows();
+    std::memcpy(a, enc.a.data().data(), sizeof(double) * rows * hidden);
+    std::memcpy(h, enc.h.data().data(), sizeof(double) * rows * hidden);
+    std::memcpy(e, enc.e.data().data(), sizeof(float) * rows * hidden);
+    std::memcpy(targets, enc.targets.data(), sizeof(int64_t) * rows);
+    DenseMatrixD dhm(rows, hidden);
+    std::memcpy(dhm.data().data(), dh, sizeof(double) * rows * hidden);
+    EncoderGrads g(catalog, hidden);
+    encoder_backward(p, windows, enc, dhm, g);
+    std::memcpy(d_emb, g.d_emb.data().data(), sizeof(double) * catalog * hidden);
+    std::memcpy(d_W, g.d_w.data().data(), sizeof(double) * hidden * hidden);
+    std::memcpy(d_b, g.d_b.data(), sizeof(double) * hidden);
+  });
+}
+
 // The initial parameters of ToyEncoderParams::Init in the same concatenated order.
 int ref_encoder_init(std::size_t catalog, std::size_t hidden, uint64_t seed, float* params_out) {
   return guard([&] {

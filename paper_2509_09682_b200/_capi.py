@@ -26,7 +26,7 @@ EXPORTS = (
     "lf_profile_enable", "lf_profile_read", "lf_profile_reset", "lf_classifier_to_items",
     "lf_convert_rows", "lf_items_grad_to_classifier", "lf_widen_grad", "lf_sample_uniform",
     "lf_ce_forward", "lf_ce_backward", "lf_eval_rank_topk", "lf_eval_merge", "lf_eval_summary",
-    "lf_evaluate", "lf_adam_step",
+    "lf_evaluate", "lf_adam_step", "lf_encode_batch", "lf_encoder_backward",
 )
 KERNEL_KINDS = ("cce_fwd", "cce_bwd_dx", "cce_bwd_de", "cce_simt", "ccem_fwd", "ccem_bwd", "aux",
                 "eval")
@@ -91,6 +91,10 @@ def lib():
                                   C.POINTER(C.c_double), vp]
         L.lf_adam_step.argtypes = [vp, vp, C.c_int32, vp, vp, i64, C.c_double, C.c_double,
                                    C.c_double, C.c_double, i64, vp, C.c_int32, vp]
+        L.lf_encode_batch.argtypes = [vp, vp, i64, vp, vp, vp, i64, i64, i64, C.c_int32, vp, vp, vp,
+                                      vp, vp, vp, vp]
+        L.lf_encoder_backward.argtypes = [vp, vp, i64, vp, i64, i64, vp, vp, vp, i64, vp, C.c_int32,
+                                          vp, vp, vp, vp]
         L.lf_launch_count.restype = C.c_uint64
         L.lf_profile_enable.argtypes = [C.c_int]
         L.lf_profile_enable.restype = C.c_int
@@ -103,7 +107,7 @@ def lib():
                      "lf_sample_uniform", "lf_classifier_to_items", "lf_convert_rows",
                      "lf_items_grad_to_classifier", "lf_widen_grad", "lf_ce_forward",
                      "lf_ce_backward", "lf_eval_rank_topk", "lf_eval_merge", "lf_eval_summary",
-                     "lf_evaluate", "lf_adam_step"):
+                     "lf_evaluate", "lf_adam_step", "lf_encode_batch", "lf_encoder_backward"):
             getattr(L, name).restype = C.c_int
         if L.lf_abi_version() != 1:
             raise ImportError("liblseforge_b200.so ABI mismatch")

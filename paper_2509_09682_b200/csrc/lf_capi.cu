@@ -441,6 +441,24 @@ int lf_evaluate(const void* d_X, const void* d_E, const int64_t* d_targets, int6
   return rc;
 }
 
+int lf_encode_batch(const int64_t* d_items, const int64_t* d_win_off, int64_t n_windows,
+                    const float* d_emb, const float* d_W, const float* d_b, int64_t catalog, int64_t d,
+                    int64_t rows, int32_t x_dtype, void* d_X, double* d_a, double* d_h,
+                    int64_t* d_targets, int64_t* d_row_window, int64_t* d_row_pos, void* stream) {
+  if (x_dtype != LF_F32 && x_dtype != LF_F64 && x_dtype != LF_BF16)
+    return fail(LF_EINVAL, "encode_batch: unknown dtype " + std::to_string(x_dtype));
+  return encode_batch(d_items, d_win_off, n_windows, d_emb, d_W, d_b, catalog, static_cast<int>(d), rows,
+                      x_dtype, d_X, d_a, d_h, d_targets, d_row_window, d_row_pos, as_stream(stream));
+}
+
+int lf_encoder_backward(const int64_t* d_items, const int64_t* d_win_off, int64_t n_windows,
+                        const float* d_W, int64_t catalog, int64_t d, const double* d_a,
+                        const double* d_h, const int64_t* d_row_pos, int64_t rows, const void* d_dh,
+                        int32_t dh_dtype, double* d_demb, double* d_dW, double* d_db, void* stream) {
+  return encoder_backward(d_items, d_win_off, n_windows, d_W, catalog, static_cast<int>(d), d_a, d_h,
+                          d_row_pos, rows, d_dh, dh_dtype, d_demb, d_dW, d_db, as_stream(stream));
+}
+
 int lf_adam_step(float* d_param, const void* d_grad, int32_t grad_dtype, double* d_m, double* d_v,
                  int64_t count, double lr, double beta1, double beta2, double eps, int64_t t,
                  void* d_shadow, int32_t shadow_dtype, void* stream) {

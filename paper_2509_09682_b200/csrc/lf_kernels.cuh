@@ -70,6 +70,16 @@ int launch_add_one(int64_t* x, int64_t n, cudaStream_t st);
 int eval_summary(const int64_t* rank, const int64_t* top_idx, int64_t n, int k, const int64_t* pop,
                  int64_t v, double* out3_host, cudaStream_t st);
 
+// ---- encoder (lf_encoder.cu) ----
+int encode_batch(const int64_t* items, const int64_t* win_off, int64_t n_windows, const float* emb,
+                 const float* W, const float* bias, int64_t catalog, int D, int64_t rows, int x_dtype,
+                 void* X, double* a, double* h, int64_t* targets, int64_t* row_window,
+                 int64_t* row_pos, cudaStream_t st);
+int encoder_backward(const int64_t* items, const int64_t* win_off, int64_t n_windows, const float* W,
+                     int64_t catalog, int D, const double* a, const double* h, const int64_t* row_pos,
+                     int64_t rows, const void* dh, int dh_dtype, double* d_emb, double* dW, double* db,
+                     cudaStream_t st);
+
 // ---- optimizer (lf_adam.cu) ----
 int adam_step(float* param, const void* grad, int grad_dtype, double* m, double* v, int64_t n,
               double lr, double b1, double b2, double eps, int64_t t, void* shadow, int shadow_dtype,

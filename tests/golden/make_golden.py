@@ -78,6 +78,7 @@ def main():
     np.savez_compressed(os.path.join(HERE, "ccem_ref.npz"), **ccem)
     eval_fixtures()
     adam_fixtures()
+    encoder_fixtures()
     print("wrote", sorted(f for f in os.listdir(HERE) if f.endswith(".npz")))
 
 
@@ -112,8 +113,27 @@ def adam_fixtures():
                         hp=np.array([lr, b1, b2, eps]))
 
 
+def encoder_fixtures():
+    """encode_batch + encoder_backward (encoder.cpp:64-173) run by the
+    reference on random parameters, ragged windows and d_h."""
+    g = np.random.default_rng(77)
+    cat, d = 50, 16
+    emb = (g.standard_normal((cat, d)) * 0.3).astype(np.float32)
+    W = (g.standard_normal((d, d)) * 0.3).astype(np.float32)
+    b = (g.standard_normal(d) * 0.1).astype(np.float32)
+    lens = g.integers(2, 12, 20)
+    win_off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    items = g.integers(0, cat, int(win_off[-1])).astype(np.int64)
+    dh = g.standard_normal((int(np.sum(lens - 1)), d))
+    r = ob.ref_encoder(emb, W, b, items, win_off, dh)
+    np.savez_compressed(os.path.join(HERE, "encoder_ref.npz"), emb=emb, W=W, b=b, items=items,
+                        win_off=win_off, dh=dh, **r)
+
+
 if __name__ == "__main__":
-    if sys.argv[1:] == ["adam"]:
+    if sys.argv[1:] == ["encoder"]:
+        encoder_fixtures()
+    elif sys.argv[1:] == ["adam"]:
         adam_fixtures()
     elif sys.argv[1:] == ["eval"]:
         eval_fixtures()

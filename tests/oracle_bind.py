@@ -78,6 +78,10 @@ def orc():
                                          _i64p, _i64p, _f64p]
         L.orc_eval_summary.argtypes = [_i64p, _i64p, _sz, _sz, _i64p, _sz, _f64p]
         L.orc_eval_summary.restype = C.c_int
+        L.orc_encode_batch.argtypes = [_i64p, _i64p, _sz, _f32p, _f32p, _f32p, _sz, _f64p, _f64p,
+                                       _f32p, _i64p, _i64p]
+        L.orc_encoder_backward.argtypes = [_i64p, _i64p, _sz, _f32p, _sz, _sz, _f64p, _f64p, _i64p,
+                                           _sz, _f64p, _f64p, _f64p, _f64p]
         L.orc_adam_apply.argtypes = [_f32p, _f64p, _f64p, _f64p, _sz, C.c_double, C.c_double,
                                      C.c_double, C.c_double, C.c_uint64]
         _orc = L
@@ -122,6 +126,8 @@ def ref():
                                         C.c_int, _f64p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.ref_adam_steps.argtypes = [_sz, _sz, C.c_uint64, C.c_double, C.c_double, C.c_double,
                                      C.c_double, C.c_int, _f64p, _f32p]
+        L.ref_encoder.argtypes = [_sz, _sz, _f32p, _f32p, _f32p, _i64p, _i64p, _sz, _f64p, _f64p,
+                                  _f64p, _f32p, _i64p, _f64p, _f64p, _f64p]
         L.ref_encoder_init.argtypes = [_sz, _sz, C.c_uint64, _f32p]
         _ref = L
     return _ref
@@ -286,6 +292,28 @@ def evaluate(H, Cm, targets, k, counts):
     return eval_summary(ahead + 1, top, counts)
 
 
+def encoder(emb, W, b, items, win_off, dh=None):
+    """orc_encode_batch (+ orc_encoder_backward when dh is given).
+    Returns dict(a, h, e, targets, row_pos[, d_emb, d_W, d_b])."""
+    catalog, d = emb.shape
+    nw = len(win_off) - 1
+    rows = int(np.sum(np.diff(win_off) - 1))
+    out = dict(a=np.empty((rows, d)), h=np.empty((rows, d)), e=np.empty((rows, d), np.float32),
+               targets=np.empty(rows, np.int64), row_pos=np.empty(rows, np.int64))
+    items = np.ascontiguousarray(items, np.int64)
+    win_off = np.ascontiguousarray(win_off, np.int64)
+    orc().orc_encode_batch(items, win_off, nw, np.ascontiguousarray(emb, np.float32),
+                           np.ascontiguousarray(W, np.float32), np.ascontiguousarray(b, np.float32), d,
+                           out["a"], out["h"], out["e"], out["targets"], out["row_pos"])
+    if dh is not None:
+        out.update(d_emb=np.empty((catalog, d)), d_W=np.empty((d, d)), d_b=np.empty(d))
+        orc().orc_encoder_backward(items, win_off, nw, np.ascontiguousarray(W, np.float32), catalog, d,
+                                   out["a"], out["h"], out["row_pos"], rows,
+                                   np.ascontiguousarray(dh, np.float64), out["d_emb"], out["d_W"],
+                                   out["d_b"])
+    return out
+
+
 def adam_apply(param, grad, m, v, lr, b1, b2, eps, t):
     """adam.cpp:22-36 in place on float32 param / float64 m, v (numpy)."""
     orc().orc_adam_apply(param, np.ascontiguousarray(grad, np.float64), m, v, param.size, lr, b1, b2,
@@ -430,4 +458,20 @@ def ref_encoder_init(catalog, hidden, seed):
     L = ref()
     out = np.empty(catalog * hidden * 2 + hidden * hidden + hidden, np.float32)
     _chk(L.ref_encoder_init(catalog, hidden, seed, out), L)
+    return out
+
+
+def ref_encoder(emb, W, b, items, win_off, dh):
+    """The reference's encode_batch + encoder_backward (oracle/_ref)."""
+    L = ref()
+    catalog, d = emb.shape
+    rows = int(np.sum(np.diff(win_off) - 1))
+    out = dict(a=np.empty((rows, d)), h=np.empty((rows, d)), e=np.empty((rows, d), np.float32),
+               targets=np.empty(rows, np.int64), d_emb=np.empty((catalog, d)), d_W=np.empty((d, d)),
+               d_b=np.empty(d))
+    _chk(L.ref_encoder(catalog, d, np.ascontiguousarray(emb, np.float32), np.ascontiguousarray(W, np.float32),
+                       np.ascontiguousarray(b, np.float32), np.ascontiguousarray(items, np.int64),
+                       np.ascontiguousarray(win_off, np.int64), len(win_off) - 1,
+                       np.ascontiguousarray(dh, np.float64), out["a"], out["h"], out["e"], out["targets"],
+                       out["d_emb"], out["d_W"], out["d_b"]), L)
     return out
