@@ -53,6 +53,9 @@
 #ifndef LF_SL_FWD
 #define LF_SL_FWD 64  // forward epilogue slab (columns held in registers at once)
 #endif
+#ifndef LF_FWD_LD64
+#define LF_FWD_LD64 1  // forward / EVAL: one 32x32b.x64 TMEM load per 64-column slab
+#endif
 #ifndef LF_NWG_EVAL
 #define LF_NWG_EVAL 2
 #endif
@@ -557,8 +560,16 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
           float v[SL];
           {
             uint32_t* r = reinterpret_cast<uint32_t*>(v);
+#if LF_FWD_LD64
+            if constexpr (SL % 64 == 0) {
 #pragma unroll
-            for (int q = 0; q < SL / 32; ++q) LF_TMEM_LD32(ta + h * SL + q * 32, (r + q * 32));
+              for (int q = 0; q < SL / 64; ++q) LF_TMEM_LD64(ta + h * SL + q * 64, (r + q * 64));
+            } else
+#endif
+            {
+#pragma unroll
+              for (int q = 0; q < SL / 32; ++q) LF_TMEM_LD32(ta + h * SL + q * 32, (r + q * 32));
+            }
             tmem_ld_wait();
           }
           if (h + 1 == BN / SL) {
@@ -619,8 +630,15 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
 #pragma unroll 1
           for (int h = 0; h < BN / 64; ++h) {
             float w[2][32];
+#if LF_FWD_LD64
+            {
+              uint32_t* r = reinterpret_cast<uint32_t*>(&w[0][0]);
+              LF_TMEM_LD64(ta + h * 64, r);
+            }
+#else
             LF_TMEM_LD32(ta + h * 64, reinterpret_cast<uint32_t*>(w[0]));
             LF_TMEM_LD32(ta + h * 64 + 32, reinterpret_cast<uint32_t*>(w[1]));
+#endif
             tmem_ld_wait();
             if (h + 1 == BN / 64) {
               tc_fence_before();
