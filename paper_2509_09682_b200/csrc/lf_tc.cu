@@ -59,6 +59,9 @@
 #ifndef LF_NWG_EVAL
 #define LF_NWG_EVAL 2
 #endif
+#ifndef LF_BWD_LD64
+#define LF_BWD_LD64 0  // backward: 64-column TMEM loads (two chunks), no prefetch
+#endif
 #ifndef LF_BWD_PREFETCH
 #define LF_BWD_PREFETCH 1  // backward epilogue: double-buffered 32-column TMEM loads
 #endif
@@ -748,12 +751,16 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
           auto process = [&](auto test_tag) -> bool {
           constexpr bool TEST = decltype(test_tag)::value;
           bool any_below = false;
-#if LF_BWD_PREFETCH
+#if LF_BWD_LD64
+          uint32_t ra[64];  // two 32-column chunks per tcgen05.ld
+          LF_TMEM_LD64(ta, ra);
+#elif LF_BWD_PREFETCH
           uint32_t ra[32], rb[32];
+          LF_TMEM_LD32(ta, ra);
 #else
           uint32_t ra[32];
-#endif
           LF_TMEM_LD32(ta, ra);
+#endif
           tmem_ld_wait();
 #ifdef LF_DIAG_EARLY  // timing diagnostic only (wrong results): hand G over before computing it
           tc_fence_before();
@@ -762,7 +769,13 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
 #endif
 #pragma unroll
           for (int q = 0; q < NQ; ++q) {
-#if LF_BWD_PREFETCH
+#if LF_BWD_LD64
+            if (q > 0 && (q & 1) == 0) {
+              LF_TMEM_LD64(ta + q * 32, ra);
+              tmem_ld_wait();
+            }
+            uint32_t(&cur)[32] = *reinterpret_cast<uint32_t(*)[32]>(ra + (q & 1) * 32);
+#elif LF_BWD_PREFETCH
             // the next chunk's tcgen05.ld in flight while this one is processed
             uint32_t(&cur)[32] = (q & 1) ? rb : ra;
             uint32_t(&nxt)[32] = (q & 1) ? ra : rb;
@@ -865,7 +878,7 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
               for (int c = 0; c < 16; ++c) g[c] = pack_bf16x2(x[2 * c], x[2 * c + 1]);
               LF_TMEM_ST16(ta + q * 16, g);
             }
-#if LF_BWD_PREFETCH
+#if LF_BWD_PREFETCH && !LF_BWD_LD64
             if (q + 1 < NQ) tmem_ld_wait();
 #endif
           }
