@@ -82,3 +82,26 @@ def test_config_validation_messages():
     with pytest.raises(ValueError, match="filter_eps must be >= 0"):
         lf.CceConfig(filter_eps=float("nan")).validate()
     assert lf.CceConfig.Fp16SaturationPreset().filter_eps == lf.kFp16MinPositive == 6e-8
+
+
+def test_new_entry_points_validate_before_touching_the_gpu():
+    from paper_2509_09682_b200 import _capi
+    L = _capi.lib()
+    # metrics.cpp:16-22
+    assert L.lf_evaluate(None, None, None, 0, 64, 10, 10, 2, None, None, None) == _capi.LF_EINVAL
+    assert "no eval pairs" in L.lf_last_error().decode()
+    assert L.lf_evaluate(None, None, None, 4, 64, 10, 0, 2, None, None, None) == _capi.LF_EINVAL
+    assert "k must be >= 1" in L.lf_last_error().decode()
+    assert L.lf_eval_rank_topk(None, None, None, None, 4, 64, 100, 0, 17, 2, None, None, None,
+                               None) == _capi.LF_EUNSUPPORTED
+    # adam.cpp:14-19
+    assert L.lf_adam_step(None, None, 0, None, None, 4, 1e-3, 1.0, 0.999, 1e-8, 1, None, -1,
+                          None) == _capi.LF_EINVAL
+    assert "betas must lie in [0, 1)" in L.lf_last_error().decode()
+    assert L.lf_adam_step(None, None, 0, None, None, 4, 1e-3, 0.9, 0.999, 0.0, 1, None, -1,
+                          None) == _capi.LF_EINVAL
+    assert "eps must be positive" in L.lf_last_error().decode()
+    # encoder.cpp:23-25 analogue
+    assert L.lf_encode_batch(None, None, 1, None, None, None, 0, 4, 1, 2, None, None, None, None,
+                             None, None, None) == _capi.LF_EINVAL
+    assert "catalog and hidden must be >= 1" in L.lf_last_error().decode()
