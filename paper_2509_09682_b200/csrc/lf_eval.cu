@@ -235,10 +235,11 @@ int eval_rank_topk(int dtype, const void* X, const void* E, const int64_t* targe
   int P = 0;
   const unsigned blocks = static_cast<unsigned>(ceil_div(n, 8));
   if (tc) {
-    rc = tc_eval_partials(X, E, Et.ptr, tl.as<int32_t>(), n, D, v, cnt, val, idx, &P, st);
+    int K = 16;
+    rc = tc_eval_partials(X, E, Et.ptr, tl.as<int32_t>(), n, D, v, k, cnt, val, idx, &P, &K, st);
     if (rc) return rc;
     eval_combine<uint32_t, float, int32_t><<<blocks, 256, 0, st>>>(
-        cnt.as<uint32_t>(), val.as<float>(), idx.as<int32_t>(), P, 16, n, k, v_offset, 0, ahead,
+        cnt.as<uint32_t>(), val.as<float>(), idx.as<int32_t>(), P, K, n, k, v_offset, 0, ahead,
         top_idx, top_score);
   } else if (dtype == LF_F32) {
     rc = simt_eval_partials<float>(static_cast<const float*>(X), static_cast<const float*>(E),

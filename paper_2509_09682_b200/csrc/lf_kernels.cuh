@@ -51,8 +51,8 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
 // (ceil(n/128)*128 rows), tl = clamped local target index; per (chunk, row)
 // count (uint32), top-16 values (float) and local indices (int32).
 int tc_eval_partials(const void* X, const void* E, const void* Et, const int32_t* tl, int64_t n,
-                     int D, int64_t v, Scratch& cnt, Scratch& val, Scratch& idx, int* P_out,
-                     cudaStream_t st);
+                     int D, int64_t v, int k, Scratch& cnt, Scratch& val, Scratch& idx, int* P_out,
+                     int* K_out, cudaStream_t st);
 // Same for fp32 / fp64 (lf_simt.cu), top-K per chunk with K = k.
 template <class T>
 int simt_eval_partials(const T* X, const T* E, const T* Et, const int32_t* tl, int64_t n, int D,

@@ -79,7 +79,11 @@ namespace {
 constexpr int BM = 128;  // owner tile (TMEM lanes)
 
 enum Mode : int { FWD = 0, BWD_ROWS = 1, BWD_ITEMS = 2, EVAL = 3 };
-constexpr int kEvalK = 16;  // per-row top-K kept by the EVAL epilogue
+constexpr int kEvalK = 16;  // largest per-row top-K the EVAL epilogue keeps
+// EVAL list length by FLAGS (a shorter list for small k rises faster, so
+// fewer slabs reach the insertion path): 0 -> 16, 1 -> 12, 2 -> 8
+template <int MODE, int FLAGS>
+constexpr int kEvalKOf = MODE != EVAL ? kEvalK : (FLAGS == 1 ? 12 : (FLAGS == 2 ? 8 : 16));
 // Backward variants: kFilt = filter_eps > 0 (flush below eps, sub-tile skip);
 // kCount = also count skipped elements / sub-tiles (only when stats are read).
 // kTgtIn = handle each row's own target inside the tile loop (exact for any
@@ -112,7 +116,7 @@ struct TcParams {
   // EVAL (tgt = the target's local index clamped to [-1, n_stream]: -1 = before
   // the shard, n_stream = after it)
   uint32_t* ev_count;    // [n_chunks][n_owner] items of the chunk ranked ahead of the target
-  float* ev_val;         // [n_chunks][n_owner][kEvalK] top scores, descending
+  float* ev_val;         // [n_chunks][n_owner][K] top scores, descending (K = kEvalKOf)
   int32_t* ev_idx;       // same, local item index (INT32_MAX = empty)
 };
 
@@ -258,9 +262,10 @@ __device__ __forceinline__ float next_down(float x) {
 
 // Insert (cv, ci) into a descending top-K list, ties to the smaller index
 // (metrics.cpp:64-71 order); a no-op when it ranks below the K-th entry.
-__device__ __forceinline__ void topk_insert(float (&kv)[kEvalK], int (&ki)[kEvalK], float cv, int ci) {
+template <int K>
+__device__ __forceinline__ void topk_insert(float (&kv)[K], int (&ki)[K], float cv, int ci) {
 #pragma unroll
-  for (int k = 0; k < kEvalK; ++k) {
+  for (int k = 0; k < K; ++k) {
     const bool bt = cv > kv[k] || (cv == kv[k] && ci < ki[k]);
     const float t = kv[k];
     const int u = ki[k];
@@ -282,6 +287,8 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
   constexpr int BN = G::BN;
   constexpr int NWG = G::NWG;
   constexpr int NQ = G::NQ;
+  constexpr int KK = kEvalKOf<MODE, FLAGS>;  // EVAL: per-row list length
+  constexpr int RS = 2 * KK + 1;             // EVAL: merge record stride (words)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1 KB alignment by plain pointer arithmetic on the __shared__ array, so
   // every pointer derived from `base` stays in the shared address space
@@ -490,8 +497,8 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
     // EVAL state, carried across the consecutive units of one owner tile:
     // items ranked ahead of the target, running top-k
     uint32_t ecnt = 0;
-    float kv[kEvalK];
-    int ki[kEvalK];
+    float kv[KK];
+    int ki[KK];
     for (int64_t u = U.begin; u < U.end; u += U.step, ++j) {
       const int64_t chunk = U.chunk(u), ot = U.owner(u);
       const bool run_first = u == U.begin || U.owner(u - 1) != ot;
@@ -512,7 +519,7 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
       if (MODE == EVAL && run_first) {
         ecnt = 0;
 #pragma unroll
-        for (int k = 0; k < kEvalK; ++k) {
+        for (int k = 0; k < KK; ++k) {
           kv[k] = -INFINITY;
           ki[k] = 0x7fffffff;
         }
@@ -677,8 +684,8 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
             }
 #ifndef LF_DIAG_NOTOPK
             const float g0 = max32(w[0]), g1 = max32(w[1]);
-            if (fmaxf(g0, g1) > kv[kEvalK - 1]) {  // divergent, rare once the list has filled
-              const float kth = kv[kEvalK - 1];
+            if (fmaxf(g0, g1) > kv[KK - 1]) {  // divergent, rare once the list has filled
+              const float kth = kv[KK - 1];
               uint32_t m0 = 0, m1 = 0;
               if (g0 > kth) {
 #pragma unroll
@@ -697,7 +704,7 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
                   const int c = __ffsll(static_cast<long long>(msk)) - 1;
                   msk &= msk - 1ull;
                   const float cv = c < 32 ? select_reg(w[0], c) : select_reg(w[1], c - 32);
-                  if (cv > kv[kEvalK - 1]) topk_insert(kv, ki, cv, base + c);
+                  if (cv > kv[KK - 1]) topk_insert(kv, ki, cv, base + c);
                 } while (msk);
               }
             }
@@ -925,42 +932,42 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
         if (wg == 0 && orow < p.n_owner) {
           const int64_t rowp = chunk * p.n_owner + orow;
           p.ev_count[rowp] = 0;
-          int4* di = reinterpret_cast<int4*>(p.ev_idx + rowp * kEvalK);
+          int4* di = reinterpret_cast<int4*>(p.ev_idx + rowp * KK);
 #pragma unroll
-          for (int k = 0; k < kEvalK; k += 4) di[k / 4] = make_int4(0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff);
+          for (int k = 0; k < KK; k += 4) di[k / 4] = make_int4(0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff);
         }
       } else if (MODE == EVAL) {
         // end of the run: merge the warpgroups' counts and top-k lists, one
         // record per row
         uint32_t* rec = reinterpret_cast<uint32_t*>(merge);
         if (wg > 0) {
-          uint32_t* r = rec + ((wg - 1) * BM + lrow) * C::kEvalStride;
+          uint32_t* r = rec + ((wg - 1) * BM + lrow) * RS;
           r[0] = ecnt;
 #pragma unroll
-          for (int k = 0; k < kEvalK; ++k) {
+          for (int k = 0; k < KK; ++k) {
             r[1 + k] = __float_as_uint(kv[k]);
-            r[1 + kEvalK + k] = static_cast<uint32_t>(ki[k]);
+            r[1 + KK + k] = static_cast<uint32_t>(ki[k]);
           }
         }
         named_bar_sync(1, G::kEpiThreads);
         if (wg == 0) {
           for (int o = 0; o < NWG - 1; ++o) {
-            const uint32_t* r = rec + (o * BM + lrow) * C::kEvalStride;
+            const uint32_t* r = rec + (o * BM + lrow) * RS;
             ecnt += r[0];
-            for (int k = 0; k < kEvalK; ++k) {  // descending: stop at the first that does not fit
+            for (int k = 0; k < KK; ++k) {  // descending: stop at the first that does not fit
               const float cv = __uint_as_float(r[1 + k]);
-              const int ci = static_cast<int>(r[1 + kEvalK + k]);
-              if (!(cv > kv[kEvalK - 1] || (cv == kv[kEvalK - 1] && ci < ki[kEvalK - 1]))) break;
+              const int ci = static_cast<int>(r[1 + KK + k]);
+              if (!(cv > kv[KK - 1] || (cv == kv[KK - 1] && ci < ki[KK - 1]))) break;
               topk_insert(kv, ki, cv, ci);
             }
           }
           if (orow < p.n_owner) {
             const int64_t rowp = chunk * p.n_owner + orow;
             p.ev_count[rowp] = ecnt;
-            float4* dv = reinterpret_cast<float4*>(p.ev_val + rowp * kEvalK);
-            int4* di = reinterpret_cast<int4*>(p.ev_idx + rowp * kEvalK);
+            float4* dv = reinterpret_cast<float4*>(p.ev_val + rowp * KK);
+            int4* di = reinterpret_cast<int4*>(p.ev_idx + rowp * KK);
 #pragma unroll
-            for (int k = 0; k < kEvalK; k += 4) {
+            for (int k = 0; k < KK; k += 4) {
               dv[k / 4] = make_float4(kv[k], kv[k + 1], kv[k + 2], kv[k + 3]);
               di[k / 4] = make_int4(ki[k], ki[k + 1], ki[k + 2], ki[k + 3]);
             }
@@ -1148,7 +1155,11 @@ int launch_mode(const CUtensorMap& mo, const CUtensorMap& ms, const CUtensorMap&
 template <int D, int MODE>
 int launch_flags(int flags, const CUtensorMap& mo, const CUtensorMap& ms, const CUtensorMap& mb,
                  const CUtensorMap& m1, const TcParams& p, cudaStream_t st) {
-  if constexpr (MODE == FWD || MODE == EVAL) {
+  if constexpr (MODE == FWD) {
+    return launch_mode<D, MODE, 0>(mo, ms, mb, m1, p, st);
+  } else if constexpr (MODE == EVAL) {  // flags = list-length class (kEvalKOf)
+    if (flags == 2) return launch_mode<D, MODE, 2>(mo, ms, mb, m1, p, st);
+    if (flags == 1) return launch_mode<D, MODE, 1>(mo, ms, mb, m1, p, st);
     return launch_mode<D, MODE, 0>(mo, ms, mb, m1, p, st);
   } else {
     switch (flags) {
@@ -1238,8 +1249,10 @@ int tc_cce_forward_partials(const void* X, const void* E, const int64_t* targets
 }
 
 int tc_eval_partials(const void* X, const void* E, const void* Et, const int32_t* tl, int64_t n,
-                     int D, int64_t v, Scratch& cnt, Scratch& val, Scratch& idx, int* P_out,
-                     cudaStream_t st) {
+                     int D, int64_t v, int k, Scratch& cnt, Scratch& val, Scratch& idx, int* P_out,
+                     int* K_out, cudaStream_t st) {
+  const int kclass = k <= 8 ? 2 : (k <= 12 ? 1 : 0);
+  const int K = kclass == 2 ? 8 : (kclass == 1 ? 12 : 16);
   constexpr int BN = Geo<EVAL>::BN;
   const int64_t owner_tiles = ceil_div(n, BM);
   const int64_t stream_tiles = ceil_div(v, BN);
@@ -1250,8 +1263,8 @@ int tc_eval_partials(const void* X, const void* E, const void* Et, const int32_t
   const int64_t tiles_per = ceil_div(stream_tiles, chunks);
   const int64_t P = ceil_div(stream_tiles, tiles_per);
   int rc = cnt.alloc(sizeof(uint32_t) * P * n, st);
-  if (!rc) rc = val.alloc(sizeof(float) * P * n * kEvalK, st);
-  if (!rc) rc = idx.alloc(sizeof(int32_t) * P * n * kEvalK, st);
+  if (!rc) rc = val.alloc(sizeof(float) * P * n * K, st);
+  if (!rc) rc = idx.alloc(sizeof(int32_t) * P * n * K, st);
   if (rc) return rc;
   CUtensorMap mo, ms, mt;
   rc = make_map(&mo, X, n, D, BM);
@@ -1269,9 +1282,10 @@ int tc_eval_partials(const void* X, const void* E, const void* Et, const int32_t
   p.ev_count = cnt.as<uint32_t>();
   p.ev_val = val.as<float>();
   p.ev_idx = idx.as<int32_t>();
-  rc = launch_d<EVAL>(D, 0, mo, ms, mt, mo, p, st);
+  rc = launch_d<EVAL>(D, kclass, mo, ms, mt, mo, p, st);
   if (rc) return rc;
   *P_out = static_cast<int>(P);
+  *K_out = K;
   return LF_OK;
 }
 
