@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", choices=["collective", "peer"], default="collective",
+                    help="N>1: torch.distributed collectives (NCCL) or the peer-memory exchange "
+                         "fused into the producing kernels (CUDA IPC)")
     return ap.parse_args()
 
 
@@ -211,7 +214,7 @@ def run_ours(args):
     from paper_2509_09682_b200.sharded import ShardedCce
 
     L = _capi.lib()
-    sh = ShardedCce(V)
+    sh = ShardedCce(V, exchange=args.exchange if world > 1 else "collective")
     v0, v1 = sh.v_begin, sh.v_end
     g = torch.Generator(device=dev).manual_seed(SEED)
     X = (torch.rand(N_ROWS, D, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
@@ -374,7 +377,8 @@ def run_ours(args):
                 "dtype": "bf16", "data": "synthetic",
                 "config": {"workload": WORKLOAD, "n_positions": N_ROWS, "d": D, "v": V,
                            "filter_eps": EPS, "seed": SEED,
-                           "parallelism": f"catalog-sharded over {world} GPU(s)" if world > 1 else "single GPU",
+                           "parallelism": (f"catalog-sharded over {world} GPU(s), {args.exchange} exchange"
+                                           if world > 1 else "single GPU"),
                            "l2": "inputs (134.6 MB) exceed L2 (126 MB) and a 256 MB L2 flush runs "
                                  "before every timed step (outside the events)"},
                 "peak_hbm_gb": peak_hbm, "loss": loss_val,

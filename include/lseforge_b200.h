@@ -130,6 +130,42 @@ LF_API int lf_cce_backward_shard(const void* d_X, const void* d_E_shard, const i
                           const lf_cce_config* cfg, void* d_dX_partial, void* d_dE_shard,
                           lf_cce_stats* stats, void* stream);
 
+/* ------------------------------- catalog sharding over peer memory ---- */
+/* The same two exchanges without NCCL: each rank maps every peer's exchange
+ * buffer (CUDA IPC: lf_peer_alloc exports a cudaMalloc'd buffer as a 64-byte
+ * handle, the handles are exchanged by the caller, lf_peer_open maps them) and
+ * the producing kernel stores its contribution straight into slot [rank] of
+ * every peer's buffer (d_peer_*: DEVICE array of `world` pointers, this
+ * rank's own buffer at index rank; parity_off = element offset of the
+ * epoch-parity half, so consecutive exchanges alternate halves).
+ *   forward:  lf_cce_forward_partial_peer — the per-chunk partial fold fused
+ *             with the all-gather; each buffer holds [world][n] float4 —
+ *             then lf_peer_barrier, then lf_cce_combine on the local block.
+ *   backward: lf_cce_backward_shard_peer — the dX V-chunk reduction fused with
+ *             the all-gather of the rank's partial ([world][n x d] floats),
+ *             then lf_peer_barrier, then lf_peer_sum (fixed rank order: every
+ *             rank gets identical bits).  bf16 / f32. */
+LF_API int lf_peer_alloc(uint64_t bytes, void** d_ptr, void* ipc_handle /* 64 bytes out */);
+LF_API int lf_peer_open(const void* ipc_handle, void** d_ptr);
+LF_API int lf_peer_close(void* d_ptr);
+LF_API int lf_peer_free(void* d_ptr);
+/* Signal every peer (d_peer_flags: device array of `world` pointers to each
+ * rank's uint32 flag array of `world` entries) that this rank's stores for
+ * `epoch` are done, then wait (stream-ordered, on the device) for all peers'. */
+LF_API int lf_peer_barrier(uint32_t* const* d_peer_flags, int32_t world, int32_t rank, uint32_t epoch,
+                           void* stream);
+LF_API int lf_peer_sum(const float* d_slots, int32_t world, int64_t count, float* d_out, void* stream);
+LF_API int lf_cce_forward_partial_peer(const void* d_X, const void* d_E_shard, const int64_t* d_targets,
+                                       int64_t n, int64_t d, int64_t v_shard, int64_t v_offset,
+                                       const lf_cce_config* cfg, float* const* d_peer_parts,
+                                       int32_t world, int32_t rank, int64_t parity_off, void* stream);
+LF_API int lf_cce_backward_shard_peer(const void* d_X, const void* d_E_shard, const int64_t* d_targets,
+                                      const double* d_lse, double upstream, int64_t n, int64_t d,
+                                      int64_t v_shard, int64_t v_offset, int64_t v_total,
+                                      const lf_cce_config* cfg, void* d_dE_shard, lf_cce_stats* stats,
+                                      float* const* d_peer_dx, int32_t world, int32_t rank,
+                                      int64_t parity_off, void* stream);
+
 /* ---------------------------------------------------------------- CCE- --- */
 
 /* Replaces lseforge::ccem_forward (ccem.hpp:19-20, ccem.cpp:48-105). */

@@ -26,7 +26,9 @@ EXPORTS = (
     "lf_profile_enable", "lf_profile_read", "lf_profile_reset", "lf_classifier_to_items",
     "lf_convert_rows", "lf_items_grad_to_classifier", "lf_widen_grad", "lf_sample_uniform",
     "lf_ce_forward", "lf_ce_backward", "lf_eval_rank_topk", "lf_eval_merge", "lf_eval_summary",
-    "lf_evaluate", "lf_adam_step", "lf_encode_batch", "lf_encoder_backward",
+    "lf_evaluate", "lf_adam_step", "lf_encode_batch", "lf_encoder_backward", "lf_peer_alloc",
+    "lf_peer_open", "lf_peer_close", "lf_peer_free", "lf_peer_barrier", "lf_peer_sum",
+    "lf_cce_forward_partial_peer", "lf_cce_backward_shard_peer",
 )
 KERNEL_KINDS = ("cce_fwd", "cce_bwd_dx", "cce_bwd_de", "cce_simt", "ccem_fwd", "ccem_bwd", "aux",
                 "eval")
@@ -95,6 +97,16 @@ def lib():
                                       vp, vp, vp, vp]
         L.lf_encoder_backward.argtypes = [vp, vp, i64, vp, i64, i64, vp, vp, vp, i64, vp, C.c_int32,
                                           vp, vp, vp, vp]
+        L.lf_peer_alloc.argtypes = [C.c_uint64, C.POINTER(C.c_void_p), C.c_void_p]
+        L.lf_peer_open.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
+        L.lf_peer_close.argtypes = [vp]
+        L.lf_peer_free.argtypes = [vp]
+        L.lf_peer_barrier.argtypes = [vp, C.c_int32, C.c_int32, C.c_uint32, vp]
+        L.lf_peer_sum.argtypes = [vp, C.c_int32, i64, vp, vp]
+        L.lf_cce_forward_partial_peer.argtypes = [vp, vp, vp, i64, i64, i64, i64, cfgp, vp, C.c_int32,
+                                                  C.c_int32, i64, vp]
+        L.lf_cce_backward_shard_peer.argtypes = [vp, vp, vp, dp, C.c_double, i64, i64, i64, i64, i64,
+                                                 cfgp, vp, stp, vp, C.c_int32, C.c_int32, i64, vp]
         L.lf_launch_count.restype = C.c_uint64
         L.lf_profile_enable.argtypes = [C.c_int]
         L.lf_profile_enable.restype = C.c_int
@@ -107,7 +119,10 @@ def lib():
                      "lf_sample_uniform", "lf_classifier_to_items", "lf_convert_rows",
                      "lf_items_grad_to_classifier", "lf_widen_grad", "lf_ce_forward",
                      "lf_ce_backward", "lf_eval_rank_topk", "lf_eval_merge", "lf_eval_summary",
-                     "lf_evaluate", "lf_adam_step", "lf_encode_batch", "lf_encoder_backward"):
+                     "lf_evaluate", "lf_adam_step", "lf_encode_batch", "lf_encoder_backward",
+                     "lf_peer_alloc", "lf_peer_open", "lf_peer_close", "lf_peer_free",
+                     "lf_peer_barrier", "lf_peer_sum", "lf_cce_forward_partial_peer",
+                     "lf_cce_backward_shard_peer"):
             getattr(L, name).restype = C.c_int
         if L.lf_abi_version() != 1:
             raise ImportError("liblseforge_b200.so ABI mismatch")

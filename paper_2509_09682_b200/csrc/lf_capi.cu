@@ -181,7 +181,7 @@ int read_stats(Counters& c, lf_cce_stats* stats, int64_t n, int64_t v_total, cud
 int backward_impl(const void* X, const void* E, const int64_t* targets, const double* lse,
                   double upstream, int64_t n, int64_t d, int64_t v_shard, int64_t v_offset,
                   int64_t v_total, const lf_cce_config* cfg, void* dX, void* dE,
-                  lf_cce_stats* stats, cudaStream_t st) {
+                  lf_cce_stats* stats, cudaStream_t st, const PeerPush* push = nullptr) {
   int rc = check_cfg(cfg);
   if (!rc) rc = check_shapes(n, d, v_shard);
   if (rc) return rc;
@@ -196,13 +196,16 @@ int backward_impl(const void* X, const void* E, const int64_t* targets, const do
       if (!rc)
         rc = tc_cce_backward(X, E, targets, lse, scale, cfg->filter_eps, n, static_cast<int>(d),
                              v_shard, v_offset, static_cast<float*>(dX), static_cast<float*>(dE),
-                             stats ? c.ptr() : nullptr, st);
+                             stats ? c.ptr() : nullptr, st, push);
       break;
     case LF_F32:
       rc = simt_cce_backward<float>(static_cast<const float*>(X), static_cast<const float*>(E),
                                     targets, lse, scale, cfg->filter_eps, n, static_cast<int>(d),
                                     v_shard, v_offset, static_cast<float*>(dX),
                                     static_cast<float*>(dE), c.ptr(), st);
+      if (!rc && push)
+        rc = peer_reduce_push(static_cast<const float*>(dX), 1, n * d, push->peers, push->world,
+                              push->rank, push->parity_off, st);
       break;
     default:
       rc = simt_cce_backward<double>(static_cast<const double*>(X),
@@ -310,6 +313,62 @@ int lf_cce_backward_shard(const void* d_X, const void* d_E_shard, const int64_t*
                           lf_cce_stats* stats, void* stream) {
   return backward_impl(d_X, d_E_shard, d_targets, d_lse, upstream, n, d, v_shard, v_offset,
                        v_total, cfg, d_dX_partial, d_dE_shard, stats, as_stream(stream));
+}
+
+int lf_cce_forward_partial_peer(const void* d_X, const void* d_E_shard, const int64_t* d_targets,
+                                int64_t n, int64_t d, int64_t v_shard, int64_t v_offset,
+                                const lf_cce_config* cfg, float* const* d_peer_parts, int32_t world,
+                                int32_t rank, int64_t parity_off, void* stream) {
+  int rc = check_cfg(cfg);
+  if (!rc) rc = check_shapes(n, d, v_shard);
+  if (rc) return rc;
+  if (world < 1 || rank < 0 || rank >= world || !d_peer_parts)
+    return fail(LF_EINVAL, "peer exchange: bad world / rank / peer table");
+  cudaStream_t st = as_stream(stream);
+  Scratch ws;
+  float* part = nullptr;
+  int P = 1;
+  if (cfg->dtype == LF_BF16) {
+    rc = check_bf16_d(d);
+    if (!rc)
+      rc = tc_cce_forward_partials(d_X, d_E_shard, d_targets, n, static_cast<int>(d), v_shard, v_offset,
+                                   ws, &part, &P, st);
+  } else {
+    rc = ws.alloc(sizeof(float) * 4 * n, st);
+    part = ws.as<float>();
+    if (!rc && cfg->dtype == LF_F32)
+      rc = simt_cce_forward_partial_log2<float>(static_cast<const float*>(d_X),
+                                                static_cast<const float*>(d_E_shard), d_targets, n,
+                                                static_cast<int>(d), v_shard, v_offset, part, st);
+    else if (!rc)
+      rc = simt_cce_forward_partial_log2<double>(static_cast<const double*>(d_X),
+                                                 static_cast<const double*>(d_E_shard), d_targets, n,
+                                                 static_cast<int>(d), v_shard, v_offset, part, st);
+  }
+  if (rc) return rc;
+  // the chunk fold fused with the all-gather: each row's partial lands in
+  // slot [rank] of every peer's buffer
+  return peer_fold_push(part, P, n, d_peer_parts, world, rank, parity_off, st);
+}
+
+int lf_cce_backward_shard_peer(const void* d_X, const void* d_E_shard, const int64_t* d_targets,
+                               const double* d_lse, double upstream, int64_t n, int64_t d,
+                               int64_t v_shard, int64_t v_offset, int64_t v_total,
+                               const lf_cce_config* cfg, void* d_dE_shard, lf_cce_stats* stats,
+                               float* const* d_peer_dx, int32_t world, int32_t rank,
+                               int64_t parity_off, void* stream) {
+  if (!cfg || (cfg->dtype != LF_BF16 && cfg->dtype != LF_F32))
+    return fail(LF_EUNSUPPORTED, "peer exchange: bf16 or f32 only (fp32 dX slots)");
+  if (world < 1 || rank < 0 || rank >= world || !d_peer_dx)
+    return fail(LF_EINVAL, "peer exchange: bad world / rank / peer table");
+  if (n < 0 || d < 0) return fail(LF_EINVAL, "cce: negative extent");
+  cudaStream_t st = as_stream(stream);
+  Scratch dx;
+  int rc = dx.alloc(sizeof(float) * std::max<int64_t>(n * d, 1), st);
+  if (rc) return rc;
+  const PeerPush push{d_peer_dx, world, rank, parity_off};
+  return backward_impl(d_X, d_E_shard, d_targets, d_lse, upstream, n, d, v_shard, v_offset, v_total,
+                       cfg, dx.ptr, d_dE_shard, stats, st, &push);
 }
 
 int lf_ccem_forward(const void* d_X, const void* d_E, const int64_t* d_inds, int64_t n,

@@ -43,9 +43,25 @@ int launch_mean_loss(const double* lse, const double* pos, int64_t n, double* lo
 int tc_cce_forward_partials(const void* X, const void* E, const int64_t* targets, int64_t n,
                             int D, int64_t v, int64_t v_offset, Scratch& ws, float** part_out,
                             int* P_out, cudaStream_t st);
+// Peer-memory exchange target (lf_peer.cu): rank `rank`'s contribution goes to
+// slot [rank] of every peer's buffer (peers: device array of `world`
+// pointers), offset by parity_off floats (epoch double-buffering).
+struct PeerPush {
+  float* const* peers;
+  int world, rank;
+  int64_t parity_off;
+};
+int peer_fold_push(const float* part, int P, int64_t n, float* const* peers, int world, int rank,
+                   int64_t parity_off_floats, cudaStream_t st);
+int peer_reduce_push(const float* part, int P, int64_t count, float* const* peers, int world, int rank,
+                     int64_t parity_off_floats, cudaStream_t st);
+
+// With `push`, dX is not reduced into dX: the V-chunk reduction is fused with
+// the store of the rank's dX partial into every peer's slot (dX is scratch).
 int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const double* lse,
                     double scale, double eps, int64_t n, int D, int64_t v, int64_t v_offset,
-                    float* dX, float* dE, unsigned long long* counters, cudaStream_t st);
+                    float* dX, float* dE, unsigned long long* counters, cudaStream_t st,
+                    const PeerPush* push = nullptr);
 
 // EVAL-mode partials over the shard (bf16): Et = the rows' target item rows
 // (ceil(n/128)*128 rows), tl = clamped local target index; per (chunk, row)

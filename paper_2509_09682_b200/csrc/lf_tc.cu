@@ -1291,10 +1291,12 @@ int tc_eval_partials(const void* X, const void* E, const void* Et, const int32_t
 
 int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const double* lse,
                     double scale, double eps, int64_t n, int D, int64_t v, int64_t v_offset,
-                    float* dX, float* dE, unsigned long long* counters, cudaStream_t st) {
+                    float* dX, float* dE, unsigned long long* counters, cudaStream_t st,
+                    const PeerPush* push) {
   if (scale == 0.0) {
     LF_CUDA(cudaMemsetAsync(dX, 0, sizeof(float) * n * D, st));
     LF_CUDA(cudaMemsetAsync(dE, 0, sizeof(float) * v * D, st));
+    if (push) return peer_reduce_push(dX, 1, n * D, push->peers, push->world, push->rank, push->parity_off, st);
     return LF_OK;
   }
   // G domain.  No filter: G = softmax * |scale| (lse2 = lse log2e - log2|scale|).
@@ -1361,7 +1363,11 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
   p.fix_scale = static_cast<float>(scale);
   rc = launch_d<BWD_ROWS>(D, flags, mx_own, me_str, mx_own, mx_own, p, st);
   if (rc) return rc;
-  if (P > 1) {
+  if (push) {  // chunk reduction fused with the all-gather of this rank's dX partial
+    rc = peer_reduce_push(dx_out, static_cast<int>(P), n * D, push->peers, push->world, push->rank,
+                          push->parity_off, st);
+    if (rc) return rc;
+  } else if (P > 1) {
     rc = launch_reduce_f32(dx_out, static_cast<int>(P), n * D, dX, st);
     if (rc) return rc;
   }

@@ -155,16 +155,142 @@ class ShardedEval:
         return self.kernels.summarize(rank, top, popularity)
 
 
-class ShardedCce:
-    """Catalog-sharded cce_forward / cce_backward over a process group."""
+class PeerExchange:
+    """Exchange buffers every rank maps (CUDA IPC): rank p's buffer holds
+    [2 parities][world slots][slot_elems] plus a flag array.  Handles are
+    swapped once over the process group (any backend); the data never goes
+    through NCCL — the producing kernels store into peers' slots directly and
+    lf_peer_barrier orders the exchange on the device."""
 
-    def __init__(self, v_total: int, group=None, kernels=None):
+    def __init__(self, slot_bytes: int, group=None, device=None):
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.slot_bytes = (int(slot_bytes) + 255) // 256 * 256
+        self.half = self.world * self.slot_bytes
+        L = _capi.lib()
+        self.flag_bytes = 256 * ((4 * self.world + 255) // 256)
+        total = self.flag_bytes + 2 * self.half
+        base = C.c_void_p()
+        handle = (C.c_char * 64)()
+        _capi.check(L.lf_peer_alloc(total, C.byref(base), handle))
+        self.local = base.value
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(handle), group=self.group)
+        self.bases = []
+        for r, h in enumerate(handles):
+            if r == self.rank:
+                self.bases.append(self.local)
+            else:
+                ptr = C.c_void_p()
+                _capi.check(L.lf_peer_open((C.c_char * 64).from_buffer_copy(h), C.byref(ptr)))
+                self.bases.append(ptr.value)
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.flags_dev = torch.tensor(self.bases, dtype=torch.int64, device=dev)
+        self.slots_dev = torch.tensor([b + self.flag_bytes for b in self.bases], dtype=torch.int64, device=dev)
+        self.epoch = 0
+
+    def next_epoch(self):
+        self.epoch += 1
+        return self.epoch, (self.epoch & 1) * self.half  # byte offset of this epoch's half
+
+    def local_view(self, parity_off: int, shape, dtype=torch.float32):
+        """The local buffer's current half as a tensor [world, *shape] (no copy)."""
+        numel = self.world * int(torch.Size(shape).numel())
+        esize = torch.tensor([], dtype=dtype).element_size()
+        ptr = self.local + self.flag_bytes + parity_off
+        # wrap the raw device pointer (no copy) through __cuda_array_interface__;
+        # ordering is the caller's stream (the barrier kernel precedes every read)
+        class _Arr:
+            __cuda_array_interface__ = {"shape": (numel,), "typestr": "<f4" if esize == 4 else "<f8",
+                                        "data": (ptr, False), "version": 2}
+        flat = torch.as_tensor(_Arr(), device=self.flags_dev.device)
+        per = numel // self.world
+        return flat.view(self.world, *shape) if per else flat
+
+    def barrier(self, epoch: int, stream) -> None:
+        _capi.check(_capi.lib().lf_peer_barrier(self.flags_dev.data_ptr(), self.world, self.rank,
+                                                epoch, stream))
+
+    def close(self):
+        L = _capi.lib()
+        for r, b in enumerate(self.bases):
+            if r != self.rank:
+                L.lf_peer_close(b)
+        L.lf_peer_free(self.local)
+
+
+class ShardedCce:
+    """Catalog-sharded cce_forward / cce_backward over a process group.
+
+    exchange="collective": torch.distributed collectives (NCCL on GPUs).
+    exchange="peer": peer-memory exchange (PeerExchange) with the collective
+    fused into the producing kernels (bf16 / f32)."""
+
+    def __init__(self, v_total: int, group=None, kernels=None, exchange: str = "collective"):
         self.group = group
         self.P = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.v_total = v_total
         self.v_begin, self.v_end = shard_bounds(v_total, self.P, self.rank)
         self.kernels = kernels if kernels is not None else DeviceKernels()
+        if exchange not in ("collective", "peer"):
+            raise ValueError(f"sharded cce: unknown exchange {exchange!r}")
+        self.exchange = exchange
+        self._peer = None
+
+    def _peer_for(self, slot_bytes: int) -> PeerExchange:
+        if self._peer is None or self._peer.slot_bytes < slot_bytes:
+            if self._peer is not None:
+                torch.cuda.synchronize()
+                dist.barrier(group=self.group)
+                self._peer.close()
+            self._peer = PeerExchange(slot_bytes, self.group)
+        return self._peer
+
+    def _forward_peer(self, X, E_shard, targets, cfg):
+        n, d = X.shape
+        px = self._peer_for(max(16 * n, 4 * n * d))
+        epoch, off = px.next_epoch()
+        c = cfg.to_c(lf_dtype(X))
+        st = _stream(X)
+        _capi.check(_capi.lib().lf_cce_forward_partial_peer(
+            X.data_ptr(), E_shard.data_ptr(), targets.data_ptr(), n, d, E_shard.shape[0], self.v_begin,
+            C.byref(c), self._slot_table(px, off), self.P,
+            self.rank, 0, st))
+        px.barrier(epoch, st)
+        parts = px.local_view(off, (n, 4))
+        return self.kernels.combine(parts)
+
+    def _slot_table(self, px: PeerExchange, off: int) -> int:
+        # device table of this epoch's slot bases (peer bases + flag area + parity half)
+        key = ("tab", off)
+        tab = getattr(px, "_tabs", {})
+        if key not in tab:
+            tab[key] = px.slots_dev + off
+            px._tabs = tab
+        return tab[key].data_ptr()
+
+    def _backward_peer(self, X, E_shard, targets, lse, upstream, cfg, stats):
+        n, d = X.shape
+        vs = E_shard.shape[0]
+        px = self._peer_for(max(16 * n, 4 * n * d))
+        epoch, off = px.next_epoch()
+        dE = torch.empty((vs, d), dtype=torch.float32, device=X.device)
+        c = cfg.to_c(lf_dtype(X))
+        stc = _capi.CceStatsC()
+        st = _stream(X)
+        _capi.check(_capi.lib().lf_cce_backward_shard_peer(
+            X.data_ptr(), E_shard.data_ptr(), targets.data_ptr(),
+            lse.to(torch.float64).contiguous().data_ptr(), float(upstream), n, d, vs, self.v_begin,
+            self.v_total, C.byref(c), dE.data_ptr(), C.byref(stc) if stats else None,
+            self._slot_table(px, off), self.P, self.rank, 0, st))
+        px.barrier(epoch, st)
+        dX = torch.empty((n, d), dtype=torch.float32, device=X.device)
+        slots = px.local_view(off, (n, d))
+        _capi.check(_capi.lib().lf_peer_sum(slots.data_ptr(), self.P, n * d, dX.data_ptr(), st))
+        s = ShardStats(int(stc.skipped_elems), int(stc.skipped_tiles), int(stc.total_tiles)) if stats else None
+        return dX, dE, s
 
     @property
     def v_shard(self) -> int:
@@ -174,6 +300,8 @@ class ShardedCce:
         if E_shard.shape[0] != self.v_shard:
             raise ValueError(f"sharded cce: rank {self.rank} expects {self.v_shard} item rows, "
                              f"got {E_shard.shape[0]}")
+        if self.exchange == "peer":
+            return self._forward_peer(X, E_shard, targets, cfg)
         part = self.kernels.forward_partial(X, E_shard, targets, self.v_begin, cfg)
         if self.P == 1:
             return self.kernels.combine(part.unsqueeze(0))
@@ -185,10 +313,13 @@ class ShardedCce:
 
     def backward(self, X, E_shard, targets, lse, upstream: float = 1.0,
                  cfg: CceConfig = CceConfig(), stats: bool = True) -> CceBackwardResult:
-        dX, dE, st = self.kernels.backward_shard(X, E_shard, targets, lse, upstream, self.v_begin,
-                                                 self.v_total, cfg, stats)
-        if self.P > 1:
-            dist.all_reduce(dX, op=dist.ReduceOp.SUM, group=self.group)
+        if self.exchange == "peer":
+            dX, dE, st = self._backward_peer(X, E_shard, targets, lse, upstream, cfg, stats)
+        else:
+            dX, dE, st = self.kernels.backward_shard(X, E_shard, targets, lse, upstream, self.v_begin,
+                                                     self.v_total, cfg, stats)
+            if self.P > 1:
+                dist.all_reduce(dX, op=dist.ReduceOp.SUM, group=self.group)
         res = CceBackwardResult(GradPair(dX, dE))
         if stats:
             cnt = torch.tensor([st.skipped_elems, st.skipped_tiles, st.total_tiles],

@@ -33,13 +33,16 @@ def test_bench_one_rank(cuda):
     assert abs(j["loss"] - 17.3) < 0.1  # uniform logits: lse ~ ln(V) + var/2
 
 
-def test_bench_two_ranks_sharded(cuda):
+@pytest.mark.parametrize("exchange,port", [("collective", 29571), ("peer", 29573)])
+def test_bench_two_ranks_sharded(cuda, exchange, port):
     env = dict(os.environ, LF_BENCH_SHARE_GPU="1")
     p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                         "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
-                        "29571", "bench.py", "--gpus", "2", "--steps", "2", "--warmup", "3"],
+                        str(port), "bench.py", "--gpus", "2", "--steps", "2", "--warmup", "3",
+                        "--exchange", exchange],
                        cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
     assert p.returncode == 0, (p.stdout[-2000:], p.stderr[-2000:])
     j = last_json(p.stdout)
     assert j["n_gpus"] == 2 and "sharded" in j["config"]["parallelism"]
+    assert exchange in j["config"]["parallelism"]
     assert abs(j["loss"] - 17.3) < 0.1  # the combined sharded loss equals the unsharded one
