@@ -293,6 +293,18 @@ LF_API int lf_adam_step(float* d_param, const void* d_grad, int32_t grad_dtype, 
                         double* d_v, int64_t count, double lr, double beta1, double beta2,
                         double eps, int64_t t, void* d_shadow, int32_t shadow_dtype, void* stream);
 
+/* Replaces lseforge::sample_popularity (sampler.hpp, sampler.cpp:77-127):
+ * inverse CDF over the running sum of count^exponent (d_counts: catalog
+ * int64 training counts), row i from SplitMix64(seed).derived(i), one
+ * uniform() per attempt, retry_cap failed attempts in a row -> LF_ERUNTIME.
+ * Same indices as the reference for exponent == 1 (the running sums are exact
+ * integers); for other exponents the device pow may differ in the last ulp.
+ * LF_EINVAL with the reference's messages (negative count, positive outside
+ * the catalog, ns too large, all weights zero).  Synchronizes `stream`. */
+LF_API int lf_sample_popularity(const int64_t* d_positives, int64_t n, int64_t ns,
+                                const int64_t* d_counts, int64_t catalog, double exponent,
+                                uint64_t seed, int32_t retry_cap, int64_t* d_inds, void* stream);
+
 /* ----------------------------------------------------------- validation --- */
 /* Replaces validate_loss_inputs' index scan (losses.cpp:58-67) for device
  * targets.  Synchronizes `stream`.  On failure returns LF_EINVAL with the

@@ -115,6 +115,52 @@ int orc_sample_uniform(const int64_t* positives, size_t n, size_t ns, size_t cat
   return failed ? -1 : 0;
 }
 
+int orc_sample_popularity(const int64_t* positives, size_t n, size_t ns, const int64_t* counts,
+                          size_t catalog, double exponent, uint64_t rng_seed, int retry_cap,
+                          int64_t* inds) { /* sampler.cpp:77-127 */
+  double* cum = (double*)malloc(sizeof(double) * (catalog ? catalog : 1));
+  double running = 0.0;
+  for (size_t v = 0; v < catalog; ++v) { /* sampler.cpp:93-99 */
+    const double c = (double)counts[v];
+    running += exponent == 1.0 ? c : pow(c, exponent);
+    cum[v] = running;
+  }
+  if (!(running > 0.0)) {
+    free(cum);
+    return -2;
+  }
+  const size_t w = 1 + ns;
+  orc_rng base;
+  orc_rng_init(&base, rng_seed);
+  int failed = 0;
+#pragma omp parallel for schedule(static) reduction(| : failed)
+  for (size_t i = 0; i < n; ++i) {
+    orc_rng row;
+    orc_rng_derived(&base, i, &row);
+    inds[i * w] = positives[i];
+    for (size_t s = 1; s <= ns; ++s) {
+      int placed = 0;
+      for (int attempt = 0; attempt < retry_cap; ++attempt) {
+        const double u = orc_rng_uniform(&row) * running;
+        size_t lo = 0, hi = catalog; /* upper_bound: first cum[v] > u */
+        while (lo < hi) {
+          const size_t mid = lo + (hi - lo) / 2;
+          if (!(u < cum[mid])) lo = mid + 1; else hi = mid;
+        }
+        if (lo == catalog) continue; /* u rounded up to the total: redraw */
+        if ((int64_t)lo != positives[i]) {
+          inds[i * w + s] = (int64_t)lo;
+          placed = 1;
+          break;
+        }
+      }
+      if (!placed) failed = 1;
+    }
+  }
+  free(cum);
+  return failed ? -1 : 0;
+}
+
 /* ------------------------------------------------------------------------ */
 /* Logit tile — cce.cpp:40-55: tile[i][j] = sum_k E[i][k]*C[k][j], double,   */
 /* k ascending, starting from 0.0.                                           */

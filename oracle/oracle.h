@@ -97,6 +97,13 @@ int64_t orc_validate_inds(const int64_t* inds, size_t n, size_t w, size_t v);
 void orc_estimate_flops(size_t n, size_t d, size_t v, size_t ns, int backend, uint64_t* fwd,
                         uint64_t* bwd);
 
+/* sample_popularity (sampler.cpp:77-127): inverse CDF over the running sum of
+ * count^exponent (exponent 1: the counts), per-row rng.derived(i), one
+ * uniform() per attempt; returns 0, -1 (retry cap), -2 (all weights zero). */
+int orc_sample_popularity(const int64_t* positives, size_t n, size_t ns, const int64_t* counts,
+                          size_t catalog, double exponent, uint64_t rng_seed, int retry_cap,
+                          int64_t* inds);
+
 /* ---- full-catalog evaluation (metrics.cpp:13-103, minus the encoder) ------
  * H : n x d double (encode() output, metrics.cpp:46); C : d x v float.
  * Scores s_j = sum_k H[k] * (double)C[k][j], k ascending (metrics.cpp:49-54).

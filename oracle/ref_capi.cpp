@@ -115,6 +115,19 @@ int ref_sample_uniform(const int64_t* positives, std::size_t n, std::size_t ns,
   });
 }
 
+int ref_sample_popularity(const int64_t* positives, std::size_t n, std::size_t ns,
+                          const int64_t* counts, std::size_t catalog, double exponent,
+                          uint64_t seed, int64_t* inds) {
+  return guard([&] {
+    PopularityTable pop = PopularityTable::FromCounts(std::vector<int64_t>(counts, counts + catalog));
+    SamplerConfig cfg;
+    cfg.popularity_exponent = exponent;
+    NegIndexMatrix m = sample_popularity(std::span<const int64_t>(positives, n), ns, pop,
+                                         SplitMix64(seed), cfg);
+    std::memcpy(inds, m.data().data(), sizeof(int64_t) * n * (1 + ns));
+  });
+}
+
 // ---- cce.cpp ---------------------------------------------------------------
 int ref_cce_forward(const float* E, const float* C, const int64_t* x, std::size_t n,
                     std::size_t d, std::size_t v, std::size_t rb, std::size_t cb, int workers,

@@ -14,13 +14,13 @@ from .ccem import (Backend, FlopEstimate, backend_is_sampled, ccem_backward, cce
 from .losses import GradPair, LossOutput, ce_full_backward, ce_full_forward, validate_loss_inputs
 from .adam import AdamConfig, DeviceAdam
 from .metrics import EvalSummary, evaluate
-from .sampler import sample_uniform
+from .sampler import sample_popularity, sample_uniform
 
 __all__ = [
     "CceConfig", "CceBackwardResult", "cce_forward", "cce_backward", "kFp16MinPositive",
     "ccem_forward", "ccem_backward", "ccem_backward_rows", "estimate_flops", "FlopEstimate",
     "Backend", "backend_is_sampled", "LossOutput", "GradPair", "validate_loss_inputs",
-    "MemAccountant", "Report", "ScalarKind", "sample_uniform", "ce_full_forward",
+    "MemAccountant", "Report", "ScalarKind", "sample_uniform", "sample_popularity", "ce_full_forward",
     "ce_full_backward", "EvalSummary", "evaluate", "AdamConfig", "DeviceAdam", "lib",
 ]
 

@@ -28,7 +28,7 @@ EXPORTS = (
     "lf_ce_forward", "lf_ce_backward", "lf_eval_rank_topk", "lf_eval_merge", "lf_eval_summary",
     "lf_evaluate", "lf_adam_step", "lf_encode_batch", "lf_encoder_backward", "lf_peer_alloc",
     "lf_peer_open", "lf_peer_close", "lf_peer_free", "lf_peer_barrier", "lf_peer_sum",
-    "lf_cce_forward_partial_peer", "lf_cce_backward_shard_peer",
+    "lf_cce_forward_partial_peer", "lf_cce_backward_shard_peer", "lf_sample_popularity",
 )
 KERNEL_KINDS = ("cce_fwd", "cce_bwd_dx", "cce_bwd_de", "cce_simt", "ccem_fwd", "ccem_bwd", "aux",
                 "eval")
@@ -107,6 +107,8 @@ def lib():
                                                   C.c_int32, i64, vp]
         L.lf_cce_backward_shard_peer.argtypes = [vp, vp, vp, dp, C.c_double, i64, i64, i64, i64, i64,
                                                  cfgp, vp, stp, vp, C.c_int32, C.c_int32, i64, vp]
+        L.lf_sample_popularity.argtypes = [vp, i64, i64, vp, i64, C.c_double, C.c_uint64, C.c_int32,
+                                           vp, vp]
         L.lf_launch_count.restype = C.c_uint64
         L.lf_profile_enable.argtypes = [C.c_int]
         L.lf_profile_enable.restype = C.c_int
@@ -122,7 +124,7 @@ def lib():
                      "lf_evaluate", "lf_adam_step", "lf_encode_batch", "lf_encoder_backward",
                      "lf_peer_alloc", "lf_peer_open", "lf_peer_close", "lf_peer_free",
                      "lf_peer_barrier", "lf_peer_sum", "lf_cce_forward_partial_peer",
-                     "lf_cce_backward_shard_peer"):
+                     "lf_cce_backward_shard_peer", "lf_sample_popularity"):
             getattr(L, name).restype = C.c_int
         if L.lf_abi_version() != 1:
             raise ImportError("liblseforge_b200.so ABI mismatch")

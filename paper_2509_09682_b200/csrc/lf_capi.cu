@@ -525,6 +525,14 @@ int lf_adam_step(float* d_param, const void* d_grad, int32_t grad_dtype, double*
                    shadow_dtype, as_stream(stream));
 }
 
+int lf_sample_popularity(const int64_t* d_positives, int64_t n, int64_t ns, const int64_t* d_counts,
+                         int64_t catalog, double exponent, uint64_t seed, int32_t retry_cap,
+                         int64_t* d_inds, void* stream) {
+  if (retry_cap < 1) return fail(LF_EINVAL, "sample_popularity: retry_cap must be >= 1");
+  return sample_popularity(d_positives, n, ns, d_counts, catalog, exponent, seed, retry_cap, d_inds,
+                           as_stream(stream));
+}
+
 int lf_estimate_flops(int64_t n, int64_t d, int64_t v, int64_t ns, int32_t backend,
                       uint64_t* forward, uint64_t* backward) {
   // ccem.cpp:207-235

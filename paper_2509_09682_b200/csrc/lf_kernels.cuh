@@ -124,6 +124,9 @@ int ce_backward(int dtype, const void* X, const void* E, const int64_t* targets,
 // ---- negative sampler (lf_sampler.cu) ----
 int sample_uniform(const int64_t* positives, int64_t n, int64_t ns, int64_t catalog,
                    uint64_t seed, int retry_cap, int64_t* inds, cudaStream_t st);
+int sample_popularity(const int64_t* positives, int64_t n, int64_t ns, const int64_t* counts,
+                      int64_t catalog, double exponent, uint64_t seed, int retry_cap, int64_t* inds,
+                      cudaStream_t st);
 
 // ---- validation (lf_ccem.cu) ----
 int validate_targets(const int64_t* targets, int64_t n, int64_t v, cudaStream_t st);

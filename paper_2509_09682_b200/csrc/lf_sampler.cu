@@ -10,6 +10,7 @@
 // SplitMix64 is a counter generator: draw k of a stream is mix(s + (k+1) g),
 // so a warp evaluates 32 consecutive draws of one row at once and places the
 // accepted ones with a ballot prefix count — same sequence as the serial loop.
+#include <algorithm>
 #include <cstdint>
 #include <string>
 
@@ -104,7 +105,162 @@ __global__ void first_bad_positive(const int64_t* __restrict__ pos, int64_t n, i
     if (pos[i] < 0 || pos[i] >= catalog) atomicMin(first, static_cast<unsigned long long>(i));
 }
 
+// ---- popularity sampler (sampler.cpp:77-127) ----
+// Weights and their running sum.  exponent == 1: weights are the integer
+// counts, every partial sum is an exact integer in double, so a blocked scan
+// gives the reference's bits; otherwise a single thread keeps the reference's
+// summation order (pow itself may differ from glibc's in the last ulp).
+// flags[0] = first negative count, flags[1] = 1 if the total is not > 0.
+__global__ void pop_cumulative(const int64_t* __restrict__ counts, int64_t catalog, double exponent,
+                               double* __restrict__ cum, unsigned long long* __restrict__ flags,
+                               double* __restrict__ total) {
+  __shared__ double seg[1024];
+  const int T = blockDim.x;
+  const int64_t len = ceil_div(catalog, T);
+  const int64_t lo = threadIdx.x * len, hi = min(catalog, lo + len);
+  double run = 0.0;
+  for (int64_t v = lo; v < hi; ++v) {
+    const int64_t c = counts[v];
+    if (c < 0) atomicMin(flags, static_cast<unsigned long long>(v));
+    run += exponent == 1.0 ? static_cast<double>(c) : pow(static_cast<double>(c), exponent);
+    cum[v] = run;
+  }
+  seg[threadIdx.x] = run;
+  __syncthreads();
+  if (threadIdx.x == 0) {  // exclusive scan of the segment sums, in order
+    double acc = 0.0;
+    for (int t = 0; t < T; ++t) {
+      const double x = seg[t];
+      seg[t] = acc;
+      acc += x;
+    }
+    *total = acc;
+    if (!(acc > 0.0)) flags[1] = 1;
+  }
+  __syncthreads();
+  const double off = seg[threadIdx.x];
+  if (off != 0.0)
+    for (int64_t v = lo; v < hi; ++v) cum[v] += off;
+}
+
+__device__ __forceinline__ int64_t upper_bound(const double* __restrict__ cum, int64_t n, double u) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = lo + ((hi - lo) >> 1);
+    if (!(u < cum[mid])) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// Warp per row, 32 consecutive draws at once (one uniform() per attempt);
+// every rejected draw (index past the table, or the positive) is one failed
+// attempt of the current slot, retry_cap in a row is an error.
+__global__ void __launch_bounds__(256) sample_popularity_rows(
+    const int64_t* __restrict__ pos, int64_t n, int64_t ns, const double* __restrict__ cum,
+    int64_t catalog, const double* __restrict__ total, uint64_t seed, int retry_cap,
+    int64_t* __restrict__ inds, unsigned long long* __restrict__ status) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (row >= n) return;
+  const int64_t w = ns + 1;
+  const int64_t p = pos[row];
+  const double running = *total;
+  int64_t* out = inds + row * w;
+  if (lane == 0) out[0] = p;
+  const uint64_t s = mix64(seed + kGolden * static_cast<uint64_t>(row + 1));
+  int64_t filled = 0;
+  int run = 0;
+  const unsigned lt = (1u << lane) - 1u;
+  for (uint64_t k0 = 0; filled < ns; k0 += 32) {
+    const uint64_t z = mix64(s + (k0 + lane + 1) * kGolden);
+    const double u = static_cast<double>(z >> 11) * 0x1.0p-53 * running;  // rng.hpp:41
+    const int64_t v = upper_bound(cum, catalog, u);
+    const bool acc = v < catalog && v != p;
+    const unsigned am = __ballot_sync(0xffffffffu, acc);
+    const unsigned fm = ~am;
+    if (fm) {  // walk the batch in order (rare)
+      int64_t f = filled;
+      int r = run;
+      bool failed = false;
+      for (int b = 0; b < 32 && f < ns; ++b) {
+        if ((am >> b) & 1u) {
+          ++f;
+          r = 0;
+        } else if (++r >= retry_cap) {
+          failed = true;
+          break;
+        }
+      }
+      if (failed) {
+        if (lane == 0) atomicMin(status, static_cast<unsigned long long>(row));
+        return;
+      }
+      run = r;
+    } else {
+      run = 0;
+    }
+    if (acc) {
+      const int64_t slot = filled + __popc(am & lt) + 1;
+      if (slot <= ns) out[slot] = v;
+    }
+    filled += __popc(am);
+  }
+}
+
 }  // namespace
+
+int sample_popularity(const int64_t* positives, int64_t n, int64_t ns, const int64_t* counts,
+                      int64_t catalog, double exponent, uint64_t seed, int retry_cap, int64_t* inds,
+                      cudaStream_t st) {
+  if (catalog <= 0) return fail(LF_EINVAL, "sample_popularity: empty popularity table");
+  if (n < 0 || ns < 0) return fail(LF_EINVAL, "sample_popularity: negative extent");
+  Scratch flag, cum, tot;
+  int rc = flag.alloc(4 * sizeof(unsigned long long), st);
+  if (!rc) rc = cum.alloc(sizeof(double) * catalog, st);
+  if (!rc) rc = tot.alloc(sizeof(double), st);
+  if (rc) return rc;
+  LF_CUDA(cudaMemsetAsync(flag.ptr, 0xFF, sizeof(unsigned long long), st));
+  LF_CUDA(cudaMemsetAsync(flag.as<unsigned long long>() + 1, 0, sizeof(unsigned long long), st));
+  LF_CUDA(cudaMemsetAsync(flag.as<unsigned long long>() + 2, 0xFF, 2 * sizeof(unsigned long long), st));
+  unsigned long long* f = flag.as<unsigned long long>();
+  pop_cumulative<<<1, exponent == 1.0 ? 1024 : 1, 0, st>>>(counts, catalog, exponent, cum.as<double>(), f,
+                                                            tot.as<double>());
+  LF_LAUNCHED();
+  first_bad_positive<<<static_cast<unsigned>(std::min<int64_t>(std::max<int64_t>(ceil_div(n, 256), 1), 1024)),
+                       256, 0, st>>>(positives, n, catalog, f + 2);
+  LF_LAUNCHED();
+  unsigned long long h[3];
+  LF_CUDA(cudaMemcpyAsync(h, f, sizeof(h), cudaMemcpyDeviceToHost, st));
+  LF_CUDA(cudaStreamSynchronize(st));
+  if (h[0] != ~0ull) {  // PopularityTable::FromCounts (sampler.cpp:30-42)
+    int64_t c = 0;
+    LF_CUDA(cudaMemcpy(&c, counts + h[0], sizeof(c), cudaMemcpyDeviceToHost));
+    return fail(LF_EINVAL, "PopularityTable: item " + std::to_string(h[0]) + " has negative count " +
+                               std::to_string(c));
+  }
+  if (h[2] != ~0ull) {  // sampler.cpp:12-20
+    int64_t bad = 0;
+    LF_CUDA(cudaMemcpy(&bad, positives + h[2], sizeof(bad), cudaMemcpyDeviceToHost));
+    return fail(LF_EINVAL, "sampler: row " + std::to_string(h[2]) + " positive " + std::to_string(bad) +
+                               " outside catalog of " + std::to_string(catalog));
+  }
+  if (ns > catalog - 1)
+    return fail(LF_EINVAL, "sample_popularity: ns = " + std::to_string(ns) +
+                               " exceeds catalog minus positive (" + std::to_string(catalog - 1) + ")");
+  if (h[1]) return fail(LF_EINVAL, "sample_popularity: all item weights are zero");
+  if (n == 0) return LF_OK;
+  sample_popularity_rows<<<static_cast<unsigned>(ceil_div(n, 8)), 256, 0, st>>>(
+      positives, n, ns, cum.as<double>(), catalog, tot.as<double>(), seed, retry_cap, inds, f + 3);
+  LF_LAUNCHED();
+  unsigned long long bad = 0;
+  LF_CUDA(cudaMemcpyAsync(&bad, f + 3, sizeof(bad), cudaMemcpyDeviceToHost, st));
+  LF_CUDA(cudaStreamSynchronize(st));
+  if (bad != ~0ull)  // sampler.cpp:22-27
+    return fail(LF_ERUNTIME, "sampler: row " + std::to_string(bad) + " exhausted " + std::to_string(retry_cap) +
+                                 " rejection retries; the distribution leaves no valid negative");
+  return LF_OK;
+}
 
 int sample_uniform(const int64_t* positives, int64_t n, int64_t ns, int64_t catalog,
                    uint64_t seed, int retry_cap, int64_t* inds, cudaStream_t st) {

@@ -79,6 +79,7 @@ def main():
     eval_fixtures()
     adam_fixtures()
     encoder_fixtures()
+    popularity_fixtures()
     print("wrote", sorted(f for f in os.listdir(HERE) if f.endswith(".npz")))
 
 
@@ -130,8 +131,28 @@ def encoder_fixtures():
                         win_off=win_off, dh=dh, **r)
 
 
+def popularity_fixtures():
+    """sample_popularity (sampler.cpp:77-127) run by the reference: skewed
+    counts with zero-weight items, exponents 1 and 0.75."""
+    g = np.random.default_rng(31)
+    out = {}
+    for c, (cat, n, ns, exp, seed) in enumerate(((2000, 64, 31, 1.0, 0xB2000005), (500, 40, 9, 0.75, 7),
+                                                 (12, 30, 11, 1.0, 11))):
+        counts = (g.zipf(1.3, cat) % 1000).astype(np.int64)
+        counts[g.integers(0, cat, cat // 4)] = 0
+        pos = g.integers(0, cat, n).astype(np.int64)
+        counts[pos] = np.maximum(counts[pos], 0)
+        out.update({f"{c}_counts": counts, f"{c}_pos": pos, f"{c}_ns": np.int64(ns),
+                    f"{c}_exp": np.float64(exp), f"{c}_seed": np.uint64(seed),
+                    f"{c}_inds": ob.ref_sample_popularity(pos, ns, counts, seed, exp)})
+    out["count"] = np.int64(3)
+    np.savez_compressed(os.path.join(HERE, "popularity_ref.npz"), **out)
+
+
 if __name__ == "__main__":
-    if sys.argv[1:] == ["encoder"]:
+    if sys.argv[1:] == ["popularity"]:
+        popularity_fixtures()
+    elif sys.argv[1:] == ["encoder"]:
         encoder_fixtures()
     elif sys.argv[1:] == ["adam"]:
         adam_fixtures()

@@ -82,6 +82,9 @@ def orc():
                                        _f32p, _i64p, _i64p]
         L.orc_encoder_backward.argtypes = [_i64p, _i64p, _sz, _f32p, _sz, _sz, _f64p, _f64p, _i64p,
                                            _sz, _f64p, _f64p, _f64p, _f64p]
+        L.orc_sample_popularity.argtypes = [_i64p, _sz, _sz, _i64p, _sz, C.c_double, C.c_uint64,
+                                            C.c_int, _i64p]
+        L.orc_sample_popularity.restype = C.c_int
         L.orc_adam_apply.argtypes = [_f32p, _f64p, _f64p, _f64p, _sz, C.c_double, C.c_double,
                                      C.c_double, C.c_double, C.c_uint64]
         _orc = L
@@ -124,6 +127,8 @@ def ref():
                                          C.POINTER(C.c_uint64)]
         L.ref_eval_instance.argtypes = [_sz, _sz, C.c_uint64, _sz, _sz, _i64p, _i64p, _sz, _i64p,
                                         C.c_int, _f64p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.ref_sample_popularity.argtypes = [_i64p, _sz, _sz, _i64p, _sz, C.c_double, C.c_uint64,
+                                            _i64p]
         L.ref_adam_steps.argtypes = [_sz, _sz, C.c_uint64, C.c_double, C.c_double, C.c_double,
                                      C.c_double, C.c_int, _f64p, _f32p]
         L.ref_encoder.argtypes = [_sz, _sz, _f32p, _f32p, _f32p, _i64p, _i64p, _sz, _f64p, _f64p,
@@ -190,6 +195,29 @@ def sample_uniform(positives: np.ndarray, ns: int, catalog: int, seed: int, retr
                                   retry_cap, inds)
     if rc != 0:
         raise RuntimeError("sampler: retry cap exhausted")
+    return inds
+
+
+def sample_popularity(positives, ns, counts, seed, exponent=1.0, retry_cap=100):
+    n = len(positives)
+    inds = np.empty((n, 1 + ns), np.int64)
+    rc = orc().orc_sample_popularity(np.ascontiguousarray(positives, np.int64), n, ns,
+                                     np.ascontiguousarray(counts, np.int64), len(counts), exponent,
+                                     seed, retry_cap, inds)
+    if rc == -2:
+        raise ValueError("sample_popularity: all item weights are zero")
+    if rc:
+        raise RuntimeError("sampler: retry cap exhausted")
+    return inds
+
+
+def ref_sample_popularity(positives, ns, counts, seed, exponent=1.0):
+    L = ref()
+    n = len(positives)
+    inds = np.empty((n, 1 + ns), np.int64)
+    _chk(L.ref_sample_popularity(np.ascontiguousarray(positives, np.int64), n, ns,
+                                 np.ascontiguousarray(counts, np.int64), len(counts), exponent, seed,
+                                 inds), L)
     return inds
 
 

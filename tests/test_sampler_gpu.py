@@ -56,3 +56,42 @@ def test_feeds_ccem_directly(lf):
     Eh, Ch = X.float().cpu().numpy(), E.float().cpu().numpy().T.copy()
     loss, _, _ = ob.ccem_forward(Eh, Ch, inds.cpu().numpy())
     assert abs(float(out.loss) - loss) <= 1e-2 * max(1.0, abs(loss))
+
+
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def test_popularity_matches_reference_golden(lf):
+    g = np.load(os.path.join(GOLDEN, "popularity_ref.npz"))
+    for c in range(int(g["count"])):
+        if float(g[f"{c}_exp"]) != 1.0:
+            continue  # device pow may differ from glibc's in the last ulp (documented)
+        got = lf.sample_popularity(torch.from_numpy(g[f"{c}_pos"]).cuda(), int(g[f"{c}_ns"]),
+                                   torch.from_numpy(g[f"{c}_counts"]), int(g[f"{c}_seed"])).cpu().numpy()
+        assert np.array_equal(got, g[f"{c}_inds"])
+
+
+@pytest.mark.parametrize("cat,n,ns,seed", [(1_000_000, 2048, 512, 3), (50, 300, 49, 9), (2, 10, 1, 1)])
+def test_popularity_matches_oracle(lf, cat, n, ns, seed):
+    rng = np.random.default_rng(seed)
+    counts = rng.integers(0, 100, cat).astype(np.int64)
+    pos = rng.integers(0, cat, n).astype(np.int64)
+    counts[pos] += 1  # keep positives drawable; other items may have weight 0
+    if cat == 2:
+        counts[:] = 5
+    want = ob.sample_popularity(pos, ns, counts, seed)
+    got = lf.sample_popularity(torch.from_numpy(pos).cuda(), ns, torch.from_numpy(counts), seed).cpu().numpy()
+    assert np.array_equal(got, want)
+
+
+def test_popularity_errors(lf):
+    pos = torch.tensor([0, 1], device="cuda")
+    with pytest.raises(ValueError, match="all item weights are zero"):
+        lf.sample_popularity(pos, 1, torch.zeros(5, dtype=torch.int64), 1)
+    with pytest.raises(ValueError, match="item 2 has negative count -3"):
+        lf.sample_popularity(pos, 1, torch.tensor([1, 1, -3, 1]), 1)
+    with pytest.raises(ValueError, match="exceeds catalog minus positive"):
+        lf.sample_popularity(pos, 4, torch.ones(4, dtype=torch.int64), 1)
+    with pytest.raises(RuntimeError, match="rejection retries"):
+        # only the positive has weight: every draw is rejected
+        lf.sample_popularity(torch.tensor([0], device="cuda"), 1, torch.tensor([5, 0, 0]), 1, retry_cap=7)
