@@ -197,6 +197,18 @@ LF_API int lf_ce_backward(const void* d_X, const void* d_E, const int64_t* d_tar
                           double upstream, int64_t n, int64_t d, int64_t v,
                           const lf_cce_config* cfg, void* d_dX, void* d_dE, void* stream);
 
+/* Replace lseforge::ce_sampled_forward / ce_sampled_backward (losses.cpp:142-221):
+ * the materialising CE- baseline (backend "cem").  The n x w candidate logits
+ * ARE written to device memory (and G over them in the backward); dE is
+ * scattered with atomics (duplicate candidates accumulate).  Same outputs and
+ * layouts as lf_ccem_forward / lf_ccem_backward (d_inds: n x w, slot 0 = positive). */
+LF_API int lf_cem_forward(const void* d_X, const void* d_E, const int64_t* d_inds, int64_t n,
+                          int64_t d, int64_t v, int64_t w, const lf_cce_config* cfg, double* d_lse,
+                          double* d_pos, double* d_loss, void* stream);
+LF_API int lf_cem_backward(const void* d_X, const void* d_E, const int64_t* d_inds, double upstream,
+                           int64_t n, int64_t d, int64_t v, int64_t w, const lf_cce_config* cfg,
+                           void* d_dX, void* d_dE, void* stream);
+
 /* ------------------------------------------------------- negative sampler -- */
 /* Replaces lseforge::sample_uniform (sampler.hpp, sampler.cpp:44-75) with a
  * device restatement that produces the SAME indices: row i draws from

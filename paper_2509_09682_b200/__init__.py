@@ -11,7 +11,8 @@ from .accountant import MemAccountant, Report, ScalarKind
 from .cce import CceBackwardResult, CceConfig, cce_backward, cce_forward, kFp16MinPositive
 from .ccem import (Backend, FlopEstimate, backend_is_sampled, ccem_backward, ccem_backward_rows,
                    ccem_forward, estimate_flops)
-from .losses import GradPair, LossOutput, ce_full_backward, ce_full_forward, validate_loss_inputs
+from .losses import (GradPair, LossOutput, ce_full_backward, ce_full_forward, ce_sampled_backward,
+                     ce_sampled_forward, validate_loss_inputs)
 from .adam import AdamConfig, DeviceAdam
 from .metrics import EvalSummary, evaluate
 from .sampler import sample_popularity, sample_uniform

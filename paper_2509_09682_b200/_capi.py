@@ -29,6 +29,7 @@ EXPORTS = (
     "lf_evaluate", "lf_adam_step", "lf_encode_batch", "lf_encoder_backward", "lf_peer_alloc",
     "lf_peer_open", "lf_peer_close", "lf_peer_free", "lf_peer_barrier", "lf_peer_sum",
     "lf_cce_forward_partial_peer", "lf_cce_backward_shard_peer", "lf_sample_popularity",
+    "lf_cem_forward", "lf_cem_backward",
 )
 KERNEL_KINDS = ("cce_fwd", "cce_bwd_dx", "cce_bwd_de", "cce_simt", "ccem_fwd", "ccem_bwd", "aux",
                 "eval")
@@ -109,6 +110,8 @@ def lib():
                                                  cfgp, vp, stp, vp, C.c_int32, C.c_int32, i64, vp]
         L.lf_sample_popularity.argtypes = [vp, i64, i64, vp, i64, C.c_double, C.c_uint64, C.c_int32,
                                            vp, vp]
+        L.lf_cem_forward.argtypes = [vp, vp, vp, i64, i64, i64, i64, cfgp, dp, dp, dp, vp]
+        L.lf_cem_backward.argtypes = [vp, vp, vp, C.c_double, i64, i64, i64, i64, cfgp, vp, vp, vp]
         L.lf_launch_count.restype = C.c_uint64
         L.lf_profile_enable.argtypes = [C.c_int]
         L.lf_profile_enable.restype = C.c_int
@@ -124,7 +127,8 @@ def lib():
                      "lf_evaluate", "lf_adam_step", "lf_encode_batch", "lf_encoder_backward",
                      "lf_peer_alloc", "lf_peer_open", "lf_peer_close", "lf_peer_free",
                      "lf_peer_barrier", "lf_peer_sum", "lf_cce_forward_partial_peer",
-                     "lf_cce_backward_shard_peer", "lf_sample_popularity"):
+                     "lf_cce_backward_shard_peer", "lf_sample_popularity", "lf_cem_forward",
+                     "lf_cem_backward"):
             getattr(L, name).restype = C.c_int
         if L.lf_abi_version() != 1:
             raise ImportError("liblseforge_b200.so ABI mismatch")

@@ -450,6 +450,30 @@ int lf_ce_backward(const void* d_X, const void* d_E, const int64_t* d_targets, d
                      d_dE, as_stream(stream));
 }
 
+int lf_cem_forward(const void* d_X, const void* d_E, const int64_t* d_inds, int64_t n, int64_t d,
+                   int64_t v, int64_t w, const lf_cce_config* cfg, double* d_lse, double* d_pos,
+                   double* d_loss, void* stream) {
+  int rc = check_cfg(cfg);
+  if (rc) return rc;
+  if (n <= 0) return fail(LF_EINVAL, "loss: embedding matrix has zero rows; the mean loss is undefined");
+  if (w < 1) return fail(LF_EINVAL, "NegIndexMatrix: width must be at least 1 (the positive slot)");
+  if (d <= 0 || v <= 0) return fail(LF_EINVAL, "loss: empty embedding or catalog");
+  return cem_forward(cfg->dtype, d_X, d_E, d_inds, n, static_cast<int>(d), w, d_lse, d_pos, d_loss,
+                     as_stream(stream));
+}
+
+int lf_cem_backward(const void* d_X, const void* d_E, const int64_t* d_inds, double upstream, int64_t n,
+                    int64_t d, int64_t v, int64_t w, const lf_cce_config* cfg, void* d_dX, void* d_dE,
+                    void* stream) {
+  int rc = check_cfg(cfg);
+  if (rc) return rc;
+  if (n <= 0) return fail(LF_EINVAL, "loss: embedding matrix has zero rows; the mean loss is undefined");
+  if (w < 1) return fail(LF_EINVAL, "NegIndexMatrix: width must be at least 1 (the positive slot)");
+  if (d <= 0 || v <= 0) return fail(LF_EINVAL, "loss: empty embedding or catalog");
+  return cem_backward(cfg->dtype, d_X, d_E, d_inds, upstream, n, static_cast<int>(d), v, w, d_dX, d_dE,
+                      as_stream(stream));
+}
+
 int lf_sample_uniform(const int64_t* d_positives, int64_t n, int64_t ns, int64_t catalog,
                       uint64_t seed, int32_t retry_cap, int64_t* d_inds, void* stream) {
   if (retry_cap < 1) return fail(LF_EINVAL, "sample_uniform: retry_cap must be >= 1");

@@ -5,7 +5,9 @@
 // the softmax / log-sum-exp are row kernels over it, and the gradients are two
 // more GEMMs over a materialised bf16 coefficient matrix G.  Used to reproduce
 // the paper's CE-vs-CCE memory and time comparisons on B200;
-// peak scratch is n * v * 6 bytes.
+// peak scratch is n * v * 6 bytes.  Also the sampled variant ce_sampled_forward /
+// backward (losses.cpp:142-221): the n x (1+K) candidate logits written to HBM,
+// G written over them, dE scattered with atomics.
 #include <cublas_v2.h>
 #include <cuda_bf16.h>
 
@@ -98,7 +100,145 @@ __global__ void softmax_grad(const T* __restrict__ logits, int64_t n, int64_t v,
 
 int grid_for(int64_t count) { return static_cast<int>(std::min<int64_t>(ceil_div(count, 256), 148 * 32)); }
 
+// ---- materialising sampled CE (losses.cpp:142-221) ----
+template <class TI>
+__device__ __forceinline__ double to_d(TI x) { return static_cast<double>(x); }
+template <>
+__device__ __forceinline__ double to_d<__nv_bfloat16>(__nv_bfloat16 x) { return static_cast<double>(__bfloat162float(x)); }
+
+// Warp per row: the n x w candidate logits are WRITTEN (this is the baseline).
+template <class TI, class T>
+__global__ void __launch_bounds__(256) cem_logits(const TI* __restrict__ X, const TI* __restrict__ E,
+                                                 const int64_t* __restrict__ inds, int64_t n, int D,
+                                                 int64_t w, T* __restrict__ logits) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (row >= n) return;
+  for (int64_t s = lane; s < w; s += 32) {
+    const TI* er = E + inds[row * w + s] * D;
+    const TI* xr = X + row * D;
+    T acc = 0;
+    for (int k = 0; k < D; ++k) acc += static_cast<T>(to_d(xr[k])) * static_cast<T>(to_d(er[k]));
+    logits[row * w + s] = acc;
+  }
+}
+
+// Warp per row: lse, pos (slot 0); optionally G = (softmax - [s == 0]) * scale
+// written back over the logits.
+template <class T>
+__global__ void __launch_bounds__(256) cem_rows(T* __restrict__ logits, int64_t n, int64_t w,
+                                               double* __restrict__ lse, double* __restrict__ pos,
+                                               double scale, bool grad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (row >= n) return;
+  T* o = logits + row * w;
+  T mx = -INFINITY;
+  for (int64_t s = lane; s < w; s += 32) mx = max(mx, o[s]);
+  for (int off = 16; off > 0; off >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  double sum = 0.0;
+  for (int64_t s = lane; s < w; s += 32) sum += exp(static_cast<double>(o[s] - mx));
+  for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+  const double l = static_cast<double>(mx) + log(sum);
+  if (!grad) {
+    if (lane == 0) {
+      lse[row] = l;
+      pos[row] = static_cast<double>(o[0]);
+    }
+    return;
+  }
+  for (int64_t s = lane; s < w; s += 32) {
+    const double g = exp(static_cast<double>(o[s]) - l) * scale;
+    o[s] = static_cast<T>(s == 0 ? g - scale : g);
+  }
+}
+
+// dX row = sum_s G[s] E[inds[s]] (warp per row, lanes over k); dE scattered
+// with atomics (duplicates accumulate, losses.cpp:211-218).
+template <class TI, class T>
+__global__ void __launch_bounds__(256) cem_grads(const TI* __restrict__ X, const TI* __restrict__ E,
+                                                const int64_t* __restrict__ inds, const T* __restrict__ G,
+                                                int64_t n, int D, int64_t w, T* __restrict__ dX,
+                                                T* __restrict__ dE) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (row >= n) return;
+  for (int k = lane; k < D; k += 32) {
+    T acc = 0;
+    const T xk = static_cast<T>(to_d(X[row * D + k]));
+    for (int64_t s = 0; s < w; ++s) {
+      const int64_t item = inds[row * w + s];
+      const T g = G[row * w + s];
+      acc += g * static_cast<T>(to_d(E[item * D + k]));
+      atomicAdd(dE + item * D + k, g * xk);
+    }
+    dX[row * D + k] = acc;
+  }
+}
+
 }  // namespace
+
+int cem_forward(int dtype, const void* X, const void* E, const int64_t* inds, int64_t n, int D, int64_t w,
+                double* lse, double* pos, double* loss, cudaStream_t st) {
+  const bool f64 = dtype == LF_F64;
+  Scratch logits;
+  int rc = logits.alloc((f64 ? 8 : 4) * n * w, st);
+  if (rc) return rc;
+  const unsigned blocks = static_cast<unsigned>(ceil_div(n, 8));
+  if (f64) {
+    cem_logits<double, double><<<blocks, 256, 0, st>>>(static_cast<const double*>(X), static_cast<const double*>(E),
+                                                      inds, n, D, w, logits.as<double>());
+    cem_rows<double><<<blocks, 256, 0, st>>>(logits.as<double>(), n, w, lse, pos, 0.0, false);
+  } else if (dtype == LF_F32) {
+    cem_logits<float, float><<<blocks, 256, 0, st>>>(static_cast<const float*>(X), static_cast<const float*>(E),
+                                                    inds, n, D, w, logits.as<float>());
+    cem_rows<float><<<blocks, 256, 0, st>>>(logits.as<float>(), n, w, lse, pos, 0.0, false);
+  } else {
+    cem_logits<__nv_bfloat16, float><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(X),
+                                                            static_cast<const __nv_bfloat16*>(E), inds, n, D,
+                                                            w, logits.as<float>());
+    cem_rows<float><<<blocks, 256, 0, st>>>(logits.as<float>(), n, w, lse, pos, 0.0, false);
+  }
+  LF_LAUNCHED();
+  return launch_mean_loss(lse, pos, n, loss, st);
+}
+
+int cem_backward(int dtype, const void* X, const void* E, const int64_t* inds, double upstream, int64_t n,
+                 int D, int64_t v, int64_t w, void* dX, void* dE, cudaStream_t st) {
+  const bool f64 = dtype == LF_F64;
+  Scratch logits;
+  int rc = logits.alloc((f64 ? 8 : 4) * n * w, st);
+  if (rc) return rc;
+  LF_CUDA(cudaMemsetAsync(dE, 0, (f64 ? 8 : 4) * v * D, st));
+  const double scale = upstream / static_cast<double>(n);
+  const unsigned blocks = static_cast<unsigned>(ceil_div(n, 8));
+  if (f64) {
+    cem_logits<double, double><<<blocks, 256, 0, st>>>(static_cast<const double*>(X), static_cast<const double*>(E),
+                                                      inds, n, D, w, logits.as<double>());
+    cem_rows<double><<<blocks, 256, 0, st>>>(logits.as<double>(), n, w, nullptr, nullptr, scale, true);
+    cem_grads<double, double><<<blocks, 256, 0, st>>>(static_cast<const double*>(X), static_cast<const double*>(E),
+                                                     inds, logits.as<double>(), n, D, w,
+                                                     static_cast<double*>(dX), static_cast<double*>(dE));
+  } else if (dtype == LF_F32) {
+    cem_logits<float, float><<<blocks, 256, 0, st>>>(static_cast<const float*>(X), static_cast<const float*>(E),
+                                                    inds, n, D, w, logits.as<float>());
+    cem_rows<float><<<blocks, 256, 0, st>>>(logits.as<float>(), n, w, nullptr, nullptr, scale, true);
+    cem_grads<float, float><<<blocks, 256, 0, st>>>(static_cast<const float*>(X), static_cast<const float*>(E), inds,
+                                                   logits.as<float>(), n, D, w, static_cast<float*>(dX),
+                                                   static_cast<float*>(dE));
+  } else {
+    cem_logits<__nv_bfloat16, float><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(X),
+                                                            static_cast<const __nv_bfloat16*>(E), inds, n, D,
+                                                            w, logits.as<float>());
+    cem_rows<float><<<blocks, 256, 0, st>>>(logits.as<float>(), n, w, nullptr, nullptr, scale, true);
+    cem_grads<__nv_bfloat16, float><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(X),
+                                                           static_cast<const __nv_bfloat16*>(E), inds,
+                                                           logits.as<float>(), n, D, w, static_cast<float*>(dX),
+                                                           static_cast<float*>(dE));
+  }
+  LF_LAUNCHED();
+  return LF_OK;
+}
 
 int ce_forward(int dtype, const void* X, const void* E, const int64_t* targets, int64_t n, int D,
                int64_t v, double* lse, double* pos, double* loss, cudaStream_t st) {

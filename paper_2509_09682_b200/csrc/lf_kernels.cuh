@@ -120,6 +120,10 @@ int ce_forward(int dtype, const void* X, const void* E, const int64_t* targets, 
                int64_t v, double* lse, double* pos, double* loss, cudaStream_t st);
 int ce_backward(int dtype, const void* X, const void* E, const int64_t* targets, double upstream,
                 int64_t n, int D, int64_t v, void* dX, void* dE, cudaStream_t st);
+int cem_forward(int dtype, const void* X, const void* E, const int64_t* inds, int64_t n, int D, int64_t w,
+                double* lse, double* pos, double* loss, cudaStream_t st);
+int cem_backward(int dtype, const void* X, const void* E, const int64_t* inds, double upstream, int64_t n,
+                 int D, int64_t v, int64_t w, void* dX, void* dE, cudaStream_t st);
 
 // ---- negative sampler (lf_sampler.cu) ----
 int sample_uniform(const int64_t* positives, int64_t n, int64_t ns, int64_t catalog,

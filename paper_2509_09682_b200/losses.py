@@ -117,3 +117,38 @@ def ce_full_backward(X: torch.Tensor, E: torch.Tensor, x: torch.Tensor, upstream
                                            float(upstream), n, d, v, C.byref(c), dX.data_ptr(),
                                            dE.data_ptr(), _stream(X)))
     return GradPair(dX, dE)
+
+
+def ce_sampled_forward(X: torch.Tensor, E: torch.Tensor, inds: torch.Tensor) -> LossOutput:
+    """losses.cpp:142-173 — the MATERIALISING sampled baseline ("cem"): the
+    n x (1+K) candidate logits are written to device memory."""
+    import ctypes as C
+    n, d = X.shape
+    v = E.shape[0]
+    I = inds.to(torch.int64).contiguous()
+    lse = torch.empty(n, dtype=torch.float64, device=X.device)
+    pos = torch.empty(n, dtype=torch.float64, device=X.device)
+    loss = torch.empty((), dtype=torch.float64, device=X.device)
+    c = _capi.CceConfigC(0.0, lf_dtype(X), 0)
+    _capi.check(_capi.lib().lf_cem_forward(X.contiguous().data_ptr(), E.contiguous().data_ptr(),
+                                           I.data_ptr(), n, d, v, I.shape[1], C.byref(c),
+                                           lse.data_ptr(), pos.data_ptr(), loss.data_ptr(), _stream(X)))
+    return LossOutput(loss, pos, lse)
+
+
+def ce_sampled_backward(X: torch.Tensor, E: torch.Tensor, inds: torch.Tensor,
+                        upstream: float = 1.0) -> GradPair:
+    """losses.cpp:175-221 — materialised logits and coefficients, dE scattered
+    with atomics (duplicate candidates accumulate)."""
+    import ctypes as C
+    n, d = X.shape
+    v = E.shape[0]
+    I = inds.to(torch.int64).contiguous()
+    gd = grad_dtype(X)
+    dX = torch.empty((n, d), dtype=gd, device=X.device)
+    dE = torch.empty((v, d), dtype=gd, device=X.device)
+    c = _capi.CceConfigC(0.0, lf_dtype(X), 0)
+    _capi.check(_capi.lib().lf_cem_backward(X.contiguous().data_ptr(), E.contiguous().data_ptr(),
+                                            I.data_ptr(), float(upstream), n, d, v, I.shape[1],
+                                            C.byref(c), dX.data_ptr(), dE.data_ptr(), _stream(X)))
+    return GradPair(dX, dE)

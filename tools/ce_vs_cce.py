@@ -61,3 +61,25 @@ for n, d, v in [(51200, 64, 100_000), (51200, 64, 200_000), (51200, 64, 400_000)
     row["speedup"] = row["ce_ms"] / row["cce_ms"]
     row["memory_reduction"] = 1 - row["cce_peak_gb"] / row["ce_peak_gb"]
     print(json.dumps(row), flush=True)
+
+# the sampled pair: materialising CE- (losses.cpp:142-221) vs fused CCE- at cfg3
+for n, d, v, K in [(51200, 64, 1_000_000, 512), (51200, 64, 1_000_000, 2048)]:
+    g = torch.Generator(device="cuda").manual_seed(2)
+    X = (torch.rand(n, d, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    E = (torch.rand(v, d, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    I = torch.randint(0, v, (n, 1 + K), device="cuda", generator=g)
+
+    def cem():
+        lf.ce_sampled_forward(X, E, I)
+        lf.ce_sampled_backward(X, E, I, 1.0)
+
+    def ccem():
+        o = lf.ccem_forward(X, E, I, validate=False)
+        lf.ccem_backward(X, E, I, o.lse, 1.0, validate=False)
+
+    row = {"sampled": True, "n": n, "d": d, "v": v, "K": K, "logits_gb_fp32": n * (1 + K) * 4 / 1e9,
+           "cem_ms": timed(cem), "ccem_ms": timed(ccem), "cem_peak_gb": peak_gb(cem),
+           "ccem_peak_gb": peak_gb(ccem)}
+    row["speedup"] = row["cem_ms"] / row["ccem_ms"]
+    row["memory_reduction"] = 1 - row["ccem_peak_gb"] / row["cem_peak_gb"]
+    print(json.dumps(row), flush=True)
