@@ -545,8 +545,19 @@ int ccem_forward(int dtype, const void* X, const void* E, const int64_t* inds, i
 // Sort (item, key) pairs stably by item; returns sorted keys (slot ids) and
 // per-item offsets (v+1).
 // Segment offsets of the entries grouped by item: item_off[v + 1].
+__global__ void max_count(const uint32_t* __restrict__ counts, int64_t v, uint32_t* __restrict__ out) {
+  uint32_t m = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < v;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    m = max(m, counts[i]);
+  for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+// Per-item segment offsets; with d_max, also the longest segment (*d_max must
+// be zeroed by the caller).
 static int group_offsets(const int64_t* inds, int64_t count, int64_t v, Scratch& item_off,
-                         cudaStream_t st) {
+                         cudaStream_t st, uint32_t* d_max = nullptr) {
   Scratch counts;
   int rc = counts.alloc(sizeof(uint32_t) * (v + 1), st);
   if (!rc) rc = item_off.alloc(sizeof(uint32_t) * (v + 1), st);
@@ -555,7 +566,19 @@ static int group_offsets(const int64_t* inds, int64_t count, int64_t v, Scratch&
   item_hist<<<std::min<int64_t>(ceil_div(count, 256), 8 * num_sms()), 256, 0, st>>>(
       inds, count, counts.as<uint32_t>());
   LF_LAUNCHED();
+  if (d_max) {
+    max_count<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(v, 256), 4 * num_sms())), 256, 0, st>>>(
+        counts.as<uint32_t>(), v, d_max);
+    LF_LAUNCHED();
+  }
   return exclusive_scan(counts.as<uint32_t>(), item_off.as<uint32_t>(), v + 1, st);
+}
+
+// Pinned slot for the longest-segment read-back (one per host thread).
+uint32_t* pinned_u32() {
+  thread_local uint32_t* p = nullptr;
+  if (!p && cudaMallocHost(&p, sizeof(uint32_t)) != cudaSuccess) p = nullptr;
+  return p;
 }
 
 // Entry indices stably grouped by item (LSD radix, kDigitBits per pass).
@@ -616,20 +639,28 @@ __global__ void scatter_by_item(const int64_t* __restrict__ inds, int64_t count,
     grouped[atomicAdd(&cursor[inds[i]], 1u)] = static_cast<uint32_t>(i);
 }
 
-// Ascending bitonic sort of 64 keys held as k[r] at index r*32 + lane.
-__device__ __forceinline__ void warp_sort64(uint32_t (&k)[2]) {
+// Ascending bitonic sort of 32R keys held as k[r] at index r*32 + lane:
+// strides >= 32 pair registers of one lane, shorter ones pair lanes.
+template <int R>
+__device__ __forceinline__ void warp_sort(uint32_t (&k)[R]) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
-  for (int size = 2; size <= 64; size <<= 1) {
+  for (int size = 2; size <= 32 * R; size <<= 1) {
 #pragma unroll
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      if (stride == 32) {
-        const uint32_t lo = min(k[0], k[1]), hi = max(k[0], k[1]);
-        k[0] = lo;
-        k[1] = hi;
+      if (stride >= 32) {
+        const int m = stride / 32;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (r & m) continue;
+          const bool up = ((r * 32 + lane) & size) == 0;
+          const uint32_t lo = min(k[r], k[r | m]), hi = max(k[r], k[r | m]);
+          k[r] = up ? lo : hi;
+          k[r | m] = up ? hi : lo;
+        }
       } else {
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
+        for (int r = 0; r < R; ++r) {
           const int idx = r * 32 + lane;
           const uint32_t other = __shfl_xor_sync(0xffffffffu, k[r], stride);
           const bool up = (idx & size) == 0;
@@ -641,11 +672,11 @@ __device__ __forceinline__ void warp_sort64(uint32_t (&k)[2]) {
   }
 }
 
-// dE for items with at most 64 entries, in entry-index order (the unstable
+// dE for items with at most 32R entries, in entry-index order (the unstable
 // grouping sorted back per segment), four X rows in flight, partial sums
 // combined in a fixed order.  Longer segments set *long_flag and are left to
-// segment_reduce_long (radix-grouped).
-template <class TX, int D>
+// segment_reduce_vec over the radix grouping.
+template <class TX, int D, int R>
 __global__ void __launch_bounds__(256) segment_reduce_sorted(
     const TX* __restrict__ X, const float* __restrict__ coeff, const uint32_t* __restrict__ grouped,
     const uint32_t* __restrict__ item_off, int64_t v, int64_t w, float* __restrict__ dE,
@@ -655,20 +686,24 @@ __global__ void __launch_bounds__(256) segment_reduce_sorted(
   const int64_t item = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   if (item >= v) return;
   const uint32_t b = item_off[item], L = item_off[item + 1] - b;
-  if (L > 64) {
+  if (L > 32u * R) {
     if (lane == 0) *long_flag = 1u;
     return;
   }
-  uint32_t k[2];
-  k[0] = lane < static_cast<int>(L) ? grouped[b + lane] : 0xffffffffu;
-  k[1] = lane + 32 < static_cast<int>(L) ? grouped[b + 32 + lane] : 0xffffffffu;
-  if (L > 1) warp_sort64(k);
+  uint32_t k[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) k[r] = r * 32 + lane < static_cast<int>(L) ? grouped[b + r * 32 + lane] : 0xffffffffu;
+  if (L > 1) warp_sort<R>(k);
   float acc[DPL];
 #pragma unroll
   for (int i = 0; i < DPL; ++i) acc[i] = 0.f;
   for (uint32_t j0 = 0; j0 < L; j0 += 4) {
     const uint32_t j = j0 + g;
-    const uint32_t key = __shfl_sync(0xffffffffu, j0 < 32 ? k[0] : k[1], static_cast<int>(j & 31));
+    uint32_t src = k[0];
+#pragma unroll
+    for (int r = 1; r < R; ++r)
+      if ((j0 >> 5) == static_cast<uint32_t>(r)) src = k[r];  // warp-uniform register pick
+    const uint32_t key = __shfl_sync(0xffffffffu, src, static_cast<int>(j & 31));
     if (j < L) {
       const float gk = __ldg(coeff + key);
       const TX* xr = X + static_cast<int64_t>(key / w) * D + c * DPL;
@@ -748,43 +783,67 @@ int ccem_backward(int dtype, const void* X, const void* E, const int64_t* inds,
     // Deterministic dE without a full sort when segments are short (uniform
     // negatives: ~26 entries per item at cfg3): segment offsets, an unstable
     // atomic grouping, then one warp per item sorts its <= 64 entry indices
-    // back into index order and reduces.  Items with longer segments raise a
-    // device flag; only then do the (gated, otherwise no-op) radix grouping
-    // and the long-segment reduce run — no host round trip either way.
+    // back into index order and reduces (a 64-, 128- or 256-key warp sort,
+    // picked from the longest segment, which is read back while the rows pass
+    // and the grouping run).  Only if some item has more than 256 entries do
+    // the radix grouping (4 x count words of scratch) and the long-segment
+    // reduce run.
     if (count >= (int64_t(1) << 32)) return fail(LF_EUNSUPPORTED, "ccem: n*w must be < 2^32");
     Scratch item_off, cursor, grouped, flag, sorted_vals;
-    int rc = group_offsets(inds, count, v, item_off, st);
+    int rc = flag.alloc(2 * sizeof(uint32_t), st);  // [0] long-segment flag, [1] longest segment
+    if (rc) return rc;
+    LF_CUDA(cudaMemsetAsync(flag.ptr, 0, 2 * sizeof(uint32_t), st));
+    rc = group_offsets(inds, count, v, item_off, st, flag.as<uint32_t>() + 1);
     if (!rc) rc = cursor.alloc(sizeof(uint32_t) * v, st);
     if (!rc) rc = grouped.alloc(sizeof(uint32_t) * count, st);
-    if (!rc) rc = flag.alloc(sizeof(uint32_t), st);
     if (rc) return rc;
+    // the longest segment comes back while the GPU works on the passes below;
+    // the radix fallback (and its 4 x count words of scratch) only runs if
+    // some item has more than 64 entries
+    uint32_t* longest = pinned_u32();
+    if (!longest) return fail(LF_ENOMEM, "ccem: cudaMallocHost failed");
+    *longest = 0xffffffffu;
+    LF_CUDA(cudaMemcpyAsync(longest, flag.as<uint32_t>() + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    cudaEvent_t seen;
+    LF_CUDA(cudaEventCreateWithFlags(&seen, cudaEventDisableTiming));
+    LF_CUDA(cudaEventRecord(seen, st));
     LF_CUDA(cudaMemcpyAsync(cursor.ptr, item_off.ptr, sizeof(uint32_t) * v, cudaMemcpyDeviceToDevice, st));
-    LF_CUDA(cudaMemsetAsync(flag.ptr, 0, sizeof(uint32_t), st));
     scatter_by_item<<<std::min<int64_t>(ceil_div(count, 256), 16 * num_sms()), 256, 0, st>>>(
         inds, count, cursor.as<uint32_t>(), grouped.as<uint32_t>());
     LF_LAUNCHED();
-#define LF_SEG2(TX, DD)                                                                           \
-  segment_reduce_sorted<TX, DD><<<sgrid, 256, 0, st>>>(                                          \
+    const cudaError_t se = cudaEventSynchronize(seen);
+    cudaEventDestroy(seen);
+    if (se != cudaSuccess) return cuda_fail(se, "cudaEventSynchronize");
+    const uint32_t lmax = *longest;
+    const int R = lmax <= 64u ? 2 : (lmax <= 128u ? 4 : 8);
+#define LF_SEG2(TX, DD, RR)                                                                       \
+  segment_reduce_sorted<TX, DD, RR><<<sgrid, 256, 0, st>>>(                                      \
       static_cast<const TX*>(X), coeff.as<float>(), grouped.as<uint32_t>(), item_off.as<uint32_t>(), \
       v, w, static_cast<float*>(dE), flag.as<uint32_t>())
+#define LF_SEG2_R(TX, DD)            \
+  if (R == 2) LF_SEG2(TX, DD, 2);     \
+  else if (R == 4) LF_SEG2(TX, DD, 4); \
+  else LF_SEG2(TX, DD, 8);
     if (dtype == LF_BF16) {
-      if (D == 64) LF_SEG2(__nv_bfloat16, 64);
-      else if (D == 128) LF_SEG2(__nv_bfloat16, 128);
-      else LF_SEG2(__nv_bfloat16, 256);
+      if (D == 64) { LF_SEG2_R(__nv_bfloat16, 64) }
+      else if (D == 128) { LF_SEG2_R(__nv_bfloat16, 128) }
+      else { LF_SEG2_R(__nv_bfloat16, 256) }
     } else {
-      if (D == 64) LF_SEG2(float, 64);
-      else if (D == 128) LF_SEG2(float, 128);
-      else LF_SEG2(float, 256);
+      if (D == 64) { LF_SEG2_R(float, 64) }
+      else if (D == 128) { LF_SEG2_R(float, 128) }
+      else { LF_SEG2_R(float, 256) }
     }
+#undef LF_SEG2_R
 #undef LF_SEG2
     LF_LAUNCHED();
+    if (lmax <= 256u) return LF_OK;  // every item went through the sorted path
     rc = radix_group(inds, count, v, sorted_vals, st, flag.as<uint32_t>());
     if (rc) return rc;
 #define LF_SEG(TX, DD)                                                                          \
   segment_reduce_vec<TX, DD><<<sgrid, 256, 0, st>>>(static_cast<const TX*>(X), coeff.as<float>(), \
                                                     sorted_vals.as<uint32_t>(),                \
                                                     item_off.as<uint32_t>(), v, w,             \
-                                                    static_cast<float*>(dE), 64u,              \
+                                                    static_cast<float*>(dE), 256u,             \
                                                     flag.as<uint32_t>())
     if (dtype == LF_BF16) {
       if (D == 64) LF_SEG(__nv_bfloat16, 64);

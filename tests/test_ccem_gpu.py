@@ -230,3 +230,17 @@ def test_invalid_indices_name_the_row(lf):  # neg_index.cpp:13-25
     I = torch.from_numpy(bad).cuda()
     with pytest.raises(ValueError, match="row 1 slot 2 holds 10, outside catalog of 10"):
         lf.ccem_forward(X, E, I)
+
+
+@pytest.mark.parametrize("v", [300, 150, 40])
+def test_segment_length_classes(lf, v):
+    # items with ~85, ~170 and ~640 entries: the 128- and 256-key warp sorts
+    # and the radix fallback of the deterministic dE; exact against the
+    # oracle's tolerance and bitwise stable
+    rng = ob.Rng(900 + v)
+    inst = ob.make_instance(rng, 400, 64, v)
+    inds = ob.make_candidates(rng, inst.targets, 63, v)
+    X, E, I, Eh, Ch = to_dev(inst.E, inst.C, inds, torch.bfloat16)
+    out, g = compare(lf, X, E, I, Eh, Ch, inds, torch.bfloat16)
+    g2 = lf.ccem_backward(X, E, I, out.lse)
+    assert torch.equal(g.d_classifier, g2.d_classifier)
