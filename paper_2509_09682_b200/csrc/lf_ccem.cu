@@ -31,6 +31,10 @@ namespace {
 // ------------------------------------------------------------------ loads --
 template <class T>
 struct Vec8;  // 8 consecutive elements of row storage, widened to float
+#ifndef LF_CCEM_BWD_U
+#define LF_CCEM_BWD_U 4  // CCE- backward rows pass: slots per 8-lane group per step
+#endif
+
 template <>
 struct Vec8<__nv_bfloat16> {
   static __device__ __forceinline__ void load(const __nv_bfloat16* p, float (&f)[8]) {
@@ -152,42 +156,55 @@ __global__ void __launch_bounds__(256) ccem_bwd_rows_vec(
   const float rl = static_cast<float>(lse[row]);
   const float u = static_cast<float>(row_up ? row_up[row] : upstream_over_n);
   const int64_t* irow = inds + row * w;
-  for (int64_t s0 = 0; s0 < w; s0 += 4) {
-    const int64_t slot = s0 + g;
-    if (slot < w) {  // uniform within each 8-lane group
-      const int64_t item = __ldg(irow + slot);
-      const TE* er = E + item * D + c * DPL;
-      float ev[DPL];
-      float dot = 0.f;
+  // LF_CCEM_BWD_U slots per group per step: their E rows are all requested
+  // before any arithmetic (the pass is latency-bound on the gathers); the
+  // per-group slot order, and so every sum, is unchanged.
+  constexpr int U = LF_CCEM_BWD_U;
+  const unsigned gm = 0xFFu << (8 * g);
+  for (int64_t s0 = 0; s0 < w; s0 += 4 * U) {
+    int64_t items[U];
+    float ev[U][DPL];
 #pragma unroll
-      for (int b = 0; b < DPL / 8; ++b) {
-        float f[8];
-        Vec8<TE>::load(er + 8 * b, f);
+    for (int q = 0; q < U; ++q) {
+      const int64_t slot = s0 + 4 * q + g;
+      items[q] = slot < w ? __ldg(irow + slot) : -1;
+      if (slot < w) {  // uniform within each 8-lane group
+        const TE* er = E + items[q] * D + c * DPL;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          ev[8 * b + i] = f[i];
-          dot = fmaf(xr[8 * b + i], f[i], dot);
+        for (int b = 0; b < DPL / 8; ++b) {
+          float f[8];
+          Vec8<TE>::load(er + 8 * b, f);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) ev[q][8 * b + i] = f[i];
         }
       }
-      const unsigned gm = 0xFFu << (8 * g);
-      dot += __shfl_xor_sync(gm, dot, 1);
-      dot += __shfl_xor_sync(gm, dot, 2);
-      dot += __shfl_xor_sync(gm, dot, 4);
-      const float soft = __expf(dot - rl);
-      const float gcoef = (slot == 0 ? soft - 1.f : soft) * u;
+    }
 #pragma unroll
-      for (int i = 0; i < DPL; ++i) acc[i] = fmaf(gcoef, ev[i], acc[i]);
-      if (ATOMIC) {
-        float* dst = dE + item * D + c * DPL;
+    for (int q = 0; q < U; ++q) {
+      const int64_t slot = s0 + 4 * q + g;
+      if (slot < w) {
+        float dot = 0.f;
 #pragma unroll
-        for (int i = 0; i < DPL; i += 4) {
-          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + i),
-                       "f"(gcoef * xr[i]), "f"(gcoef * xr[i + 1]), "f"(gcoef * xr[i + 2]),
-                       "f"(gcoef * xr[i + 3])
-                       : "memory");
+        for (int i = 0; i < DPL; ++i) dot = fmaf(xr[i], ev[q][i], dot);
+        dot += __shfl_xor_sync(gm, dot, 1);
+        dot += __shfl_xor_sync(gm, dot, 2);
+        dot += __shfl_xor_sync(gm, dot, 4);
+        const float soft = __expf(dot - rl);
+        const float gcoef = (slot == 0 ? soft - 1.f : soft) * u;
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) acc[i] = fmaf(gcoef, ev[q][i], acc[i]);
+        if (ATOMIC) {
+          float* dst = dE + items[q] * D + c * DPL;
+#pragma unroll
+          for (int i = 0; i < DPL; i += 4) {
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + i),
+                         "f"(gcoef * xr[i]), "f"(gcoef * xr[i + 1]), "f"(gcoef * xr[i + 2]),
+                         "f"(gcoef * xr[i + 3])
+                         : "memory");
+          }
+        } else if (c == 0) {
+          coeff[row * w + slot] = gcoef;
         }
-      } else if (c == 0) {
-        coeff[row * w + slot] = gcoef;
       }
     }
   }
