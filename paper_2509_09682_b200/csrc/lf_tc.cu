@@ -168,6 +168,9 @@ struct Cfg {
   static constexpr int kNBMax = (MODE == FWD || MODE == EVAL ? 512 : 512 - D) / BN;  // S buffers in TMEM
   static constexpr int kNB = kNBMax > 8 ? 8 : kNBMax;
   static_assert(MODE == FWD || MODE == EVAL || kNB >= 2, "not enough TMEM for the backward pipeline");
+  // every epilogue warpgroup holds one S buffer while it works on a tile
+  // (BN = 256 forward tiles with 3 warpgroups leave 2 buffers: measured to hang)
+  static_assert(kNB >= G::NWG, "fewer TMEM S buffers than epilogue warpgroups");
   static constexpr int kAccCol = kNB * BN;
   static constexpr int kSmem = 1024 /*align slack*/ + kOwnerBytes + kOnesBytes + kStages * kStageBytes +
                                1024 /*barriers*/ + (MODE == FWD ? (G::NWG - 1) * BM * 16 : 0) +
