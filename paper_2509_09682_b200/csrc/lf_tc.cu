@@ -81,9 +81,9 @@ constexpr int BM = 128;  // owner tile (TMEM lanes)
 enum Mode : int { FWD = 0, BWD_ROWS = 1, BWD_ITEMS = 2, EVAL = 3 };
 constexpr int kEvalK = 16;  // largest per-row top-K the EVAL epilogue keeps
 // EVAL list length by FLAGS (a shorter list for small k rises faster, so
-// fewer slabs reach the insertion path): 0 -> 16, 1 -> 12, 2 -> 8
+// fewer slabs reach the insertion path): 0 -> 16, 1 -> 12, 2 -> 8, 3 -> 4
 template <int MODE, int FLAGS>
-constexpr int kEvalKOf = MODE != EVAL ? kEvalK : (FLAGS == 1 ? 12 : (FLAGS == 2 ? 8 : 16));
+constexpr int kEvalKOf = MODE != EVAL ? kEvalK : (FLAGS == 1 ? 12 : (FLAGS == 2 ? 8 : (FLAGS == 3 ? 4 : 16)));
 // Backward variants: kFilt = filter_eps > 0 (flush below eps, sub-tile skip);
 // kCount = also count skipped elements / sub-tiles (only when stats are read).
 // kTgtIn = handle each row's own target inside the tile loop (exact for any
@@ -1161,6 +1161,7 @@ int launch_flags(int flags, const CUtensorMap& mo, const CUtensorMap& ms, const 
   if constexpr (MODE == FWD) {
     return launch_mode<D, MODE, 0>(mo, ms, mb, m1, p, st);
   } else if constexpr (MODE == EVAL) {  // flags = list-length class (kEvalKOf)
+    if (flags == 3) return launch_mode<D, MODE, 3>(mo, ms, mb, m1, p, st);
     if (flags == 2) return launch_mode<D, MODE, 2>(mo, ms, mb, m1, p, st);
     if (flags == 1) return launch_mode<D, MODE, 1>(mo, ms, mb, m1, p, st);
     return launch_mode<D, MODE, 0>(mo, ms, mb, m1, p, st);
@@ -1254,8 +1255,8 @@ int tc_cce_forward_partials(const void* X, const void* E, const int64_t* targets
 int tc_eval_partials(const void* X, const void* E, const void* Et, const int32_t* tl, int64_t n,
                      int D, int64_t v, int k, Scratch& cnt, Scratch& val, Scratch& idx, int* P_out,
                      int* K_out, cudaStream_t st) {
-  const int kclass = k <= 8 ? 2 : (k <= 12 ? 1 : 0);
-  const int K = kclass == 2 ? 8 : (kclass == 1 ? 12 : 16);
+  const int kclass = k <= 4 ? 3 : (k <= 8 ? 2 : (k <= 12 ? 1 : 0));
+  const int K = kclass == 3 ? 4 : (kclass == 2 ? 8 : (kclass == 1 ? 12 : 16));
   constexpr int BN = Geo<EVAL>::BN;
   const int64_t owner_tiles = ceil_div(n, BM);
   const int64_t stream_tiles = ceil_div(v, BN);

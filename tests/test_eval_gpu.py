@@ -89,7 +89,8 @@ def _check_rounded(X, E, tg, ahead, top, score, k):
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("n,d,v,k", [(1, 64, 1000, 10), (300, 64, 5000, 16), (129, 128, 777, 5),
-                                     (257, 64, 130, 16), (64, 256, 3000, 10), (200, 192, 1500, 8)])
+                                     (257, 64, 130, 16), (64, 256, 3000, 10), (200, 192, 1500, 8),
+                                     (300, 64, 4000, 3), (128, 64, 900, 1)])
 def test_rounded_dtypes_rank_within_tolerance(M, dtype, n, d, v, k):
     g = torch.Generator(device="cpu").manual_seed(n * 31 + v)
     X = (torch.randn(n, d, generator=g) * 0.5).to(dtype).cuda()
