@@ -814,9 +814,9 @@ int ccem_backward(int dtype, const void* X, const void* E, const int64_t* inds,
     if (!rc) rc = cursor.alloc(sizeof(uint32_t) * v, st);
     if (!rc) rc = grouped.alloc(sizeof(uint32_t) * count, st);
     if (rc) return rc;
-    // the longest segment comes back while the GPU works on the passes below;
-    // the radix fallback (and its 4 x count words of scratch) only runs if
-    // some item has more than 64 entries
+    // the longest segment comes back while the GPU works on the scatter; it
+    // picks the warp-sort width, and the radix fallback (with its 4 x count
+    // words of scratch) only runs if some item has more than 256 entries
     uint32_t* longest = pinned_u32();
     if (!longest) return fail(LF_ENOMEM, "ccem: cudaMallocHost failed");
     *longest = 0xffffffffu;
