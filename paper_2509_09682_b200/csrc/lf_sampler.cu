@@ -106,10 +106,9 @@ __global__ void first_bad_positive(const int64_t* __restrict__ pos, int64_t n, i
 }
 
 // ---- popularity sampler (sampler.cpp:77-127) ----
-// Weights and their running sum.  exponent == 1: weights are the integer
-// counts, every partial sum is an exact integer in double, so a blocked scan
-// gives the reference's bits; otherwise a single thread keeps the reference's
-// summation order (pow itself may differ from glibc's in the last ulp).
+// Weights and their running sum for exponent != 1: a single thread keeps the
+// reference's summation order (pow itself may differ from glibc's in the last
+// ulp).  (exponent == 1 uses the blocked scan below.)
 // flags[0] = first negative count, flags[1] = 1 if the total is not > 0.
 __global__ void pop_cumulative(const int64_t* __restrict__ counts, int64_t catalog, double exponent,
                                double* __restrict__ cum, unsigned long long* __restrict__ flags,
@@ -143,6 +142,84 @@ __global__ void pop_cumulative(const int64_t* __restrict__ counts, int64_t catal
     for (int64_t v = lo; v < hi; ++v) cum[v] += off;
 }
 
+// exponent == 1: a three-kernel blocked scan over all SMs (exact: every
+// partial sum of integer counts is an integer below 2^53).  Block = 256
+// threads x 16 consecutive items.
+constexpr int kScanPer = 16, kScanBlock = 256 * kScanPer;
+
+__device__ __forceinline__ double block_exclusive_scan(double x, double* warp_tot, double* block_total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double inc = x;
+  for (int off = 1; off < 32; off <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, inc, off);
+    if (lane >= off) inc += y;
+  }
+  if (lane == 31) warp_tot[warp] = inc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) {
+      const double t = warp_tot[w];
+      warp_tot[w] = acc;
+      acc += t;
+    }
+    *block_total = acc;
+  }
+  __syncthreads();
+  return warp_tot[warp] + inc - x;
+}
+
+__global__ void __launch_bounds__(256) pop_block_sums(const int64_t* __restrict__ counts, int64_t catalog,
+                                                    double* __restrict__ block_sums,
+                                                    unsigned long long* __restrict__ flags) {
+  __shared__ double wt[8], bt;
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kScanBlock + threadIdx.x * kScanPer;
+  double x = 0.0;
+  for (int q = 0; q < kScanPer; ++q) {
+    const int64_t v = i0 + q;
+    if (v < catalog) {
+      const int64_t c = counts[v];
+      if (c < 0) atomicMin(flags, static_cast<unsigned long long>(v));
+      x += static_cast<double>(c);
+    }
+  }
+  block_exclusive_scan(x, wt, &bt);
+  if (threadIdx.x == 0) block_sums[blockIdx.x] = bt;
+}
+
+__global__ void pop_scan_blocks(double* __restrict__ block_sums, int64_t nb, double* __restrict__ total,
+                                unsigned long long* __restrict__ flags) {
+  if (threadIdx.x != 0) return;
+  double acc = 0.0;
+  for (int64_t b = 0; b < nb; ++b) {
+    const double t = block_sums[b];
+    block_sums[b] = acc;
+    acc += t;
+  }
+  *total = acc;
+  if (!(acc > 0.0)) flags[1] = 1;
+}
+
+__global__ void __launch_bounds__(256) pop_block_scan(const int64_t* __restrict__ counts, int64_t catalog,
+                                                    const double* __restrict__ block_off,
+                                                    double* __restrict__ cum) {
+  __shared__ double wt[8], bt;
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kScanBlock + threadIdx.x * kScanPer;
+  double w[kScanPer], x = 0.0;
+#pragma unroll
+  for (int q = 0; q < kScanPer; ++q) {
+    const int64_t v = i0 + q;
+    w[q] = v < catalog ? static_cast<double>(counts[v]) : 0.0;
+    x += w[q];
+  }
+  double run = block_off[blockIdx.x] + block_exclusive_scan(x, wt, &bt);
+#pragma unroll
+  for (int q = 0; q < kScanPer; ++q) {
+    run += w[q];
+    if (i0 + q < catalog) cum[i0 + q] = run;
+  }
+}
+
 __device__ __forceinline__ int64_t upper_bound(const double* __restrict__ cum, int64_t n, double u) {
   int64_t lo = 0, hi = n;
   while (lo < hi) {
@@ -153,19 +230,44 @@ __device__ __forceinline__ int64_t upper_bound(const double* __restrict__ cum, i
   return lo;
 }
 
+// Guide table (Chen's method): guide[j] = upper_bound(cum, (j - 1) total / G),
+// so a draw u in bucket j = floor(u G / total) has its answer in
+// [guide[j], guide[j + 2]); a few probes instead of ~20.  The result is
+// verified against its neighbours and falls back to the full search, so it is
+// always exactly upper_bound(cum, u) (the reference's std::upper_bound).
+__global__ void build_guide(const double* __restrict__ cum, int64_t catalog, const double* __restrict__ total,
+                            int64_t G, int64_t* __restrict__ guide) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= G) return;
+  const double t = static_cast<double>(j - 1) * (*total / static_cast<double>(G));
+  guide[j] = j == 0 ? 0 : upper_bound(cum, catalog, t);
+}
+
+__device__ __forceinline__ int64_t guided_upper_bound(const double* __restrict__ cum, int64_t catalog,
+                                                      const int64_t* __restrict__ guide, int64_t G,
+                                                      double scale, double u) {
+  int64_t j = static_cast<int64_t>(u * scale);
+  j = j < 0 ? 0 : (j >= G ? G - 1 : j);
+  const int64_t lo = guide[j], hi = j + 2 < G ? guide[j + 2] : catalog;
+  int64_t r = lo + upper_bound(cum + lo, hi - lo, u);
+  const bool ok = (r == catalog || u < cum[r]) && (r == 0 || !(u < cum[r - 1]));
+  return ok ? r : upper_bound(cum, catalog, u);
+}
+
 // Warp per row, 32 consecutive draws at once (one uniform() per attempt);
 // every rejected draw (index past the table, or the positive) is one failed
 // attempt of the current slot, retry_cap in a row is an error.
 __global__ void __launch_bounds__(256) sample_popularity_rows(
     const int64_t* __restrict__ pos, int64_t n, int64_t ns, const double* __restrict__ cum,
-    int64_t catalog, const double* __restrict__ total, uint64_t seed, int retry_cap,
-    int64_t* __restrict__ inds, unsigned long long* __restrict__ status) {
+    int64_t catalog, const double* __restrict__ total, const int64_t* __restrict__ guide, int64_t G,
+    uint64_t seed, int retry_cap, int64_t* __restrict__ inds, unsigned long long* __restrict__ status) {
   const int lane = threadIdx.x & 31;
   const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   if (row >= n) return;
   const int64_t w = ns + 1;
   const int64_t p = pos[row];
   const double running = *total;
+  const double scale = static_cast<double>(G) / running;
   int64_t* out = inds + row * w;
   if (lane == 0) out[0] = p;
   const uint64_t s = mix64(seed + kGolden * static_cast<uint64_t>(row + 1));
@@ -175,7 +277,7 @@ __global__ void __launch_bounds__(256) sample_popularity_rows(
   for (uint64_t k0 = 0; filled < ns; k0 += 32) {
     const uint64_t z = mix64(s + (k0 + lane + 1) * kGolden);
     const double u = static_cast<double>(z >> 11) * 0x1.0p-53 * running;  // rng.hpp:41
-    const int64_t v = upper_bound(cum, catalog, u);
+    const int64_t v = guided_upper_bound(cum, catalog, guide, G, scale, u);
     const bool acc = v < catalog && v != p;
     const unsigned am = __ballot_sync(0xffffffffu, acc);
     const unsigned fm = ~am;
@@ -224,8 +326,17 @@ int sample_popularity(const int64_t* positives, int64_t n, int64_t ns, const int
   LF_CUDA(cudaMemsetAsync(flag.as<unsigned long long>() + 1, 0, sizeof(unsigned long long), st));
   LF_CUDA(cudaMemsetAsync(flag.as<unsigned long long>() + 2, 0xFF, 2 * sizeof(unsigned long long), st));
   unsigned long long* f = flag.as<unsigned long long>();
-  pop_cumulative<<<1, exponent == 1.0 ? 1024 : 1, 0, st>>>(counts, catalog, exponent, cum.as<double>(), f,
-                                                            tot.as<double>());
+  Scratch bsums;
+  if (exponent == 1.0) {
+    const int64_t nb = ceil_div(catalog, kScanBlock);
+    rc = bsums.alloc(sizeof(double) * nb, st);
+    if (rc) return rc;
+    pop_block_sums<<<static_cast<unsigned>(nb), 256, 0, st>>>(counts, catalog, bsums.as<double>(), f);
+    pop_scan_blocks<<<1, 32, 0, st>>>(bsums.as<double>(), nb, tot.as<double>(), f);
+    pop_block_scan<<<static_cast<unsigned>(nb), 256, 0, st>>>(counts, catalog, bsums.as<double>(), cum.as<double>());
+  } else {  // the reference's summation order (sampler.cpp:93-99), one thread
+    pop_cumulative<<<1, 1, 0, st>>>(counts, catalog, exponent, cum.as<double>(), f, tot.as<double>());
+  }
   LF_LAUNCHED();
   first_bad_positive<<<static_cast<unsigned>(std::min<int64_t>(std::max<int64_t>(ceil_div(n, 256), 1), 1024)),
                        256, 0, st>>>(positives, n, catalog, f + 2);
@@ -250,8 +361,16 @@ int sample_popularity(const int64_t* positives, int64_t n, int64_t ns, const int
                                " exceeds catalog minus positive (" + std::to_string(catalog - 1) + ")");
   if (h[1]) return fail(LF_EINVAL, "sample_popularity: all item weights are zero");
   if (n == 0) return LF_OK;
+  const int64_t G = catalog;
+  Scratch guide;
+  rc = guide.alloc(sizeof(int64_t) * G, st);
+  if (rc) return rc;
+  build_guide<<<static_cast<unsigned>(ceil_div(G, 256)), 256, 0, st>>>(cum.as<double>(), catalog, tot.as<double>(),
+                                                                       G, guide.as<int64_t>());
+  LF_LAUNCHED();
   sample_popularity_rows<<<static_cast<unsigned>(ceil_div(n, 8)), 256, 0, st>>>(
-      positives, n, ns, cum.as<double>(), catalog, tot.as<double>(), seed, retry_cap, inds, f + 3);
+      positives, n, ns, cum.as<double>(), catalog, tot.as<double>(), guide.as<int64_t>(), G, seed,
+      retry_cap, inds, f + 3);
   LF_LAUNCHED();
   unsigned long long bad = 0;
   LF_CUDA(cudaMemcpyAsync(&bad, f + 3, sizeof(bad), cudaMemcpyDeviceToHost, st));
