@@ -80,6 +80,9 @@ constexpr int BM = 128;  // owner tile (TMEM lanes)
 
 enum Mode : int { FWD = 0, BWD_ROWS = 1, BWD_ITEMS = 2, EVAL = 3 };
 constexpr int kEvalK = 16;  // largest per-row top-K the EVAL epilogue keeps
+// "no published k-th score yet" (the 0x80 byte-fill; below the key of any
+// score above -3.4e38)
+constexpr int kFloorNone = static_cast<int>(0x80808080u);
 // EVAL list length by FLAGS (a shorter list for small k rises faster, so
 // fewer slabs reach the insertion path): 0 -> 16, 1 -> 12, 2 -> 8, 3 -> 4
 template <int MODE, int FLAGS>
@@ -118,6 +121,8 @@ struct TcParams {
   uint32_t* ev_count;    // [n_chunks][n_owner] items of the chunk ranked ahead of the target
   float* ev_val;         // [n_chunks][n_owner][K] top scores, descending (K = kEvalKOf)
   int32_t* ev_idx;       // same, local item index (INT32_MAX = empty)
+  int32_t* ev_floor;     // [owner rows] order-preserving bits of the best known k-th score
+                         // (kFloorNone = none): runs of the same rows share it
 };
 
 // Position + phase in an N-slot mbarrier ring.
@@ -520,10 +525,19 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
       float m = -INFINITY, s = 0.f, tv = 0.f, has = 0.f;
       float st = 0.f, st_dn = 0.f;  // EVAL: the row's target score
       if (MODE == EVAL && run_first) {
+        // Seed the list with placeholders just below the k-th score another
+        // run of these rows has already published: at least k real items
+        // score >= it, so nothing below it can make the final list, while
+        // ties with it still enter (v > next_down(floor) == v >= floor).
         ecnt = 0;
+        float seed = -INFINITY;
+        if (orow < p.n_owner) {
+          const int fk = __ldcg(p.ev_floor + orow);
+          if (fk != kFloorNone) seed = next_down(__int_as_float(fk >= 0 ? fk : fk ^ 0x7fffffff));
+        }
 #pragma unroll
         for (int k = 0; k < KK; ++k) {
-          kv[k] = -INFINITY;
+          kv[k] = seed;
           ki[k] = 0x7fffffff;
         }
       }
@@ -964,6 +978,10 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
               topk_insert(kv, ki, cv, ci);
             }
           }
+          if (orow < p.n_owner && ki[KK - 1] != 0x7fffffff) {  // publish a real k-th score
+            const int b = __float_as_int(kv[KK - 1]);
+            atomicMax(p.ev_floor + orow, b >= 0 ? b : b ^ 0x7fffffff);
+          }
           if (orow < p.n_owner) {
             const int64_t rowp = chunk * p.n_owner + orow;
             p.ev_count[rowp] = ecnt;
@@ -1255,6 +1273,12 @@ int tc_cce_forward_partials(const void* X, const void* E, const int64_t* targets
 int tc_eval_partials(const void* X, const void* E, const void* Et, const int32_t* tl, int64_t n,
                      int D, int64_t v, int k, Scratch& cnt, Scratch& val, Scratch& idx, int* P_out,
                      int* K_out, cudaStream_t st) {
+  Scratch floor;
+  {
+    const int rc0 = floor.alloc(sizeof(int32_t) * ceil_div(n, BM) * BM, st);
+    if (rc0) return rc0;
+    LF_CUDA(cudaMemsetAsync(floor.ptr, 0x80, sizeof(int32_t) * ceil_div(n, BM) * BM, st));  // below any key
+  }
   const int kclass = k <= 4 ? 3 : (k <= 8 ? 2 : (k <= 12 ? 1 : 0));
   const int K = kclass == 3 ? 4 : (kclass == 2 ? 8 : (kclass == 1 ? 12 : 16));
   constexpr int BN = Geo<EVAL>::BN;
@@ -1286,6 +1310,7 @@ int tc_eval_partials(const void* X, const void* E, const void* Et, const int32_t
   p.ev_count = cnt.as<uint32_t>();
   p.ev_val = val.as<float>();
   p.ev_idx = idx.as<int32_t>();
+  p.ev_floor = floor.as<int32_t>();
   rc = launch_d<EVAL>(D, kclass, mo, ms, mt, mo, p, st);
   if (rc) return rc;
   *P_out = static_cast<int>(P);
