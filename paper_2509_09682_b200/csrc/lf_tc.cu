@@ -56,6 +56,9 @@
 #ifndef LF_FWD_LD64
 #define LF_FWD_LD64 1  // forward / EVAL: one 32x32b.x64 TMEM load per 64-column slab
 #endif
+#ifndef LF_EVAL_CONTIG
+#define LF_EVAL_CONTIG 1  // EVAL: CTA-contiguous owner-tile-major units (0: chunk-major round robin)
+#endif
 #ifndef LF_NWG_EVAL
 #define LF_NWG_EVAL 2
 #endif
@@ -247,7 +250,7 @@ template <int MODE>
 struct Units {
   int64_t begin, end, step, P, OT;
   __device__ Units(const TcParams& p) : P(p.n_chunks), OT(p.owner_tiles) {
-    if (MODE == EVAL) {
+    if (MODE == EVAL && LF_EVAL_CONTIG) {
       begin = blockIdx.x * p.units / gridDim.x;
       end = (blockIdx.x + 1) * p.units / gridDim.x;
       step = 1;
@@ -257,8 +260,8 @@ struct Units {
       step = gridDim.x;
     }
   }
-  __device__ int64_t chunk(int64_t u) const { return MODE == EVAL ? u % P : u / OT; }
-  __device__ int64_t owner(int64_t u) const { return MODE == EVAL ? u / P : u % OT; }
+  __device__ int64_t chunk(int64_t u) const { return MODE == EVAL && LF_EVAL_CONTIG ? u % P : u / OT; }
+  __device__ int64_t owner(int64_t u) const { return MODE == EVAL && LF_EVAL_CONTIG ? u / P : u % OT; }
 };
 
 // Largest float below x (finite x): "score >= x" == "score > next_down(x)".
@@ -509,8 +512,8 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
     int ki[KK];
     for (int64_t u = U.begin; u < U.end; u += U.step, ++j) {
       const int64_t chunk = U.chunk(u), ot = U.owner(u);
-      const bool run_first = u == U.begin || U.owner(u - 1) != ot;
-      const bool run_last = u + 1 == U.end || U.owner(u + 1) != ot;
+      const bool run_first = u == U.begin || U.owner(u - U.step) != ot;
+      const bool run_last = u + U.step >= U.end || U.owner(u + U.step) != ot;
       const int64_t s_begin = chunk * p.chunk;
       const int64_t s_end = min(p.n_stream, s_begin + p.chunk);
       const int64_t ntile = ceil_div(s_end - s_begin, BN);
