@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(256) ccem_bwd_rows_vec(
   // LF_CCEM_BWD_U slots per group per step: their E rows are all requested
   // before any arithmetic (the pass is latency-bound on the gathers); the
   // per-group slot order, and so every sum, is unchanged.
-  constexpr int U = LF_CCEM_BWD_U;
+  constexpr int U = D <= 64 ? LF_CCEM_BWD_U : (D <= 128 ? 2 : 1);  // registers: U x D/8 floats
   const unsigned gm = 0xFFu << (8 * g);
   for (int64_t s0 = 0; s0 < w; s0 += 4 * U) {
     int64_t items[U];
