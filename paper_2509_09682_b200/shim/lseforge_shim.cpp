@@ -10,9 +10,12 @@
 //   lseforge::ccem_backward_rows   ccem.hpp:34-36  (reference ccem.cpp:107-194)
 //   lseforge::estimate_flops       ccem.hpp:48-49  (reference ccem.cpp:207-235)
 //   lseforge::evaluate             metrics.hpp:18-24 (reference metrics.cpp:13-103)
+//   lseforge::sample_uniform,      sampler.hpp:26-40 (reference sampler.cpp:30-127,
+//     sample_popularity,           index for index; PopularityTable::FromCounts is
+//     PopularityTable::FromCounts  restated on the host)
 //
 // It is compiled against the reference's own headers (-I proj/include) and
-// linked in place of cce.cpp + ccem.cpp + metrics.cpp; everything else in liblseforge
+// linked in place of cce.cpp + ccem.cpp + metrics.cpp + sampler.cpp; everything else in liblseforge
 // (losses.cpp validation and oracles, neg_index.cpp, accountant.cpp, the
 // trainer) is unchanged.  Each call: validate on the host with the
 // reference's own functions and messages -> upload the host matrices ->
@@ -59,6 +62,7 @@
 #include "lseforge/matrix.hpp"
 #include "lseforge/metrics.hpp"
 #include "lseforge/neg_index.hpp"
+#include "lseforge/sampler.hpp"
 #include "lseforge/split.hpp"
 #include "lseforge/threads.hpp"
 #include "lseforge_b200.h"
@@ -359,6 +363,56 @@ FlopEstimate estimate_flops(std::size_t n, std::size_t d, std::size_t v, std::si
                                    static_cast<int32_t>(backend), &f.forward, &f.backward);
   if (rc != LF_OK) throw_status(rc, "lf_estimate_flops");
   return f;
+}
+
+PopularityTable PopularityTable::FromCounts(std::vector<std::int64_t> counts) {
+  // sampler.cpp:30-42: reject negative counts, keep the total
+  PopularityTable t;
+  for (std::size_t v = 0; v < counts.size(); ++v) {
+    if (counts[v] < 0)
+      throw std::invalid_argument("PopularityTable: item " + std::to_string(v) + " has negative count " +
+                                  std::to_string(counts[v]));
+    t.total += counts[v];
+  }
+  t.counts = std::move(counts);
+  return t;
+}
+
+namespace {
+NegIndexMatrix download_inds(const Dev& d, std::size_t n, std::size_t w) {
+  std::vector<int64_t> h(n * w);
+  download(h.data(), d.p, sizeof(int64_t) * n * w);
+  NegIndexMatrix m(n, w);
+  for (std::size_t i = 0; i < n; ++i)
+    for (std::size_t s = 0; s < w; ++s) m(i, s) = h[i * w + s];
+  return m;
+}
+}  // namespace
+
+NegIndexMatrix sample_uniform(std::span<const std::int64_t> positives, std::size_t ns, std::size_t catalog,
+                              const SplitMix64& rng, const SamplerConfig& cfg) {
+  // rows draw from rng.derived(i), which depends only on the construction seed
+  const std::size_t n = positives.size();
+  Dev pos(n * 8), out(n * (1 + ns) * 8);
+  upload(pos.p, positives.data(), n * 8);
+  check(lf_sample_uniform(pos.as<int64_t>(), static_cast<int64_t>(n), static_cast<int64_t>(ns),
+                          static_cast<int64_t>(catalog), rng.seed(), cfg.retry_cap, out.as<int64_t>(), nullptr),
+        "lf_sample_uniform");
+  return download_inds(out, n, 1 + ns);
+}
+
+NegIndexMatrix sample_popularity(std::span<const std::int64_t> positives, std::size_t ns,
+                                 const PopularityTable& pop, const SplitMix64& rng, const SamplerConfig& cfg) {
+  const std::size_t n = positives.size(), catalog = pop.counts.size();
+  if (catalog == 0) throw std::invalid_argument("sample_popularity: empty popularity table");
+  Dev pos(n * 8), counts(catalog * 8), out(n * (1 + ns) * 8);
+  upload(pos.p, positives.data(), n * 8);
+  upload(counts.p, pop.counts.data(), catalog * 8);
+  check(lf_sample_popularity(pos.as<int64_t>(), static_cast<int64_t>(n), static_cast<int64_t>(ns),
+                             counts.as<int64_t>(), static_cast<int64_t>(catalog), cfg.popularity_exponent,
+                             rng.seed(), cfg.retry_cap, out.as<int64_t>(), nullptr),
+        "lf_sample_popularity");
+  return download_inds(out, n, 1 + ns);
 }
 
 EvalSummary evaluate(const ToyEncoderParams& params, std::span<const EvalPair> pairs, std::size_t k,

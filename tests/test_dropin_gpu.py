@@ -1,7 +1,7 @@
 """GPU: the reference's OWN test programs, compiled in place from
 /root/reference/proj/tests and linked against the C++ drop-in
 (paper_2509_09682_b200/shim/lseforge_shim.cpp + liblseforge_b200.so) in place
-of the reference's cce.cpp / ccem.cpp / metrics.cpp (recipe: oracle/Makefile `dropin`; the
+of the reference's cce.cpp / ccem.cpp / metrics.cpp / sampler.cpp (recipe: oracle/Makefile `dropin`; the
 binaries are built in the container and travel to the GPU box prebuilt).
 
 Default device dtype is the exact (f64) mode, which must pass everything the
@@ -64,6 +64,12 @@ def test_reference_test_harness_passes_in_exact_mode(cuda):
     # includes evaluate()'s rank / tie / coverage / surprisal cases
     # (test_harness.cpp:771-860), now served by lf_evaluate on the GPU
     rc, out = run("test_harness")
+    assert rc == 0 and "| 0 failed" in out, out[-3000:]
+
+
+def test_reference_test_sampler_passes(cuda):
+    # the reference's sampler suite (test_sampler.cpp) on the GPU samplers
+    rc, out = run("test_sampler")
     assert rc == 0 and "| 0 failed" in out, out[-3000:]
 
 
