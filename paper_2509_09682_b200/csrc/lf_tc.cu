@@ -56,6 +56,9 @@
 #ifndef LF_FWD_LD64
 #define LF_FWD_LD64 1  // forward / EVAL: one 32x32b.x64 TMEM load per 64-column slab
 #endif
+#ifndef LF_FWD_MAXCHUNKS
+#define LF_FWD_MAXCHUNKS 64  // forward: most V chunks pick_chunks may choose
+#endif
 #ifndef LF_EVAL_CONTIG
 #define LF_EVAL_CONTIG 1  // EVAL: CTA-contiguous owner-tile-major units (0: chunk-major round robin)
 #endif
@@ -1242,7 +1245,7 @@ int tc_cce_forward_partials(const void* X, const void* E, const int64_t* targets
   constexpr int BN = Geo<FWD>::BN;
   const int64_t owner_tiles = ceil_div(n, BM);
   const int64_t stream_tiles = ceil_div(v, BN);
-  const int64_t chunks = pick_chunks(owner_tiles, stream_tiles, 64);
+  const int64_t chunks = pick_chunks(owner_tiles, stream_tiles, LF_FWD_MAXCHUNKS);
   const int64_t tiles_per = ceil_div(stream_tiles, chunks);
   const int64_t P = ceil_div(stream_tiles, tiles_per);
   const int64_t n_pad = owner_tiles * BM;
