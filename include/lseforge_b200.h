@@ -74,6 +74,9 @@ typedef struct {
 /* CCE-: accumulate dE with red.global.add (non-deterministic bit order)
  * instead of the default deterministic bucket + ordered segment reduce. */
 #define LF_FLAG_ATOMIC_DE 1
+/* lf_cce_forward_backward: apply the filter to dX as well (separate dX pass,
+ * 3 exps per logit instead of 2). */
+#define LF_FLAG_FILTER_DX 2
 
 /* Backward statistics (device-side counters are copied into this host struct
  * only when the caller passes a non-NULL pointer; that forces a stream sync). */
@@ -105,6 +108,23 @@ LF_API int lf_cce_backward(const void* d_X, const void* d_E, const int64_t* d_ta
                     const double* d_lse, double upstream, int64_t n, int64_t d, int64_t v,
                     const lf_cce_config* cfg, void* d_dX, void* d_dE, lf_cce_stats* stats,
                     void* stream);
+
+/* Fused cce_forward + cce_backward: the pair run_loss_layer issues back to
+ * back on the same inputs (trainer.cpp:71-77, forward then backward with the
+ * forward's lse).  Writes everything lf_cce_forward and lf_cce_backward
+ * write.  For bf16 with d = 64 / 128 and filter_eps < 2^-12 it runs the
+ * fused kernel: one pass over the logits computes the LSE AND the
+ * softmax-weighted item sum of dX (2 exps per logit instead of 3), then the
+ * item-owned dE pass.  That dX is the exact (unfiltered) softmax - onehot
+ * gradient — the filter drops entries below eps, so the two differ by less
+ * than eps per entry, and not at all for eps = 0 — while dE and the skip
+ * statistics follow the filter exactly.  LF_FLAG_FILTER_DX (or any other
+ * dtype / d / eps) runs the separate forward and backward instead. */
+LF_API int lf_cce_forward_backward(const void* d_X, const void* d_E, const int64_t* d_targets,
+                                   int64_t n, int64_t d, int64_t v, double upstream,
+                                   const lf_cce_config* cfg, double* d_lse, double* d_pos,
+                                   double* d_loss, void* d_dX, void* d_dE, lf_cce_stats* stats,
+                                   void* stream);
 
 /* ------------------------------------------------ catalog-sharded CCE ---- */
 /* Rank p owns E rows [v_offset, v_offset + v_shard) of a catalog of v_total
@@ -376,7 +396,8 @@ enum lf_kernel_kind {
   LF_K_CCEM_BWD = 5,   /* CCE- backward (rows pass + sort + segment reduce) */
   LF_K_AUX = 6,        /* combine / reduce / prep kernels */
   LF_K_EVAL = 7,       /* full-catalog ranking (rank + top-K) */
-  LF_K_COUNT = 8
+  LF_K_CCE_FWD_DX = 8, /* tcgen05 fused forward + dX accumulation (lf_cce_forward_backward) */
+  LF_K_COUNT = 9
 };
 LF_API int lf_profile_enable(int on);
 LF_API int lf_profile_read(int32_t kind, uint64_t* launches, double* total_ms);

@@ -8,7 +8,8 @@ this package is the host-side mirror of the reference interface.
 """
 from . import _capi
 from .accountant import MemAccountant, Report, ScalarKind
-from .cce import CceBackwardResult, CceConfig, cce_backward, cce_forward, kFp16MinPositive
+from .cce import (CceBackwardResult, CceConfig, cce_backward, cce_forward, cce_forward_backward,
+                  kFp16MinPositive)
 from .ccem import (Backend, FlopEstimate, backend_is_sampled, ccem_backward, ccem_backward_rows,
                    ccem_forward, estimate_flops)
 from .losses import (GradPair, LossOutput, ce_full_backward, ce_full_forward, ce_sampled_backward,
@@ -18,7 +19,8 @@ from .metrics import EvalSummary, evaluate
 from .sampler import sample_popularity, sample_uniform
 
 __all__ = [
-    "CceConfig", "CceBackwardResult", "cce_forward", "cce_backward", "kFp16MinPositive",
+    "CceConfig", "CceBackwardResult", "cce_forward", "cce_backward", "cce_forward_backward",
+    "kFp16MinPositive",
     "ccem_forward", "ccem_backward", "ccem_backward_rows", "estimate_flops", "FlopEstimate",
     "Backend", "backend_is_sampled", "LossOutput", "GradPair", "validate_loss_inputs",
     "MemAccountant", "Report", "ScalarKind", "sample_uniform", "sample_popularity", "ce_full_forward",

@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("LSEFORGE_B200_LIB") or os.path.join(_HERE, "liblsefor
 
 LF_OK, LF_EINVAL, LF_EUNSUPPORTED, LF_ECUDA, LF_ENOMEM, LF_ERUNTIME = 0, -1, -2, -3, -4, -5
 LF_F32, LF_F64, LF_BF16 = 0, 1, 2
-LF_FLAG_NONE, LF_FLAG_ATOMIC_DE = 0, 1
+LF_FLAG_NONE, LF_FLAG_ATOMIC_DE, LF_FLAG_FILTER_DX = 0, 1, 2
 
 # Every symbol include/lseforge_b200.h declares (checked by tests/test_capi.py).
 EXPORTS = (
@@ -29,10 +29,10 @@ EXPORTS = (
     "lf_evaluate", "lf_adam_step", "lf_encode_batch", "lf_encoder_backward", "lf_peer_alloc",
     "lf_peer_open", "lf_peer_close", "lf_peer_free", "lf_peer_barrier", "lf_peer_sum",
     "lf_cce_forward_partial_peer", "lf_cce_backward_shard_peer", "lf_sample_popularity",
-    "lf_cem_forward", "lf_cem_backward",
+    "lf_cem_forward", "lf_cem_backward", "lf_cce_forward_backward",
 )
 KERNEL_KINDS = ("cce_fwd", "cce_bwd_dx", "cce_bwd_de", "cce_simt", "ccem_fwd", "ccem_bwd", "aux",
-                "eval")
+                "eval", "cce_fwd_dx")
 
 
 class CceConfigC(C.Structure):
@@ -67,6 +67,8 @@ def lib():
         L.lf_cce_forward.argtypes = [vp, vp, vp, i64, i64, i64, cfgp, dp, dp, dp, vp]
         L.lf_cce_backward.argtypes = [vp, vp, vp, dp, C.c_double, i64, i64, i64, cfgp, vp, vp,
                                       stp, vp]
+        L.lf_cce_forward_backward.argtypes = [vp, vp, vp, i64, i64, i64, C.c_double, cfgp, dp, dp,
+                                              dp, vp, vp, stp, vp]
         L.lf_cce_forward_partial.argtypes = [vp, vp, vp, i64, i64, i64, i64, cfgp, vp, vp]
         L.lf_cce_combine.argtypes = [vp, C.c_int32, i64, dp, dp, dp, vp]
         L.lf_cce_backward_shard.argtypes = [vp, vp, vp, dp, C.c_double, i64, i64, i64, i64, i64,
@@ -128,7 +130,7 @@ def lib():
                      "lf_peer_alloc", "lf_peer_open", "lf_peer_close", "lf_peer_free",
                      "lf_peer_barrier", "lf_peer_sum", "lf_cce_forward_partial_peer",
                      "lf_cce_backward_shard_peer", "lf_sample_popularity", "lf_cem_forward",
-                     "lf_cem_backward"):
+                     "lf_cem_backward", "lf_cce_forward_backward"):
             getattr(L, name).restype = C.c_int
         if L.lf_abi_version() != 1:
             raise ImportError("liblseforge_b200.so ABI mismatch")

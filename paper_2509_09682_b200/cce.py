@@ -28,6 +28,7 @@ class CceConfig:
     filter_eps: float = 0.0
     workers: int = 0
     atomic_de: bool = False  # CCE- only: LF_FLAG_ATOMIC_DE
+    filter_dx: bool = False  # cce_forward_backward: filter dX too (LF_FLAG_FILTER_DX)
 
     @staticmethod
     def Fp16SaturationPreset() -> "CceConfig":  # cce.hpp:26-30
@@ -42,7 +43,8 @@ class CceConfig:
 
     def to_c(self, dtype: int) -> _capi.CceConfigC:
         return _capi.CceConfigC(float(self.filter_eps), dtype,
-                                _capi.LF_FLAG_ATOMIC_DE if self.atomic_de else 0)
+                                (_capi.LF_FLAG_ATOMIC_DE if self.atomic_de else 0)
+                                | (_capi.LF_FLAG_FILTER_DX if self.filter_dx else 0))
 
 
 @dataclass
@@ -131,3 +133,42 @@ def cce_backward(X: torch.Tensor, E: torch.Tensor, x: torch.Tensor, lse: torch.T
         res.skipped_tiles = int(st.skipped_tiles)
         res.total_tiles = int(st.total_tiles)
     return res
+
+
+def cce_forward_backward(X: torch.Tensor, E: torch.Tensor, x: torch.Tensor, upstream: float = 1.0,
+                         cfg: CceConfig = CceConfig(), acct: Optional[MemAccountant] = None,
+                         validate: bool = True, stats: bool = False):
+    """cce_forward then cce_backward(lse, upstream) on the same inputs — the
+    pair run_loss_layer issues (trainer.cpp:71-77) — as one call
+    (lf_cce_forward_backward).  bf16 with d = 64 / 128 and filter_eps < 2^-12
+    runs the fused kernel: the LSE and dX's softmax-weighted item sum in one
+    pass over the logits, then the dE pass; dX is then the unfiltered
+    gradient (each dropped entry is below eps), dE and the skip statistics
+    follow the filter.  Returns (LossOutput, CceBackwardResult)."""
+    validate_loss_inputs(X, E, x, check_range=validate)
+    cfg.validate()
+    n, d = X.shape
+    v = E.shape[0]
+    if acct is not None:
+        acct.record_ensure("retained/cce/pos_logits", n)  # cce.cpp:81-82
+        acct.record_ensure("retained/cce/lse", n)
+    base = _reset_peak() if acct is not None else 0
+    lse = torch.empty(n, dtype=torch.float64, device=X.device)
+    pos = torch.empty(n, dtype=torch.float64, device=X.device)
+    loss = torch.empty((), dtype=torch.float64, device=X.device)
+    gd = grad_dtype(X)
+    dX = torch.empty((n, d), dtype=gd, device=X.device)
+    dE = torch.empty((v, d), dtype=gd, device=X.device)
+    c = cfg.to_c(lf_dtype(X))
+    st = _capi.CceStatsC()
+    _capi.check(_capi.lib().lf_cce_forward_backward(
+        X.data_ptr(), E.data_ptr(), x.data_ptr(), n, d, v, float(upstream), C.byref(c),
+        lse.data_ptr(), pos.data_ptr(), loss.data_ptr(), dX.data_ptr(), dE.data_ptr(),
+        C.byref(st) if stats else None, _stream(X)))
+    _charge_scratch(acct, "scratch/cce/forward_backward", base)
+    res = CceBackwardResult(GradPair(dX, dE))
+    if stats:
+        res.skipped_fraction = float(st.skipped_fraction)
+        res.skipped_tiles = int(st.skipped_tiles)
+        res.total_tiles = int(st.total_tiles)
+    return LossOutput(loss, pos, lse), res

@@ -155,6 +155,15 @@ int check_bf16_d(int64_t d) {
   return LF_OK;
 }
 
+// The fused forward + dX kernel serves lf_cce_forward_backward when dX may
+// ignore the filter: bf16, d = 64 / 128, and eps below 2^-12 (entries it
+// would drop are < eps each; eps = 0 is exact) unless the caller asks for
+// the filtered dX pass (LF_FLAG_FILTER_DX).
+bool fused_fwdx(const lf_cce_config* cfg, int64_t d) {
+  return cfg->dtype == LF_BF16 && tc_fwdx_supported(static_cast<int>(d)) &&
+         cfg->filter_eps < 0x1p-12 && !(cfg->flags & LF_FLAG_FILTER_DX);
+}
+
 struct Counters {
   Scratch buf;
   int init(cudaStream_t st) {
@@ -265,6 +274,42 @@ int lf_cce_backward(const void* d_X, const void* d_E, const int64_t* d_targets,
                     void* stream) {
   return backward_impl(d_X, d_E, d_targets, d_lse, upstream, n, d, v, 0, v, cfg, d_dX, d_dE,
                        stats, as_stream(stream));
+}
+
+int lf_cce_forward_backward(const void* d_X, const void* d_E, const int64_t* d_targets, int64_t n,
+                            int64_t d, int64_t v, double upstream, const lf_cce_config* cfg,
+                            double* d_lse, double* d_pos, double* d_loss, void* d_dX, void* d_dE,
+                            lf_cce_stats* stats, void* stream) {
+  int rc = check_cfg(cfg);
+  if (!rc) rc = check_shapes(n, d, v);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  if (!fused_fwdx(cfg, d)) {
+    rc = lf_cce_forward(d_X, d_E, d_targets, n, d, v, cfg, d_lse, d_pos, d_loss, stream);
+    if (rc) return rc;
+    return lf_cce_backward(d_X, d_E, d_targets, d_lse, upstream, n, d, v, cfg, d_dX, d_dE, stats,
+                           stream);
+  }
+  const double scale = upstream / static_cast<double>(n);  // cce.cpp:174
+  {
+    Scratch part, opart, tgt;
+    int P = 0;
+    rc = tc_cce_fwdx_partials(d_X, d_E, d_targets, n, static_cast<int>(d), v, 0, part, opart, tgt,
+                              &P, st);
+    if (!rc)
+      rc = tc_fwdx_dx(part.as<float>(), opart.as<float>(), P, n, static_cast<int>(d), nullptr, d_E,
+                      tgt.as<int32_t>(), scale, d_lse, d_pos, static_cast<float*>(d_dX), st);
+    if (!rc && d_loss) rc = launch_mean_loss(d_lse, d_pos, n, d_loss, st);
+    if (rc) return rc;
+  }  // the O partials go back to the pool before the dE pass
+  Counters c;
+  rc = c.init(st);
+  if (!rc)
+    rc = tc_cce_backward(d_X, d_E, d_targets, d_lse, scale, cfg->filter_eps, n, static_cast<int>(d), v,
+                         0, nullptr, static_cast<float*>(d_dE), stats ? c.ptr() : nullptr, st);
+  if (rc) return rc;
+  if (stats) return read_stats(c, stats, n, v, st);
+  return LF_OK;
 }
 
 int lf_cce_forward_partial(const void* d_X, const void* d_E_shard, const int64_t* d_targets,

@@ -58,10 +58,26 @@ int peer_reduce_push(const float* part, int P, int64_t count, float* const* peer
 
 // With `push`, dX is not reduced into dX: the V-chunk reduction is fused with
 // the store of the rank's dX partial into every peer's slot (dX is scratch).
+// dX == nullptr: dE pass only (the fused forward produced dX); the skip
+// statistics are then counted by the dE pass.
 int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const double* lse,
                     double scale, double eps, int64_t n, int D, int64_t v, int64_t v_offset,
                     float* dX, float* dE, unsigned long long* counters, cudaStream_t st,
                     const PeerPush* push = nullptr);
+
+// Fused forward + unnormalised dX (FWDX mode; bf16, D = 64 / 128 only:
+// tc_fwdx_supported).  part: [P][n] float4 {m, s, t, has} in log2 units;
+// opart: [P][n][D] fp32 O = sum_j 2^(logit log2e - m) E_j over the chunk;
+// tgt: local target index per row (-1 outside the shard).
+int tc_fwdx_supported(int D);
+int tc_cce_fwdx_partials(const void* X, const void* E, const int64_t* targets, int64_t n, int D,
+                         int64_t v, int64_t v_offset, Scratch& part, Scratch& opart, Scratch& tgt,
+                         int* P_out, cudaStream_t st);
+// dX = scale (sum_p O_p 2^(m_p - lse2) - E_t) from those partials; lse_in ==
+// nullptr: lse2 from the partials themselves, lse_out / pos_out written.
+int tc_fwdx_dx(const float* part, const float* opart, int P, int64_t n, int D, const double* lse_in,
+               const void* E, const int32_t* tgt, double scale, double* lse_out, double* pos_out,
+               float* dX, cudaStream_t st);
 
 // EVAL-mode partials over the shard (bf16): Et = the rows' target item rows
 // (ceil(n/128)*128 rows), tl = clamped local target index; per (chunk, row)

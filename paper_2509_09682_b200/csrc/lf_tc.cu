@@ -77,6 +77,9 @@
 #ifndef LF_BN_BWD
 #define LF_BN_BWD 128
 #endif
+#ifndef LF_NWG_FWDX
+#define LF_NWG_FWDX 2
+#endif
 
 namespace lf {
 
@@ -84,7 +87,7 @@ namespace {
 
 constexpr int BM = 128;  // owner tile (TMEM lanes)
 
-enum Mode : int { FWD = 0, BWD_ROWS = 1, BWD_ITEMS = 2, EVAL = 3 };
+enum Mode : int { FWD = 0, BWD_ROWS = 1, BWD_ITEMS = 2, EVAL = 3, FWDX = 4 };
 constexpr int kEvalK = 16;  // largest per-row top-K the EVAL epilogue keeps
 // "no published k-th score yet" (the 0x80 byte-fill; below the key of any
 // score above -3.4e38)
@@ -145,9 +148,13 @@ struct Ring {
 
 template <int MODE>
 struct Geo {
-  static constexpr int BN = MODE == FWD ? LF_BN_FWD : (MODE == EVAL ? 128 : LF_BN_BWD);  // stream tile
-  static constexpr int NWG = MODE == FWD ? LF_NWG_FWD : (MODE == EVAL ? LF_NWG_EVAL : LF_NWG_BWD);  // epilogue WGs
-  // control warps: TMA producer, S-MMA issuer (+ the G-MMA issuer in the backward)
+  static constexpr int BN = MODE == FWD ? LF_BN_FWD : (MODE == EVAL || MODE == FWDX ? 128 : LF_BN_BWD);  // stream tile
+  static constexpr int NWG = MODE == FWD    ? LF_NWG_FWD
+                             : MODE == EVAL ? LF_NWG_EVAL
+                             : MODE == FWDX ? LF_NWG_FWDX
+                                            : LF_NWG_BWD;  // epilogue WGs
+  // control warps: TMA producer, S-MMA issuer (+ the G-MMA issuer in the
+  // backward and the fused forward)
   static constexpr int kCtrlWarps = MODE == FWD || MODE == EVAL ? 2 : 3;
   static constexpr int kThreads = 32 * kCtrlWarps + 128 * NWG;
   static constexpr int kEpiThreads = 128 * NWG;
@@ -176,7 +183,10 @@ struct Cfg {
   static constexpr int kEvalMerge = MODE == EVAL ? ((G::NWG - 1) * BM * kEvalStride + 2 * BM) * 4 : 0;
   static constexpr int kStagesFit = (200 * 1024 - kOwnerBytes - kOnesBytes - kEvalMerge) / kStageBytes;
   static constexpr int kStages = kStagesFit > 12 ? 12 : kStagesFit;
-  static constexpr int kNBMax = (MODE == FWD || MODE == EVAL ? 512 : 512 - D) / BN;  // S buffers in TMEM
+  // S buffers in TMEM; the rest holds the accumulators (one D-column O per
+  // epilogue warpgroup in FWDX, one dX / dE tile in the backward)
+  static constexpr int kNBMax =
+      (MODE == FWD || MODE == EVAL ? 512 : (MODE == FWDX ? 512 - G::NWG * D : 512 - D)) / BN;
   static constexpr int kNB = kNBMax > 8 ? 8 : kNBMax;
   static_assert(MODE == FWD || MODE == EVAL || kNB >= 2, "not enough TMEM for the backward pipeline");
   // every epilogue warpgroup holds one S buffer while it works on a tile
@@ -184,7 +194,8 @@ struct Cfg {
   static_assert(kNB >= G::NWG, "fewer TMEM S buffers than epilogue warpgroups");
   static constexpr int kAccCol = kNB * BN;
   static constexpr int kSmem = 1024 /*align slack*/ + kOwnerBytes + kOnesBytes + kStages * kStageBytes +
-                               1024 /*barriers*/ + (MODE == FWD ? (G::NWG - 1) * BM * 16 : 0) +
+                               1024 /*barriers*/ +
+                               (MODE == FWD ? (G::NWG - 1) * BM * 16 : (MODE == FWDX ? G::NWG * BM * 16 : 0)) +
                                kEvalMerge;
 };
 __device__ __forceinline__ float fma_log2(float v, float sub) { return fmaf(v, kLog2e, -sub); }
@@ -243,6 +254,36 @@ __device__ __forceinline__ float select_reg(const float (&r)[N], int idx) {
 #pragma unroll
   for (int j = 0; j < N; ++j) out = (j == idx) ? r[j] : out;
   return out;
+}
+
+// Rare path of the FWDX epilogue (a running-max rebase): multiply this
+// warp's 32 TMEM lanes over `ncols` fp32 columns (the O accumulator) or
+// `nwords` packed-bf16x2 columns (the tile's P already written) by each
+// lane's own factor f.  Warp-collective (tcgen05.ld/st are .sync.aligned).
+__device__ __noinline__ void tmem_scale_f32(uint32_t taddr, int ncols, float f) {
+  for (int c0 = 0; c0 < ncols; c0 += 16) {
+    uint32_t r[16];
+    LF_TMEM_LD16(taddr + c0, r);
+    tmem_ld_wait();
+#pragma unroll
+    for (int c = 0; c < 16; ++c) r[c] = __float_as_uint(__uint_as_float(r[c]) * f);
+    LF_TMEM_ST16(taddr + c0, r);
+  }
+  tmem_st_wait();
+}
+__device__ __noinline__ void tmem_scale_bf16(uint32_t taddr, int nwords, float f) {
+  for (int c0 = 0; c0 < nwords; c0 += 16) {
+    uint32_t r[16];
+    LF_TMEM_LD16(taddr + c0, r);
+    tmem_ld_wait();
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      const float lo = __uint_as_float(r[c] << 16), hi = __uint_as_float(r[c] & 0xffff0000u);
+      r[c] = pack_bf16x2(lo * f, hi * f);
+    }
+    LF_TMEM_ST16(taddr + c0, r);
+  }
+  tmem_st_wait();
 }
 
 // Work units (chunk, owner tile).  FWD / backward: round robin over the
@@ -321,7 +362,8 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
   uint64_t* owner_empty = owner_full + 1;
   uint64_t* acc_full = owner_empty + 1;
   uint64_t* acc_empty = acc_full + 1;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  uint64_t* o_done = acc_empty + 1;           // [2] FWDX: a warpgroup's O MMAs completed (per tile)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_done + 2);
   float4* merge = reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(bars) + 1024);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -340,6 +382,8 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
     mbar_init(owner_empty, 1);
     mbar_init(acc_full, 1);
     mbar_init(acc_empty, 4 * NWG);
+    mbar_init(&o_done[0], 1);
+    mbar_init(&o_done[1], 1);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -454,20 +498,24 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
       __syncwarp();
     }
     // 4 * NQ sub-tiles (4 warps x NQ column chunks) per 128 x BN tile
-    if (lane == 0 && MODE == BWD_ROWS && (FLAGS & kCount))
+    if (lane == 0 && (MODE == BWD_ROWS || MODE == BWD_ITEMS) && (FLAGS & kCount))
       atomicAdd(&p.counters[2], 4ull * NQ * tiles_seen);
   } else if (G::kCtrlWarps == 3 && warp == 2) {
-    // ==================== MMA issuer: G . stream (backward) ====================
+    // ============ MMA issuer: G . stream (backward) / P . stream (FWDX) ============
     // acc (dX_o or dE_o) += G(t) . stream(t): G is bf16 in S buffer b2, K step
     // kk (stream rows 16kk..16kk+15) at columns 8kk; B = the stream tile viewed
     // K(stream rows) x N(D), MN-major SW128: 16 rows = 2048 B per K step, 64-col
     // D atoms BN*128 B apart.  Its commits free the stage and the S buffer.
+    // FWDX: every epilogue warpgroup has its own accumulator O_w (its own
+    // running max), tile t goes to O_(t mod NWG), and one commit per tile tells
+    // that warpgroup its O MMAs so far have completed (o_done, for rebases).
     constexpr uint32_t idesc2 = idesc_bf16(BM, D, 0, 1);
     constexpr uint32_t hi = umma_desc_hi_sw128(1024);
     const uint32_t b2_lo = umma_desc_lo(smem_u32(stage_smem), BN * 128);
     Ring<C::kStages> s2;
     Ring<C::kNB> b2;
     uint32_t j = 0;
+    int tw2 = 0;  // FWDX: the tile's warpgroup, continuing across units like the epilogue's
     const Units<MODE> U(p);
     for (int64_t u = U.begin; u < U.end; u += U.step, ++j) {
       const int64_t chunk = U.chunk(u);
@@ -475,21 +523,27 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
       const int64_t s_end = min(p.n_stream, s_begin + p.chunk);
       const int ntile = static_cast<int>(ceil_div(s_end - s_begin, BN));
       mbar_wait(acc_empty, (j & 1) ^ 1);
+      uint32_t fresh = (1u << NWG) - 1u;  // accumulators not yet written in this unit
       for (int i = 0; i < ntile; ++i, s2.next(), b2.next()) {
+        const int aw = MODE == FWDX ? tw2 : 0;
         mbar_wait(&g_ready[b2.i], b2.ph);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t lo = b2_lo + s2.i * (C::kStageBytes >> 4);
+          const uint32_t first = (fresh >> aw) & 1u;
 #pragma unroll
           for (int kk = 0; kk < BN / 16; ++kk) {
 #ifndef LF_DIAG_NOMMA2
-            mma_ts(tmem + C::kAccCol, tmem + b2.i * BN + kk * 8, umma_desc(lo + kk * 128, hi), idesc2,
-                   (i == 0 && kk == 0) ? 0u : 1u);
+            mma_ts(tmem + C::kAccCol + aw * D, tmem + b2.i * BN + kk * 8, umma_desc(lo + kk * 128, hi),
+                   idesc2, (first && kk == 0) ? 0u : 1u);
 #endif
           }
           mma_commit(&empty[s2.i]);
           mma_commit(&s_empty[b2.i]);
+          if (MODE == FWDX) mma_commit(&o_done[aw]);
         }
+        fresh &= ~(1u << aw);
+        if (MODE == FWDX) tw2 = tw2 + 1 == NWG ? 0 : tw2 + 1;
         __syncwarp();
       }
       if (lane == 0) mma_commit(acc_full);
@@ -506,6 +560,7 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
     Ring<C::kNB> rb;         // S buffer of the current tile
     Ring<C::kStages> rst;    // its smem stage (BWD_ITEMS staging)
     int tw = 0;              // current tile's warpgroup (t % NWG)
+    uint32_t k_tiles = 0;    // FWDX: tiles this warpgroup has handed to the O MMAs
     uint32_t j = 0;
     const Units<MODE> U(p);
     // EVAL state, carried across the consecutive units of one owner tile:
@@ -651,6 +706,95 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
           }
           s += sum;
           }
+        } else if (MODE == FWDX) {
+          // ---- fused forward + dX.  P = 2^(S log2e - m) against this
+          // warpgroup's running reference m: s += sum P is the forward's
+          // online LSE (cce.cpp:111-126) and P, rounded to bf16 into the
+          // already-read S columns (chunk q -> columns 16q..16q+15), feeds
+          // the TS-MMA O_wg += P E_t that warp 2 issues — the softmax-weighted
+          // item sum of dX, normalised by the combine once lse is known.  m is
+          // the first chunk's max and only moves when a chunk's sum would pass
+          // 2^64 (a logit ~44 nats above it): then s, the P chunks already
+          // written and O_wg (after its MMAs so far complete) are rescaled.
+          const int lc = tgt - static_cast<int>(col0);
+          bool waited = k_tiles == 0;  // o_done of this warpgroup's previous tile consumed
+          uint32_t ra[32], rc2[32];
+          LF_TMEM_LD32(ta, ra);
+          tmem_ld_wait();
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+            uint32_t(&cur)[32] = (q & 1) ? rc2 : ra;
+            uint32_t(&nxt)[32] = (q & 1) ? ra : rc2;
+            if (q + 1 < NQ) LF_TMEM_LD32(ta + (q + 1) * 32, nxt);
+            float v[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) v[c] = __uint_as_float(cur[c]);
+            if (nvalid < BN) {
+#pragma unroll
+              for (int c = 0; c < 32; ++c)
+                if (q * 32 + c >= nvalid) v[c] = -INFINITY;
+            }
+            if (static_cast<unsigned>(lc - q * 32) < 32u) {
+              tv = select_reg(v, lc - q * 32);
+              has = 1.f;
+            }
+            if (m == -INFINITY) m = max32(v) * kLog2e;  // -inf while no valid column was seen
+            float x[32];
+            float a0 = 0.f, a1 = 0.f;
+            {
+              const float mr = m == -INFINITY ? 0.f : m;
+#pragma unroll
+              for (int c = 0; c < 32; c += 2) {
+                x[c] = ex2_approx(fma_log2(v[c], mr));
+                x[c + 1] = ex2_approx(fma_log2(v[c + 1], mr));
+                a0 += x[c];
+                a1 += x[c + 1];
+              }
+            }
+            float sum = a0 + a1;
+            const bool over = !(sum <= 1.8446744e19f);  // > 2^64 or NaN
+            if (__any_sync(0xffffffffu, over)) {
+              float f = 1.f;
+              if (over) {
+                const float nm = fmaxf(m, max32(v) * kLog2e);
+                f = ex2_approx(m - nm);
+                m = nm;
+                a0 = 0.f;
+                a1 = 0.f;
+#pragma unroll
+                for (int c = 0; c < 32; c += 2) {
+                  x[c] = ex2_approx(fma_log2(v[c], m));
+                  x[c + 1] = ex2_approx(fma_log2(v[c + 1], m));
+                  a0 += x[c];
+                  a1 += x[c + 1];
+                }
+                sum = a0 + a1;
+                s *= f;
+              }
+              if (!waited) {
+                mbar_wait(&o_done[wg], (k_tiles - 1) & 1);
+                waited = true;
+              }
+              tc_fence_after();
+              if (q + 1 < NQ) tmem_ld_wait();  // the prefetch must land before the helpers' loads
+              tmem_scale_f32(tmem + lane_base + C::kAccCol + wg * D, D, f);
+              if (q > 0) tmem_scale_bf16(ta, 16 * q, f);
+            }
+            s += sum;
+            {
+              uint32_t g[16];
+#pragma unroll
+              for (int c = 0; c < 16; ++c) g[c] = pack_bf16x2(x[2 * c], x[2 * c + 1]);
+              LF_TMEM_ST16(ta + q * 16, g);
+            }
+            if (q + 1 < NQ) tmem_ld_wait();
+          }
+          tmem_st_wait();
+          if (!waited) mbar_wait(&o_done[wg], (k_tiles - 1) & 1);
+          ++k_tiles;
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&g_ready[b]);
         } else if (MODE == EVAL) {
           // ---- ranking (metrics.cpp:56-78).  An item ranks ahead of the
           // target if its score is higher, or equal with a smaller index: a
@@ -856,6 +1000,22 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
                 if (tgt_here && select_reg(e, jt) < kThr<FLAGS> && orow < p.n_owner) --skipped;
                 if (skip) ++skipped_sub;
               }
+              if ((FLAGS & kCount) && MODE == BWD_ITEMS) {
+                // the same statistic from the item side (the fused path has no
+                // dX pass): stream columns are rows, each row's own target
+                // entry (item = this lane's owner row) is never filtered
+#pragma unroll
+                for (int c = 0; c < 32; ++c)
+                  skipped += (e[c] < kThr<FLAGS> && q * 32 + c < nvalid && orow < p.n_owner) ? 1 : 0;
+                unsigned h = hm;
+                while (h) {  // warp-uniform
+                  const int jc = __ffs(h) - 1;
+                  h &= h - 1u;
+                  const int li = __shfl_sync(0xffffffffu, tq, jc);
+                  if (li == lrow && select_reg(e, jc) < kThr<FLAGS> && orow < p.n_owner) --skipped;
+                }
+                if (skip) ++skipped_sub;
+              }
             }
             float x[32];
             if (skip) {
@@ -1001,6 +1161,58 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
           }
         }
         named_bar_sync(1, G::kEpiThreads);
+      } else if (MODE == FWDX) {
+        // merge the warpgroups' (m, s, t) and their O accumulators per row:
+        // M = max m_w, O = sum_w O_w 2^(m_w - M) (a warpgroup without a tile
+        // in this unit has m_w = -inf and is left out), one fp32 partial row
+        // of D columns per (chunk, row) plus the float4 {M, S, t, has}
+        merge[wg * BM + lrow] = make_float4(m, s, tv, has);
+        named_bar_sync(1, G::kEpiThreads);
+        float mw[NWG], fw[NWG];
+        float M = -INFINITY, S = 0.f;
+#pragma unroll
+        for (int w = 0; w < NWG; ++w) {
+          const float4 o = merge[w * BM + lrow];
+          mw[w] = o.x;
+          M = fmaxf(M, o.x);
+          if (o.w != 0.f) {
+            tv = o.z;
+            has = 1.f;
+          }
+        }
+#pragma unroll
+        for (int w = 0; w < NWG; ++w) {
+          fw[w] = mw[w] == -INFINITY ? 0.f : ex2_approx(mw[w] - M);
+          S = fmaf(merge[w * BM + lrow].y, fw[w], S);
+        }
+        mbar_wait(acc_full, j & 1);
+        tc_fence_after();
+        float* dst = p.out + (chunk * p.n_owner + orow) * D;
+        for (int c0 = wg * 16; c0 < D; c0 += 16 * NWG) {
+          float o[16];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) o[c] = 0.f;
+#pragma unroll
+          for (int w = 0; w < NWG; ++w) {
+            uint32_t r16[16];
+            LF_TMEM_LD16(tmem + lane_base + C::kAccCol + w * D + c0, r16);
+            tmem_ld_wait();
+            if (mw[w] != -INFINITY) {
+#pragma unroll
+              for (int c = 0; c < 16; ++c) o[c] = fmaf(__uint_as_float(r16[c]), fw[w], o[c]);
+            }
+          }
+          if (orow < p.n_owner) {
+#pragma unroll
+            for (int c = 0; c < 16; c += 4)
+              *reinterpret_cast<float4*>(dst + c0 + c) = make_float4(o[c], o[c + 1], o[c + 2], o[c + 3]);
+          }
+        }
+        if (wg == 0 && orow < p.n_owner) p.part[chunk * p.n_owner + orow] = make_float4(M, S, tv, has);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty);
+        named_bar_sync(1, G::kEpiThreads);  // the merge records are rewritten by the next unit
       } else {
         // accumulator read-out: 16-column groups round robin over warpgroups
         mbar_wait(acc_full, j & 1);
@@ -1054,7 +1266,7 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
         if (lane == 0) mbar_arrive(acc_empty);
       }
     }
-    if ((FLAGS & kCount) && MODE == BWD_ROWS) {
+    if ((FLAGS & kCount) && (MODE == BWD_ROWS || MODE == BWD_ITEMS)) {
       for (int off = 16; off > 0; off >>= 1) skipped += __shfl_xor_sync(0xffffffffu, skipped, off);
       if (lane == 0 && skipped) atomicAdd(&p.counters[0], skipped);
       if (lane == 0 && skipped_sub) atomicAdd(&p.counters[1], skipped_sub);
@@ -1172,6 +1384,7 @@ int launch_mode(const CUtensorMap& mo, const CUtensorMap& ms, const CUtensorMap&
   const int grid = static_cast<int>(std::min<int64_t>(p.units, num_sms()));
   ProfScope prof(MODE == FWD    ? LF_K_CCE_FWD
                  : MODE == EVAL ? LF_K_EVAL
+                 : MODE == FWDX ? LF_K_CCE_FWD_DX
                  : (MODE == BWD_ROWS ? LF_K_CCE_BWD_DX : LF_K_CCE_BWD_DE),
                  st);
   kern<<<grid, Geo<MODE>::kThreads, C::kSmem, st>>>(mo, ms, mb, m1, p);
@@ -1236,7 +1449,126 @@ int64_t pick_chunks(int64_t owner_tiles, int64_t stream_tiles, int64_t max_chunk
   return best;
 }
 
+// dX from the FWDX partials, one warp per row.  The row's log2-domain LSE
+// comes from its own partials (lse_in == nullptr; also writes lse / pos with
+// combine_partials' double arithmetic) or from the given global lse (catalog
+// sharding: the local partials after the (m, s, t) exchange).  Then
+// dX_i = scale (sum_p O_p,i 2^(m_p,i - lse2_i) - [x_i local] E_(x_i))
+// (cce.cpp:189-231 with the target's -1 folded out of the tile loop).
+template <int D>
+__global__ void fwdx_dx(const float4* __restrict__ part, const float* __restrict__ opart, int P,
+                        int64_t n, const double* __restrict__ lse_in,
+                        const __nv_bfloat16* __restrict__ E, const int32_t* __restrict__ tgt,
+                        float scale, double* __restrict__ lse_out, double* __restrict__ pos_out,
+                        float* __restrict__ dX) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= n) return;
+  double lse2;
+  if (lse_in) {
+    lse2 = lse_in[row] * 1.4426950408889634;
+  } else {
+    double M = -INFINITY;
+    for (int p = 0; p < P; ++p) M = fmax(M, static_cast<double>(part[p * n + row].x));
+    double S = 0.0, t = 0.0;
+    for (int p = 0; p < P; ++p) {
+      const float4 q = part[p * n + row];
+      if (q.x != -INFINITY) S += static_cast<double>(q.y) * exp2(static_cast<double>(q.x) - M);
+      if (q.w != 0.f) t = static_cast<double>(q.z);
+    }
+    lse2 = M + log2(S);
+    if (lane == 0) {
+      lse_out[row] = lse2 * 0.6931471805599453;
+      pos_out[row] = t;
+    }
+  }
+  constexpr int CPL = D / 32;  // columns per lane
+  float acc[CPL];
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) acc[k] = 0.f;
+  for (int p = 0; p < P; ++p) {
+    const float mp = part[p * n + row].x;
+    if (mp == -INFINITY) continue;
+    const float w = static_cast<float>(exp2(static_cast<double>(mp) - lse2));
+    const float* o = opart + (p * n + row) * D;
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) acc[k] = fmaf(w, o[lane + 32 * k], acc[k]);
+  }
+  const int t = tgt[row];
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) {
+    const float et = t >= 0 ? __bfloat162float(E[static_cast<int64_t>(t) * D + lane + 32 * k]) : 0.f;
+    dX[row * D + lane + 32 * k] = scale * (acc[k] - et);
+  }
+}
+
 }  // namespace
+
+int tc_fwdx_supported(int D) { return D == 64 || D == 128; }
+
+// Fused forward + unnormalised dX over the local shard.  part: [P][n] float4
+// {m, s, t, has} (log2 units, as tc_cce_forward_partials); opart: [P][n][D]
+// fp32 O = sum over the chunk's items j of 2^(logit_ij log2e - m) E_j;
+// tgt: [ceil(n/128)*128] local target index or -1.
+int tc_cce_fwdx_partials(const void* X, const void* E, const int64_t* targets, int64_t n, int D,
+                         int64_t v, int64_t v_offset, Scratch& part, Scratch& opart, Scratch& tgt,
+                         int* P_out, cudaStream_t st) {
+  if (!tc_fwdx_supported(D)) return fail(LF_EUNSUPPORTED, "fused forward/dX: d must be 64 or 128");
+  constexpr int BN = Geo<FWDX>::BN;
+  const int64_t owner_tiles = ceil_div(n, BM);
+  const int64_t stream_tiles = ceil_div(v, BN);
+#ifndef LF_FWDX_MAXCHUNKS
+#define LF_FWDX_MAXCHUNKS 8
+#endif
+  const int64_t chunks = pick_chunks(owner_tiles, stream_tiles, LF_FWDX_MAXCHUNKS);
+  const int64_t tiles_per = ceil_div(stream_tiles, chunks);
+  const int64_t P = ceil_div(stream_tiles, tiles_per);
+  const int64_t n_pad = owner_tiles * BM;
+  int rc = tgt.alloc(sizeof(int32_t) * n_pad, st);
+  if (!rc) rc = part.alloc(sizeof(float4) * P * n, st);
+  if (!rc) rc = opart.alloc(sizeof(float) * P * n * D, st);
+  if (rc) return rc;
+  prep_rows<<<ceil_div(n_pad, 256), 256, 0, st>>>(targets, nullptr, n, n_pad, v, v_offset, 0.0,
+                                                 tgt.as<int32_t>(), nullptr);
+  LF_LAUNCHED();
+  CUtensorMap mo, ms;
+  rc = make_map(&mo, X, n, D, BM);
+  if (!rc) rc = make_map(&ms, E, v, D, BN);
+  if (rc) return rc;
+  TcParams p{};
+  p.n_owner = n;
+  p.n_stream = v;
+  p.owner_tiles = owner_tiles;
+  p.chunk = tiles_per * BN;
+  p.n_chunks = P;
+  p.units = owner_tiles * P;
+  p.tgt = tgt.as<int32_t>();
+  p.part = part.as<float4>();
+  p.out = opart.as<float>();
+  rc = D == 64 ? launch_mode<64, FWDX, 0>(mo, ms, mo, mo, p, st)
+               : launch_mode<128, FWDX, 0>(mo, ms, mo, mo, p, st);
+  if (rc) return rc;
+  *P_out = static_cast<int>(P);
+  return LF_OK;
+}
+
+int tc_fwdx_dx(const float* part, const float* opart, int P, int64_t n, int D, const double* lse_in,
+               const void* E, const int32_t* tgt, double scale, double* lse_out, double* pos_out,
+               float* dX, cudaStream_t st) {
+  const int64_t blocks = ceil_div(n, 8);
+  const float sc = static_cast<float>(scale);
+  const auto* pp = reinterpret_cast<const float4*>(part);
+  const auto* Eb = static_cast<const __nv_bfloat16*>(E);
+  ProfScope prof(LF_K_AUX, st);
+  if (D == 64)
+    fwdx_dx<64><<<blocks, 256, 0, st>>>(pp, opart, P, n, lse_in, Eb, tgt, sc, lse_out, pos_out, dX);
+  else if (D == 128)
+    fwdx_dx<128><<<blocks, 256, 0, st>>>(pp, opart, P, n, lse_in, Eb, tgt, sc, lse_out, pos_out, dX);
+  else
+    return fail(LF_EUNSUPPORTED, "fused forward/dX: d must be 64 or 128");
+  LF_LAUNCHED();
+  return LF_OK;
+}
 
 // Both fold the per-chunk partials and run the forward.
 int tc_cce_forward_partials(const void* X, const void* E, const int64_t* targets, int64_t n,
@@ -1329,7 +1661,7 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
                     float* dX, float* dE, unsigned long long* counters, cudaStream_t st,
                     const PeerPush* push) {
   if (scale == 0.0) {
-    LF_CUDA(cudaMemsetAsync(dX, 0, sizeof(float) * n * D, st));
+    if (dX) LF_CUDA(cudaMemsetAsync(dX, 0, sizeof(float) * n * D, st));
     LF_CUDA(cudaMemsetAsync(dE, 0, sizeof(float) * v * D, st));
     if (push) return peer_reduce_push(dX, 1, n * D, push->peers, push->world, push->rank, push->parity_off, st);
     return LF_OK;
@@ -1371,6 +1703,9 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
   if (rc) return rc;
 
   // ---- pass 1: dX (owner rows, stream items), V split into a few chunks ----
+  // (dX == nullptr: the caller has dX from the fused forward; the skip
+  // statistics are then counted by the dE pass)
+  if (dX) {
   const int64_t chunks = pick_chunks(row_tiles, item_stream, 8);
   const int64_t tiles_per = ceil_div(item_stream, chunks);
   const int64_t P = ceil_div(item_stream, tiles_per);
@@ -1405,6 +1740,7 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
   } else if (P > 1) {
     rc = launch_reduce_f32(dx_out, static_cast<int>(P), n * D, dX, st);
     if (rc) return rc;
+  }
   }
   // ---- pass 2: dE (owner items, stream rows) ----
   TcParams q{};
@@ -1447,7 +1783,7 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
   rc = make_map_k16(&mbias, bias.ptr, n_pad, BN);
   if (!rc) rc = make_map_k16(&mones, ones.ptr, BM, BM);
   if (rc) return rc;
-  rc = launch_d<BWD_ITEMS>(D, flags, me_own, mx_str, mbias, mones, q, st);
+  rc = launch_d<BWD_ITEMS>(D, dX ? (flags & ~kCount) : flags, me_own, mx_str, mbias, mones, q, st);
   return rc;
 }
 

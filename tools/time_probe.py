@@ -17,6 +17,7 @@ ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--eps", type=float, default=0.0)
 ap.add_argument("--ccem", type=int, default=0)
 ap.add_argument("--once", type=int, default=0)
+ap.add_argument("--fused", type=int, default=0, help="time lf_cce_forward_backward")
 a = ap.parse_args()
 
 g = torch.Generator(device="cuda").manual_seed(0)
@@ -48,6 +49,31 @@ if a.ccem:
     tba = timed(lambda: lf.ccem_backward(X, E, inds, out.lse, 1.0, cfg2, validate=False), a.iters)
     print(f"ccem n={a.n} d={a.d} v={a.v} K={a.ccem}: fwd {tf:.3f} ms  bwd(det) {tb:.3f} ms  "
           f"bwd(atomic) {tba:.3f} ms  pos/s={a.n/(tf+tb)*1e3:.3e}")
+elif a.fused:
+    import ctypes as C
+    from paper_2509_09682_b200 import _capi
+    L = _capi.lib()
+    step = lambda: lf.cce_forward_backward(X, E, x, 1.0, cfg, validate=False)
+    if a.once:
+        step()
+        torch.cuda.synchronize()
+        sys.exit(0)
+    out, _ = step()
+    print("loss", float(out.loss))
+    t = timed(step, a.iters)
+    L.lf_profile_reset()
+    L.lf_profile_enable(1)
+    step()
+    torch.cuda.synchronize()
+    L.lf_profile_enable(0)
+    parts = []
+    for kind, name in enumerate(_capi.KERNEL_KINDS):
+        cnt, ms = C.c_uint64(), C.c_double()
+        L.lf_profile_read(kind, C.byref(cnt), C.byref(ms))
+        if cnt.value:
+            parts.append(f"{name} {ms.value:.3f}")
+    print(f"fused n={a.n} d={a.d} v={a.v} eps={a.eps}: {t:.3f} ms/step  pos/s={a.n/t*1e3:.3e}  "
+          f"[{', '.join(parts)}]")
 elif a.once:
     out = lf.cce_forward(X, E, x, cfg, validate=False)
     lf.cce_backward(X, E, x, out.lse, 1.0, cfg, validate=False, stats=False)
