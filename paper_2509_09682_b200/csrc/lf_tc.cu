@@ -247,10 +247,25 @@ __device__ __forceinline__ float max32(const float (&e)[32]) {
   return fmaxf(fmaxf(b[0], b[1]), fmaxf(b[2], b[3]));
 }
 
+// Max of the first nv (<= 32) entries of 32 raw fp32 registers (-inf if none).
+__device__ __forceinline__ float max32_valid(const uint32_t (&r)[32], int nv) {
+  float e[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) e[c] = c < nv ? __uint_as_float(r[c]) : -INFINITY;
+  return max32(e);
+}
+
 // Select r[idx] from a register array without dynamic indexing.
 template <int N>
 __device__ __forceinline__ float select_reg(const float (&r)[N], int idx) {
   float out = 0.f;
+#pragma unroll
+  for (int j = 0; j < N; ++j) out = (j == idx) ? r[j] : out;
+  return out;
+}
+template <int N>
+__device__ __forceinline__ uint32_t select_reg(const uint32_t (&r)[N], int idx) {
+  uint32_t out = 0u;
 #pragma unroll
   for (int j = 0; j < N; ++j) out = (j == idx) ? r[j] : out;
   return out;
@@ -284,6 +299,79 @@ __device__ __noinline__ void tmem_scale_bf16(uint32_t taddr, int nwords, float f
     LF_TMEM_ST16(taddr + c0, r);
   }
   tmem_st_wait();
+}
+
+// Out-of-line paths of the FWDX epilogue (warp-collective; tcgen05.ld/st are
+// .sync.aligned, so every lane of the warp calls them).  ta = the tile's S
+// buffer at this warp's lanes, o_addr = this warpgroup's O accumulator.
+
+// Rebase chunk q (valid columns nv) of the tile: lanes with `over` move their
+// reference to the chunk's max; P chunk q is recomputed from S (still intact
+// in TMEM), stored, and O and the P chunks already written are rescaled by
+// f = 2^(m - m_new).  Returns {m_new, f, sum of the chunk's P}.
+__device__ __noinline__ float4 fwdx_rebase(uint32_t ta, uint32_t o_addr, int D, int q, int nv, float m,
+                                           bool over) {
+  uint32_t r[32];
+  LF_TMEM_LD32(ta + q * 32, r);
+  tmem_ld_wait();
+  float f = 1.f, nm = m;
+  if (over) {
+    nm = fmaxf(m, max32_valid(r, nv) * kLog2e);
+    f = m == -INFINITY ? 0.f : ex2_approx(m - nm);
+  }
+  const float mr = nm == -INFINITY ? 0.f : nm;
+  float x[32], a = 0.f;
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    x[c] = c < nv ? ex2_approx(fma_log2(__uint_as_float(r[c]), mr)) : 0.f;
+    a += x[c];
+  }
+  uint32_t g[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) g[c] = pack_bf16x2(x[2 * c], x[2 * c + 1]);
+  LF_TMEM_ST16(ta + q * 16, g);
+  tmem_st_wait();
+  tmem_scale_f32(o_addr, D, f);
+  if (q > 0) tmem_scale_bf16(ta, 16 * q, f);
+  return make_float4(nm, f, a, 0.f);
+}
+
+// The target logit of rows whose target lies in this 128-column tile (read
+// before P overwrites the S columns).
+__device__ __noinline__ float2 fwdx_capture(uint32_t ta, int lc, float tv, float has) {
+#pragma unroll 1
+  for (int q = 0; q < 4; ++q) {
+    const bool here = static_cast<unsigned>(lc - q * 32) < 32u;
+    if (!__any_sync(0xffffffffu, here)) continue;
+    uint32_t r[32];
+    LF_TMEM_LD32(ta + q * 32, r);
+    tmem_ld_wait();
+    if (here) {
+      tv = __uint_as_float(select_reg(r, lc - q * 32));
+      has = 1.f;
+    }
+  }
+  return make_float2(tv, has);
+}
+
+// The catalog's last, partial tile (nvalid < 128 columns): capture, masked
+// max / P, rebase by max, store.  Returns the new {m, s, t, has}.
+__device__ __noinline__ float4 fwdx_tile_tail(uint32_t ta, uint32_t o_addr, int D, int nvalid, int lc,
+                                              float m, float s, float tv, float has) {
+  const float2 t2 = fwdx_capture(ta, lc, tv, has);
+#pragma unroll 1
+  for (int q = 0; q < 4; ++q) {
+    const int nv = nvalid - q * 32;
+    uint32_t r[32];
+    LF_TMEM_LD32(ta + q * 32, r);
+    tmem_ld_wait();
+    const float mm = max32_valid(r, nv) * kLog2e;
+    const bool over = mm > (m == -INFINITY ? -INFINITY : m + 64.f);
+    const float4 o = fwdx_rebase(ta, o_addr, D, q, nv, m, over);
+    m = o.x;
+    s = fmaf(s, o.y, o.z);
+  }
+  return make_float4(m, s, t2.x, t2.y);
 }
 
 // Work units (chunk, owner tile).  FWD / backward: round robin over the
@@ -718,76 +806,70 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
           // written and O_wg (after its MMAs so far complete) are rescaled.
           const int lc = tgt - static_cast<int>(col0);
           bool waited = k_tiles == 0;  // o_done of this warpgroup's previous tile consumed
-          uint32_t ra[32], rc2[32];
-          LF_TMEM_LD32(ta, ra);
-          tmem_ld_wait();
-#pragma unroll
-          for (int q = 0; q < NQ; ++q) {
-            uint32_t(&cur)[32] = (q & 1) ? rc2 : ra;
-            uint32_t(&nxt)[32] = (q & 1) ? ra : rc2;
-            if (q + 1 < NQ) LF_TMEM_LD32(ta + (q + 1) * 32, nxt);
-            float v[32];
-#pragma unroll
-            for (int c = 0; c < 32; ++c) v[c] = __uint_as_float(cur[c]);
-            if (nvalid < BN) {
-#pragma unroll
-              for (int c = 0; c < 32; ++c)
-                if (q * 32 + c >= nvalid) v[c] = -INFINITY;
+          const uint32_t o_addr = tmem + lane_base + C::kAccCol + wg * D;
+          if (nvalid < BN) {
+            // the catalog's last, partial tile: out of line (masking)
+            if (!waited) {
+              mbar_wait(&o_done[wg], (k_tiles - 1) & 1);
+              waited = true;
             }
-            if (static_cast<unsigned>(lc - q * 32) < 32u) {
-              tv = select_reg(v, lc - q * 32);
-              has = 1.f;
+            tc_fence_after();
+            const float4 r = fwdx_tile_tail(ta, o_addr, D, nvalid, lc, m, s, tv, has);
+            m = r.x;
+            s = r.y;
+            tv = r.z;
+            has = r.w;
+          } else {
+            if (__any_sync(0xffffffffu, static_cast<unsigned>(lc) < static_cast<unsigned>(BN))) {
+              const float2 r = fwdx_capture(ta, lc, tv, has);  // before P overwrites S
+              tv = r.x;
+              has = r.y;
             }
-            if (m == -INFINITY) m = max32(v) * kLog2e;  // -inf while no valid column was seen
-            float x[32];
-            float a0 = 0.f, a1 = 0.f;
-            {
-              const float mr = m == -INFINITY ? 0.f : m;
+            uint32_t ra[32], rc2[32];
+            LF_TMEM_LD32(ta, ra);
+            tmem_ld_wait();
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+              uint32_t(&cur)[32] = (q & 1) ? rc2 : ra;
+              uint32_t(&nxt)[32] = (q & 1) ? ra : rc2;
+              if (q + 1 < NQ) LF_TMEM_LD32(ta + (q + 1) * 32, nxt);
+              if (m == -INFINITY) {  // this warpgroup's first chunk of the unit
+                float e[32];
+#pragma unroll
+                for (int c = 0; c < 32; ++c) e[c] = __uint_as_float(cur[c]);
+                m = max32(e) * kLog2e;
+              }
+              float x[32];
+#pragma unroll
+              for (int c = 0; c < 32; ++c) x[c] = ex2_approx(fma_log2(__uint_as_float(cur[c]), m));
+              float a0 = 0.f, a1 = 0.f;
 #pragma unroll
               for (int c = 0; c < 32; c += 2) {
-                x[c] = ex2_approx(fma_log2(v[c], mr));
-                x[c + 1] = ex2_approx(fma_log2(v[c + 1], mr));
                 a0 += x[c];
                 a1 += x[c + 1];
               }
-            }
-            float sum = a0 + a1;
-            const bool over = !(sum <= 1.8446744e19f);  // > 2^64 or NaN
-            if (__any_sync(0xffffffffu, over)) {
-              float f = 1.f;
-              if (over) {
-                const float nm = fmaxf(m, max32(v) * kLog2e);
-                f = ex2_approx(m - nm);
-                m = nm;
-                a0 = 0.f;
-                a1 = 0.f;
-#pragma unroll
-                for (int c = 0; c < 32; c += 2) {
-                  x[c] = ex2_approx(fma_log2(v[c], m));
-                  x[c + 1] = ex2_approx(fma_log2(v[c + 1], m));
-                  a0 += x[c];
-                  a1 += x[c + 1];
+              const float sum = a0 + a1;
+              const bool over = !(sum <= 1.8446744e19f);  // > 2^64 or NaN
+              if (__any_sync(0xffffffffu, over)) {
+                // rare: move the reference; out of line, P chunk q stored there
+                if (q + 1 < NQ) tmem_ld_wait();
+                if (!waited) {
+                  mbar_wait(&o_done[wg], (k_tiles - 1) & 1);
+                  waited = true;
                 }
-                sum = a0 + a1;
-                s *= f;
-              }
-              if (!waited) {
-                mbar_wait(&o_done[wg], (k_tiles - 1) & 1);
-                waited = true;
-              }
-              tc_fence_after();
-              if (q + 1 < NQ) tmem_ld_wait();  // the prefetch must land before the helpers' loads
-              tmem_scale_f32(tmem + lane_base + C::kAccCol + wg * D, D, f);
-              if (q > 0) tmem_scale_bf16(ta, 16 * q, f);
-            }
-            s += sum;
-            {
-              uint32_t g[16];
+                tc_fence_after();
+                const float4 r = fwdx_rebase(ta, o_addr, D, q, 32, m, over);
+                m = r.x;
+                s = fmaf(s, r.y, r.z);
+              } else {
+                s += sum;
+                uint32_t g[16];
 #pragma unroll
-              for (int c = 0; c < 16; ++c) g[c] = pack_bf16x2(x[2 * c], x[2 * c + 1]);
-              LF_TMEM_ST16(ta + q * 16, g);
+                for (int c = 0; c < 16; ++c) g[c] = pack_bf16x2(x[2 * c], x[2 * c + 1]);
+                LF_TMEM_ST16(ta + q * 16, g);
+              }
+              if (q + 1 < NQ) tmem_ld_wait();
             }
-            if (q + 1 < NQ) tmem_ld_wait();
           }
           tmem_st_wait();
           if (!waited) mbar_wait(&o_done[wg], (k_tiles - 1) & 1);
