@@ -80,6 +80,12 @@
 #ifndef LF_NWG_FWDX
 #define LF_NWG_FWDX 2
 #endif
+#ifndef LF_BN_FWDX
+#define LF_BN_FWDX 128
+#endif
+#ifndef LF_FWDX_X2
+#define LF_FWDX_X2 1  // FWDX: packed FFMA2 exponent arguments and an FADD2 tree for the row sum
+#endif
 
 namespace lf {
 
@@ -115,7 +121,7 @@ struct TcParams {
   int64_t n_chunks;
   int64_t units;
   const int32_t* tgt;    // FWD/BWD_ROWS: per owner row (local item or -1); BWD_ITEMS: per stream row
-  const float* lse2;     // lse*log2e - log2|scale| per row (padded; +inf pad)
+  const float* lse2;     // lse*log2e - log2|scale| per row (padded; +inf pad); FWDX: logit bound
   float abs_scale;       // |upstream / n| in the kernel's (possibly rescaled) G domain
   float out_scale;       // multiplies the dX / dE accumulators on read-out
   const __nv_bfloat16* fix_rows;  // !kTgtIn read-out: BWD_ROWS E, BWD_ITEMS X (bf16)
@@ -148,7 +154,9 @@ struct Ring {
 
 template <int MODE>
 struct Geo {
-  static constexpr int BN = MODE == FWD ? LF_BN_FWD : (MODE == EVAL || MODE == FWDX ? 128 : LF_BN_BWD);  // stream tile
+  static constexpr int BN = MODE == FWD    ? LF_BN_FWD
+                            : MODE == FWDX ? LF_BN_FWDX
+                            : (MODE == EVAL ? 128 : LF_BN_BWD);  // stream tile
   static constexpr int NWG = MODE == FWD    ? LF_NWG_FWD
                              : MODE == EVAL ? LF_NWG_EVAL
                              : MODE == FWDX ? LF_NWG_FWDX
@@ -338,9 +346,9 @@ __device__ __noinline__ float4 fwdx_rebase(uint32_t ta, uint32_t o_addr, int D, 
 
 // The target logit of rows whose target lies in this 128-column tile (read
 // before P overwrites the S columns).
-__device__ __noinline__ float2 fwdx_capture(uint32_t ta, int lc, float tv, float has) {
+__device__ __noinline__ float2 fwdx_capture(uint32_t ta, int nq, int lc, float tv, float has) {
 #pragma unroll 1
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < nq; ++q) {
     const bool here = static_cast<unsigned>(lc - q * 32) < 32u;
     if (!__any_sync(0xffffffffu, here)) continue;
     uint32_t r[32];
@@ -356,11 +364,11 @@ __device__ __noinline__ float2 fwdx_capture(uint32_t ta, int lc, float tv, float
 
 // The catalog's last, partial tile (nvalid < 128 columns): capture, masked
 // max / P, rebase by max, store.  Returns the new {m, s, t, has}.
-__device__ __noinline__ float4 fwdx_tile_tail(uint32_t ta, uint32_t o_addr, int D, int nvalid, int lc,
-                                              float m, float s, float tv, float has) {
-  const float2 t2 = fwdx_capture(ta, lc, tv, has);
+__device__ __noinline__ float4 fwdx_tile_tail(uint32_t ta, uint32_t o_addr, int D, int nq, int nvalid,
+                                              int lc, float m, float s, float tv, float has) {
+  const float2 t2 = fwdx_capture(ta, nq, lc, tv, has);
 #pragma unroll 1
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < nq; ++q) {
     const int nv = nvalid - q * 32;
     uint32_t r[32];
     LF_TMEM_LD32(ta + q * 32, r);
@@ -450,8 +458,8 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
   uint64_t* owner_empty = owner_full + 1;
   uint64_t* acc_full = owner_empty + 1;
   uint64_t* acc_empty = acc_full + 1;
-  uint64_t* o_done = acc_empty + 1;           // [2] FWDX: a warpgroup's O MMAs completed (per tile)
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_done + 2);
+  uint64_t* o_done = acc_empty + 1;           // [4] FWDX: a warpgroup's O MMAs completed (per tile)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_done + 4);
   float4* merge = reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(bars) + 1024);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -470,8 +478,7 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
     mbar_init(owner_empty, 1);
     mbar_init(acc_full, 1);
     mbar_init(acc_empty, 4 * NWG);
-    mbar_init(&o_done[0], 1);
-    mbar_init(&o_done[1], 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&o_done[i], 1);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -672,6 +679,7 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
         if (MODE == BWD_ROWS) lse2 = p.lse2[orow];
       }
       float m = -INFINITY, s = 0.f, tv = 0.f, has = 0.f;
+      bool fast = false;  // FWDX: this warp's rows cannot overflow (set with m)
       float st = 0.f, st_dn = 0.f;  // EVAL: the row's target score
       if (MODE == EVAL && run_first) {
         // Seed the list with placeholders just below the k-th score another
@@ -814,65 +822,97 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
               waited = true;
             }
             tc_fence_after();
-            const float4 r = fwdx_tile_tail(ta, o_addr, D, nvalid, lc, m, s, tv, has);
+            const float4 r = fwdx_tile_tail(ta, o_addr, D, NQ, nvalid, lc, m, s, tv, has);
             m = r.x;
             s = r.y;
             tv = r.z;
             has = r.w;
           } else {
             if (__any_sync(0xffffffffu, static_cast<unsigned>(lc) < static_cast<unsigned>(BN))) {
-              const float2 r = fwdx_capture(ta, lc, tv, has);  // before P overwrites S
+              const float2 r = fwdx_capture(ta, NQ, lc, tv, has);  // before P overwrites S
               tv = r.x;
               has = r.y;
             }
             uint32_t ra[32], rc2[32];
             LF_TMEM_LD32(ta, ra);
             tmem_ld_wait();
+            if (m == -INFINITY) {  // this warpgroup's first tile of the unit
+              float e[32];
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-              uint32_t(&cur)[32] = (q & 1) ? rc2 : ra;
-              uint32_t(&nxt)[32] = (q & 1) ? ra : rc2;
-              if (q + 1 < NQ) LF_TMEM_LD32(ta + (q + 1) * 32, nxt);
-              if (m == -INFINITY) {  // this warpgroup's first chunk of the unit
-                float e[32];
+              for (int c = 0; c < 32; ++c) e[c] = __uint_as_float(ra[c]);
+              m = max32(e) * kLog2e;
+              // no logit exceeds the Cauchy-Schwarz bound |x_i| max_j |e_j|, so
+              // with m at most 64 below it no chunk sum can pass 2^64: such
+              // warps run the tile body without the per-chunk overflow check
+              fast = __all_sync(0xffffffffu, !(m < p.lse2[orow] - 64.f));
+            }
+            // CHECK: per-chunk overflow vote (rebase out of line); !CHECK:
+            // straight-line code, chunk q's pack / store overlaps chunk q+1's exps
+            auto body = [&](auto check_tag) {
+              constexpr bool CHECK = decltype(check_tag)::value;
 #pragma unroll
-                for (int c = 0; c < 32; ++c) e[c] = __uint_as_float(cur[c]);
-                m = max32(e) * kLog2e;
-              }
-              float x[32];
+              for (int q = 0; q < NQ; ++q) {
+                uint32_t(&cur)[32] = (q & 1) ? rc2 : ra;
+                uint32_t(&nxt)[32] = (q & 1) ? ra : rc2;
+                if (q + 1 < NQ) LF_TMEM_LD32(ta + (q + 1) * 32, nxt);
+                float x[32];
+#if LF_FWDX_X2
 #pragma unroll
-              for (int c = 0; c < 32; ++c) x[c] = ex2_approx(fma_log2(__uint_as_float(cur[c]), m));
-              float a0 = 0.f, a1 = 0.f;
+                for (int c = 0; c < 32; c += 2)
+                  ffma2(x[c], x[c + 1], __uint_as_float(cur[c]), __uint_as_float(cur[c + 1]), kLog2e, kLog2e,
+                        -m, -m);
 #pragma unroll
-              for (int c = 0; c < 32; c += 2) {
-                a0 += x[c];
-                a1 += x[c + 1];
-              }
-              const float sum = a0 + a1;
-              const bool over = !(sum <= 1.8446744e19f);  // > 2^64 or NaN
-              if (__any_sync(0xffffffffu, over)) {
-                // rare: move the reference; out of line, P chunk q stored there
-                if (q + 1 < NQ) tmem_ld_wait();
-                if (!waited) {
-                  mbar_wait(&o_done[wg], (k_tiles - 1) & 1);
-                  waited = true;
+                for (int c = 0; c < 32; ++c) x[c] = ex2_approx(x[c]);
+                const float sum = sum32_x2(x);
+#else
+#pragma unroll
+                for (int c = 0; c < 32; ++c) x[c] = ex2_approx(fma_log2(__uint_as_float(cur[c]), m));
+                float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+                for (int c = 0; c < 32; c += 2) {
+                  a0 += x[c];
+                  a1 += x[c + 1];
                 }
-                tc_fence_after();
-                const float4 r = fwdx_rebase(ta, o_addr, D, q, 32, m, over);
-                m = r.x;
-                s = fmaf(s, r.y, r.z);
-              } else {
-                s += sum;
-                uint32_t g[16];
+                const float sum = a0 + a1;
+#endif
+                bool stored = false;
+                if (CHECK) {
+                  const bool over = !(sum <= 1.8446744e19f);  // > 2^64 or NaN
+                  if (__any_sync(0xffffffffu, over)) {
+                    // rare: move the reference; out of line, P chunk q stored there
+                    if (q + 1 < NQ) tmem_ld_wait();
+                    if (!waited) {
+                      mbar_wait(&o_done[wg], (k_tiles - 1) & 1);
+                      waited = true;
+                    }
+                    tc_fence_after();
+                    const float4 r = fwdx_rebase(ta, o_addr, D, q, 32, m, over);
+                    m = r.x;
+                    s = fmaf(s, r.y, r.z);
+                    stored = true;
+                  }
+                }
+                if (!stored) {
+                  s += sum;
+                  uint32_t g[16];
 #pragma unroll
-                for (int c = 0; c < 16; ++c) g[c] = pack_bf16x2(x[2 * c], x[2 * c + 1]);
-                LF_TMEM_ST16(ta + q * 16, g);
+                  for (int c = 0; c < 16; ++c) g[c] = pack_bf16x2(x[2 * c], x[2 * c + 1]);
+                  LF_TMEM_ST16(ta + q * 16, g);
+                }
+                if (q + 1 < NQ) tmem_ld_wait();
               }
-              if (q + 1 < NQ) tmem_ld_wait();
+            };
+            if (fast) {
+              body(std::false_type{});
+            } else {
+              body(std::true_type{});
+              fast = __all_sync(0xffffffffu, !(m < p.lse2[orow] - 64.f));  // after a rebase
             }
           }
           tmem_st_wait();
+#ifndef LF_DIAG_NO_ODONE  // timing diagnostic only (unsafe if a rebase happens)
           if (!waited) mbar_wait(&o_done[wg], (k_tiles - 1) & 1);
+#endif
           ++k_tiles;
           tc_fence_before();
           __syncwarp();
@@ -1434,6 +1474,49 @@ __global__ void bias_columns(const double* __restrict__ lse, int64_t n, int64_t 
   for (int k = 0; k < 16; ++k) bias[i * 16 + k] = __float2bfloat16_rn(k < 3 ? c[k] : 0.f);
 }
 
+// max_j |E_j|_2 over the catalog (non-negative floats order like their bits).
+template <int D>
+__global__ void max_row_norm(const __nv_bfloat16* __restrict__ E, int64_t v, unsigned* __restrict__ out) {
+  float best = 0.f;
+  for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < v;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint4* r = reinterpret_cast<const uint4*>(E + j * D);
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < D / 8; ++k) {
+      const uint4 w = __ldg(r + k);
+      const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const float lo = __uint_as_float(u[h] << 16), hi = __uint_as_float(u[h] & 0xffff0000u);
+        acc = fmaf(lo, lo, fmaf(hi, hi, acc));
+      }
+    }
+    best = fmaxf(best, acc);
+  }
+  for (int o = 16; o > 0; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(sqrtf(best)));
+}
+
+// FWDX per-row overflow bound in log2 units: |x_i| max_j |e_j| log2e (plus a
+// rounding margin) bounds every logit of the row; padding rows get -inf.
+template <int D>
+__global__ void row_bounds(const __nv_bfloat16* __restrict__ X, int64_t n, int64_t n_pad,
+                           const unsigned* __restrict__ emax, float* __restrict__ bound) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n_pad) return;
+  float b = -INFINITY;
+  if (i < n) {
+    float acc = 0.f;
+    for (int k = 0; k < D; ++k) {
+      const float x = __bfloat162float(X[i * D + k]);
+      acc = fmaf(x, x, acc);
+    }
+    b = sqrtf(acc) * __uint_as_float(*emax) * kLog2e * (1.f + 0x1p-10f) + 1.f;
+  }
+  bound[i] = b;
+}
+
 __global__ void prep_rows(const int64_t* __restrict__ targets, const double* __restrict__ lse,
                           int64_t n, int64_t n_pad, int64_t v_shard, int64_t v_offset,
                           double lse_sub, int32_t* __restrict__ tgt,
@@ -1609,10 +1692,27 @@ int tc_cce_fwdx_partials(const void* X, const void* E, const int64_t* targets, i
   int rc = tgt.alloc(sizeof(int32_t) * n_pad, st);
   if (!rc) rc = part.alloc(sizeof(float4) * P * n, st);
   if (!rc) rc = opart.alloc(sizeof(float) * P * n * D, st);
+  Scratch bound;  // [n_pad] floats, then the catalog's max item norm
+  if (!rc) rc = bound.alloc(sizeof(float) * (n_pad + 1), st);
   if (rc) return rc;
   prep_rows<<<ceil_div(n_pad, 256), 256, 0, st>>>(targets, nullptr, n, n_pad, v, v_offset, 0.0,
                                                  tgt.as<int32_t>(), nullptr);
   LF_LAUNCHED();
+  unsigned* emax = reinterpret_cast<unsigned*>(bound.as<float>() + n_pad);
+  LF_CUDA(cudaMemsetAsync(emax, 0, sizeof(unsigned), st));
+  {
+    const auto* Eb = static_cast<const __nv_bfloat16*>(E);
+    const auto* Xb = static_cast<const __nv_bfloat16*>(X);
+    const int g = static_cast<int>(std::min<int64_t>(ceil_div(v, 256), 4 * num_sms()));
+    if (D == 64) {
+      max_row_norm<64><<<g, 256, 0, st>>>(Eb, v, emax);
+      row_bounds<64><<<ceil_div(n_pad, 256), 256, 0, st>>>(Xb, n, n_pad, emax, bound.as<float>());
+    } else {
+      max_row_norm<128><<<g, 256, 0, st>>>(Eb, v, emax);
+      row_bounds<128><<<ceil_div(n_pad, 256), 256, 0, st>>>(Xb, n, n_pad, emax, bound.as<float>());
+    }
+    LF_LAUNCHED();
+  }
   CUtensorMap mo, ms;
   rc = make_map(&mo, X, n, D, BM);
   if (!rc) rc = make_map(&ms, E, v, D, BN);
@@ -1625,10 +1725,15 @@ int tc_cce_fwdx_partials(const void* X, const void* E, const int64_t* targets, i
   p.n_chunks = P;
   p.units = owner_tiles * P;
   p.tgt = tgt.as<int32_t>();
+  p.lse2 = bound.as<float>();  // FWDX: the per-row overflow bound
   p.part = part.as<float4>();
   p.out = opart.as<float>();
+#ifdef LF_VARIANT_D64_ONLY
+  rc = launch_mode<64, FWDX, 0>(mo, ms, mo, mo, p, st);
+#else
   rc = D == 64 ? launch_mode<64, FWDX, 0>(mo, ms, mo, mo, p, st)
                : launch_mode<128, FWDX, 0>(mo, ms, mo, mo, p, st);
+#endif
   if (rc) return rc;
   *P_out = static_cast<int>(P);
   return LF_OK;
