@@ -150,6 +150,89 @@ LF_API int lf_cce_backward_shard(const void* d_X, const void* d_E_shard, const i
                           const lf_cce_config* cfg, void* d_dX_partial, void* d_dE_shard,
                           lf_cce_stats* stats, void* stream);
 
+/* ------------------------------- catalog sharding from C / C++ ---------- */
+/* The reference's only production caller of the loss (run_loss_layer,
+ * trainer.cpp:59-110) is C++; these entries let it shard the catalog over
+ * GPUs without PyTorch.  lf_comm is a stream-ordered communicator: an
+ * all-gather of `bytes` per rank (rank order) and an in-place float sum
+ * all-reduce.  Backends: NCCL (lf_comm_nccl: wraps an ncclComm_t the caller
+ * created, libnccl.so.2 bound at run time) and peer memory over CUDA IPC
+ * (lf_peer_comm_*: every rank maps every rank's exchange buffer; on an
+ * NVSwitch box the stores travel over NVLink).  Any other transport can
+ * fill the two callbacks itself. */
+typedef struct lf_comm {
+  void* ctx;
+  int32_t world, rank;
+  int (*allgather)(void* ctx, const void* d_send, void* d_recv, uint64_t bytes, void* stream);
+  int (*allreduce_sum_f32)(void* ctx, float* d_buf, uint64_t count, void* stream);
+} lf_comm;
+
+/* 1 if lf_cce_forward_backward (and the sharded variant) run the fused
+ * forward + dX kernel for this config and width, else 0. */
+LF_API int lf_cce_fused_supported(const lf_cce_config* cfg, int64_t d);
+
+/* nccl_comm: an ncclComm_t of `world` ranks (this process = `rank`). */
+LF_API int lf_comm_nccl(void* nccl_comm, int32_t world, int32_t rank, lf_comm* out);
+
+/* Peer-memory communicator.  create: allocate this rank's exchange buffer
+ * (two epoch halves of `world` slots of slot_bytes) and flags, export
+ * lf_peer_comm_handle_bytes() bytes of CUDA IPC handles into handle_out;
+ * the caller gathers every rank's handle block in rank order (any
+ * bootstrap), then open maps them and fills `out`.  Barriers are bounded:
+ * a peer that never arrives (LSEFORGE_PEER_TIMEOUT_MS, default 60 s) or
+ * raises lf_peer_comm_abort releases the others, and lf_peer_comm_status
+ * then reports LF_ERUNTIME instead of every rank spinning forever. */
+typedef struct lf_peer_comm lf_peer_comm;
+LF_API uint64_t lf_peer_comm_handle_bytes(void);
+LF_API int lf_peer_comm_create(uint64_t slot_bytes, int32_t world, int32_t rank, lf_peer_comm** out,
+                               void* handle_out);
+LF_API int lf_peer_comm_open(lf_peer_comm* pc, const void* all_handles, lf_comm* out);
+LF_API int lf_peer_comm_abort(lf_peer_comm* pc, void* stream);
+LF_API int lf_peer_comm_status(void);
+LF_API int lf_peer_comm_destroy(lf_peer_comm* pc);
+
+/* cce_forward over a catalog shard E [v_shard x d] = items [v_offset,
+ * v_offset + v_shard) of the full catalog, targets GLOBAL: local partials,
+ * one all-gather of n float4, combine -> every rank holds lse / pos / loss. */
+LF_API int lf_cce_forward_sharded(const void* d_X, const void* d_E_shard, const int64_t* d_targets,
+                                  int64_t n, int64_t d, int64_t v_shard, int64_t v_offset,
+                                  const lf_cce_config* cfg, const lf_comm* comm, double* d_lse,
+                                  double* d_pos, double* d_loss, void* stream);
+/* cce_backward over the shard: dE rows of the shard; dX summed over ranks
+ * (one all-reduce of n x d floats; bf16 / f32).  stats: this rank's counts
+ * (skipped_fraction of the GLOBAL n (v_total - 1): sum it over ranks). */
+LF_API int lf_cce_backward_sharded(const void* d_X, const void* d_E_shard, const int64_t* d_targets,
+                                   const double* d_lse, double upstream, int64_t n, int64_t d,
+                                   int64_t v_shard, int64_t v_offset, int64_t v_total,
+                                   const lf_cce_config* cfg, const lf_comm* comm, void* d_dX,
+                                   void* d_dE_shard, lf_cce_stats* stats, void* stream);
+/* Both, fused when lf_cce_fused_supported (one pass over the shard's logits
+ * for the LSE partials and dX's item sum, the all-gather, dX normalised by
+ * the global lse, the dE pass, the dX all-reduce). */
+LF_API int lf_cce_forward_backward_sharded(const void* d_X, const void* d_E_shard,
+                                           const int64_t* d_targets, int64_t n, int64_t d,
+                                           int64_t v_shard, int64_t v_offset, int64_t v_total,
+                                           double upstream, const lf_cce_config* cfg,
+                                           const lf_comm* comm, double* d_lse, double* d_pos,
+                                           double* d_loss, void* d_dX, void* d_dE_shard,
+                                           lf_cce_stats* stats, void* stream);
+/* The fused sharded step in two phases, for callers with their own
+ * collectives (e.g. torch.distributed): begin writes this shard's folded
+ * partials d_part[n] (float4 {m, s, t, has}, log2 units) and keeps the dX
+ * partials in *work; gather the ranks' d_part blocks (rank order) and call
+ * end, which writes lse / pos / loss, this shard's dX PARTIAL (sum it over
+ * ranks) and dE rows, and releases *work (lf_cce_work_free on abandon). */
+typedef struct lf_cce_work lf_cce_work;
+LF_API int lf_cce_fwdx_shard_begin(const void* d_X, const void* d_E_shard, const int64_t* d_targets,
+                                   int64_t n, int64_t d, int64_t v_shard, int64_t v_offset,
+                                   const lf_cce_config* cfg, float* d_part, lf_cce_work** work,
+                                   void* stream);
+LF_API int lf_cce_fwdx_shard_end(lf_cce_work* work, const float* d_parts, int32_t P, double upstream,
+                                 int64_t v_total, double* d_lse, double* d_pos, double* d_loss,
+                                 void* d_dX_partial, void* d_dE_shard, lf_cce_stats* stats,
+                                 void* stream);
+LF_API int lf_cce_work_free(lf_cce_work* work);
+
 /* ------------------------------- catalog sharding over peer memory ---- */
 /* The same two exchanges without NCCL: each rank maps every peer's exchange
  * buffer (CUDA IPC: lf_peer_alloc exports a cudaMalloc'd buffer as a 64-byte
@@ -174,6 +257,10 @@ LF_API int lf_peer_free(void* d_ptr);
  * `epoch` are done, then wait (stream-ordered, on the device) for all peers'. */
 LF_API int lf_peer_barrier(uint32_t* const* d_peer_flags, int32_t world, int32_t rank, uint32_t epoch,
                            void* stream);
+/* The barrier waits at most LSEFORGE_PEER_TIMEOUT_MS (default 60 s) per peer
+ * and then gives up instead of hanging the GPU; lf_peer_status returns
+ * LF_ERUNTIME if any barrier of this process gave up (synchronizes). */
+LF_API int lf_peer_status(void);
 LF_API int lf_peer_sum(const float* d_slots, int32_t world, int64_t count, float* d_out, void* stream);
 LF_API int lf_cce_forward_partial_peer(const void* d_X, const void* d_E_shard, const int64_t* d_targets,
                                        int64_t n, int64_t d, int64_t v_shard, int64_t v_offset,

@@ -29,7 +29,11 @@ EXPORTS = (
     "lf_evaluate", "lf_adam_step", "lf_encode_batch", "lf_encoder_backward", "lf_peer_alloc",
     "lf_peer_open", "lf_peer_close", "lf_peer_free", "lf_peer_barrier", "lf_peer_sum",
     "lf_cce_forward_partial_peer", "lf_cce_backward_shard_peer", "lf_sample_popularity",
-    "lf_cem_forward", "lf_cem_backward", "lf_cce_forward_backward",
+    "lf_cem_forward", "lf_cem_backward", "lf_cce_forward_backward", "lf_cce_fused_supported",
+    "lf_comm_nccl", "lf_peer_comm_handle_bytes", "lf_peer_comm_create", "lf_peer_comm_open",
+    "lf_peer_comm_abort", "lf_peer_comm_status", "lf_peer_comm_destroy", "lf_cce_forward_sharded",
+    "lf_cce_backward_sharded", "lf_cce_forward_backward_sharded", "lf_cce_fwdx_shard_begin",
+    "lf_cce_fwdx_shard_end", "lf_cce_work_free", "lf_peer_status",
 )
 KERNEL_KINDS = ("cce_fwd", "cce_bwd_dx", "cce_bwd_de", "cce_simt", "ccem_fwd", "ccem_bwd", "aux",
                 "eval", "cce_fwd_dx")
@@ -69,6 +73,12 @@ def lib():
                                       stp, vp]
         L.lf_cce_forward_backward.argtypes = [vp, vp, vp, i64, i64, i64, C.c_double, cfgp, dp, dp,
                                               dp, vp, vp, stp, vp]
+        L.lf_cce_fused_supported.argtypes = [cfgp, i64]
+        L.lf_cce_fwdx_shard_begin.argtypes = [vp, vp, vp, i64, i64, i64, i64, cfgp, vp,
+                                              C.POINTER(C.c_void_p), vp]
+        L.lf_cce_fwdx_shard_end.argtypes = [vp, vp, C.c_int32, C.c_double, i64, dp, dp, dp, vp, vp,
+                                            stp, vp]
+        L.lf_cce_work_free.argtypes = [vp]
         L.lf_cce_forward_partial.argtypes = [vp, vp, vp, i64, i64, i64, i64, cfgp, vp, vp]
         L.lf_cce_combine.argtypes = [vp, C.c_int32, i64, dp, dp, dp, vp]
         L.lf_cce_backward_shard.argtypes = [vp, vp, vp, dp, C.c_double, i64, i64, i64, i64, i64,
@@ -130,7 +140,9 @@ def lib():
                      "lf_peer_alloc", "lf_peer_open", "lf_peer_close", "lf_peer_free",
                      "lf_peer_barrier", "lf_peer_sum", "lf_cce_forward_partial_peer",
                      "lf_cce_backward_shard_peer", "lf_sample_popularity", "lf_cem_forward",
-                     "lf_cem_backward", "lf_cce_forward_backward"):
+                     "lf_cem_backward", "lf_cce_forward_backward", "lf_cce_fused_supported",
+                     "lf_cce_fwdx_shard_begin", "lf_cce_fwdx_shard_end", "lf_cce_work_free",
+                     "lf_peer_status", "lf_peer_comm_status"):
             getattr(L, name).restype = C.c_int
         if L.lf_abi_version() != 1:
             raise ImportError("liblseforge_b200.so ABI mismatch")

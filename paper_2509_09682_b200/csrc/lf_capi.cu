@@ -155,15 +155,6 @@ int check_bf16_d(int64_t d) {
   return LF_OK;
 }
 
-// The fused forward + dX kernel serves lf_cce_forward_backward when dX may
-// ignore the filter: bf16, d = 64 / 128, and eps below 2^-12 (entries it
-// would drop are < eps each; eps = 0 is exact) unless the caller asks for
-// the filtered dX pass (LF_FLAG_FILTER_DX).
-bool fused_fwdx(const lf_cce_config* cfg, int64_t d) {
-  return cfg->dtype == LF_BF16 && tc_fwdx_supported(static_cast<int>(d)) &&
-         cfg->filter_eps < 0x1p-12 && !(cfg->flags & LF_FLAG_FILTER_DX);
-}
-
 struct Counters {
   Scratch buf;
   int init(cudaStream_t st) {
@@ -236,6 +227,15 @@ using namespace lf;
 extern "C" {
 
 int lf_abi_version(void) { return LF_ABI_VERSION; }
+
+// The fused forward + dX kernel serves lf_cce_forward_backward when dX may
+// ignore the filter: bf16, d = 64 / 128, and eps below 2^-12 (entries it
+// would drop are < eps each; eps = 0 is exact) unless the caller asks for
+// the filtered dX pass (LF_FLAG_FILTER_DX).
+int lf_cce_fused_supported(const lf_cce_config* cfg, int64_t d) {
+  return cfg && cfg->dtype == LF_BF16 && tc_fwdx_supported(static_cast<int>(d)) &&
+         cfg->filter_eps < 0x1p-12 && !(cfg->flags & LF_FLAG_FILTER_DX);
+}
 const char* lf_last_error(void) { return g_last_error.c_str(); }
 
 int lf_cce_forward(const void* d_X, const void* d_E, const int64_t* d_targets, int64_t n,
@@ -284,7 +284,7 @@ int lf_cce_forward_backward(const void* d_X, const void* d_E, const int64_t* d_t
   if (!rc) rc = check_shapes(n, d, v);
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
-  if (!fused_fwdx(cfg, d)) {
+  if (!lf_cce_fused_supported(cfg, d)) {
     rc = lf_cce_forward(d_X, d_E, d_targets, n, d, v, cfg, d_lse, d_pos, d_loss, stream);
     if (rc) return rc;
     return lf_cce_backward(d_X, d_E, d_targets, d_lse, upstream, n, d, v, cfg, d_dX, d_dE, stats,

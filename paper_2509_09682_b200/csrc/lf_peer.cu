@@ -17,6 +17,7 @@
 // system-scope acquires.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -71,18 +72,35 @@ __global__ void reduce_push(const float* __restrict__ part, int P, int64_t count
   }
 }
 
-// One block: thread q < world signals peer q, then waits for peer q's signal.
-__global__ void peer_barrier(uint32_t* const* __restrict__ flags, int world, int rank, uint32_t epoch) {
+__device__ unsigned g_barrier_timeout = 0;  // a barrier gave up waiting (lf_peer_status)
+
+// One block: thread q < world signals peer q, then waits for peer q's signal
+// — for at most timeout_ns (a rank that died or raised an error before its
+// signal must not hang every other rank's GPU): then it records the timeout
+// and returns, and lf_peer_status reports it.
+__global__ void peer_barrier(uint32_t* const* __restrict__ flags, int world, int rank, uint32_t epoch,
+                             uint64_t timeout_ns) {
   const int q = threadIdx.x;
   if (q >= world) return;
   __threadfence_system();
   uint32_t* remote = flags[q] + rank;
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(remote), "r"(epoch) : "memory");
   const uint32_t* mine = flags[rank] + q;
-  uint32_t seen = 0;
-  do {
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+  for (uint32_t spin = 0;; ++spin) {
+    uint32_t seen;
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(seen) : "l"(mine) : "memory");
-  } while (static_cast<int32_t>(seen - epoch) < 0);
+    if (static_cast<int32_t>(seen - epoch) >= 0) return;
+    if ((spin & 255) == 0) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      if (t - t0 > timeout_ns) {
+        atomicExch(&g_barrier_timeout, 1u);
+        return;
+      }
+    }
+  }
 }
 
 __global__ void sum_slots(const float* __restrict__ slots, int world, int64_t count, float* __restrict__ out) {
@@ -157,8 +175,18 @@ LF_API int lf_peer_free(void* d_ptr) {
 LF_API int lf_peer_barrier(uint32_t* const* d_peer_flags, int32_t world, int32_t rank, uint32_t epoch,
                            void* stream) {
   if (world < 1 || world > 1024 || rank < 0 || rank >= world) return fail(LF_EINVAL, "lf_peer_barrier: bad world/rank");
-  peer_barrier<<<1, 32 * ((world + 31) / 32), 0, as_st(stream)>>>(d_peer_flags, world, rank, epoch);
+  const char* e = std::getenv("LSEFORGE_PEER_TIMEOUT_MS");
+  const double ms = e && std::atof(e) > 0 ? std::atof(e) : 60000.0;
+  peer_barrier<<<1, 32 * ((world + 31) / 32), 0, as_st(stream)>>>(d_peer_flags, world, rank, epoch,
+                                                                  static_cast<uint64_t>(ms * 1e6));
   LF_LAUNCHED();
+  return LF_OK;
+}
+
+LF_API int lf_peer_status(void) {
+  unsigned v = 0;
+  LF_CUDA(cudaMemcpyFromSymbol(&v, g_barrier_timeout, sizeof(v)));
+  if (v) return fail(LF_ERUNTIME, "peer exchange: lf_peer_barrier timed out waiting for a peer (LSEFORGE_PEER_TIMEOUT_MS)");
   return LF_OK;
 }
 

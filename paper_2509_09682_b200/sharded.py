@@ -85,6 +85,41 @@ class DeviceKernels:
         return dX, dE, s
 
 
+    # ---- the fused step (lf_cce_fwdx_shard_begin / _end) ----
+    def fused_supported(self, X, cfg: CceConfig) -> bool:
+        c = cfg.to_c(lf_dtype(X))
+        return bool(_capi.lib().lf_cce_fused_supported(C.byref(c), X.shape[1]))
+
+    def fwdx_begin(self, X, E_shard, targets, v_offset: int, cfg: CceConfig):
+        n, d = X.shape
+        part = torch.empty((n, 4), dtype=torch.float32, device=X.device)
+        c = cfg.to_c(lf_dtype(X))
+        work = C.c_void_p()
+        _capi.check(_capi.lib().lf_cce_fwdx_shard_begin(
+            X.data_ptr(), E_shard.data_ptr(), targets.data_ptr(), n, d, E_shard.shape[0], v_offset,
+            C.byref(c), part.data_ptr(), C.byref(work), _stream(X)))
+        return part, work
+
+    def fwdx_end(self, work, parts, X, E_shard, upstream, v_total, stats: bool):
+        P, n, _ = parts.shape
+        d = X.shape[1]
+        lse = torch.empty(n, dtype=torch.float64, device=X.device)
+        pos = torch.empty(n, dtype=torch.float64, device=X.device)
+        loss = torch.empty((), dtype=torch.float64, device=X.device)
+        dX = torch.empty((n, d), dtype=torch.float32, device=X.device)
+        dE = torch.empty((E_shard.shape[0], d), dtype=torch.float32, device=X.device)
+        st = _capi.CceStatsC()
+        _capi.check(_capi.lib().lf_cce_fwdx_shard_end(
+            work, parts.data_ptr(), P, float(upstream), v_total, lse.data_ptr(), pos.data_ptr(),
+            loss.data_ptr(), dX.data_ptr(), dE.data_ptr(), C.byref(st) if stats else None,
+            _stream(X)))
+        s = ShardStats(int(st.skipped_elems), int(st.skipped_tiles), int(st.total_tiles)) if stats else None
+        return LossOutput(loss, pos, lse), dX, dE, s
+
+    def fwdx_abandon(self, work):
+        _capi.lib().lf_cce_work_free(work)
+
+
 class DeviceEvalKernels:
     """The C-ABI evaluation kernels (metrics.py) on CUDA tensors."""
 
@@ -311,6 +346,50 @@ class ShardedCce:
         dist.all_gather_into_tensor(flat, part.contiguous(), group=self.group)
         return self.kernels.combine(flat.view((self.P, n) + tuple(part.shape[1:])))
 
+    def forward_backward(self, X, E_shard, targets, upstream: float = 1.0,
+                         cfg: CceConfig = CceConfig(), stats: bool = False):
+        """forward + backward(lse, upstream) as one step.  Where the fused
+        kernel applies (bf16, d = 64 / 128, eps < 2^-12, collective exchange)
+        the shard's LSE partials and dX's item sum come from one pass over its
+        logits (lf_cce_fwdx_shard_begin), then the all-gather of the (m, s, t)
+        triples, dX normalised by the global lse and the dE pass
+        (lf_cce_fwdx_shard_end), then the dX all-reduce.  Returns
+        (LossOutput, CceBackwardResult)."""
+        if E_shard.shape[0] != self.v_shard:
+            raise ValueError(f"sharded cce: rank {self.rank} expects {self.v_shard} item rows, "
+                             f"got {E_shard.shape[0]}")
+        fused = getattr(self.kernels, "fused_supported", None)
+        if self.exchange == "peer" or fused is None or not fused(X, cfg):
+            out = self.forward(X, E_shard, targets, cfg)
+            return out, self.backward(X, E_shard, targets, out.lse, upstream, cfg, stats)
+        part, work = self.kernels.fwdx_begin(X, E_shard, targets, self.v_begin, cfg)
+        try:
+            n = part.shape[0]
+            if self.P == 1:
+                parts = part.unsqueeze(0)
+            else:
+                flat = torch.empty((self.P * n, 4), dtype=part.dtype, device=part.device)
+                dist.all_gather_into_tensor(flat, part.contiguous(), group=self.group)
+                parts = flat.view(self.P, n, 4)
+        except Exception:
+            self.kernels.fwdx_abandon(work)
+            raise
+        out, dX, dE, st = self.kernels.fwdx_end(work, parts, X, E_shard, upstream, self.v_total, stats)
+        if self.P > 1:
+            dist.all_reduce(dX, op=dist.ReduceOp.SUM, group=self.group)
+        return out, self._with_stats(CceBackwardResult(GradPair(dX, dE)), st, X.shape[0], stats)
+
+    def _with_stats(self, res: CceBackwardResult, st, n: int, stats: bool) -> CceBackwardResult:
+        if stats:
+            cnt = torch.tensor([st.skipped_elems, st.skipped_tiles, st.total_tiles],
+                               dtype=torch.float64, device=res.grads.d_embeddings.device)
+            if self.P > 1:
+                dist.all_reduce(cnt, op=dist.ReduceOp.SUM, group=self.group)
+            off = n * (self.v_total - 1)
+            res.skipped_fraction = float(cnt[0]) / off if off else 0.0
+            res.skipped_tiles, res.total_tiles = int(cnt[1]), int(cnt[2])
+        return res
+
     def backward(self, X, E_shard, targets, lse, upstream: float = 1.0,
                  cfg: CceConfig = CceConfig(), stats: bool = True) -> CceBackwardResult:
         if self.exchange == "peer":
@@ -320,14 +399,4 @@ class ShardedCce:
                                                      self.v_total, cfg, stats)
             if self.P > 1:
                 dist.all_reduce(dX, op=dist.ReduceOp.SUM, group=self.group)
-        res = CceBackwardResult(GradPair(dX, dE))
-        if stats:
-            cnt = torch.tensor([st.skipped_elems, st.skipped_tiles, st.total_tiles],
-                               dtype=torch.float64, device=dX.device)
-            if self.P > 1:
-                dist.all_reduce(cnt, op=dist.ReduceOp.SUM, group=self.group)
-            n = X.shape[0]
-            off = n * (self.v_total - 1)
-            res.skipped_fraction = float(cnt[0]) / off if off else 0.0
-            res.skipped_tiles, res.total_tiles = int(cnt[1]), int(cnt[2])
-        return res
+        return self._with_stats(CceBackwardResult(GradPair(dX, dE)), st, X.shape[0], stats)

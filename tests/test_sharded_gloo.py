@@ -51,13 +51,35 @@ class OracleKernels:
                 ShardStats(int(sk), 0, 0))
 
 
+class FusedOracleKernels(OracleKernels):
+    """Test backend for ShardedCce.forward_backward's fused phases
+    (lf_cce_fwdx_shard_begin / _end): begin = the shard's folded (m, s, t)
+    partial, end = combine + the shard's dX partial and dE rows."""
+
+    def fused_supported(self, X, cfg):
+        return True
+
+    def fwdx_begin(self, X, E_shard, targets, v_offset, cfg):
+        return self.forward_partial(X, E_shard, targets, v_offset, cfg), (v_offset, E_shard, cfg)
+
+    def fwdx_end(self, work, parts, X, E_shard, upstream, v_total, stats):
+        v_offset, E_shard, cfg = work
+        out = self.combine(parts)
+        dX, dE, st = self.backward_shard(X, E_shard, None, out.lse, upstream, v_offset, v_total, cfg,
+                                         stats)
+        return out, dX, dE, st
+
+    def fwdx_abandon(self, work):
+        pass
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, seed, n, d, v, eps, q):
+def _worker(rank, world, port, seed, n, d, v, eps, q, fused=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -66,14 +88,18 @@ def _worker(rank, world, port, seed, n, d, v, eps, q):
         from paper_2509_09682_b200.sharded import ShardedCce, shard_bounds
         rng = ob.Rng(seed)
         inst = ob.make_instance(rng, n, d, v)
-        sh = ShardedCce(v, kernels=OracleKernels(inst.E, inst.C, inst.targets))
+        K = FusedOracleKernels if fused else OracleKernels
+        sh = ShardedCce(v, kernels=K(inst.E, inst.C, inst.targets))
         assert (sh.v_begin, sh.v_end) == shard_bounds(v, world, rank)
         X = torch.from_numpy(inst.E)
         E_shard = torch.from_numpy(np.ascontiguousarray(inst.C.T[sh.v_begin:sh.v_end]))
         x = torch.from_numpy(inst.targets)
         cfg = CceConfig(filter_eps=eps)
-        out = sh.forward(X, E_shard, x, cfg)
-        res = sh.backward(X, E_shard, x, out.lse, 1.0, cfg)
+        if fused:
+            out, res = sh.forward_backward(X, E_shard, x, 1.0, cfg, stats=True)
+        else:
+            out = sh.forward(X, E_shard, x, cfg)
+            res = sh.backward(X, E_shard, x, out.lse, 1.0, cfg)
         q.put((rank, sh.v_begin, sh.v_end, float(out.loss), out.lse.numpy(),
                out.pos_logits.numpy(), res.grads.d_embeddings.numpy(),
                res.grads.d_classifier.numpy(), res.skipped_fraction))
@@ -81,13 +107,13 @@ def _worker(rank, world, port, seed, n, d, v, eps, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("eps", [0.0, 1e-3])
-def test_two_rank_catalog_sharding_matches_unsharded(eps):
+@pytest.mark.parametrize("eps,fused", [(0.0, False), (1e-3, False), (0.0, True), (1e-3, True)])
+def test_two_rank_catalog_sharding_matches_unsharded(eps, fused):
     world, seed, n, d, v = 2, 4242, 23, 7, 101
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, seed, n, d, v, eps, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, seed, n, d, v, eps, q, fused))
              for r in range(world)]
     for p in procs:
         p.start()

@@ -69,3 +69,34 @@ def test_sharded_config_shapes_reduced_catalog(cuda, d, P, v, n):
     dX_o, dC_o, _, _ = ob.cce_backward(Eh, Ch, t, lse, 1.0, 6e-8)
     check_grad(dX, dX_o, torch.bfloat16, "dX")
     check_grad(torch.cat(dE), dC_o.T, torch.bfloat16, "dE")
+
+
+@pytest.mark.parametrize("d,P,v,n,eps", [(64, 2, 20011, 700, 6e-8), (64, 8, 100000, 512, 0.0),
+                                         (128, 4, 30000, 300, 6e-8)])
+def test_fused_sharded_phases_equal_oracle(cuda, d, P, v, n, eps):
+    """The fused sharded step (lf_cce_fwdx_shard_begin on every shard, the
+    ranks' (m, s, t) blocks gathered, lf_cce_fwdx_shard_end, dX partials
+    summed) — the exchange ShardedCce.forward_backward runs across ranks —
+    against the oracle; skip counts from the dE passes summed over shards."""
+    from paper_2509_09682_b200.sharded import DeviceKernels, shard_bounds
+    import paper_2509_09682_b200 as lf
+    X, E, x, Eh, Ch, t = instance(0xF5ED + P + d, n, d, v, torch.bfloat16)
+    cfg = lf.CceConfig(filter_eps=eps)
+    K = DeviceKernels()
+    assert K.fused_supported(X, cfg)
+    bounds = [shard_bounds(v, P, p) for p in range(P)]
+    begun = [K.fwdx_begin(X, E[b:e], x, b, cfg) for b, e in bounds]
+    parts = torch.stack([p for p, _ in begun])
+    dX, dE, skipped = None, [], 0
+    for (b, e), (_, work) in zip(bounds, begun):
+        out, dx, de, st = K.fwdx_end(work, parts, X, E[b:e], 1.0, v, True)
+        dX = dx if dX is None else dX + dx
+        dE.append(de)
+        skipped += st.skipped_elems
+    loss, pos, lse = ob.cce_forward(Eh, Ch, t)
+    assert ob.rel_err(float(out.loss), loss) < 1e-2
+    assert ob.rel_err(out.lse.cpu().numpy(), lse).max() < 1e-3
+    dX_o, dC_o, frac, _ = ob.cce_backward(Eh, Ch, t, lse, 1.0, eps)
+    check_grad(dX, dX_o, torch.bfloat16, "dX")
+    check_grad(torch.cat(dE), dC_o.T, torch.bfloat16, "dE")
+    assert abs(skipped / (n * (v - 1)) - frac) <= 2e-3
