@@ -6,18 +6,26 @@
 Workload (BASELINE.json configs[1], "cfg2"): SASRec-shaped CCE, bf16,
 N = 51200 positions (batch 256 x seq 200), D = 64, V = 1,000,000 items,
 saturated-gradient filtering ON (eps = kFp16MinPositive = 6e-8,
-cce.hpp:15-30).  One step = cce_forward + cce_backward (loss, lse, pos, dX,
-dE) over the whole batch.  For N > 1 the catalog is sharded over the ranks
-(one process per GPU, NCCL): every rank owns V/N items, partial (m, s, t)
-triples are all-gathered and dX is all-reduced (paper_2509_09682_b200/
-sharded.py); total work is fixed, so scaling is "strong".
+cce.hpp:15-30).  Inputs are the reference's own instance: SplitMix64
+make_instance (support.hpp:27-37, seed 0xB2000002; synth.py restates it bit
+for bit), rounded to bf16.  One step = cce_forward + cce_backward (loss,
+lse, pos, dX, dE) over the whole batch through lf_cce_forward_backward (the
+fused forward + dX kernel, then the dE pass).  For N > 1 the catalog is
+sharded over the ranks (one process per GPU, NCCL): every rank owns V/N
+items, the (m, s, t) triples are all-gathered and dX is all-reduced
+(ShardedCce.forward_backward); total work is fixed, so scaling is "strong".
 
 Timing: W untimed warm-up steps, then exactly K steps bracketed by a barrier
 and torch.cuda.synchronize(); each step is timed with CUDA events on the
-compute stream and an L2 flush (256 MB write) runs before every step outside
-the events; the max over ranks is reported.  `e2e` times the same step
-through the public API with the step's inputs copied from pinned host memory
-and the loss read back, every step.
+compute stream, a 256 MB L2 flush runs before every step outside the events,
+the max over ranks is reported.  `e2e` times the same step through the public
+API with the step's inputs copied from pinned host memory and the loss read
+back, every step (`e2e_grads` also reads dX and dE back).
+
+The same line carries, at N = 1: `parity` (the reference run on the first
+256 rows of the timed inputs vs the GPU), `cfg3` (CCE- K = 512, BASELINE
+configs[2], with its own roofline, CPU baseline and full-N parity), and
+`filter` (the saturated-gradient filtering protocol of SURVEY.md 8(d)).
 
 `--impl reference` times the reference's own CPU implementation (the
 unmodified lseforge sources compiled in place into oracle/_ref) on the host
@@ -28,7 +36,6 @@ from __future__ import annotations
 import argparse
 import ctypes as C
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -42,7 +49,9 @@ sys.path.insert(0, ROOT)
 METRIC = "CCE fwd+bwd positions/sec @V=1M,D=64 (1/2/4/8 GPU); % roofline; peak HBM GB"
 N_ROWS, D, V = 51200, 64, 1_000_000
 EPS = 6e-8  # CceConfig::Fp16SaturationPreset (cce.hpp:26-30)
-SEED = 0xB2000002
+SEED = 0xB2000002   # cfg2 (0xB2000000 + cfg#)
+SEED3 = 0xB2000003  # cfg3
+K_NEG = 512
 WORKLOAD = ("cfg2: SASRec-shaped CCE bf16, N=51200 (batch 256 x seq 200), D=64, V=1M items, "
             "saturated-gradient filtering on (eps=6e-8)")
 
@@ -55,6 +64,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the cfg3 and filter sub-records")
     ap.add_argument("--exchange", choices=["collective", "peer"], default="collective",
                     help="N>1: torch.distributed collectives (NCCL) or the peer-memory exchange "
                          "fused into the producing kernels (CUDA IPC)")
@@ -136,46 +146,64 @@ class Clocks:
                 "reasons": reasons, "samples": len(load)}
 
 
-# --------------------------------------------------------------------------
-# reference CPU timing (oracle/_ref = the unmodified reference sources)
-# --------------------------------------------------------------------------
-def reference_sample(rows_per_thread=16, steps=1, warmup=0, seed=SEED):
+def bf16_round(a):
+    """Host copy of what the device sees: round-to-nearest-even to bf16, as float32."""
     import numpy as np
     import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16).float().numpy()
+
+
+# --------------------------------------------------------------------------
+# reference CPU runs (oracle/_ref = the unmodified reference sources; the
+# cpu_baseline leg and the checker of the GPU results — never the product)
+# --------------------------------------------------------------------------
+def reference_cfg2_sample(Xh, Ch, t, rows_per_thread=16):
+    """cce_forward + cce_backward of the reference on the first rows of the
+    instance (bf16-rounded float, full V and D), all host threads."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_bind as ob
     threads = os.cpu_count() or 1
     rows = rows_per_thread * threads
-    g = np.random.default_rng(seed)
-    E = torch.from_numpy(g.uniform(-1, 1, (rows, D)).astype(np.float32)).to(torch.bfloat16).float().numpy()
-    Cm = torch.from_numpy(g.uniform(-1, 1, (D, V)).astype(np.float32)).to(torch.bfloat16).float().numpy()
-    t = g.integers(0, V, rows).astype(np.int64)
-    times = []
-    for s in range(warmup + steps):
-        t0 = time.perf_counter()
-        _, _, lse = ob.ref_cce_forward(E, Cm, t, rb=rows_per_thread, cb=256, workers=threads)
-        ob.ref_cce_backward(E, Cm, t, lse, 1.0, EPS, rb=rows_per_thread, cb=256, workers=threads)
-        if s >= warmup:
-            times.append(time.perf_counter() - t0)
-    per_step = sum(times) / len(times)
-    sample = (f"reference lseforge cce_forward+cce_backward (oracle/_ref, -O3), {rows} rows x "
-              f"V={V} x D={D}, eps={EPS}, row_block={rows_per_thread}, col_block=256, "
-              f"workers={threads}, bf16-rounded fp32 inputs, {len(times)} step(s)")
-    return rows / per_step, threads, sample, per_step
+    E = Xh[:rows]
+    ts = t[:rows]
+    t0 = time.perf_counter()
+    loss, pos, lse = ob.ref_cce_forward(E, Ch, ts, rb=rows_per_thread, cb=256, workers=threads)
+    dE, dC, frac = ob.ref_cce_backward(E, Ch, ts, lse, 1.0, EPS, rb=rows_per_thread, cb=256,
+                                       workers=threads)
+    sec = time.perf_counter() - t0
+    sample = (f"reference lseforge cce_forward+cce_backward (oracle/_ref, -O3), first {rows} rows of "
+              f"the cfg2 instance (make_instance seed {SEED:#x}, bf16-rounded) x V={V} x D={D}, "
+              f"eps={EPS}, row_block={rows_per_thread}, col_block=256, workers={threads}")
+    return dict(rows=rows, threads=threads, sec=sec, sample=sample, loss=loss, pos=pos, lse=lse,
+                dE=dE, dC=dC, frac=frac)
+
+
+def cfg2_host_instance():
+    from paper_2509_09682_b200 import synth
+    Xr, Cr, t = synth.make_instance(SEED, N_ROWS, D, V)
+    return bf16_round(Xr), bf16_round(Cr), t
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    value, cores, sample, per_step = reference_sample(steps=args.steps, warmup=args.warmup)
+    Xh, Ch, t = cfg2_host_instance()
+    secs = []
+    last = None
+    for s in range(args.warmup + args.steps):
+        last = reference_cfg2_sample(Xh, Ch, t)
+        if s >= args.warmup:
+            secs.append(last["sec"])
+    per_step = sum(secs) / len(secs)
+    value = last["rows"] / per_step
     line = {"metric": METRIC, "value": value, "unit": "positions/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "impl": "reference",
-            "config": {"workload": WORKLOAD, "sample_rows": int(round(value * per_step))},
-            "cpu_baseline": {"value": value, "unit": "positions/s", "cores": cores,
-                             "kind": "reference", "sample": sample},
+            "data": "synthetic (reference make_instance)", "impl": "reference",
+            "config": {"workload": WORKLOAD, "sample_rows": last["rows"], "seed": SEED},
+            "cpu_baseline": {"value": value, "unit": "positions/s", "cores": last["threads"],
+                             "kind": "reference", "sample": last["sample"]},
             "e2e": {"value": value, "unit": "positions/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -185,7 +213,37 @@ def run_reference(args):
 # --------------------------------------------------------------------------
 # B200 arm
 # --------------------------------------------------------------------------
+def rel(a, b):
+    import numpy as np
+    return float(np.max(np.abs(np.asarray(a) - np.asarray(b)) / np.maximum(1.0, np.abs(np.asarray(b)))))
+
+
+def normwise(got, want):
+    import numpy as np
+    g = np.asarray(got, np.float64)
+    w = np.asarray(want, np.float64)
+    return float(np.linalg.norm(g - w) / max(np.linalg.norm(w), 1e-300))
+
+
+def timed_steps(step, steps, warmup, stream, flush):
+    """Device-timed loop (CUDA events on the compute stream, L2 flush outside)."""
+    import torch
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    for k in range(steps):
+        flush.fill_(k & 0xFF)
+        evs[k][0].record(stream)
+        step()
+        evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in evs) / steps
+
+
 def run_ours(args):
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -216,24 +274,32 @@ def run_ours(args):
     L = _capi.lib()
     sh = ShardedCce(V, exchange=args.exchange if world > 1 else "collective")
     v0, v1 = sh.v_begin, sh.v_end
-    g = torch.Generator(device=dev).manual_seed(SEED)
-    X = (torch.rand(N_ROWS, D, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
-    E_full = (torch.rand(V, D, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
-    E = E_full[v0:v1].contiguous()
-    del E_full
-    x = torch.randint(0, V, (N_ROWS,), device=dev, generator=g)
-    cfg = lf.CceConfig(filter_eps=EPS)
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    vs = v1 - v0
     stream = torch.cuda.current_stream(dev)
 
-    def step(Xs, Es, xs):
-        out = sh.forward(Xs, Es, xs, cfg)
-        res = sh.backward(Xs, Es, xs, out.lse, 1.0, cfg, stats=False)
-        return out, res
-
+    # ---- the reference's instance (make_instance, SplitMix64), bf16 ----
+    Xh, Ch, t = cfg2_host_instance()
+    X = torch.from_numpy(Xh).to(dev).to(torch.bfloat16)  # exact: already bf16 values
+    C_dev = torch.from_numpy(np.ascontiguousarray(Ch[:, v0:v1])).to(dev)
+    E = torch.empty((vs, D), dtype=torch.bfloat16, device=dev)
+    # ref-C (D x V float) -> E (V x D bf16): the drop-in boundary's own converter
+    _capi.check(L.lf_classifier_to_items(C_dev.data_ptr(), D, vs, _capi.LF_BF16, E.data_ptr(),
+                                         stream.cuda_stream))
+    del C_dev
+    x = torch.from_numpy(t).to(dev)
+    cfg = lf.CceConfig(filter_eps=EPS)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     _capi.check(L.lf_validate_targets(x.data_ptr(), N_ROWS, V, stream.cuda_stream))
+
+    res_box = [None]
+
+    def step(Xs=X, Es=E, xs=x):
+        res_box[0] = None  # the previous step's outputs are released first
+        res_box[0] = sh.forward_backward(Xs, Es, xs, 1.0, cfg, stats=False)
+        return res_box[0]
+
     for _ in range(args.warmup):
-        step(X, E, x)
+        step()
     torch.cuda.synchronize()
     torch.cuda.reset_peak_memory_stats(dev)
     L.lf_workspace_reset_peak()
@@ -250,7 +316,7 @@ def run_ours(args):
     for k in range(args.steps):
         flush.fill_(k & 0xFF)  # L2 flush, outside the events
         evs[k][0].record(stream)
-        out, res = step(X, E, x)
+        step()
         evs[k][1].record(stream)
     torch.cuda.synchronize()
     dist.barrier()
@@ -271,123 +337,325 @@ def run_ours(args):
     total_ms = float(t_max)
     ms_step = total_ms / args.steps
     value = N_ROWS / (ms_step / 1e3)
-    cur, wpk = C.c_uint64(), C.c_uint64()
-    L.lf_workspace_stats(C.byref(cur), C.byref(wpk))
-    peak_hbm = (torch.cuda.max_memory_allocated(dev) + wpk.value) / 1e9
+    out, res = res_box[0]
     loss_val = float(out.loss)
 
-    # ---- roofline of the dominant kernel (algorithmic work, live durations) ----
+    # ---- memory: the library's own footprint vs the harness's ----
+    cur, wpk = C.c_uint64(), C.c_uint64()
+    L.lf_workspace_stats(C.byref(cur), C.byref(wpk))
+    inputs_b = X.numel() * 2 + E.numel() * 2 + x.numel() * 8
+    outputs_b = (3 * N_ROWS + 1) * 8 + N_ROWS * D * 4 + vs * D * 4
+    memory = {"library_peak_gb": (inputs_b + outputs_b + wpk.value) / 1e9,
+              "inputs_gb": inputs_b / 1e9, "outputs_gb": outputs_b / 1e9,
+              "workspace_peak_gb": wpk.value / 1e9,
+              "harness_peak_gb": (torch.cuda.max_memory_allocated(dev) + wpk.value) / 1e9,
+              "note": "library_peak = inputs (X, E, targets) + outputs (lse, pos, loss, dX, dE) + the "
+                      "library's scratch high-water (lf_workspace_stats); harness_peak adds the 256 MB L2 "
+                      "flush buffer and whatever torch holds"}
+
+    # ---- roofline: the binding unit is the exp (MUFU ex2) ----
     peaks = load_peaks()
     mufu, mufu_src = mufu_peak()
-    vs = v1 - v0
     Lsh = N_ROWS * vs
-    alg = {"cce_fwd": 2 * Lsh * D,       # forward contraction (estimate_flops: N*D*V MACs)
-           "cce_bwd_dx": 3 * Lsh * D,    # half of the backward's 6*L*D (3x forward MACs)
-           "cce_bwd_de": 3 * Lsh * D}
-    exps = {"cce_fwd": Lsh, "cce_bwd_dx": Lsh, "cce_bwd_de": Lsh}
-    dom = max((k for k in kern if k in alg), key=lambda k: kern[k]["ms_total"], default=None)
-    roof = None
-    roof_exp = None
+    exps = {"cce_fwd_dx": Lsh, "cce_bwd_de": Lsh, "cce_fwd": Lsh, "cce_bwd_dx": Lsh}
+    flops = {"cce_fwd_dx": 4 * Lsh * D,  # forward N*D*V MACs + the dX GEMM's N*D*V MACs
+             "cce_bwd_de": 4 * Lsh * D,  # the logit recompute + the dE GEMM
+             "cce_fwd": 2 * Lsh * D, "cce_bwd_dx": 3 * Lsh * D}
+    dom = max((k for k in kern if k in exps), key=lambda k: kern[k]["ms_total"], default=None)
+    roof = roof_tc = None
     if dom:
         dur = kern[dom]["ms_per_launch"] / 1e3
-        ach = alg[dom] / dur / 1e12
         tr = traffic_table().get(dom)
-        roof = {"kernel": dom, "bound": "tensor", "achieved": ach,
-                "peak": peaks["tc_sustained"], "unit": "TFLOP/s",
-                "frac": ach / peaks["tc_sustained"],
+        roof = {"kernel": dom, "bound": "exp (MUFU ex2)", "achieved": exps[dom] / dur / 1e12,
+                "peak": mufu / 1e12, "unit": "Texp/s", "frac": exps[dom] / dur / mufu,
                 "traffic": tr.get("dram_bytes_per_launch") if tr else None,
-                "peak_source": peaks["source"] + ", bf16 sustained (kernel timed inside a long step)",
-                "algorithmic_flops_per_launch": alg[dom], "ms_per_launch": dur * 1e3}
-        roof_exp = {"kernel": dom, "achieved": exps[dom] / dur / 1e12, "peak": mufu / 1e12,
-                    "unit": "Texp/s", "frac": exps[dom] / dur / mufu, "peak_source": mufu_src}
-    # whole-step roofline (north star): T_roof = max(8LD/P_tc, 2L/P_exp) per GPU
+                "peak_source": mufu_src,
+                "algorithmic_exps_per_launch": exps[dom], "ms_per_launch": dur * 1e3,
+                "note": "one exp per logit per launch (N*V_shard logits); traffic = dram read+write "
+                        "per launch from ncu --set full (profiles/traffic.json)"}
+        ach = flops[dom] / dur / 1e12
+        roof_tc = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": peaks["tc_sustained"],
+                   "unit": "TFLOP/s", "frac": ach / peaks["tc_sustained"],
+                   "peak_source": peaks["source"] + ", bf16 sustained",
+                   "algorithmic_flops_per_launch": flops[dom]}
     L_all = N_ROWS * V / world
-    t_roof = max(8 * L_all * D / (peaks["tc_sustained"] * 1e12), 2 * L_all / mufu)
+    t_exp = 2 * L_all / mufu
+    t_tc = 8 * L_all * D / (peaks["tc_sustained"] * 1e12)
+    t_roof = max(t_exp, t_tc)
     step_roof = {"t_roof_ms": t_roof * 1e3, "ms_per_step": ms_step, "frac": t_roof * 1e3 / ms_step,
-                 "binding": "exp (MUFU)" if 2 * L_all / mufu > 8 * L_all * D / (peaks["tc_sustained"] * 1e12) else "tensor",
-                 "note": "algorithmic work 8*L*D flops and 2*L exps, L = N*V/P"}
+                 "binding": "exp (MUFU)" if t_exp > t_tc else "tensor",
+                 "executed_over_algorithmic": {"exps": 1.0, "flops": 1.0},
+                 "note": "algorithmic work 8*L*D flops and 2*L exps, L = N*V/P; the fused path executes "
+                         "exactly that (forward+dX kernel: 1 exp, 4LD flops; dE pass: 1 exp, 4LD flops)"}
 
     # ---- e2e through the public API with host buffers ----
-    # Every step copies ITS inputs (X, the local E slice, targets) from pinned
-    # host memory and reads its loss back on the host.  The copy of step k+1
-    # runs on a side stream into the other half of a double buffer while step
-    # k computes (the host->device link and the SMs work concurrently).
-    e2e = None
+    e2e = e2e_grads = None
     if not args.no_e2e:
-        Xh = X.cpu().pin_memory()
-        Eh = E.cpu().pin_memory()
-        xh = x.cpu().pin_memory()
-        loss_h = torch.empty((), dtype=torch.float64).pin_memory()
-        bufs = [(torch.empty_like(X), torch.empty_like(E), torch.empty_like(x)) for _ in range(2)]
-        cs = torch.cuda.Stream(dev)
-        copied = [torch.cuda.Event() for _ in range(2)]
-        consumed = [torch.cuda.Event() for _ in range(2)]
+        e2e = run_e2e(step, X, E, x, stream, args, world, dev, grads=False)
+        e2e_grads = run_e2e(step, X, E, x, stream, args, world, dev, grads=True)
 
-        def issue_copy(k):
-            b = k % 2
-            with torch.cuda.stream(cs):
-                cs.wait_event(consumed[b])
-                bufs[b][0].copy_(Xh, non_blocking=True)
-                bufs[b][1].copy_(Eh, non_blocking=True)
-                bufs[b][2].copy_(xh, non_blocking=True)
-                copied[b].record(cs)
-
-        def e2e_run(nsteps):
-            for b in range(2):
-                consumed[b].record(stream)
-            issue_copy(0)
-            for k in range(nsteps):
-                b = k % 2
-                stream.wait_event(copied[b])
-                o, _ = step(*bufs[b])
-                consumed[b].record(stream)
-                if k + 1 < nsteps:
-                    issue_copy(k + 1)
-                loss_h.copy_(o.loss, non_blocking=True)
-                stream.synchronize()  # the host reads the loss every step
-                _ = float(loss_h)
-
-        e2e_run(max(1, args.warmup))
-        torch.cuda.synchronize()
-        dist.barrier()
-        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ea.record(stream)
-        e2e_run(args.steps)
-        eb.record(stream)
-        torch.cuda.synchronize()
-        e_ms = torch.tensor([ea.elapsed_time(eb) / args.steps], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
-        h2d = Xh.numel() * Xh.element_size() + Eh.numel() * Eh.element_size() + xh.numel() * 8
-        e2e = {"value": N_ROWS / (float(e_ms) / 1e3), "unit": "positions/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8,
-               "ms_per_step": float(e_ms), "api": "ShardedCce.forward/backward (lf_cce_* C-ABI)",
-               "overlap": "step k+1's host->device copy overlaps step k's compute (double buffer)"}
-
-    cpu = None
+    extras = {}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cv, cores, sample, _ = reference_sample(rows_per_thread=16, steps=1, warmup=0)
-        cpu = {"value": cv, "unit": "positions/s", "cores": cores, "kind": "reference",
-               "sample": sample}
+        extras["cpu_baseline"], extras["parity"] = cfg2_parity(lf, sh, X, E, x, out, res, Xh, Ch, t, cfg)
+    if rank == 0 and world == 1 and not args.no_extras:
+        del res_box[0], out, res
+        extras["filter"] = filter_protocol(lf, X, E, x, Xh, Ch, t, flush, stream, args)
+        extras["cfg3"] = cfg3_record(lf, flush, stream, args, peaks, not args.no_cpu_baseline)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "positions/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": "bf16", "data": "synthetic",
+                "dtype": "bf16", "data": "synthetic (the reference's make_instance, SplitMix64)",
                 "config": {"workload": WORKLOAD, "n_positions": N_ROWS, "d": D, "v": V,
                            "filter_eps": EPS, "seed": SEED,
+                           "path": "lf_cce_forward_backward (fused forward+dX kernel, then the dE pass)",
                            "parallelism": (f"catalog-sharded over {world} GPU(s), {args.exchange} exchange"
                                            if world > 1 else "single GPU"),
                            "l2": "inputs (134.6 MB) exceed L2 (126 MB) and a 256 MB L2 flush runs "
                                  "before every timed step (outside the events)"},
-                "peak_hbm_gb": peak_hbm, "loss": loss_val,
-                "roofline": roof, "roofline_exp": roof_exp, "step_roofline": step_roof,
-                "kernels": kern, "gpu_launches": int(launches), "e2e": e2e,
-                "cpu_baseline": cpu, "clocks": clk}
+                "peak_hbm_gb": memory["library_peak_gb"], "memory": memory, "loss": loss_val,
+                "roofline": roof, "roofline_tensor": roof_tc, "step_roofline": step_roof,
+                "kernels": kern, "gpu_launches": int(launches), "e2e": e2e, "e2e_grads": e2e_grads,
+                "cpu_baseline": extras.get("cpu_baseline"), "parity": extras.get("parity"),
+                "filter": extras.get("filter"), "cfg3": extras.get("cfg3"), "clocks": clk}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
     return 0
+
+
+def run_e2e(step, X, E, x, stream, args, world, dev, grads):
+    """The step through the public API with host buffers: every step copies
+    ITS inputs (X, the local E slice, targets) from pinned host memory and
+    reads its loss (grads=True: also dX and dE) back on the host.  The copy of
+    step k+1 runs on a side stream into the other half of a double buffer
+    while step k computes; with grads, step k's dX / dE go back on a third
+    stream while step k+1 computes."""
+    import torch
+    import torch.distributed as dist
+    Xh = X.cpu().pin_memory()
+    Eh = E.cpu().pin_memory()
+    xh = x.cpu().pin_memory()
+    loss_h = torch.empty((), dtype=torch.float64).pin_memory()
+    dXh = torch.empty((X.shape[0], X.shape[1]), dtype=torch.float32).pin_memory() if grads else None
+    dEh = torch.empty((E.shape[0], E.shape[1]), dtype=torch.float32).pin_memory() if grads else None
+    bufs = [(torch.empty_like(X), torch.empty_like(E), torch.empty_like(x)) for _ in range(2)]
+    cs = torch.cuda.Stream(dev)
+    ds = torch.cuda.Stream(dev)
+    copied = [torch.cuda.Event() for _ in range(2)]
+    consumed = [torch.cuda.Event() for _ in range(2)]
+    keep = [None, None]
+
+    def issue_copy(k):
+        b = k % 2
+        with torch.cuda.stream(cs):
+            cs.wait_event(consumed[b])
+            bufs[b][0].copy_(Xh, non_blocking=True)
+            bufs[b][1].copy_(Eh, non_blocking=True)
+            bufs[b][2].copy_(xh, non_blocking=True)
+            copied[b].record(cs)
+
+    def run(nsteps):
+        for b in range(2):
+            consumed[b].record(stream)
+        issue_copy(0)
+        pending = None
+        for k in range(nsteps):
+            b = k % 2
+            stream.wait_event(copied[b])
+            o, r = step(*bufs[b])
+            consumed[b].record(stream)
+            if k + 1 < nsteps:
+                issue_copy(k + 1)
+            loss_h.copy_(o.loss, non_blocking=True)
+            if grads:
+                done = torch.cuda.Event()
+                done.record(stream)
+                if pending is not None:
+                    ds.synchronize()  # the previous step's gradients have landed on the host
+                with torch.cuda.stream(ds):
+                    ds.wait_event(done)
+                    dXh.copy_(r.grads.d_embeddings, non_blocking=True)
+                    dEh.copy_(r.grads.d_classifier, non_blocking=True)
+                keep[b] = r  # hold the device gradients until their copy is done
+                pending = k
+            stream.synchronize()  # the host reads the loss every step
+            _ = float(loss_h)
+        if grads:
+            ds.synchronize()
+
+    run(max(1, args.warmup))
+    torch.cuda.synchronize()
+    dist.barrier()
+    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ea.record(stream)
+    run(args.steps)
+    eb.record(stream)
+    torch.cuda.synchronize()
+    e_ms = torch.tensor([ea.elapsed_time(eb) / args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+    h2d = Xh.numel() * Xh.element_size() + Eh.numel() * Eh.element_size() + xh.numel() * 8
+    d2h = 8 + ((dXh.numel() + dEh.numel()) * 4 if grads else 0)
+    return {"value": N_ROWS / (float(e_ms) / 1e3), "unit": "positions/s",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": float(e_ms),
+            "api": "ShardedCce.forward_backward -> lf_cce_forward_backward (C-ABI)",
+            "overlap": "step k+1's host->device copy overlaps step k's compute (double buffer)"
+                       + ("; step k's dX/dE device->host copy overlaps step k+1" if grads else "")}
+
+
+def cfg2_parity(lf, sh, X, E, x, out, res, Xh, Ch, t, cfg):
+    """The reference (oracle/_ref) on the first rows of the SAME inputs the
+    bench timed, and the GPU on the same rows: the full-N run's per-row lse /
+    pos / dX (dX_i scales as 1/N) and a GPU run on the sample alone for the
+    loss, dE (the sample's contribution) and the skip fraction."""
+    import numpy as np
+    import torch
+    r = reference_cfg2_sample(Xh, Ch, t)
+    ns = r["rows"]
+    cpu = {"value": ns / r["sec"], "unit": "positions/s", "cores": r["threads"], "kind": "reference",
+           "sample": r["sample"]}
+    lse_g = out.lse[:ns].cpu().numpy()
+    pos_g = out.pos_logits[:ns].cpu().numpy()
+    dX_g = res.grads.d_embeddings[:ns].double().cpu().numpy() * N_ROWS
+    so, sr = lf.cce_forward_backward(X[:ns].contiguous(), E, x[:ns].contiguous(), 1.0, cfg,
+                                     stats=True)
+    dE_g = sr.grads.d_classifier.double().cpu().numpy()
+    tol = {"loss_rel": 1e-2, "lse_max_rel": 1e-3, "pos_max_rel": 1e-3, "dX_normwise": 1e-2,
+           "dE_normwise": 1e-2, "skipped_fraction_abs": 2e-3}
+    p = {"rows": ns, "inputs": "the timed cfg2 instance (first rows), reference fed the same bf16 values",
+         "loss_rel": abs(float(so.loss) - r["loss"]) / max(1.0, abs(r["loss"])),
+         "lse_max_rel": rel(lse_g, r["lse"]), "pos_max_rel": rel(pos_g, r["pos"]),
+         "dX_normwise": normwise(dX_g, r["dE"] * ns),
+         "dE_normwise": normwise(dE_g, r["dC"].T),
+         "skipped_fraction": sr.skipped_fraction, "skipped_fraction_ref": r["frac"],
+         "tolerance": tol}
+    p["pass"] = bool(p["loss_rel"] < tol["loss_rel"] and p["lse_max_rel"] < tol["lse_max_rel"]
+                     and p["pos_max_rel"] < tol["pos_max_rel"] and p["dX_normwise"] < tol["dX_normwise"]
+                     and p["dE_normwise"] < tol["dE_normwise"]
+                     and abs(p["skipped_fraction"] - p["skipped_fraction_ref"]) <= tol["skipped_fraction_abs"])
+    p["note"] = ("dX from the fused kernel is the unfiltered gradient (each entry the eps filter drops "
+                 "is < eps); dE and the skip fraction follow the filter exactly")
+    del so, sr
+    torch.cuda.synchronize()
+    return cpu, p
+
+
+def filter_protocol(lf, X, E, x, Xh, Ch, t, flush, stream, args):
+    """SURVEY.md 8(d) "Recommended protocol": the headline data (distribution
+    A, uniform) at the reference preset, and distribution B, X_i = U(-1,1)^D
+    + gamma E_(x_i), for gamma in {1, 2} and eps in {6e-8, 1e-6, 2^-12,
+    2^-8}: per-element skipped_fraction (reference definition,
+    cce.cpp:264-268), skipped / total 32 x 32 sub-tiles at the kernel's skip
+    granularity, and positions/s of the production step (stats off)."""
+    import numpy as np
+    import torch
+    rows = []
+    steps = max(3, min(args.steps, 5))
+
+    def measure(Xd, dist_name, gamma, eps):
+        cfg = lf.CceConfig(filter_eps=eps)
+        fb = lambda: lf.cce_forward_backward(Xd, E, x, 1.0, cfg, validate=False)
+        ms = timed_steps(fb, steps, 1, stream, flush)
+        o, r = lf.cce_forward_backward(Xd, E, x, 1.0, cfg, validate=False, stats=True)
+        fused = bool(lf._capi.lib().lf_cce_fused_supported(C.byref(cfg.to_c(lf._capi.LF_BF16)), D))
+        rows.append({"dist": dist_name, "gamma": gamma, "eps": eps, "loss": float(o.loss),
+                     "skipped_fraction": r.skipped_fraction, "skipped_subtiles": r.skipped_tiles,
+                     "total_subtiles": r.total_tiles,
+                     "subtile_skip_frac": (r.skipped_tiles / r.total_tiles) if r.total_tiles else 0.0,
+                     "ms_per_step": ms, "positions_per_s": N_ROWS / (ms / 1e3),
+                     "path": "fused forward+dX, filtered dE pass" if fused
+                             else "3 passes (forward, filtered dX pass with sub-tile skipping, filtered dE pass)"})
+        del o, r
+
+    measure(X, "A (uniform, headline)", 0.0, EPS)
+    tgt_rows = np.ascontiguousarray(Ch[:, t].T)  # E_(x_i), already bf16 values
+    Xr = Xh.astype(np.float32)
+    for gamma in (1.0, 2.0):
+        XB = torch.from_numpy(Xr + gamma * tgt_rows).to(X.device).to(torch.bfloat16)
+        for eps in (6e-8, 1e-6, 2.0 ** -12, 2.0 ** -8):
+            measure(XB, "B (trained-like)", gamma, eps)
+        del XB
+    torch.cuda.synchronize()
+    return {"runs": rows, "steps_per_run": steps,
+            "skip_granularity": "32 rows x 32 items (dE pass in the fused path; dX pass in the 3-pass path)",
+            "note": "distribution B at coarse eps (>= 2^-12) runs the 3-pass path whose dX pass skips "
+                    "sub-tiles below eps; positions/s is the production step (stats off)"}
+
+
+def cfg3_record(lf, flush, stream, args, peaks, cpu):
+    """BASELINE configs[2]: CCE- bf16, N = 51200, D = 64, V = 1M, K = 512
+    uniform negatives from the reference's sample_uniform stream (the GPU
+    sampler, index-for-index the reference's), fwd + bwd (deterministic dE)."""
+    import numpy as np
+    import torch
+    from paper_2509_09682_b200 import synth
+    dev = torch.device("cuda", torch.cuda.current_device())
+    Xr, Cr, t3 = synth.make_instance(SEED3, N_ROWS, D, V)
+    Xh, Ch = bf16_round(Xr), bf16_round(Cr)
+    del Xr, Cr
+    X3 = torch.from_numpy(Xh).to(dev).to(torch.bfloat16)
+    E3 = torch.from_numpy(np.ascontiguousarray(Ch.T)).to(dev).to(torch.bfloat16)
+    x3 = torch.from_numpy(t3).to(dev)
+    sseed = synth.derived_seed(SEED3, 7)
+    inds = lf.sample_uniform(x3, K_NEG, V, sseed)
+    cfg = lf.CceConfig()
+    box = [None]
+
+    def step():
+        box[0] = None
+        o = lf.ccem_forward(X3, E3, inds, cfg, validate=False)
+        g = lf.ccem_backward(X3, E3, inds, o.lse, 1.0, cfg, validate=False)
+        box[0] = (o, g)
+
+    ms = timed_steps(step, args.steps, max(3, args.warmup), stream, flush)
+    S = N_ROWS * (1 + K_NEG)
+    alg_bytes = 2 * S * (2 * D + 8) + S * 4 * D + V * D * 4 + N_ROWS * (6 * D + 16)
+    ach = alg_bytes / (ms / 1e3) / 1e9
+    rec = {"workload": "cfg3: CCE- bf16, N=51200, D=64, V=1M, K=512 uniform negatives "
+                       f"(make_instance seed {SEED3:#x}, sample_uniform SplitMix64(seed).derived(7))",
+           "value": N_ROWS / (ms / 1e3), "unit": "positions/s", "ms_per_step": ms, "steps": args.steps,
+           "roofline": {"bound": "hbm", "achieved": ach, "peak": peaks["hbm"], "unit": "GB/s",
+                        "frac": ach / peaks["hbm"], "traffic": None,
+                        "algorithmic_bytes_per_step": alg_bytes,
+                        "note": "SURVEY.md 8(d): 2 S (2D+8) gathers + index reads (fwd, bwd) + S 4D dE "
+                                "contributions + V D 4 dE write + N (6D+16), S = N (1+K); whole step"},
+           "bar_pos_per_s": 11.8e6}
+    o, g = box[0]
+    if cpu:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import oracle_bind as ob
+        threads = os.cpu_count() or 1
+        ih = inds.cpu().numpy()
+        t0 = time.perf_counter()
+        loss, pos, lse = ob.ref_ccem_forward(Xh, Ch, ih, rb=128, workers=threads)
+        rdE, rdC = ob.ref_ccem_backward_rows(Xh, Ch, ih, lse, np.full(N_ROWS, 1.0 / N_ROWS), rb=128,
+                                             workers=threads)
+        sec = time.perf_counter() - t0
+        rec["cpu_baseline"] = {"value": N_ROWS / sec, "unit": "positions/s", "cores": threads,
+                               "kind": "reference",
+                               "sample": f"reference ccem_forward + ccem_backward_rows (oracle/_ref) at full "
+                                         f"N={N_ROWS}, K={K_NEG}, V={V}, D={D}, workers={threads}"}
+        dEg = g.d_classifier.float().cpu().numpy()
+        num = den = 0.0
+        for a in range(0, V, 1 << 17):  # column blocks: bounded host memory
+            b = min(V, a + (1 << 17))
+            w = rdC[:, a:b].T
+            num += float(np.sum((dEg[a:b] - w) ** 2))
+            den += float(np.sum(w * w))
+        tol = {"loss_rel": 1e-2, "lse_max_rel": 1e-3, "dX_normwise": 1e-2, "dE_normwise": 1e-2}
+        p = {"rows": N_ROWS, "loss_rel": abs(float(o.loss) - loss) / max(1.0, abs(loss)),
+             "lse_max_rel": rel(o.lse.cpu().numpy(), lse),
+             "pos_max_rel": rel(o.pos_logits.cpu().numpy(), pos),
+             "dX_normwise": normwise(g.d_embeddings.double().cpu().numpy(), rdE),
+             "dE_normwise": (num / den) ** 0.5 if den else 0.0, "tolerance": tol}
+        p["pass"] = bool(p["loss_rel"] < tol["loss_rel"] and p["lse_max_rel"] < tol["lse_max_rel"]
+                         and p["dX_normwise"] < tol["dX_normwise"] and p["dE_normwise"] < tol["dE_normwise"])
+        rec["parity"] = p
+    del box[0], o, g, X3, E3, x3, inds
+    torch.cuda.synchronize()
+    return rec
 
 
 def main():

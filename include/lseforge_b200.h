@@ -460,7 +460,9 @@ LF_API int lf_estimate_flops(int64_t n, int64_t d, int64_t v, int64_t ns, int32_
                       uint64_t* forward, uint64_t* backward);
 
 /* Device scratch the library itself allocates (stream-ordered pool):
- * current and high-water bytes since the last reset. */
+ * current and high-water bytes since the last reset, for the CALLING THREAD
+ * (each call's scratch is charged to the thread that made it, so concurrent
+ * callers do not see each other's). */
 LF_API int lf_workspace_stats(uint64_t* current_bytes, uint64_t* peak_bytes);
 LF_API int lf_workspace_reset_peak(void);
 

@@ -19,8 +19,12 @@ namespace lf {
 namespace {
 thread_local std::string g_last_error;
 std::atomic<uint64_t> g_launches{0};
-std::atomic<uint64_t> g_ws_current{0};
-std::atomic<uint64_t> g_ws_peak{0};
+// Scratch accounting is per calling thread: every Scratch lives on the stack
+// of the call that allocated it, so concurrent callers (e.g. the reference's
+// sweep running points in parallel, sweep.cpp:101) never charge each other's
+// scratch to their own MemAccountant.
+thread_local uint64_t g_ws_current = 0;
+thread_local uint64_t g_ws_peak = 0;
 }  // namespace
 
 void set_error(const std::string& msg) { g_last_error = msg; }
@@ -103,16 +107,14 @@ int Scratch::alloc(size_t nbytes, cudaStream_t s) {
   }
   bytes = nbytes;
   stream = s;
-  const uint64_t cur = g_ws_current.fetch_add(nbytes) + nbytes;
-  uint64_t pk = g_ws_peak.load();
-  while (cur > pk && !g_ws_peak.compare_exchange_weak(pk, cur)) {
-  }
+  g_ws_current += nbytes;
+  if (g_ws_current > g_ws_peak) g_ws_peak = g_ws_current;
   return LF_OK;
 }
 Scratch::~Scratch() {
   if (ptr) {
     cudaFreeAsync(ptr, stream);
-    g_ws_current.fetch_sub(bytes);
+    g_ws_current -= bytes;
   }
 }
 
@@ -503,6 +505,7 @@ int lf_cem_forward(const void* d_X, const void* d_E, const int64_t* d_inds, int6
   if (n <= 0) return fail(LF_EINVAL, "loss: embedding matrix has zero rows; the mean loss is undefined");
   if (w < 1) return fail(LF_EINVAL, "NegIndexMatrix: width must be at least 1 (the positive slot)");
   if (d <= 0 || v <= 0) return fail(LF_EINVAL, "loss: empty embedding or catalog");
+  if (!d_X || !d_E || !d_inds || !d_lse || !d_pos) return fail(LF_EINVAL, "ce_sampled_forward: null pointer");
   return cem_forward(cfg->dtype, d_X, d_E, d_inds, n, static_cast<int>(d), w, d_lse, d_pos, d_loss,
                      as_stream(stream));
 }
@@ -515,13 +518,13 @@ int lf_cem_backward(const void* d_X, const void* d_E, const int64_t* d_inds, dou
   if (n <= 0) return fail(LF_EINVAL, "loss: embedding matrix has zero rows; the mean loss is undefined");
   if (w < 1) return fail(LF_EINVAL, "NegIndexMatrix: width must be at least 1 (the positive slot)");
   if (d <= 0 || v <= 0) return fail(LF_EINVAL, "loss: empty embedding or catalog");
+  if (!d_X || !d_E || !d_inds || !d_dX || !d_dE) return fail(LF_EINVAL, "ce_sampled_backward: null pointer");
   return cem_backward(cfg->dtype, d_X, d_E, d_inds, upstream, n, static_cast<int>(d), v, w, d_dX, d_dE,
                       as_stream(stream));
 }
 
 int lf_sample_uniform(const int64_t* d_positives, int64_t n, int64_t ns, int64_t catalog,
                       uint64_t seed, int32_t retry_cap, int64_t* d_inds, void* stream) {
-  if (retry_cap < 1) return fail(LF_EINVAL, "sample_uniform: retry_cap must be >= 1");
   return sample_uniform(d_positives, n, ns, catalog, seed, retry_cap, d_inds, as_stream(stream));
 }
 
@@ -597,7 +600,6 @@ int lf_adam_step(float* d_param, const void* d_grad, int32_t grad_dtype, double*
 int lf_sample_popularity(const int64_t* d_positives, int64_t n, int64_t ns, const int64_t* d_counts,
                          int64_t catalog, double exponent, uint64_t seed, int32_t retry_cap,
                          int64_t* d_inds, void* stream) {
-  if (retry_cap < 1) return fail(LF_EINVAL, "sample_popularity: retry_cap must be >= 1");
   return sample_popularity(d_positives, n, ns, d_counts, catalog, exponent, seed, retry_cap, d_inds,
                            as_stream(stream));
 }
@@ -622,12 +624,12 @@ int lf_estimate_flops(int64_t n, int64_t d, int64_t v, int64_t ns, int32_t backe
 }
 
 int lf_workspace_stats(uint64_t* current_bytes, uint64_t* peak_bytes) {
-  if (current_bytes) *current_bytes = g_ws_current.load();
-  if (peak_bytes) *peak_bytes = g_ws_peak.load();
+  if (current_bytes) *current_bytes = g_ws_current;
+  if (peak_bytes) *peak_bytes = g_ws_peak;
   return LF_OK;
 }
 int lf_workspace_reset_peak(void) {
-  g_ws_peak.store(g_ws_current.load());
+  g_ws_peak = g_ws_current;
   return LF_OK;
 }
 uint64_t lf_launch_count(void) { return g_launches.load(); }

@@ -110,6 +110,19 @@ __global__ void first_bad_positive(const int64_t* __restrict__ pos, int64_t n, i
 // reference's summation order (pow itself may differ from glibc's in the last
 // ulp).  (exponent == 1 uses the blocked scan below.)
 // flags[0] = first negative count, flags[1] = 1 if the total is not > 0.
+// count^exponent for every item, in parallel (the expensive part of a
+// non-unit exponent); pop_cumulative then sums them in the reference's order.
+__global__ void pop_weights(const int64_t* __restrict__ counts, int64_t catalog, double exponent,
+                            double* __restrict__ w, unsigned long long* __restrict__ flags) {
+  for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < catalog;
+       v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = counts[v];
+    if (c < 0) atomicMin(flags, static_cast<unsigned long long>(v));
+    w[v] = pow(static_cast<double>(c), exponent);
+  }
+}
+
+// Running sum over the weights already in cum (pop_weights), in place.
 __global__ void pop_cumulative(const int64_t* __restrict__ counts, int64_t catalog, double exponent,
                                double* __restrict__ cum, unsigned long long* __restrict__ flags,
                                double* __restrict__ total) {
@@ -119,9 +132,7 @@ __global__ void pop_cumulative(const int64_t* __restrict__ counts, int64_t catal
   const int64_t lo = threadIdx.x * len, hi = min(catalog, lo + len);
   double run = 0.0;
   for (int64_t v = lo; v < hi; ++v) {
-    const int64_t c = counts[v];
-    if (c < 0) atomicMin(flags, static_cast<unsigned long long>(v));
-    run += exponent == 1.0 ? static_cast<double>(c) : pow(static_cast<double>(c), exponent);
+    run += cum[v];
     cum[v] = run;
   }
   seg[threadIdx.x] = run;
@@ -334,7 +345,9 @@ int sample_popularity(const int64_t* positives, int64_t n, int64_t ns, const int
     pop_block_sums<<<static_cast<unsigned>(nb), 256, 0, st>>>(counts, catalog, bsums.as<double>(), f);
     pop_scan_blocks<<<1, 32, 0, st>>>(bsums.as<double>(), nb, tot.as<double>(), f);
     pop_block_scan<<<static_cast<unsigned>(nb), 256, 0, st>>>(counts, catalog, bsums.as<double>(), cum.as<double>());
-  } else {  // the reference's summation order (sampler.cpp:93-99), one thread
+  } else {  // weights in parallel, then the reference's summation order (sampler.cpp:93-99)
+    pop_weights<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(catalog, 256), 8LL * num_sms())), 256, 0,
+                  st>>>(counts, catalog, exponent, cum.as<double>(), f);
     pop_cumulative<<<1, 1, 0, st>>>(counts, catalog, exponent, cum.as<double>(), f, tot.as<double>());
   }
   LF_LAUNCHED();
@@ -361,6 +374,9 @@ int sample_popularity(const int64_t* positives, int64_t n, int64_t ns, const int
                                " exceeds catalog minus positive (" + std::to_string(catalog - 1) + ")");
   if (h[1]) return fail(LF_EINVAL, "sample_popularity: all item weights are zero");
   if (n == 0) return LF_OK;
+  if (retry_cap < 1 && ns > 0)  // no attempt is made: row 0's first slot fails (sampler.cpp:62-71)
+    return fail(LF_ERUNTIME, "sampler: row 0 exhausted " + std::to_string(retry_cap) +
+                                 " rejection retries; the distribution leaves no valid negative");
   const int64_t G = catalog;
   Scratch guide;
   rc = guide.alloc(sizeof(int64_t) * G, st);
@@ -383,13 +399,16 @@ int sample_popularity(const int64_t* positives, int64_t n, int64_t ns, const int
 
 int sample_uniform(const int64_t* positives, int64_t n, int64_t ns, int64_t catalog,
                    uint64_t seed, int retry_cap, int64_t* inds, cudaStream_t st) {
+  // the reference's order (sampler.cpp:44-56): catalog, positives, ns
   if (catalog <= 0) return fail(LF_EINVAL, "sample_uniform: empty catalog");
   if (n < 0 || ns < 0) return fail(LF_EINVAL, "sample_uniform: negative extent");
-  if (ns > catalog - 1)
-    return fail(LF_EINVAL, "sample_uniform: ns = " + std::to_string(ns) +
-                               " exceeds catalog minus positive (" + std::to_string(catalog - 1) +
-                               ")");
-  if (n == 0) return LF_OK;
+  auto ns_check = [&]() {
+    return ns > catalog - 1
+               ? fail(LF_EINVAL, "sample_uniform: ns = " + std::to_string(ns) +
+                                     " exceeds catalog minus positive (" + std::to_string(catalog - 1) + ")")
+               : LF_OK;
+  };
+  if (n == 0) return ns_check();
   Scratch flag;
   int rc = flag.alloc(2 * sizeof(unsigned long long), st);
   if (rc) return rc;
@@ -407,6 +426,11 @@ int sample_uniform(const int64_t* positives, int64_t n, int64_t ns, int64_t cata
     return fail(LF_EINVAL, "sampler: row " + std::to_string(h) + " positive " + std::to_string(bad) +
                                " outside catalog of " + std::to_string(catalog));
   }
+  rc = ns_check();
+  if (rc) return rc;
+  if (retry_cap < 1 && ns > 0)  // no attempt is made: row 0's first slot fails (sampler.cpp:62-71)
+    return fail(LF_ERUNTIME, "sampler: row 0 exhausted " + std::to_string(retry_cap) +
+                                 " rejection retries; the distribution leaves no valid negative");
   sample_uniform_rows<<<static_cast<unsigned>(ceil_div(n, 8)), 256, 0, st>>>(
       positives, n, ns, static_cast<uint64_t>(catalog), seed, retry_cap, inds, f + 1);
   LF_LAUNCHED();

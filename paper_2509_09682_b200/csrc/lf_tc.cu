@@ -1683,7 +1683,7 @@ int tc_cce_fwdx_partials(const void* X, const void* E, const int64_t* targets, i
   const int64_t owner_tiles = ceil_div(n, BM);
   const int64_t stream_tiles = ceil_div(v, BN);
 #ifndef LF_FWDX_MAXCHUNKS
-#define LF_FWDX_MAXCHUNKS 8
+#define LF_FWDX_MAXCHUNKS 4
 #endif
   const int64_t chunks = pick_chunks(owner_tiles, stream_tiles, LF_FWDX_MAXCHUNKS);
   const int64_t tiles_per = ceil_div(stream_tiles, chunks);

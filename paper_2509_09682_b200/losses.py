@@ -119,10 +119,15 @@ def ce_full_backward(X: torch.Tensor, E: torch.Tensor, x: torch.Tensor, upstream
     return GradPair(dX, dE)
 
 
-def ce_sampled_forward(X: torch.Tensor, E: torch.Tensor, inds: torch.Tensor) -> LossOutput:
+def ce_sampled_forward(X: torch.Tensor, E: torch.Tensor, inds: torch.Tensor,
+                       validate: bool = True) -> LossOutput:
     """losses.cpp:142-173 — the MATERIALISING sampled baseline ("cem"): the
-    n x (1+K) candidate logits are written to device memory."""
+    n x (1+K) candidate logits are written to device memory.  Inputs are
+    checked as the reference does (losses.cpp:144-152: row count, widths,
+    inds.validate over every slot, the positives included)."""
     import ctypes as C
+    from .ccem import _validate_sampled
+    _validate_sampled(X, E, inds, validate)
     n, d = X.shape
     v = E.shape[0]
     I = inds.to(torch.int64).contiguous()
@@ -137,10 +142,13 @@ def ce_sampled_forward(X: torch.Tensor, E: torch.Tensor, inds: torch.Tensor) -> 
 
 
 def ce_sampled_backward(X: torch.Tensor, E: torch.Tensor, inds: torch.Tensor,
-                        upstream: float = 1.0) -> GradPair:
+                        upstream: float = 1.0, validate: bool = True) -> GradPair:
     """losses.cpp:175-221 — materialised logits and coefficients, dE scattered
-    with atomics (duplicate candidates accumulate)."""
+    with atomics (duplicate candidates accumulate).  Checked as
+    ce_sampled_forward."""
     import ctypes as C
+    from .ccem import _validate_sampled
+    _validate_sampled(X, E, inds, validate)
     n, d = X.shape
     v = E.shape[0]
     I = inds.to(torch.int64).contiguous()

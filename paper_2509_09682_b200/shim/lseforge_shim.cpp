@@ -11,8 +11,10 @@
 //   lseforge::estimate_flops       ccem.hpp:48-49  (reference ccem.cpp:207-235)
 //   lseforge::evaluate             metrics.hpp:18-24 (reference metrics.cpp:13-103)
 //   lseforge::sample_uniform,      sampler.hpp:26-40 (reference sampler.cpp:30-127,
-//     sample_popularity,           index for index; PopularityTable::FromCounts is
-//     PopularityTable::FromCounts  restated on the host)
+//     sample_popularity,           index for index — popularity: for exponent 1
+//     PopularityTable::FromCounts  (exact integer sums); other exponents agree to
+//                                  the device pow's last ulp; FromCounts is
+//                                  restated on the host)
 //
 // It is compiled against the reference's own headers (-I proj/include) and
 // linked in place of cce.cpp + ccem.cpp + metrics.cpp + sampler.cpp; everything else in liblseforge
@@ -74,6 +76,7 @@ namespace {
 [[noreturn]] void throw_status(int rc, const char* what) {
   const std::string msg = lf_last_error();
   if (rc == LF_EINVAL) throw std::invalid_argument(msg);
+  if (rc == LF_ERUNTIME) throw std::runtime_error(msg);  // the reference's own text (e.g. sampler.cpp:22-27)
   throw std::runtime_error(std::string(what) + ": " + msg);
 }
 
