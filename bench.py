@@ -395,6 +395,8 @@ def run_ours(args):
         e2e_grads = run_e2e(step, X, E, x, stream, args, world, dev, grads=True)
 
     extras = {}
+    if rank == 0 and world == 1 and not args.no_e2e:
+        extras["e2e_dropin"] = dropin_e2e()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         extras["cpu_baseline"], extras["parity"] = cfg2_parity(lf, sh, X, E, x, out, res, Xh, Ch, t, cfg)
     if rank == 0 and world == 1 and not args.no_extras:
@@ -417,6 +419,7 @@ def run_ours(args):
                 "peak_hbm_gb": memory["library_peak_gb"], "memory": memory, "loss": loss_val,
                 "roofline": roof, "roofline_tensor": roof_tc, "step_roofline": step_roof,
                 "kernels": kern, "gpu_launches": int(launches), "e2e": e2e, "e2e_grads": e2e_grads,
+                "e2e_dropin": extras.get("e2e_dropin"),
                 "cpu_baseline": extras.get("cpu_baseline"), "parity": extras.get("parity"),
                 "filter": extras.get("filter"), "cfg3": extras.get("cfg3"), "clocks": clk}
         print(json.dumps(line), flush=True)
@@ -503,6 +506,29 @@ def run_e2e(step, X, E, x, stream, args, world, dev, grads):
             "api": "ShardedCce.forward_backward -> lf_cce_forward_backward (C-ABI)",
             "overlap": "step k+1's host->device copy overlaps step k's compute (double buffer)"
                        + ("; step k's dX/dE device->host copy overlaps step k+1" if grads else "")}
+
+
+def dropin_e2e():
+    """cfg2 through the C++ drop-in exactly as a reference caller runs it:
+    lseforge::cce_forward + cce_backward with host DenseMatrix inputs and
+    host LossOutput / GradPair (double, d x v d_classifier) results
+    (paper_2509_09682_b200/shim/build/dropin_check, wall clock, median of 3).
+    Reported with the API's own floor — value-initialising the 512 MB d x v
+    double the signature returns — and with LSEFORGE_B200_HOST_HEAP=keep."""
+    exe = os.path.join(ROOT, "paper_2509_09682_b200", "shim", "build", "dropin_check")
+    if not os.path.exists(exe):
+        return None
+    out = {}
+    for tag, extra in (("default", {}), ("host_heap_keep", {"LSEFORGE_B200_HOST_HEAP": "keep"})):
+        env = dict(os.environ, LSEFORGE_B200_DTYPE="bf16", **extra)
+        try:
+            p = subprocess.run([exe, "bench", "3"], capture_output=True, text=True, timeout=600, env=env)
+            out[tag] = json.loads(p.stdout.strip().splitlines()[-1])
+        except Exception as e:  # reported, not fatal: the device-side bench stands on its own
+            out[tag] = {"error": repr(e)[:200]}
+    out["api"] = ("lseforge::cce_forward + cce_backward (the reference signatures) through "
+                  "shim/lseforge_shim.cpp + liblseforge_b200.so, LSEFORGE_B200_DTYPE=bf16")
+    return out
 
 
 def cfg2_parity(lf, sh, X, E, x, out, res, Xh, Ch, t, cfg):

@@ -44,15 +44,20 @@
 // returning.  The reference's CPU tile-scratch closed form
 // (memory_model.cpp:46-60) does not describe the GPU and is not imitated.
 #include <cuda_runtime.h>
+#include <malloc.h>
 
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
+#include <limits>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "lseforge/accountant.hpp"
@@ -72,6 +77,19 @@
 namespace lseforge {
 
 namespace {
+
+// LSEFORGE_B200_HOST_HEAP=keep: serve large host blocks from the heap and
+// keep them there after free (glibc mallopt), so the d x v double gradient
+// the reference signature returns every step (512 MB at cfg2) reuses
+// already-mapped pages instead of faulting in fresh ones (~170 ms per step
+// on the B200 box).  Process-wide, hence opt-in; off by default.
+const bool g_host_heap = [] {
+  const char* s = std::getenv("LSEFORGE_B200_HOST_HEAP");
+  if (!s || std::strcmp(s, "keep") != 0) return false;
+  mallopt(M_MMAP_THRESHOLD, 1 << 30);
+  mallopt(M_TRIM_THRESHOLD, std::numeric_limits<int>::max());
+  return true;
+}();
 
 [[noreturn]] void throw_status(int rc, const char* what) {
   const std::string msg = lf_last_error();
@@ -100,14 +118,16 @@ int device_dtype() {
 std::size_t elem_bytes(int dtype) { return dtype == LF_F64 ? 8 : (dtype == LF_F32 ? 4 : 2); }
 std::size_t grad_bytes(int dtype) { return dtype == LF_F64 ? 8 : 4; }
 
-// Device buffer owned for the duration of one call.
+// Device buffer owned for the duration of one call, from the device's
+// stream-ordered pool on the legacy stream every call here uses (the library
+// keeps that pool resident, so repeated calls do not pay cudaMalloc again).
 struct Dev {
   void* p = nullptr;
   explicit Dev(std::size_t bytes) {
-    if (bytes) cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
+    if (bytes) cuda_check(cudaMallocAsync(&p, bytes, nullptr), "cudaMallocAsync");
   }
   ~Dev() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, nullptr);
   }
   Dev(const Dev&) = delete;
   Dev& operator=(const Dev&) = delete;
@@ -115,11 +135,154 @@ struct Dev {
   T* as() const { return static_cast<T*>(p); }
 };
 
+// Host copies split over a few persistent threads (the pageable side of a
+// transfer is host-memory bound; one thread cannot keep PCIe busy).
+class CopyPool {
+ public:
+  explicit CopyPool(int parts) : parts_(parts) {
+    for (int k = 1; k < parts_; ++k) workers_.emplace_back([this, k] { loop(k); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  void copy(void* dst, const void* src, std::size_t len) {
+    if (parts_ == 1 || len < (1u << 20)) {
+      std::memcpy(dst, src, len);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      dst_ = static_cast<char*>(dst);
+      src_ = static_cast<const char*>(src);
+      len_ = len;
+      pending_ = parts_ - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    piece(0);
+    std::unique_lock<std::mutex> g(mu_);
+    done_.wait(g, [this] { return pending_ == 0; });
+  }
+
+ private:
+  void piece(int k) {
+    const std::size_t a = len_ * k / parts_, b = len_ * (k + 1) / parts_;
+    std::memcpy(dst_ + a, src_ + a, b - a);
+  }
+  void loop(int k) {
+    std::size_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> g(mu_);
+        cv_.wait(g, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (stop_) return;
+      }
+      piece(k);
+      {
+        std::lock_guard<std::mutex> g(mu_);
+        if (--pending_ == 0) done_.notify_one();
+      }
+    }
+  }
+  int parts_;
+  std::vector<std::thread> workers_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  std::size_t gen_ = 0;
+  int pending_ = 0;
+  bool stop_ = false;
+  char* dst_ = nullptr;
+  const char* src_ = nullptr;
+  std::size_t len_ = 0;
+};
+
+// Per-thread transfer engine: two pinned chunks; large copies are pipelined
+// (the host fills / drains one chunk while the DMA engine moves the other),
+// on the legacy stream the library calls of this file are ordered on.
+class Xfer {
+ public:
+  static Xfer& get() {
+    thread_local Xfer x;
+    return x;
+  }
+  void h2d(void* dst, const void* src, std::size_t bytes) {
+    if (bytes < kSmall) {
+      cuda_check(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice), "upload");
+      return;
+    }
+    ready();
+    int i = 0;
+    for (std::size_t off = 0; off < bytes; off += kChunk, ++i) {
+      const std::size_t len = std::min(kChunk, bytes - off);
+      const int b = i & 1;
+      cuda_check(cudaEventSynchronize(ev_[b]), "upload chunk reuse");
+      pool_.copy(pin_[b], static_cast<const char*>(src) + off, len);
+      cuda_check(cudaMemcpyAsync(static_cast<char*>(dst) + off, pin_[b], len, cudaMemcpyHostToDevice, nullptr),
+                 "upload");
+      cuda_check(cudaEventRecord(ev_[b], nullptr), "upload event");
+    }
+  }
+  void d2h(void* dst, const void* src, std::size_t bytes) {
+    if (bytes < kSmall) {
+      cuda_check(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost), "download");
+      return;
+    }
+    ready();
+    const std::size_t chunks = (bytes + kChunk - 1) / kChunk;
+    auto issue = [&](std::size_t i) {
+      const std::size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
+      cuda_check(cudaMemcpyAsync(pin_[i & 1], static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost,
+                                 nullptr),
+                 "download");
+      cuda_check(cudaEventRecord(ev_[i & 1], nullptr), "download event");
+    };
+    issue(0);
+    for (std::size_t i = 0; i < chunks; ++i) {
+      if (i + 1 < chunks) issue(i + 1);
+      cuda_check(cudaEventSynchronize(ev_[i & 1]), "download chunk");
+      const std::size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
+      pool_.copy(static_cast<char*>(dst) + off, pin_[i & 1], len);
+    }
+  }
+  ~Xfer() {
+    if (pin_[0]) {
+      cudaFreeHost(pin_[0]);
+      cudaFreeHost(pin_[1]);
+      cudaEventDestroy(ev_[0]);
+      cudaEventDestroy(ev_[1]);
+    }
+  }
+
+ private:
+  static constexpr std::size_t kChunk = std::size_t(16) << 20;
+  static constexpr std::size_t kSmall = std::size_t(1) << 20;
+  Xfer() : pool_(std::max(1, std::min(8, static_cast<int>(std::thread::hardware_concurrency()) / 2))) {}
+  void ready() {
+    if (pin_[0]) return;
+    for (int b = 0; b < 2; ++b) {
+      cuda_check(cudaHostAlloc(&pin_[b], kChunk, cudaHostAllocDefault), "cudaHostAlloc");
+      cuda_check(cudaEventCreateWithFlags(&ev_[b], cudaEventDisableTiming), "cudaEventCreate");
+      cuda_check(cudaEventRecord(ev_[b], nullptr), "cudaEventRecord");
+    }
+  }
+  CopyPool pool_;
+  void* pin_[2] = {nullptr, nullptr};
+  cudaEvent_t ev_[2] = {};
+};
+
 void upload(void* dst, const void* src, std::size_t bytes) {
-  if (bytes) cuda_check(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice), "upload");
+  if (bytes) Xfer::get().h2d(dst, src, bytes);
 }
+// synchronous on return, like the reference's host results
 void download(void* dst, const void* src, std::size_t bytes) {
-  if (bytes) cuda_check(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost), "download");
+  if (bytes) Xfer::get().d2h(dst, src, bytes);
 }
 
 // The inputs of one loss call, resident on the device in kernel layout.

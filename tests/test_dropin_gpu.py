@@ -89,3 +89,23 @@ def test_reference_acceptance_criteria(cuda):
     assert "instrumentation mismatch" in out  # criterion 4: the scratch formula only
     if 8 in failed:  # the wall-clock race only, never the FLOP identity
         assert "not faster than full" in out, out
+
+
+DROPIN_CHECK = os.path.join(ROOT, "paper_2509_09682_b200", "shim", "build", "dropin_check")
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32", "bf16"])
+def test_dropin_reference_api_parity_every_dtype(cuda, dtype):
+    """The drop-in through the reference's own API in every device dtype:
+    lseforge::cce_forward / cce_backward / ccem_forward / ccem_backward (the
+    shim: lf_convert_rows, lf_classifier_to_items, the kernels,
+    lf_widen_grad, lf_items_grad_to_classifier) vs the reference's
+    materialising oracles (losses.cpp, linked unchanged) at the stated
+    per-dtype tolerances (tests/gpu_util.py TOL), on bf16-representable
+    inputs so every dtype sees the same values."""
+    if not os.path.exists(DROPIN_CHECK):
+        pytest.skip(f"{DROPIN_CHECK} not built (needs /root/reference at build time)")
+    env = dict(os.environ, LSEFORGE_B200_DTYPE=dtype)
+    p = subprocess.run([DROPIN_CHECK, "parity"], capture_output=True, text=True, timeout=600, env=env)
+    out = p.stdout + p.stderr
+    assert p.returncode == 0 and out.strip().endswith("OK") and "FAIL" not in out, out[-4000:]
