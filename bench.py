@@ -225,20 +225,34 @@ def normwise(got, want):
     return float(np.linalg.norm(g - w) / max(np.linalg.norm(w), 1e-300))
 
 
-def timed_steps(step, steps, warmup, stream, flush):
-    """Device-timed loop (CUDA events on the compute stream, L2 flush outside)."""
+def timed_steps(step, steps, warmup, stream, flush, kernels=None):
+    """Device-timed loop (CUDA events on the compute stream, L2 flush outside).
+    kernels: a dict to fill with the library's per-kernel ms per step
+    (lf_profile_*), or None."""
     import torch
+    from paper_2509_09682_b200 import _capi
     for _ in range(warmup):
         step()
     torch.cuda.synchronize()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(steps)]
+    L = _capi.lib()
+    if kernels is not None:
+        L.lf_profile_reset()
+        L.lf_profile_enable(1)
     for k in range(steps):
         flush.fill_(k & 0xFF)
         evs[k][0].record(stream)
         step()
         evs[k][1].record(stream)
     torch.cuda.synchronize()
+    if kernels is not None:
+        L.lf_profile_enable(0)
+        for kind, name in enumerate(_capi.KERNEL_KINDS):
+            cnt, ms = C.c_uint64(), C.c_double()
+            L.lf_profile_read(kind, C.byref(cnt), C.byref(ms))
+            if cnt.value:
+                kernels[name] = round(ms.value / steps, 4)
     return sum(a.elapsed_time(b) for a, b in evs) / steps
 
 
@@ -583,14 +597,16 @@ def filter_protocol(lf, X, E, x, Xh, Ch, t, flush, stream, args):
     def measure(Xd, dist_name, gamma, eps):
         cfg = lf.CceConfig(filter_eps=eps)
         fb = lambda: lf.cce_forward_backward(Xd, E, x, 1.0, cfg, validate=False)
-        ms = timed_steps(fb, steps, 1, stream, flush)
+        kern = {}
+        ms = timed_steps(fb, steps, 1, stream, flush, kern)
         o, r = lf.cce_forward_backward(Xd, E, x, 1.0, cfg, validate=False, stats=True)
         fused = bool(lf._capi.lib().lf_cce_fused_supported(C.byref(cfg.to_c(lf._capi.LF_BF16)), D))
         rows.append({"dist": dist_name, "gamma": gamma, "eps": eps, "loss": float(o.loss),
                      "skipped_fraction": r.skipped_fraction, "skipped_subtiles": r.skipped_tiles,
                      "total_subtiles": r.total_tiles,
                      "subtile_skip_frac": (r.skipped_tiles / r.total_tiles) if r.total_tiles else 0.0,
-                     "ms_per_step": ms, "positions_per_s": N_ROWS / (ms / 1e3),
+                     "ms_per_step": ms, "kernel_ms_per_step": kern,
+                     "positions_per_s": N_ROWS / (ms / 1e3),
                      "path": "fused forward+dX, filtered dE pass" if fused
                              else "3 passes (forward, filtered dX pass with sub-tile skipping, filtered dE pass)"})
         del o, r

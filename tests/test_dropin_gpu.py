@@ -80,6 +80,18 @@ def test_reference_test_memory_only_scratch_formula_differs(cuda):
     assert bad and all(b == "rep.peak.scratch_real == want.scratch_real" for b in bad), set(bad)
 
 
+def test_reference_test_trainer_passes_in_exact_mode(cuda):
+    """proj/tests/test_trainer.cpp through the drop-in: CE == CCE and
+    CEM == CCEM loss trajectories over two epochs (test_trainer.cpp:211-237,
+    1e-5 relative, the CCE / CCE- side on the GPU), bitwise repeatability and
+    worker-count invariance (:239-269, the GPU kernels are deterministic),
+    the retained-memory closed forms (:297-317), the filter's skip rate
+    (:319-331) and the sweep machinery.  sweep.cpp is built with the nlohmann
+    json.hpp this image ships (oracle/Makefile JSON_DIR)."""
+    rc, out = run("test_trainer", timeout=1200)
+    assert rc == 0 and "| 0 failed" in out, out[-3000:]
+
+
 def test_reference_acceptance_criteria(cuda):
     rc, out = run("acceptance", timeout=1200)
     passed = set(int(m) for m in re.findall(r"^\[PASS\] criterion (\d+)", out, re.M))
