@@ -291,6 +291,22 @@ LF_API int lf_ccem_backward(const void* d_X, const void* d_E, const int64_t* d_i
                      int64_t v, int64_t w, const lf_cce_config* cfg, void* d_dX, void* d_dE,
                      void* stream);
 
+/* Fused CCE- forward + backward: lf_ccem_forward followed by lf_ccem_backward
+ * with the same upstream (the trainer's pairing, trainer.cpp:71-77 —
+ * run_loss_layer always calls the backward right after the forward on the
+ * same inputs), in ONE gather pass over the candidates' rows instead of two:
+ * the pass keeps an online-softmax-weighted row sum per row, so lse, pos, dX
+ * and each entry's logit come out together; the dE coefficients are formed
+ * from the logits and reduced as in lf_ccem_backward (bitwise the same dE).
+ * bf16 / f32 with d in {64, 128, 256} and without LF_FLAG_ATOMIC_DE run
+ * fused; anything else runs the two calls in sequence.  d_row_upstream may be
+ * NULL (scalar form).  d_loss may be NULL. */
+LF_API int lf_ccem_forward_backward(const void* d_X, const void* d_E, const int64_t* d_inds,
+                                    int64_t n, int64_t d, int64_t v, int64_t w,
+                                    const double* d_row_upstream, double upstream,
+                                    const lf_cce_config* cfg, double* d_lse, double* d_pos,
+                                    double* d_loss, void* d_dX, void* d_dE, void* stream);
+
 /* ------------------------------------------- materialising CE baseline ---- */
 /* Replace lseforge::ce_full_forward / ce_full_backward (losses.cpp:71-140):
  * the baseline CCE is measured against.  The n x v logit matrix IS written

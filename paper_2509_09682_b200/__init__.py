@@ -11,6 +11,7 @@ from .accountant import MemAccountant, Report, ScalarKind
 from .cce import (CceBackwardResult, CceConfig, cce_backward, cce_forward, cce_forward_backward,
                   kFp16MinPositive)
 from .ccem import (Backend, FlopEstimate, backend_is_sampled, ccem_backward, ccem_backward_rows,
+                   ccem_forward_backward,
                    ccem_forward, estimate_flops)
 from .losses import (GradPair, LossOutput, ce_full_backward, ce_full_forward, ce_sampled_backward,
                      ce_sampled_forward, validate_loss_inputs)
@@ -21,7 +22,8 @@ from .sampler import sample_popularity, sample_uniform
 __all__ = [
     "CceConfig", "CceBackwardResult", "cce_forward", "cce_backward", "cce_forward_backward",
     "kFp16MinPositive",
-    "ccem_forward", "ccem_backward", "ccem_backward_rows", "estimate_flops", "FlopEstimate",
+    "ccem_forward", "ccem_backward", "ccem_backward_rows", "ccem_forward_backward", "estimate_flops",
+    "FlopEstimate",
     "Backend", "backend_is_sampled", "LossOutput", "GradPair", "validate_loss_inputs",
     "MemAccountant", "Report", "ScalarKind", "sample_uniform", "sample_popularity", "ce_full_forward",
     "ce_full_backward", "EvalSummary", "evaluate", "AdamConfig", "DeviceAdam", "lib",

@@ -134,3 +134,44 @@ def ccem_backward(X: torch.Tensor, E: torch.Tensor, inds: torch.Tensor, lse: tor
     if X.shape[0] == 0:
         raise ValueError("fused sampled loss: zero rows; the mean loss is undefined")
     return ccem_backward_rows(X, E, inds, lse, None, cfg, acct, validate, upstream=upstream)
+
+
+def ccem_forward_backward(X: torch.Tensor, E: torch.Tensor, inds: torch.Tensor,
+                          upstream: float = 1.0, cfg: CceConfig = CceConfig(),
+                          row_upstream: Optional[torch.Tensor] = None,
+                          acct: Optional[MemAccountant] = None,
+                          validate: bool = True) -> tuple[LossOutput, GradPair]:
+    """ccem_forward then ccem_backward[_rows] on the same inputs (the
+    trainer's pairing, trainer.cpp:71-77) through lf_ccem_forward_backward:
+    one gather pass over the candidates gives lse, pos, dX and the entries'
+    logits (bf16 / f32, d in {64, 128, 256}, ordered dE); otherwise the two
+    calls run in sequence.  Same outputs and tolerances as the two calls."""
+    _validate_sampled(X, E, inds, validate)
+    if cfg.row_block < 1:
+        raise ValueError("CceConfig: row_block must be >= 1")
+    n, d = X.shape
+    v = E.shape[0]
+    w = inds.shape[1]
+    if row_upstream is not None:
+        if row_upstream.numel() != n:  # ccem.cpp:120-124
+            raise ValueError(f"ccem_backward: upstream vector has {row_upstream.numel()} entries "
+                             f"for {n} rows")
+        row_upstream = row_upstream.to(device=X.device, dtype=torch.float64).contiguous()
+    if acct is not None:  # ccem.cpp:63-68, 132-137
+        acct.record_ensure("retained/ccem/pos_logits", n)
+        acct.record_ensure("retained/ccem/lse", n)
+        acct.record_ensure("retained/ccem/inds", n * w, ScalarKind.kIndex)
+    base = _reset_peak() if acct is not None else 0
+    lse = torch.empty(n, dtype=torch.float64, device=X.device)
+    pos = torch.empty(n, dtype=torch.float64, device=X.device)
+    loss = torch.empty((), dtype=torch.float64, device=X.device)
+    gd = grad_dtype(X)
+    dX = torch.empty((n, d), dtype=gd, device=X.device)
+    dE = torch.empty((v, d), dtype=gd, device=X.device)
+    c = cfg.to_c(lf_dtype(X))
+    _capi.check(_capi.lib().lf_ccem_forward_backward(
+        X.data_ptr(), E.data_ptr(), inds.data_ptr(), n, d, v, w,
+        row_upstream.data_ptr() if row_upstream is not None else None, float(upstream), C.byref(c),
+        lse.data_ptr(), pos.data_ptr(), loss.data_ptr(), dX.data_ptr(), dE.data_ptr(), _stream(X)))
+    _charge_scratch(acct, "scratch/ccem/forward_backward", base)
+    return LossOutput(loss, pos, lse), GradPair(dX, dE)

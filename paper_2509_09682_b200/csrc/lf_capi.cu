@@ -445,6 +445,27 @@ int lf_ccem_backward(const void* d_X, const void* d_E, const int64_t* d_inds, co
                        d_dE, as_stream(stream));
 }
 
+int lf_ccem_forward_backward(const void* d_X, const void* d_E, const int64_t* d_inds, int64_t n,
+                             int64_t d, int64_t v, int64_t w, const double* d_row_upstream,
+                             double upstream, const lf_cce_config* cfg, double* d_lse, double* d_pos,
+                             double* d_loss, void* d_dX, void* d_dE, void* stream) {
+  int rc = check_cfg(cfg);
+  if (rc) return rc;
+  if (n <= 0) return fail(LF_EINVAL, "fused sampled loss: zero rows; the mean loss is undefined");
+  if (w < 1) return fail(LF_EINVAL, "NegIndexMatrix: width must be at least 1 (the positive slot)");
+  if (d <= 0 || v <= 0) return fail(LF_EINVAL, "fused sampled loss: empty embedding or catalog");
+  if (!d_lse || !d_pos) return fail(LF_EINVAL, "ccem_forward_backward: lse / pos outputs are null");
+  const bool atomic = (cfg->flags & LF_FLAG_ATOMIC_DE) != 0;
+  cudaStream_t st = as_stream(stream);
+  if (ccem_fused_supported(cfg->dtype, static_cast<int>(d), atomic))
+    return ccem_forward_backward(cfg->dtype, d_X, d_E, d_inds, n, static_cast<int>(d), v, w,
+                                 d_row_upstream, upstream, d_lse, d_pos, d_loss, d_dX, d_dE, st);
+  rc = ccem_forward(cfg->dtype, d_X, d_E, d_inds, n, static_cast<int>(d), v, w, d_lse, d_pos, d_loss, st);
+  if (rc) return rc;
+  return ccem_backward(cfg->dtype, d_X, d_E, d_inds, d_lse, d_row_upstream, upstream, n,
+                       static_cast<int>(d), v, w, atomic, d_dX, d_dE, st);
+}
+
 int lf_validate_targets(const int64_t* d_targets, int64_t n, int64_t v, void* stream) {
   if (n <= 0) return fail(LF_EINVAL, "loss: embedding matrix has zero rows; the mean loss is undefined");
   return validate_targets(d_targets, n, v, as_stream(stream));

@@ -221,6 +221,137 @@ __global__ void __launch_bounds__(256) ccem_bwd_rows_vec(
   }
 }
 
+// Fused CCE- forward + dX (lf_ccem_forward_backward): ONE gather pass over the
+// row's candidates instead of two (forward, then the backward's recompute).
+// Each 8-lane group keeps its own running max m, sum S and softmax-weighted
+// row sum o = sum_s 2^(o_s - m) E_s (rescaled only when its max grows, a
+// group-uniform and rare branch); the four groups merge at the end, so
+// lse = M + ln S and dX = u (o / S - E_{inds(i,0)}).  Each slot's logit (the
+// rows pass's dot, same fmaf order and shuffle tree) is stored so that
+// ccem_logit_to_coeff can form the dE coefficient g = (softmax - [s==0]) u
+// exactly as the unfused rows pass does (dE is then bitwise the unfused one).
+template <class TE, int D>
+__global__ void __launch_bounds__(256) ccem_fused_rows_vec(
+    const TE* __restrict__ X, const TE* __restrict__ E, const int64_t* __restrict__ inds,
+    int64_t n, int64_t w, const double* __restrict__ row_up, double upstream_over_n,
+    double* __restrict__ lse, double* __restrict__ pos, float* __restrict__ dX,
+    float* __restrict__ logit) {
+  constexpr int DPL = D / 8;
+  const int lane = threadIdx.x & 31, g = lane >> 3, c = lane & 7;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (row >= n) return;
+  float xr[DPL], acc[DPL], e0[DPL];
+#pragma unroll
+  for (int b = 0; b < DPL / 8; ++b) {
+    float f[8];
+    Vec8<TE>::load(X + row * D + c * DPL + 8 * b, f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      xr[8 * b + i] = f[i];
+      acc[8 * b + i] = 0.f;
+      e0[8 * b + i] = 0.f;
+    }
+  }
+  const int64_t* irow = inds + row * w;
+  float* lrow = logit + row * w;
+  constexpr int U = D <= 64 ? LF_CCEM_BWD_U : (D <= 128 ? 2 : 1);  // registers: U x D/8 floats
+  const unsigned gm = 0xFFu << (8 * g);
+  float m = -INFINITY, S = 0.f, p0 = 0.f;
+  for (int64_t s0 = 0; s0 < w; s0 += 4 * U) {
+    float ev[U][DPL];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int64_t slot = s0 + 4 * q + g;
+      if (slot < w) {  // uniform within each 8-lane group
+        const TE* er = E + __ldg(irow + slot) * D + c * DPL;
+#pragma unroll
+        for (int b = 0; b < DPL / 8; ++b) {
+          float f[8];
+          Vec8<TE>::load(er + 8 * b, f);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) ev[q][8 * b + i] = f[i];
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int64_t slot = s0 + 4 * q + g;
+      if (slot < w) {
+        float dot = 0.f;
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) dot = fmaf(xr[i], ev[q][i], dot);
+        dot += __shfl_xor_sync(gm, dot, 1);
+        dot += __shfl_xor_sync(gm, dot, 2);
+        dot += __shfl_xor_sync(gm, dot, 4);
+        if (c == 0) lrow[slot] = dot;
+        if (slot == 0) {
+          p0 = dot;
+#pragma unroll
+          for (int i = 0; i < DPL; ++i) e0[i] = ev[q][i];
+        }
+        if (dot > m) {  // the group's max grows (rare after its first slots)
+          const float f = __expf(m - dot);  // 0 while m = -inf
+          S *= f;
+#pragma unroll
+          for (int i = 0; i < DPL; ++i) acc[i] *= f;
+          m = dot;
+        }
+        const float p = __expf(dot - m);
+        S += p;
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) acc[i] = fmaf(p, ev[q][i], acc[i]);
+      }
+    }
+  }
+  // merge the 4 slot groups (lanes differing in bits 3, 4); a group without
+  // slots (w < 4) has m = -inf and contributes nothing
+#pragma unroll
+  for (int off = 8; off <= 16; off <<= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, off);
+    const float S2 = __shfl_xor_sync(0xffffffffu, S, off);
+    const float M = fmaxf(m, m2);
+    const float f1 = m == -INFINITY ? 0.f : __expf(m - M);
+    const float f2 = m2 == -INFINITY ? 0.f : __expf(m2 - M);
+    S = S * f1 + S2 * f2;
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) {
+      const float a2 = __shfl_xor_sync(0xffffffffu, acc[i], off);
+      acc[i] = acc[i] * f1 + a2 * f2;
+    }
+    m = M;
+  }
+  if (g == 0) {  // group 0 holds slot 0 (the positive) and its E row
+    const float u = static_cast<float>(row_up ? row_up[row] : upstream_over_n);
+    const float inv = 1.f / S;
+#pragma unroll
+    for (int i = 0; i < DPL; i += 4)
+      *reinterpret_cast<float4*>(dX + row * D + c * DPL + i) =
+          make_float4(u * fmaf(acc[i], inv, -e0[i]), u * fmaf(acc[i + 1], inv, -e0[i + 1]),
+                      u * fmaf(acc[i + 2], inv, -e0[i + 2]), u * fmaf(acc[i + 3], inv, -e0[i + 3]));
+    if (c == 0) {
+      lse[row] = static_cast<double>(m) + log(static_cast<double>(S));
+      pos[row] = p0;
+    }
+  }
+}
+
+// In place: logit[i, s] -> g = (softmax - [s == 0]) u, the unfused rows pass's
+// coefficient formula and rounding (soft = __expf(dot - (float)lse)).
+__global__ void ccem_logit_to_coeff(float* __restrict__ lg, int64_t n, int64_t w,
+                                    const double* __restrict__ lse, const double* __restrict__ row_up,
+                                    double upstream_over_n) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (row >= n) return;
+  const float rl = static_cast<float>(lse[row]);
+  const float u = static_cast<float>(row_up ? row_up[row] : upstream_over_n);
+  float* r = lg + row * w;
+  for (int64_t s = lane; s < w; s += 32) {
+    const float soft = __expf(r[s] - rl);
+    r[s] = (s == 0 ? soft - 1.f : soft) * u;
+  }
+}
+
 // ------------------------------------------------- generic / exact (T) -----
 template <class T>
 __device__ __forceinline__ T mac(T acc, T a, T b) { return fmaf(a, b, acc); }
@@ -746,6 +877,136 @@ __global__ void __launch_bounds__(256) segment_reduce_sorted(
   }
 }
 
+// Deterministic dE of the vectorised (bf16 / f32, D in {64, 128, 256}) CCE-
+// path from the per-entry coefficients coeff[n * w] (fp32, (i, s) order).
+static int ccem_de_vec(int dtype, const void* X, const int64_t* inds, int64_t count, int D,
+                       int64_t v, int64_t w, const float* coeff, void* dE, cudaStream_t st) {
+  const dim3 sgrid(static_cast<unsigned>(ceil_div(v, 8)));
+  // Deterministic dE without a full sort when segments are short (uniform
+  // negatives: ~26 entries per item at cfg3): segment offsets, an unstable
+  // atomic grouping, then one warp per item sorts its <= 64 entry indices
+  // back into index order and reduces (a 64-, 128- or 256-key warp sort,
+  // picked from the longest segment, which is read back while the rows pass
+  // and the grouping run).  Only if some item has more than 256 entries do
+  // the radix grouping (4 x count words of scratch) and the long-segment
+  // reduce run.
+  if (count >= (int64_t(1) << 32)) return fail(LF_EUNSUPPORTED, "ccem: n*w must be < 2^32");
+  Scratch item_off, cursor, grouped, flag, sorted_vals;
+  int rc = flag.alloc(2 * sizeof(uint32_t), st);  // [0] long-segment flag, [1] longest segment
+  if (rc) return rc;
+  LF_CUDA(cudaMemsetAsync(flag.ptr, 0, 2 * sizeof(uint32_t), st));
+  rc = group_offsets(inds, count, v, item_off, st, flag.as<uint32_t>() + 1);
+  if (!rc) rc = cursor.alloc(sizeof(uint32_t) * v, st);
+  if (!rc) rc = grouped.alloc(sizeof(uint32_t) * count, st);
+  if (rc) return rc;
+  // the longest segment comes back while the GPU works on the scatter; it
+  // picks the warp-sort width, and the radix fallback (with its 4 x count
+  // words of scratch) only runs if some item has more than 256 entries
+  uint32_t* longest = pinned_u32();
+  if (!longest) return fail(LF_ENOMEM, "ccem: cudaMallocHost failed");
+  *longest = 0xffffffffu;
+  LF_CUDA(cudaMemcpyAsync(longest, flag.as<uint32_t>() + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  cudaEvent_t seen;
+  LF_CUDA(cudaEventCreateWithFlags(&seen, cudaEventDisableTiming));
+  LF_CUDA(cudaEventRecord(seen, st));
+  LF_CUDA(cudaMemcpyAsync(cursor.ptr, item_off.ptr, sizeof(uint32_t) * v, cudaMemcpyDeviceToDevice, st));
+  scatter_by_item<<<std::min<int64_t>(ceil_div(count, 256), 16 * num_sms()), 256, 0, st>>>(
+      inds, count, cursor.as<uint32_t>(), grouped.as<uint32_t>());
+  LF_LAUNCHED();
+  const cudaError_t se = cudaEventSynchronize(seen);
+  cudaEventDestroy(seen);
+  if (se != cudaSuccess) return cuda_fail(se, "cudaEventSynchronize");
+  const uint32_t lmax = *longest;
+  const int R = lmax <= 64u ? 2 : (lmax <= 128u ? 4 : 8);
+#define LF_SEG2(TX, DD, RR)                                                                       \
+  segment_reduce_sorted<TX, DD, RR><<<sgrid, 256, 0, st>>>(                                      \
+      static_cast<const TX*>(X), coeff, grouped.as<uint32_t>(), item_off.as<uint32_t>(), \
+      v, w, static_cast<float*>(dE), flag.as<uint32_t>())
+#define LF_SEG2_R(TX, DD)            \
+  if (R == 2) LF_SEG2(TX, DD, 2);     \
+  else if (R == 4) LF_SEG2(TX, DD, 4); \
+  else LF_SEG2(TX, DD, 8);
+  if (dtype == LF_BF16) {
+    if (D == 64) { LF_SEG2_R(__nv_bfloat16, 64) }
+    else if (D == 128) { LF_SEG2_R(__nv_bfloat16, 128) }
+    else { LF_SEG2_R(__nv_bfloat16, 256) }
+  } else {
+    if (D == 64) { LF_SEG2_R(float, 64) }
+    else if (D == 128) { LF_SEG2_R(float, 128) }
+    else { LF_SEG2_R(float, 256) }
+  }
+#undef LF_SEG2_R
+#undef LF_SEG2
+  LF_LAUNCHED();
+  if (lmax <= 256u) return LF_OK;  // every item went through the sorted path
+  rc = radix_group(inds, count, v, sorted_vals, st, flag.as<uint32_t>());
+  if (rc) return rc;
+#define LF_SEG(TX, DD)                                                                          \
+  segment_reduce_vec<TX, DD><<<sgrid, 256, 0, st>>>(static_cast<const TX*>(X), coeff, \
+                                                    sorted_vals.as<uint32_t>(),                \
+                                                    item_off.as<uint32_t>(), v, w,             \
+                                                    static_cast<float*>(dE), 256u,             \
+                                                    flag.as<uint32_t>())
+  if (dtype == LF_BF16) {
+    if (D == 64) LF_SEG(__nv_bfloat16, 64);
+    else if (D == 128) LF_SEG(__nv_bfloat16, 128);
+    else LF_SEG(__nv_bfloat16, 256);
+  } else {
+    if (D == 64) LF_SEG(float, 64);
+    else if (D == 128) LF_SEG(float, 128);
+    else LF_SEG(float, 256);
+  }
+#undef LF_SEG
+  LF_LAUNCHED();
+  return LF_OK;
+}
+
+// Fused CCE- forward + backward (vectorised path only; the caller falls back
+// to ccem_forward + ccem_backward otherwise): one gather pass gives lse, pos,
+// dX and the per-entry logits, turned in place into the dE coefficients.
+bool ccem_fused_supported(int dtype, int D, bool atomic_de) {
+  return !atomic_de && (dtype == LF_BF16 || dtype == LF_F32) && (D == 64 || D == 128 || D == 256);
+}
+
+int ccem_forward_backward(int dtype, const void* X, const void* E, const int64_t* inds, int64_t n,
+                          int D, int64_t v, int64_t w, const double* row_upstream, double upstream,
+                          double* lse, double* pos, double* loss, void* dX, void* dE, cudaStream_t st) {
+  if (!ccem_fused_supported(dtype, D, false)) return fail(LF_EUNSUPPORTED, "ccem fused: bf16/f32 with d in {64,128,256}");
+  const double u_n = upstream / static_cast<double>(n);
+  const int64_t count = n * w;
+  Scratch coeff;
+  int rc = coeff.alloc(sizeof(float) * count, st);
+  if (rc) return rc;
+  const dim3 grid(static_cast<unsigned>(ceil_div(n, 8)));
+  {
+    ProfScope prof(LF_K_CCEM_FWD, st);
+#define LF_FUSED(TE, DD)                                                                          \
+  ccem_fused_rows_vec<TE, DD><<<grid, 256, 0, st>>>(static_cast<const TE*>(X),                   \
+                                                   static_cast<const TE*>(E), inds, n, w,        \
+                                                   row_upstream, u_n, lse, pos,                  \
+                                                   static_cast<float*>(dX), coeff.as<float>())
+    if (dtype == LF_BF16) {
+      if (D == 64) LF_FUSED(__nv_bfloat16, 64);
+      else if (D == 128) LF_FUSED(__nv_bfloat16, 128);
+      else LF_FUSED(__nv_bfloat16, 256);
+    } else {
+      if (D == 64) LF_FUSED(float, 64);
+      else if (D == 128) LF_FUSED(float, 128);
+      else LF_FUSED(float, 256);
+    }
+#undef LF_FUSED
+    LF_LAUNCHED();
+  }
+  if (loss) {
+    rc = launch_mean_loss(lse, pos, n, loss, st);
+    if (rc) return rc;
+  }
+  ProfScope prof(LF_K_CCEM_BWD, st);
+  ccem_logit_to_coeff<<<grid, 256, 0, st>>>(coeff.as<float>(), n, w, lse, row_upstream, u_n);
+  LF_LAUNCHED();
+  return ccem_de_vec(dtype, X, inds, count, D, v, w, coeff.as<float>(), dE, st);
+}
+
 int ccem_backward(int dtype, const void* X, const void* E, const int64_t* inds,
                   const double* lse, const double* row_upstream, double upstream, int64_t n,
                   int D, int64_t v, int64_t w, bool atomic_de, void* dX, void* dE,
@@ -795,86 +1056,8 @@ int ccem_backward(int dtype, const void* X, const void* E, const int64_t* inds,
         row_upstream, u_n, static_cast<double*>(dX), coeff.as<double>());
     LF_LAUNCHED();
   }
+  if (vec) return ccem_de_vec(dtype, X, inds, count, D, v, w, coeff.as<float>(), dE, st);
   const dim3 sgrid(static_cast<unsigned>(ceil_div(v, 8)));
-  if (vec) {
-    // Deterministic dE without a full sort when segments are short (uniform
-    // negatives: ~26 entries per item at cfg3): segment offsets, an unstable
-    // atomic grouping, then one warp per item sorts its <= 64 entry indices
-    // back into index order and reduces (a 64-, 128- or 256-key warp sort,
-    // picked from the longest segment, which is read back while the rows pass
-    // and the grouping run).  Only if some item has more than 256 entries do
-    // the radix grouping (4 x count words of scratch) and the long-segment
-    // reduce run.
-    if (count >= (int64_t(1) << 32)) return fail(LF_EUNSUPPORTED, "ccem: n*w must be < 2^32");
-    Scratch item_off, cursor, grouped, flag, sorted_vals;
-    int rc = flag.alloc(2 * sizeof(uint32_t), st);  // [0] long-segment flag, [1] longest segment
-    if (rc) return rc;
-    LF_CUDA(cudaMemsetAsync(flag.ptr, 0, 2 * sizeof(uint32_t), st));
-    rc = group_offsets(inds, count, v, item_off, st, flag.as<uint32_t>() + 1);
-    if (!rc) rc = cursor.alloc(sizeof(uint32_t) * v, st);
-    if (!rc) rc = grouped.alloc(sizeof(uint32_t) * count, st);
-    if (rc) return rc;
-    // the longest segment comes back while the GPU works on the scatter; it
-    // picks the warp-sort width, and the radix fallback (with its 4 x count
-    // words of scratch) only runs if some item has more than 256 entries
-    uint32_t* longest = pinned_u32();
-    if (!longest) return fail(LF_ENOMEM, "ccem: cudaMallocHost failed");
-    *longest = 0xffffffffu;
-    LF_CUDA(cudaMemcpyAsync(longest, flag.as<uint32_t>() + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-    cudaEvent_t seen;
-    LF_CUDA(cudaEventCreateWithFlags(&seen, cudaEventDisableTiming));
-    LF_CUDA(cudaEventRecord(seen, st));
-    LF_CUDA(cudaMemcpyAsync(cursor.ptr, item_off.ptr, sizeof(uint32_t) * v, cudaMemcpyDeviceToDevice, st));
-    scatter_by_item<<<std::min<int64_t>(ceil_div(count, 256), 16 * num_sms()), 256, 0, st>>>(
-        inds, count, cursor.as<uint32_t>(), grouped.as<uint32_t>());
-    LF_LAUNCHED();
-    const cudaError_t se = cudaEventSynchronize(seen);
-    cudaEventDestroy(seen);
-    if (se != cudaSuccess) return cuda_fail(se, "cudaEventSynchronize");
-    const uint32_t lmax = *longest;
-    const int R = lmax <= 64u ? 2 : (lmax <= 128u ? 4 : 8);
-#define LF_SEG2(TX, DD, RR)                                                                       \
-  segment_reduce_sorted<TX, DD, RR><<<sgrid, 256, 0, st>>>(                                      \
-      static_cast<const TX*>(X), coeff.as<float>(), grouped.as<uint32_t>(), item_off.as<uint32_t>(), \
-      v, w, static_cast<float*>(dE), flag.as<uint32_t>())
-#define LF_SEG2_R(TX, DD)            \
-  if (R == 2) LF_SEG2(TX, DD, 2);     \
-  else if (R == 4) LF_SEG2(TX, DD, 4); \
-  else LF_SEG2(TX, DD, 8);
-    if (dtype == LF_BF16) {
-      if (D == 64) { LF_SEG2_R(__nv_bfloat16, 64) }
-      else if (D == 128) { LF_SEG2_R(__nv_bfloat16, 128) }
-      else { LF_SEG2_R(__nv_bfloat16, 256) }
-    } else {
-      if (D == 64) { LF_SEG2_R(float, 64) }
-      else if (D == 128) { LF_SEG2_R(float, 128) }
-      else { LF_SEG2_R(float, 256) }
-    }
-#undef LF_SEG2_R
-#undef LF_SEG2
-    LF_LAUNCHED();
-    if (lmax <= 256u) return LF_OK;  // every item went through the sorted path
-    rc = radix_group(inds, count, v, sorted_vals, st, flag.as<uint32_t>());
-    if (rc) return rc;
-#define LF_SEG(TX, DD)                                                                          \
-  segment_reduce_vec<TX, DD><<<sgrid, 256, 0, st>>>(static_cast<const TX*>(X), coeff.as<float>(), \
-                                                    sorted_vals.as<uint32_t>(),                \
-                                                    item_off.as<uint32_t>(), v, w,             \
-                                                    static_cast<float*>(dE), 256u,             \
-                                                    flag.as<uint32_t>())
-    if (dtype == LF_BF16) {
-      if (D == 64) LF_SEG(__nv_bfloat16, 64);
-      else if (D == 128) LF_SEG(__nv_bfloat16, 128);
-      else LF_SEG(__nv_bfloat16, 256);
-    } else {
-      if (D == 64) LF_SEG(float, 64);
-      else if (D == 128) LF_SEG(float, 128);
-      else LF_SEG(float, 256);
-    }
-#undef LF_SEG
-    LF_LAUNCHED();
-    return LF_OK;
-  }
   Scratch sorted_vals, item_off;
   int rc = sort_by_item(inds, count, v, sorted_vals, item_off, st);
   if (rc) return rc;

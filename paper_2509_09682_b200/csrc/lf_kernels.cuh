@@ -124,6 +124,10 @@ int ccem_backward(int dtype, const void* X, const void* E, const int64_t* inds,
                   const double* lse, const double* row_upstream, double upstream, int64_t n,
                   int D, int64_t v, int64_t w, bool atomic_de, void* dX, void* dE,
                   cudaStream_t st);
+bool ccem_fused_supported(int dtype, int D, bool atomic_de);
+int ccem_forward_backward(int dtype, const void* X, const void* E, const int64_t* inds, int64_t n,
+                          int D, int64_t v, int64_t w, const double* row_upstream, double upstream,
+                          double* lse, double* pos, double* loss, void* dX, void* dE, cudaStream_t st);
 
 // Stable counting-by-radix sort of `count` entries by item (inds[i] in
 // [0, v)): sorted_vals = entry indices grouped by item in index order,

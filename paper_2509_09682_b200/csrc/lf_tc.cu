@@ -460,6 +460,9 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
   uint64_t* acc_empty = acc_full + 1;
   uint64_t* o_done = acc_empty + 1;           // [4] FWDX: a warpgroup's O MMAs completed (per tile)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_done + 4);
+  // backward: per S buffer and epilogue warp, the 32-column chunks of G it did
+  // NOT skip (bit q); warp 2 leaves out the G MMA K steps no warp needs
+  uint32_t* live_mask = tmem_holder + 1;      // [kNB][4]
   float4* merge = reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(bars) + 1024);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -625,13 +628,23 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
         tc_fence_after();
         if (lane == 0) {
           const uint32_t lo = b2_lo + s2.i * (C::kStageBytes >> 4);
-          const uint32_t first = (fresh >> aw) & 1u;
+          // saturated-gradient filtering: a K step (16 stream rows) whose G
+          // columns every epilogue warp skipped is all zeros — leave its MMA
+          // out once the accumulator has been initialised
+          uint32_t live = ~0u;
+          if ((MODE == BWD_ROWS || MODE == BWD_ITEMS) && (FLAGS & kFilt)) {
+            const uint32_t* lm = live_mask + b2.i * 4;
+            live = lm[0] | lm[1] | lm[2] | lm[3];
+          }
+          bool init = !((fresh >> aw) & 1u);
 #pragma unroll
           for (int kk = 0; kk < BN / 16; ++kk) {
+            if (init && !((live >> (kk >> 1)) & 1u)) continue;
 #ifndef LF_DIAG_NOMMA2
             mma_ts(tmem + C::kAccCol + aw * D, tmem + b2.i * BN + kk * 8, umma_desc(lo + kk * 128, hi),
-                   idesc2, (first && kk == 0) ? 0u : 1u);
+                   idesc2, init ? 1u : 0u);
 #endif
+            init = true;
           }
           mma_commit(&empty[s2.i]);
           mma_commit(&s_empty[b2.i]);
@@ -843,7 +856,13 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
               m = max32(e) * kLog2e;
               // no logit exceeds the Cauchy-Schwarz bound |x_i| max_j |e_j|, so
               // with m at most 64 below it no chunk sum can pass 2^64: such
-              // warps run the tile body without the per-chunk overflow check
+              // warps run the tile body without the per-chunk overflow check.
+              // The reference is raised toward bound - 64 by up to 60: the
+              // row's max is >= the first chunk's, so nothing within 2^-66 of
+              // it can fall under the ftz flush (m - 126), and rows whose
+              // first chunk sits up to 124 below their bound (trained-like
+              // rows: a dominant target) still take the fast body.
+              m = fmaxf(m, fminf(p.lse2[orow] - 64.f, m + 60.f));
               fast = __all_sync(0xffffffffu, !(m < p.lse2[orow] - 64.f));
             }
             // CHECK: per-chunk overflow vote (rebase out of line); !CHECK:
@@ -1044,6 +1063,7 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
           // while skippable sub-tiles keep appearing (uniform logits — the
           // headline case — never have one).  Either way the result is exact:
           // the ftz flush zeroes every entry below eps.
+          uint32_t live_bits = 0u;  // chunks of G this warp did not skip
           auto process = [&](auto test_tag) -> bool {
           constexpr bool TEST = decltype(test_tag)::value;
           bool any_below = false;
@@ -1140,6 +1160,7 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
               }
             }
             float x[32];
+            if (!skip) live_bits |= 1u << q;
             if (skip) {
 #pragma unroll
               for (int c = 0; c < 32; ++c) x[c] = 0.f;
@@ -1198,6 +1219,7 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
           };
           skip_on = skip_on ? process(std::true_type{}) : process(std::false_type{});
           tmem_st_wait();
+          if ((FLAGS & kFilt) && lane == 0) live_mask[b * 4 + quad] = live_bits;
 #ifndef LF_DIAG_EARLY
           tc_fence_before();
           __syncwarp();

@@ -47,8 +47,10 @@ if a.ccem:
     tb = timed(lambda: lf.ccem_backward(X, E, inds, out.lse, 1.0, cfg, validate=False), a.iters)
     cfg2 = lf.CceConfig(atomic_de=True)
     tba = timed(lambda: lf.ccem_backward(X, E, inds, out.lse, 1.0, cfg2, validate=False), a.iters)
+    tfb = timed(lambda: lf.ccem_forward_backward(X, E, inds, 1.0, cfg, validate=False), a.iters)
     print(f"ccem n={a.n} d={a.d} v={a.v} K={a.ccem}: fwd {tf:.3f} ms  bwd(det) {tb:.3f} ms  "
-          f"bwd(atomic) {tba:.3f} ms  pos/s={a.n/(tf+tb)*1e3:.3e}")
+          f"bwd(atomic) {tba:.3f} ms  pos/s={a.n/(tf+tb)*1e3:.3e}  fused fwd+bwd {tfb:.3f} ms "
+          f"pos/s={a.n/tfb*1e3:.3e}")
 elif a.fused:
     import ctypes as C
     from paper_2509_09682_b200 import _capi
