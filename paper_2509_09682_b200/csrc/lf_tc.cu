@@ -1103,11 +1103,13 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
               tmem_ld_wait();
             }
 #endif
+            // exp arguments a = S log2e (BWD_ITEMS: S already carries -lse2 ln 2)
+            // or S log2e - lse2 — monotone in S, so the chunk's largest a is
+            // the transform of its largest S (the skip test needs no product)
+            auto arg = [&](float v) { return MODE == BWD_ITEMS ? v * kLog2e : fmaf(v, kLog2e, -lse2); };
             float e[32];
 #pragma unroll
-            for (int c = 0; c < 32; ++c)
-              e[c] = MODE == BWD_ITEMS ? __uint_as_float(cur[c]) * kLog2e
-                                       : fmaf(__uint_as_float(cur[c]), kLog2e, -lse2);
+            for (int c = 0; c < 32; ++c) e[c] = __uint_as_float(cur[c]);
 
             // BWD_ITEMS: lane k checks stream row q*32+k; hm = rows of this chunk
             // whose target item lies in the owner tile (warp-uniform, rare).
@@ -1130,10 +1132,14 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
             bool skip = false;
             // (TEST = false samples only the first chunk of the tile)
             if ((FLAGS & kFilt) && (TEST || q == 0 || (FLAGS & kCount))) {
-              const float mx = max32(e);  // log-depth (FMNMX3 tree)
+              const float mx = arg(max32(e));  // log-depth (FMNMX3 tree) on raw S
               const bool below = __all_sync(0xffffffffu, mx < kThr<FLAGS> && !tgt_here);
               any_below |= below;
               if (TEST) skip = below;
+              if (FLAGS & kCount) {
+#pragma unroll
+                for (int c = 0; c < 32; ++c) e[c] = arg(e[c]);
+              }
               if ((FLAGS & kCount) && MODE == BWD_ROWS) {
 #pragma unroll
                 for (int c = 0; c < 32; ++c)
@@ -1159,12 +1165,19 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
                 if (skip) ++skipped_sub;
               }
             }
-            float x[32];
-            if (!skip) live_bits |= 1u << q;
             if (skip) {
+              // every G entry of the sub-tile is an exact zero
+              uint32_t z[16];
 #pragma unroll
-              for (int c = 0; c < 32; ++c) x[c] = 0.f;
+              for (int c = 0; c < 16; ++c) z[c] = 0u;
+              LF_TMEM_ST16(ta + q * 16, z);
             } else {
+              live_bits |= 1u << q;
+              if (!(FLAGS & kCount)) {
+#pragma unroll
+                for (int c = 0; c < 32; ++c) e[c] = arg(e[c]);
+              }
+              float x[32];
 #pragma unroll
               for (int c = 0; c < 32; ++c) {
                 if (c >= 32 - kPolyBwd) {  // FMA-pipe share of the exps
@@ -1204,8 +1217,6 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
                   }
                 }
               }
-            }
-            {
               uint32_t g[16];
 #pragma unroll
               for (int c = 0; c < 16; ++c) g[c] = pack_bf16x2(x[2 * c], x[2 * c + 1]);

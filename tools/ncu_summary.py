@@ -25,3 +25,9 @@ for k in keys:
         i = hdr.index(k)
         vals = [d[i][:60] for d in data]
         print(f"{k} [{units[i]}]: {vals}")
+# extra metrics: any raw-page column whose name contains one of argv[2:]
+import re as _re
+for pat in sys.argv[2:]:
+    for i, k in enumerate(hdr):
+        if _re.search(pat, k):
+            print(f"{k} [{units[i]}]: {[d[i][:60] for d in data]}")
