@@ -271,6 +271,13 @@ __device__ __forceinline__ float fset_gt(float a, float b) {
   return r;
 }
 
+// sat(a * b + c) on the FMA pipe (one rounding, then clamped to [0, 1]).
+__device__ __forceinline__ float fma_sat(float a, float b, float c) {
+  float r;
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -60,7 +60,7 @@
 #define LF_FWD_MAXCHUNKS 64  // forward: most V chunks pick_chunks may choose
 #endif
 #ifndef LF_EVAL_CONTIG
-#define LF_EVAL_CONTIG 1  // EVAL: CTA-contiguous owner-tile-major units (0: chunk-major round robin)
+#define LF_EVAL_CONTIG 1  // EVAL: 1 CTA-contiguous owner-tile-major units, 2 phase-aligned rounds of owner tiles (see Units; E read ~once per round from HBM, measured slower), 0 chunk-major round robin
 #endif
 #ifndef LF_NWG_EVAL
 #define LF_NWG_EVAL 2
@@ -386,22 +386,66 @@ __device__ __noinline__ float4 fwdx_tile_tail(uint32_t ta, uint32_t o_addr, int 
 // grid, chunk-major.  EVAL: each CTA takes a contiguous range of units in
 // owner-tile-major order, so consecutive units usually share the owner rows
 // and the per-row top-k state carries over (see the EVAL epilogue).
+//
+// EVAL, phase-aligned (LF_EVAL_CONTIG = 2, when there are at least as many
+// owner tiles as CTAs): u is a position in this CTA's own sequence.  Rounds
+// of whole owner tiles first — CTA c takes owner r*grid + c through chunks
+// 0..P-1 in order, so all CTAs stream the same region of E at the same time
+// and E comes from HBM about once per round.  Then the remaining owner
+// tiles' (owner, chunk) cells, split owner-major into one contiguous range
+// per CTA (at most two runs: the tail of one owner tile, the head of the
+// next) — each run carries its rows' state — processed head run first, so
+// that at step t every CTA is at chunk t or t + (P - range): the CTAs stay
+// within a window of E that fits L2.
 template <int MODE>
 struct Units {
   int64_t begin, end, step, P, OT;
+  // EVAL phase-aligned: phase-A units, owner tiles in phase A, the phase-B
+  // range's first owner / first chunk, its last owner, and the head run length
+  int64_t A = 0, R0 = 0, bo = 0, bj = 0, lo = 0, hl = 0;
+  bool aligned = false;
   __device__ Units(const TcParams& p) : P(p.n_chunks), OT(p.owner_tiles) {
-    if (MODE == EVAL && LF_EVAL_CONTIG) {
-      begin = blockIdx.x * p.units / gridDim.x;
-      end = (blockIdx.x + 1) * p.units / gridDim.x;
+    const int64_t G = gridDim.x, c = blockIdx.x;
+    if (MODE == EVAL && LF_EVAL_CONTIG == 2 && OT >= G) {
+      aligned = true;
+      R0 = (OT / G) * G;
+      A = (OT / G) * P;
+      const int64_t cells = (OT - R0) * P;
+      const int64_t b0 = c * cells / G, b1 = (c + 1) * cells / G;
+      begin = 0;
+      end = A + (b1 - b0);
+      step = 1;
+      if (b1 > b0) {
+        bo = b0 / P;
+        bj = b0 % P;
+        lo = (b1 - 1) / P;  // == bo or bo + 1 (the range is shorter than one owner tile)
+        hl = lo == bo ? 0 : (b1 - 1) % P + 1;
+      }
+    } else if (MODE == EVAL && LF_EVAL_CONTIG) {
+      begin = c * p.units / G;
+      end = (c + 1) * p.units / G;
       step = 1;
     } else {
-      begin = blockIdx.x;
+      begin = c;
       end = p.units;
-      step = gridDim.x;
+      step = G;
     }
   }
-  __device__ int64_t chunk(int64_t u) const { return MODE == EVAL && LF_EVAL_CONTIG ? u % P : u / OT; }
-  __device__ int64_t owner(int64_t u) const { return MODE == EVAL && LF_EVAL_CONTIG ? u / P : u % OT; }
+  __device__ int64_t chunk(int64_t u) const {
+    if (MODE == EVAL && aligned) {
+      if (u < A) return u % P;
+      const int64_t t = u - A;
+      return t < hl ? t : bj + (t - hl);
+    }
+    return MODE == EVAL && LF_EVAL_CONTIG ? u % P : u / OT;
+  }
+  __device__ int64_t owner(int64_t u) const {
+    if (MODE == EVAL && aligned) {
+      if (u < A) return (u / P) * gridDim.x + blockIdx.x;
+      return R0 + (u - A < hl ? lo : bo);
+    }
+    return MODE == EVAL && LF_EVAL_CONTIG ? u / P : u % OT;
+  }
 };
 
 // Largest float below x (finite x): "score >= x" == "score > next_down(x)".
@@ -694,6 +738,7 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
       float m = -INFINITY, s = 0.f, tv = 0.f, has = 0.f;
       bool fast = false;  // FWDX: this warp's rows cannot overflow (set with m)
       float st = 0.f, st_dn = 0.f;  // EVAL: the row's target score
+      bool cnt_fma = false;         // EVAL: rank count on the FMA pipe (see below)
       if (MODE == EVAL && run_first) {
         // Seed the list with placeholders just below the k-th score another
         // run of these rows has already published: at least k real items
@@ -738,6 +783,9 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
             st = st_sh[lrow];
           }
           st_dn = next_down(st);
+          // the rank count's FMA-pipe form needs 2^-60 <= |st| < 2^27 in every
+          // row of the warp (always, in practice); otherwise exact FSET compares
+          cnt_fma = __all_sync(0xffffffffu, fabsf(st) >= 0x1p-60f && fabsf(st) < 0x1p27f);
           continue;
         }
         if (tw != wg) continue;
@@ -980,15 +1028,34 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
                   ecnt -= cc < l ? set_ge(w[g][c], st) : (cc > l ? set_gt(w[g][c], st) : 0u);
                 }
             } else {
-              // 1.0f / 0.0f per compare (FSET.BF, ALU pipe) summed on the FMA
-              // pipe: exact (<= 64), one ALU op per item
               const float thr = l >= 64 ? st_dn : st;
-              float f[4] = {0.f, 0.f, 0.f, 0.f};
+              if (cnt_fma) {
+                // score > thr as sat(score 2^100 - thr 2^100) on the FMA pipe:
+                // the exact difference of two distinct floats of which one
+                // (thr) has 2^-60 <= |thr| < 2^27 is at least ulp(thr) >=
+                // 2^-83, so the scaled difference is >= 2^17 (or +-inf) and
+                // saturates to exactly 1.0; equal or lower scores give 0.0.
+                // Summed in pairs with FADD2 — exact (<= 64).
+                const float nk = -thr * 0x1p100f;
+                float f[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-              for (int g = 0; g < 2; ++g)
+                for (int g = 0; g < 2; ++g)
 #pragma unroll
-                for (int c = 0; c < 32; ++c) f[c & 3] += fset_gt(w[g][c], thr);
-              ecnt += static_cast<uint32_t>((f[0] + f[1]) + (f[2] + f[3]));
+                  for (int c = 0; c < 32; c += 4) {
+                    fadd2(f[0], f[1], f[0], f[1], fma_sat(w[g][c], 0x1p100f, nk), fma_sat(w[g][c + 1], 0x1p100f, nk));
+                    fadd2(f[2], f[3], f[2], f[3], fma_sat(w[g][c + 2], 0x1p100f, nk), fma_sat(w[g][c + 3], 0x1p100f, nk));
+                  }
+                ecnt += static_cast<uint32_t>((f[0] + f[1]) + (f[2] + f[3]));
+              } else {
+                // 1.0f / 0.0f per compare (FSET.BF, ALU pipe) summed on the FMA
+                // pipe: exact (<= 64), one ALU op per item
+                float f[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int g = 0; g < 2; ++g)
+#pragma unroll
+                  for (int c = 0; c < 32; ++c) f[c & 3] += fset_gt(w[g][c], thr);
+                ecnt += static_cast<uint32_t>((f[0] + f[1]) + (f[2] + f[3]));
+              }
             }
 #ifndef LF_DIAG_NOTOPK
             const float g0 = max32(w[0]), g1 = max32(w[1]);
