@@ -4,6 +4,7 @@
 // (losses.cpp:48-69, cce.cpp:17-27, ccem.cpp:16-31) with the same messages;
 // the index scans themselves are separate calls (lf_validate_*) because they
 // need a device->host sync.
+#include <nvtx3/nvToolsExt.h>
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -50,10 +51,18 @@ uint64_t g_prof_launches[LF_K_COUNT] = {};
 double g_prof_ms[LF_K_COUNT] = {};
 }  // namespace
 
+// NVTX ranges (header-only NVTX3: a no-op unless a tool such as nsys or
+// ncu --nvtx is attached) name each library phase on the host timeline.
+static const char* const kKindNames[LF_K_COUNT] = {
+    "lf.cce_fwd", "lf.cce_bwd_dx", "lf.cce_bwd_de", "lf.cce_simt", "lf.ccem_fwd",
+    "lf.ccem_bwd", "lf.aux", "lf.eval", "lf.cce_fwd_dx"};
+
 ProfScope::ProfScope(int k, cudaStream_t s) : kind(k), st(s) {
+  nvtxRangePushA(k >= 0 && k < LF_K_COUNT ? kKindNames[k] : "lf.kernel");
   if (g_prof_on.load() && cudaEventCreate(&start) == cudaSuccess) cudaEventRecord(start, st);
 }
 ProfScope::~ProfScope() {
+  nvtxRangePop();
   if (!start) return;
   cudaEvent_t end;
   if (cudaEventCreate(&end) != cudaSuccess) return;
