@@ -709,9 +709,11 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
     const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
     unsigned long long skipped = 0, skipped_sub = 0;
     bool skip_on = true;  // backward: run the skipping variant on the next tile (warp-uniform)
-    Ring<C::kNB> rb;         // S buffer of the current tile
-    Ring<C::kStages> rst;    // its smem stage (BWD_ITEMS staging)
-    int tw = 0;              // current tile's warpgroup (t % NWG)
+    // This CTA's stream tiles before the current unit: tile T (counted over
+    // the CTA's units) sits in S buffer T mod kNB (phase (T / kNB) & 1) and
+    // smem stage T mod kStages, and belongs to epilogue warpgroup T mod NWG,
+    // so a warpgroup steps straight from one of its tiles to the next.
+    uint32_t T0 = 0;
     uint32_t k_tiles = 0;    // FWDX: tiles this warpgroup has handed to the O MMAs
     uint32_t j = 0;
     const Units<MODE> U(p);
@@ -757,7 +759,12 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
         }
       }
       constexpr int kPre = MODE == EVAL ? 1 : 0;  // EVAL: the target-rows tile comes first
-      for (int64_t i = 0; i < ntile + kPre; ++i, rb.next(), rst.next(), tw = (tw + 1 == NWG ? 0 : tw + 1)) {
+      const int64_t i_first =
+          MODE == EVAL ? 0 : static_cast<int64_t>((static_cast<uint32_t>(wg) + NWG - T0 % NWG) % NWG);
+      for (int64_t i = i_first; i < ntile + kPre; i += (MODE == EVAL ? 1 : NWG)) {
+        const uint32_t T = T0 + static_cast<uint32_t>(i);
+        const int tw = static_cast<int>(T % NWG);
+        const uint32_t rbi = T % C::kNB, rbph = (T / C::kNB) & 1u, rsti = T % C::kStages;
         if (MODE == EVAL && i == 0) {
           // S = owner rows x their target rows: the diagonal is each row's
           // target score, from the same MMA as the scores it is compared with.
@@ -766,8 +773,8 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
           // every warpgroup has passed the next unit's handoff).
           float* st_sh = reinterpret_cast<float*>(merge) + (NWG - 1) * BM * C::kEvalStride + (j & 1) * BM;
           if (tw == wg) {
-            const int b = static_cast<int>(rb.i);
-            mbar_wait(&s_full[b], rb.ph);
+            const int b = static_cast<int>(rbi);
+            mbar_wait(&s_full[b], rbph);
             tc_fence_after();
             float d[32];
             LF_TMEM_LD32(tmem + lane_base + b * BN + quad * 32, reinterpret_cast<uint32_t*>(d));
@@ -789,10 +796,10 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
           continue;
         }
         if (tw != wg) continue;
-        const int b = static_cast<int>(rb.i);
+        const int b = static_cast<int>(rbi);
         const int64_t col0 = s_begin + (i - kPre) * BN;
         const int nvalid = static_cast<int>((s_end - col0 < BN ? s_end - col0 : BN));
-        mbar_wait(&s_full[b], rb.ph);
+        mbar_wait(&s_full[b], rbph);
         tc_fence_after();
         const uint32_t ta = tmem + lane_base + b * BN;
         if (MODE == FWD) {
@@ -1099,7 +1106,7 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
           const float* lse2s = nullptr;
           const int* tgts = nullptr;
           if (MODE == BWD_ITEMS) {
-            lse2s = reinterpret_cast<const float*>(stage_smem + rst.i * C::kStageBytes + C::kTileBytes);
+            lse2s = reinterpret_cast<const float*>(stage_smem + rsti * C::kStageBytes + C::kTileBytes);
             tgts = reinterpret_cast<const int*>(lse2s + 128);
           }
 #ifdef LF_DIAG_EPI
@@ -1241,8 +1248,11 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
             } else {
               live_bits |= 1u << q;
               if (!(FLAGS & kCount)) {
+                // packed: two exp arguments per FFMA2 (bitwise the scalar
+                // fmaf / multiply: one rounding each)
+                const float bias = MODE == BWD_ITEMS ? 0.f : -lse2;
 #pragma unroll
-                for (int c = 0; c < 32; ++c) e[c] = arg(e[c]);
+                for (int c = 0; c < 32; c += 2) ffma2(e[c], e[c + 1], e[c], e[c + 1], kLog2e, kLog2e, bias, bias);
               }
               float x[32];
 #pragma unroll
@@ -1305,6 +1315,7 @@ __global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
 #endif
         }
       }
+      T0 += static_cast<uint32_t>(ntile + kPre);
       if (MODE == FWD) {
         // merge the warpgroups' running states for each row
         if (wg > 0) merge[(wg - 1) * BM + lrow] = make_float4(m, s, tv, has);
