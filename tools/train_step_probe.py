@@ -1,5 +1,5 @@
 """A whole training step on the device (trainer.cpp:209-227, cfg2 shape):
-encode_batch -> CCE forward/backward (bf16, eps = 6e-8) -> encoder_backward
+encode_batch -> fused CCE forward+backward (bf16, eps = 6e-8) -> encoder_backward
 -> Adam over emb, W, b and the classifier (with the bf16 shadow of E the next
 step reads).  256 windows x 201 items -> N = 51 200 rows, V = 1M, D = 64,
 synthetic.  CUDA-event time per stage, one JSON line."""
@@ -32,8 +32,8 @@ def step():
     ev[0].record()
     batch = encoder.encode_batch(emb, W, b, items, win_off, torch.bfloat16)
     ev[1].record()
-    out = lf.cce_forward(batch.X, E, batch.targets, cfg, validate=False)
-    res = lf.cce_backward(batch.X, E, batch.targets, out.lse, 1.0, cfg, validate=False, stats=False)
+    # run_loss_layer's pairing (trainer.cpp:71-77) as one fused call
+    out, res = lf.cce_forward_backward(batch.X, E, batch.targets, 1.0, cfg, validate=False)
     ev[2].record()
     d_emb, d_W, d_b = encoder.encoder_backward(V, W, batch, res.grads.d_embeddings)
     ev[3].record()
