@@ -34,6 +34,12 @@ struct Vec8;  // 8 consecutive elements of row storage, widened to float
 #ifndef LF_CCEM_BWD_U
 #define LF_CCEM_BWD_U 4  // CCE- backward rows pass: slots per 8-lane group per step
 #endif
+#ifndef LF_CCEM_ROWS_MINB
+#define LF_CCEM_ROWS_MINB 4  // CCE- gather passes: min resident 256-thread blocks per SM (64 registers; a few spill, still faster: latency-bound gathers)
+#endif
+#ifndef LF_CCEM_RED_MINB
+#define LF_CCEM_RED_MINB 8  // sorted dE segment reduce: min resident blocks per SM (32 registers, full occupancy)
+#endif
 
 template <>
 struct Vec8<__nv_bfloat16> {
@@ -133,7 +139,7 @@ __global__ void __launch_bounds__(256) ccem_fwd_vec(const TE* __restrict__ X,
 // Backward rows pass: recompute, g = (softmax - [s==0]) * u; dX row; coeff
 // per slot (fp32) for the dE pass, or atomic scatter when ATOMIC.
 template <class TE, int D, bool ATOMIC>
-__global__ void __launch_bounds__(256) ccem_bwd_rows_vec(
+__global__ void __launch_bounds__(256, ATOMIC ? 1 : LF_CCEM_ROWS_MINB) ccem_bwd_rows_vec(
     const TE* __restrict__ X, const TE* __restrict__ E, const int64_t* __restrict__ inds,
     int64_t n, int64_t w, const double* __restrict__ lse, const double* __restrict__ row_up,
     double upstream_over_n, float* __restrict__ dX, float* __restrict__ coeff,
@@ -231,7 +237,7 @@ __global__ void __launch_bounds__(256) ccem_bwd_rows_vec(
 // ccem_logit_to_coeff can form the dE coefficient g = (softmax - [s==0]) u
 // exactly as the unfused rows pass does (dE is then bitwise the unfused one).
 template <class TE, int D>
-__global__ void __launch_bounds__(256) ccem_fused_rows_vec(
+__global__ void __launch_bounds__(256, LF_CCEM_ROWS_MINB) ccem_fused_rows_vec(
     const TE* __restrict__ X, const TE* __restrict__ E, const int64_t* __restrict__ inds,
     int64_t n, int64_t w, const double* __restrict__ row_up, double upstream_over_n,
     double* __restrict__ lse, double* __restrict__ pos, float* __restrict__ dX,
@@ -825,7 +831,7 @@ __device__ __forceinline__ void warp_sort(uint32_t (&k)[R]) {
 // combined in a fixed order.  Longer segments set *long_flag and are left to
 // segment_reduce_vec over the radix grouping.
 template <class TX, int D, int R>
-__global__ void __launch_bounds__(256) segment_reduce_sorted(
+__global__ void __launch_bounds__(256, LF_CCEM_RED_MINB) segment_reduce_sorted(
     const TX* __restrict__ X, const float* __restrict__ coeff, const uint32_t* __restrict__ grouped,
     const uint32_t* __restrict__ item_off, int64_t v, int64_t w, float* __restrict__ dE,
     uint32_t* __restrict__ long_flag) {
