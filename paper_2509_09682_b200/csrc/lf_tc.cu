@@ -152,11 +152,19 @@ struct Ring {
   }
 };
 
-template <int MODE>
+// The dE pass's stream tile (rows) at width D: at D = 256 its accumulator
+// takes half of TMEM, and 64-column S tiles leave four S buffers instead of
+// two (measured: dE pass 19.4 -> 12.4 ms at the cfg5 shard shape; 64 columns
+// are slower at D <= 128).
+constexpr int bn_items(int D) { return D >= 256 ? 64 : LF_BN_BWD; }
+
+template <int MODE, int D = 64>
 struct Geo {
   static constexpr int BN = MODE == FWD    ? LF_BN_FWD
                             : MODE == FWDX ? LF_BN_FWDX
-                            : (MODE == EVAL ? 128 : LF_BN_BWD);  // stream tile
+                            : MODE == EVAL ? 128
+                            : MODE == BWD_ITEMS ? bn_items(D)
+                                                : LF_BN_BWD;  // stream tile
   static constexpr int NWG = MODE == FWD    ? LF_NWG_FWD
                              : MODE == EVAL ? LF_NWG_EVAL
                              : MODE == FWDX ? LF_NWG_FWDX
@@ -172,7 +180,7 @@ struct Geo {
 
 template <int D, int MODE>
 struct Cfg {
-  using G = Geo<MODE>;
+  using G = Geo<MODE, D>;
   static constexpr int BN = G::BN;
   static constexpr int kAtoms = D / 64;               // 128-byte K atoms per row
   static constexpr int kOwnerBytes = BM * D * 2;
@@ -472,13 +480,13 @@ __device__ __forceinline__ void topk_insert(float (&kv)[K], int (&ki)[K], float 
 }
 
 template <int D, int MODE, int FLAGS>
-__global__ void __launch_bounds__(Geo<MODE>::kThreads, 1)
+__global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
     cce_tc_kernel(const __grid_constant__ CUtensorMap map_owner,
                   const __grid_constant__ CUtensorMap map_stream,
                   const __grid_constant__ CUtensorMap map_lsex,
                   const __grid_constant__ CUtensorMap map_ones, const TcParams p) {
   using C = Cfg<D, MODE>;
-  using G = Geo<MODE>;
+  using G = Geo<MODE, D>;
   constexpr int BN = G::BN;
   constexpr int NWG = G::NWG;
   constexpr int NQ = G::NQ;
@@ -1663,7 +1671,7 @@ int launch_mode(const CUtensorMap& mo, const CUtensorMap& ms, const CUtensorMap&
                  : MODE == FWDX ? LF_K_CCE_FWD_DX
                  : (MODE == BWD_ROWS ? LF_K_CCE_BWD_DX : LF_K_CCE_BWD_DE),
                  st);
-  kern<<<grid, Geo<MODE>::kThreads, C::kSmem, st>>>(mo, ms, mb, m1, p);
+  kern<<<grid, Geo<MODE, D>::kThreads, C::kSmem, st>>>(mo, ms, mb, m1, p);
   LF_LAUNCHED();
   return LF_OK;
 }
@@ -1981,7 +1989,8 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
   const double gscale = filt ? std::ldexp(1.0, noscale ? -126 : -62) / eps : std::fabs(scale);
   const double out_scale =
       filt ? scale * eps * std::ldexp(1.0, noscale ? 126 : 62) : (scale < 0 ? -1.0 : 1.0);
-  constexpr int BN = Geo<BWD_ROWS>::BN;
+  constexpr int BN = Geo<BWD_ROWS>::BN;        // dX pass stream tile (items)
+  const int BNi = bn_items(static_cast<int>(D));  // dE pass stream tile (rows), = Geo<BWD_ITEMS, D>::BN
   const int64_t row_tiles = ceil_div(n, BM);
   const int64_t item_tiles = ceil_div(v, BM);     // dE owner tiles
   const int64_t item_stream = ceil_div(v, BN);    // dX stream tiles
@@ -1995,7 +2004,7 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
   LF_LAUNCHED();
   CUtensorMap mx_own, mx_str, me_own, me_str;  // owner box 128 rows, stream box BN rows
   rc = make_map(&mx_own, X, n, D, BM);
-  if (!rc) rc = make_map(&mx_str, X, n, D, BN);
+  if (!rc) rc = make_map(&mx_str, X, n, D, BNi);
   if (!rc) rc = make_map(&me_own, E, v, D, BM);
   if (!rc) rc = make_map(&me_str, E, v, D, BN);
   if (rc) return rc;
@@ -2045,7 +2054,7 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
   q.n_owner = v;
   q.n_stream = n;
   q.owner_tiles = item_tiles;
-  q.chunk = ceil_div(n, BN) * BN;
+  q.chunk = ceil_div(n, BNi) * BNi;
   q.n_chunks = 1;
   q.units = item_tiles;
   q.tgt = tgt.as<int32_t>();
@@ -2078,7 +2087,7 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
                                                      ones.as<__nv_bfloat16>());
   LF_LAUNCHED();
   CUtensorMap mbias, mones;
-  rc = make_map_k16(&mbias, bias.ptr, n_pad, BN);
+  rc = make_map_k16(&mbias, bias.ptr, n_pad, BNi);
   if (!rc) rc = make_map_k16(&mones, ones.ptr, BM, BM);
   if (rc) return rc;
   rc = launch_d<BWD_ITEMS>(D, dX ? (flags & ~kCount) : flags, me_own, mx_str, mbias, mones, q, st);
