@@ -1267,8 +1267,10 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
               for (int c = 0; c < 32; ++c) {
                 if (c >= 32 - kPolyBwd) {  // FMA-pipe share of the exps
                   if (FLAGS & kFilt) {
+                    // 2^(a + 64) (valid where a >= -126 matters); the fast
+                    // (unscaled) domain takes it back down exactly
                     const float y = ex2_fma_shl<64>(e[c]);
-                    x[c] = e[c] < kThr<FLAGS> ? 0.f : y;
+                    x[c] = e[c] < kThr<FLAGS> ? 0.f : (kNoScale<FLAGS> ? y * 0x1p-64f : y);
                   } else {
                     x[c] = ex2_fma(fmaxf(e[c], -125.f));
                   }
