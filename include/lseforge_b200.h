@@ -112,7 +112,7 @@ LF_API int lf_cce_backward(const void* d_X, const void* d_E, const int64_t* d_ta
 /* Fused cce_forward + cce_backward: the pair run_loss_layer issues back to
  * back on the same inputs (trainer.cpp:71-77, forward then backward with the
  * forward's lse).  Writes everything lf_cce_forward and lf_cce_backward
- * write.  For bf16 with d = 64 / 128 and filter_eps < 2^-12 it runs the
+ * write.  For bf16 with d = 64 / 128 / 256 and filter_eps < 2^-12 it runs the
  * fused kernel: one pass over the logits computes the LSE AND the
  * softmax-weighted item sum of dX (2 exps per logit instead of 3), then the
  * item-owned dE pass.  That dX is the exact (unfiltered) softmax - onehot

@@ -140,7 +140,7 @@ def cce_forward_backward(X: torch.Tensor, E: torch.Tensor, x: torch.Tensor, upst
                          validate: bool = True, stats: bool = False):
     """cce_forward then cce_backward(lse, upstream) on the same inputs — the
     pair run_loss_layer issues (trainer.cpp:71-77) — as one call
-    (lf_cce_forward_backward).  bf16 with d = 64 / 128 and filter_eps < 2^-12
+    (lf_cce_forward_backward).  bf16 with d = 64 / 128 / 256 and filter_eps < 2^-12
     runs the fused kernel: the LSE and dX's softmax-weighted item sum in one
     pass over the logits, then the dE pass; dX is then the unfiltered
     gradient (each dropped entry is below eps), dE and the skip statistics

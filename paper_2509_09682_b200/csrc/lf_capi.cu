@@ -240,7 +240,7 @@ extern "C" {
 int lf_abi_version(void) { return LF_ABI_VERSION; }
 
 // The fused forward + dX kernel serves lf_cce_forward_backward when dX may
-// ignore the filter: bf16, d = 64 / 128, and eps below 2^-12 (entries it
+// ignore the filter: bf16, d = 64 / 128 / 256, and eps below 2^-12 (entries it
 // would drop are < eps each; eps = 0 is exact) unless the caller asks for
 // the filtered dX pass (LF_FLAG_FILTER_DX).
 int lf_cce_fused_supported(const lf_cce_config* cfg, int64_t d) {

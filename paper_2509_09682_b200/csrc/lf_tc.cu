@@ -157,17 +157,29 @@ struct Ring {
 // two (measured: dE pass 19.4 -> 12.4 ms at the cfg5 shard shape; 64 columns
 // are slower at D <= 128).
 constexpr int bn_items(int D) { return D >= 256 ? 64 : LF_BN_BWD; }
+// The fused forward + dX at D = 256: one epilogue warpgroup (its 256-column O
+// accumulator is half of TMEM) on 64-column S tiles (four S buffers).  At
+// D = 256 the tile's MMA work is four times D = 64's per logit, so one
+// warpgroup's exps keep pace with the tensor pipe.
+#ifndef LF_FWDX256_BN
+#define LF_FWDX256_BN 64
+#endif
+#ifndef LF_FWDX128_NWG
+#define LF_FWDX128_NWG LF_NWG_FWDX
+#endif
+constexpr int nwg_fwdx(int D) { return D >= 256 ? 1 : (D >= 128 ? LF_FWDX128_NWG : LF_NWG_FWDX); }
+constexpr int bn_fwdx(int D) { return D >= 256 ? LF_FWDX256_BN : LF_BN_FWDX; }
 
 template <int MODE, int D = 64>
 struct Geo {
   static constexpr int BN = MODE == FWD    ? LF_BN_FWD
-                            : MODE == FWDX ? LF_BN_FWDX
+                            : MODE == FWDX ? bn_fwdx(D)
                             : MODE == EVAL ? 128
                             : MODE == BWD_ITEMS ? bn_items(D)
                                                 : LF_BN_BWD;  // stream tile
   static constexpr int NWG = MODE == FWD    ? LF_NWG_FWD
                              : MODE == EVAL ? LF_NWG_EVAL
-                             : MODE == FWDX ? LF_NWG_FWDX
+                             : MODE == FWDX ? nwg_fwdx(D)
                                             : LF_NWG_BWD;  // epilogue WGs
   // control warps: TMA producer, S-MMA issuer (+ the G-MMA issuer in the
   // backward and the fused forward)
@@ -1790,7 +1802,7 @@ __global__ void fwdx_dx(const float4* __restrict__ part, const float* __restrict
 
 }  // namespace
 
-int tc_fwdx_supported(int D) { return D == 64 || D == 128; }
+int tc_fwdx_supported(int D) { return D == 64 || D == 128 || D == 256; }
 
 // Fused forward + unnormalised dX over the local shard.  part: [P][n] float4
 // {m, s, t, has} (log2 units, as tc_cce_forward_partials); opart: [P][n][D]
@@ -1799,8 +1811,8 @@ int tc_fwdx_supported(int D) { return D == 64 || D == 128; }
 int tc_cce_fwdx_partials(const void* X, const void* E, const int64_t* targets, int64_t n, int D,
                          int64_t v, int64_t v_offset, Scratch& part, Scratch& opart, Scratch& tgt,
                          int* P_out, cudaStream_t st) {
-  if (!tc_fwdx_supported(D)) return fail(LF_EUNSUPPORTED, "fused forward/dX: d must be 64 or 128");
-  constexpr int BN = Geo<FWDX>::BN;
+  if (!tc_fwdx_supported(D)) return fail(LF_EUNSUPPORTED, "fused forward/dX: d must be 64, 128 or 256");
+  const int BN = bn_fwdx(D);  // = Geo<FWDX, D>::BN
   const int64_t owner_tiles = ceil_div(n, BM);
   const int64_t stream_tiles = ceil_div(v, BN);
 #ifndef LF_FWDX_MAXCHUNKS
@@ -1828,9 +1840,12 @@ int tc_cce_fwdx_partials(const void* X, const void* E, const int64_t* targets, i
     if (D == 64) {
       max_row_norm<64><<<g, 256, 0, st>>>(Eb, v, emax);
       row_bounds<64><<<ceil_div(n_pad, 256), 256, 0, st>>>(Xb, n, n_pad, emax, bound.as<float>());
-    } else {
+    } else if (D == 128) {
       max_row_norm<128><<<g, 256, 0, st>>>(Eb, v, emax);
       row_bounds<128><<<ceil_div(n_pad, 256), 256, 0, st>>>(Xb, n, n_pad, emax, bound.as<float>());
+    } else {
+      max_row_norm<256><<<g, 256, 0, st>>>(Eb, v, emax);
+      row_bounds<256><<<ceil_div(n_pad, 256), 256, 0, st>>>(Xb, n, n_pad, emax, bound.as<float>());
     }
     LF_LAUNCHED();
   }
@@ -1852,8 +1867,9 @@ int tc_cce_fwdx_partials(const void* X, const void* E, const int64_t* targets, i
 #ifdef LF_VARIANT_D64_ONLY
   rc = launch_mode<64, FWDX, 0>(mo, ms, mo, mo, p, st);
 #else
-  rc = D == 64 ? launch_mode<64, FWDX, 0>(mo, ms, mo, mo, p, st)
-               : launch_mode<128, FWDX, 0>(mo, ms, mo, mo, p, st);
+  rc = D == 64    ? launch_mode<64, FWDX, 0>(mo, ms, mo, mo, p, st)
+       : D == 128 ? launch_mode<128, FWDX, 0>(mo, ms, mo, mo, p, st)
+                  : launch_mode<256, FWDX, 0>(mo, ms, mo, mo, p, st);
 #endif
   if (rc) return rc;
   *P_out = static_cast<int>(P);
@@ -1872,8 +1888,10 @@ int tc_fwdx_dx(const float* part, const float* opart, int P, int64_t n, int D, c
     fwdx_dx<64><<<blocks, 256, 0, st>>>(pp, opart, P, n, lse_in, Eb, tgt, sc, lse_out, pos_out, dX);
   else if (D == 128)
     fwdx_dx<128><<<blocks, 256, 0, st>>>(pp, opart, P, n, lse_in, Eb, tgt, sc, lse_out, pos_out, dX);
+  else if (D == 256)
+    fwdx_dx<256><<<blocks, 256, 0, st>>>(pp, opart, P, n, lse_in, Eb, tgt, sc, lse_out, pos_out, dX);
   else
-    return fail(LF_EUNSUPPORTED, "fused forward/dX: d must be 64 or 128");
+    return fail(LF_EUNSUPPORTED, "fused forward/dX: d must be 64, 128 or 256");
   LF_LAUNCHED();
   return LF_OK;
 }

@@ -349,7 +349,7 @@ class ShardedCce:
     def forward_backward(self, X, E_shard, targets, upstream: float = 1.0,
                          cfg: CceConfig = CceConfig(), stats: bool = False):
         """forward + backward(lse, upstream) as one step.  Where the fused
-        kernel applies (bf16, d = 64 / 128, eps < 2^-12, collective exchange)
+        kernel applies (bf16, d = 64 / 128 / 256, eps < 2^-12, collective exchange)
         the shard's LSE partials and dX's item sum come from one pass over its
         logits (lf_cce_fwdx_shard_begin), then the all-gather of the (m, s, t)
         triples, dX normalised by the global lse and the dE pass

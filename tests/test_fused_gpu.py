@@ -42,7 +42,8 @@ def check_against_oracle(out, bwd, Eh, Ch, t, eps=0.0, upstream=1.0, frac_tol=No
 
 @pytest.mark.parametrize("n,d,v", [(1, 64, 2), (127, 64, 129), (128, 64, 128), (300, 64, 5000),
                                    (257, 128, 3000), (1000, 128, 20000), (2048, 64, 32768),
-                                   (640, 64, 131072 + 77)])
+                                   (640, 64, 131072 + 77), (1, 256, 3), (130, 256, 1000),
+                                   (300, 256, 20000 + 33)])
 def test_fused_equals_oracle_unfiltered(lf, n, d, v):
     X, E, x, Eh, Ch, t = instance(0xB2000011 + n + v, n, d, v, torch.bfloat16)
     out, bwd = fused(lf, X, E, x)
@@ -145,3 +146,14 @@ def test_fused_agrees_with_separate_calls(lf):
         assert torch.equal(fo.lse, so.lse)
         assert torch.equal(fb.grads.d_embeddings, sb.grads.d_embeddings)
         assert torch.equal(fb.grads.d_classifier, sb.grads.d_classifier)
+
+
+def test_fused_d256_peaked_rows_and_filter(lf):
+    """D = 256 (cfg5 width; one epilogue warpgroup, 64-column tiles): the
+    rebase path on peaked rows and the filtered oracle at the preset eps."""
+    X, E, x, Eh, Ch, t = peaked(0xB2000007, 256, 256, 3000, np.arange(256) % 3 == 0)
+    out, bwd = fused(lf, X, E, x)
+    check_against_oracle(out, bwd, Eh, Ch, t)
+    X, E, x, Eh, Ch, t = instance(0xB2000008, 200, 256, 9000, torch.bfloat16)
+    out, bwd = fused(lf, X, E, x, eps=6e-8, stats=True)
+    check_against_oracle(out, bwd, Eh, Ch, t, eps=6e-8, frac_tol=2e-3)
