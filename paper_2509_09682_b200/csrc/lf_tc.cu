@@ -38,6 +38,9 @@
 #ifndef LF_POLY_FWD
 #define LF_POLY_FWD 0
 #endif
+#ifndef LF_COMMIT_ALWAYS
+#define LF_COMMIT_ALWAYS 1  // backward: release a tile's stage / S buffer by tcgen05.commit even when every G MMA was filtered away
+#endif
 #ifndef LF_POLY_BWD
 #define LF_POLY_BWD 0
 #endif
@@ -197,12 +200,11 @@ struct Cfg {
   static constexpr int kAtoms = D / 64;               // 128-byte K atoms per row
   static constexpr int kOwnerBytes = BM * D * 2;
   static constexpr int kTileBytes = BN * D * 2;
-  // BWD_ITEMS stage extras: lse2[BN] + tgt[BN] (1 KB, padded), then the
-  // stream rows' bias columns (BN rows x 16 bf16 = 32 B, SWIZZLE_32B) that
-  // fold -lse2 into the S MMA as a fifth K=16 step.
-  static constexpr int kBiasOff = kTileBytes + 1024;
+  // BWD_ITEMS stage extra: the stream rows' bias columns (BN rows x 16 bf16
+  // = 32 B, SWIZZLE_32B) that fold -lse2 into the S MMA as a fifth K=16 step.
+  static constexpr int kBiasOff = kTileBytes;
   static constexpr int kBiasBytes = BN * 32;
-  static constexpr int kExtraBytes = MODE == BWD_ITEMS ? 1024 + kBiasBytes : 0;
+  static constexpr int kExtraBytes = MODE == BWD_ITEMS ? kBiasBytes : 0;
   static constexpr int kStageBytes = kTileBytes + kExtraBytes;
   static constexpr int kOnesBytes = MODE == BWD_ITEMS ? BM * 32 : 0;  // constant A bias columns
   // EVAL: per-row merge records {count, K values, K indices} (stride 2K + 1
@@ -589,18 +591,14 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
         for (int64_t s0 = s_begin; s0 < s_end; s0 += BN, rs.next()) {
           unsigned char* stg = stage_smem + rs.i * C::kStageBytes;
           mbar_wait(&empty[rs.i], rs.ph ^ 1);
-          // BWD_ITEMS also stages the stream rows' lse2 and local targets.
-          mbar_arrive_expect_tx(&full[rs.i],
-                                C::kTileBytes + (MODE == BWD_ITEMS ? 8 * BN + C::kBiasBytes : 0));
+          // BWD_ITEMS also stages the stream rows' bias columns.
+          mbar_arrive_expect_tx(&full[rs.i], C::kTileBytes + (MODE == BWD_ITEMS ? C::kBiasBytes : 0));
 #pragma unroll
           for (int a = 0; a < C::kAtoms; ++a)
             tma_load_2d(stg + a * BN * 128, &map_stream, &full[rs.i], a * 64,
                         static_cast<int32_t>(s0), pol);
-          if (MODE == BWD_ITEMS) {
+          if (MODE == BWD_ITEMS)
             tma_load_2d(stg + C::kBiasOff, &map_lsex, &full[rs.i], 0, static_cast<int32_t>(s0), pol);
-            bulk_load(stg + C::kTileBytes, p.lse2 + s0, 4 * BN, &full[rs.i]);
-            bulk_load(stg + C::kTileBytes + 512, p.tgt + s0, 4 * BN, &full[rs.i]);
-          }
         }
       }
     }
@@ -701,6 +699,7 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
             live = lm[0] | lm[1] | lm[2] | lm[3];
           }
           bool init = !((fresh >> aw) & 1u);
+          bool issued = false;
 #pragma unroll
           for (int kk = 0; kk < BN / 16; ++kk) {
             if (init && !((live >> (kk >> 1)) & 1u)) continue;
@@ -709,9 +708,18 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
                    idesc2, init ? 1u : 0u);
 #endif
             init = true;
+            issued = true;
           }
-          mma_commit(&empty[s2.i]);
-          mma_commit(&s_empty[b2.i]);
+          if (issued || LF_COMMIT_ALWAYS) {
+            // the stage and the S buffer are free once this tile's MMAs complete
+            mma_commit(&empty[s2.i]);
+            mma_commit(&s_empty[b2.i]);
+          } else {
+            // every K step filtered away: nothing reads them any more (the
+            // epilogue's reads are ordered before g_ready) — release now
+            mbar_arrive(&empty[s2.i]);
+            mbar_arrive(&s_empty[b2.i]);
+          }
           if (MODE == FWDX) mma_commit(&o_done[aw]);
         }
         fresh &= ~(1u << aw);
@@ -731,7 +739,7 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
     bool skip_on = true;  // backward: run the skipping variant on the next tile (warp-uniform)
     // This CTA's stream tiles before the current unit: tile T (counted over
     // the CTA's units) sits in S buffer T mod kNB (phase (T / kNB) & 1) and
-    // smem stage T mod kStages, and belongs to epilogue warpgroup T mod NWG,
+    // belongs to epilogue warpgroup T mod NWG,
     // so a warpgroup steps straight from one of its tiles to the next.
     uint32_t T0 = 0;
     uint32_t k_tiles = 0;    // FWDX: tiles this warpgroup has handed to the O MMAs
@@ -784,7 +792,7 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
       for (int64_t i = i_first; i < ntile + kPre; i += (MODE == EVAL ? 1 : NWG)) {
         const uint32_t T = T0 + static_cast<uint32_t>(i);
         const int tw = static_cast<int>(T % NWG);
-        const uint32_t rbi = T % C::kNB, rbph = (T / C::kNB) & 1u, rsti = T % C::kStages;
+        const uint32_t rbi = T % C::kNB, rbph = (T / C::kNB) & 1u;
         if (MODE == EVAL && i == 0) {
           // S = owner rows x their target rows: the diagonal is each row's
           // target score, from the same MMA as the scores it is compared with.
@@ -819,6 +827,13 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
         const int b = static_cast<int>(rbi);
         const int64_t col0 = s_begin + (i - kPre) * BN;
         const int nvalid = static_cast<int>((s_end - col0 < BN ? s_end - col0 : BN));
+        // BWD_ITEMS with in-loop targets: the stream rows' local targets (read
+        // from global, in flight while this warp waits for the tile's S)
+        int tpre[NQ];
+        if (MODE == BWD_ITEMS && (FLAGS & kTgtIn)) {
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) tpre[q] = __ldg(p.tgt + col0 + q * 32 + lane);
+        }
         mbar_wait(&s_full[b], rbph);
         tc_fence_after();
         const uint32_t ta = tmem + lane_base + b * BN;
@@ -1123,12 +1138,6 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
           // undoes the factor on the accumulator.  A 32 x 32 sub-tile whose
           // largest a is below the threshold (and that holds no target) skips
           // its exps (warp vote).
-          const float* lse2s = nullptr;
-          const int* tgts = nullptr;
-          if (MODE == BWD_ITEMS) {
-            lse2s = reinterpret_cast<const float*>(stage_smem + rsti * C::kStageBytes + C::kTileBytes);
-            tgts = reinterpret_cast<const int*>(lse2s + 128);
-          }
 #ifdef LF_DIAG_EPI
           {  // timing diagnostic only (wrong results): 1 = no TMEM traffic, 2 = ld + st only
             if (LF_DIAG_EPI == 2) {
@@ -1211,7 +1220,7 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
             unsigned hm = 0;
 #ifndef LF_DIAG_NOTGT
             if (MODE == BWD_ITEMS && (FLAGS & kTgtIn)) {
-              tq = tgts[q * 32 + lane] - o0;
+              tq = tpre[q] - o0;  // the stream row's local target (p.tgt is padded to the tile grid)
               hm = __ballot_sync(0xffffffffu, static_cast<unsigned>(tq) < static_cast<unsigned>(BM));
             }
 #endif

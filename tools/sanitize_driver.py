@@ -27,7 +27,12 @@ def rnd(*shape, dtype=torch.float32):
 
 def main():
     n, v, k = 200, 1000, 15
-    for dtype, d in ((torch.bfloat16, 64), (torch.bfloat16, 128), (torch.float32, 64), (torch.float64, 16)):
+    cases = ((torch.bfloat16, 64), (torch.bfloat16, 128), (torch.bfloat16, 256), (torch.float32, 64),
+             (torch.float64, 16))
+    only = os.environ.get("LF_SANITIZE_D")  # developer filter, e.g. "256"
+    if only:
+        cases = tuple(c for c in cases if str(c[1]) == only)
+    for dtype, d in cases:
         X, E = rnd(n, d, dtype=dtype), rnd(v, d, dtype=dtype)
         x = torch.randint(0, v, (n,), device=dev, generator=g)
         for eps in (0.0, 6e-8, 2.0 ** -8, 1.0):
