@@ -327,6 +327,43 @@ __device__ __forceinline__ void fadd2(float& d0, float& d1, float a0, float a1, 
       : "=f"(d0), "=f"(d1)
       : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
 }
+// Two 2^(a + S) on the FMA pipe with packed ops (Cody-Waite: a = j + f, j =
+// round(a) by the 1.5 * 2^23 magic add (the shift S folded into it), f in
+// [-0.5, 0.5], 2^f by a degree-4 polynomial (max relative error 2.6e-6),
+// 2^(j + S) added into the exponent field).  a is clamped to >= -125 - S
+// first (valid for a + S <= 127): one FMNMX per value, then 3 FADD2 +
+// 4 FFMA2 + 2 integer adds per pair.
+template <int S>
+__device__ __forceinline__ void ex2_poly_x2(float& y0, float& y1, float a0, float a1) {
+  constexpr float kM = 12582912.f + static_cast<float>(S);
+  a0 = fmaxf(a0, -125.f - static_cast<float>(S));
+  a1 = fmaxf(a1, -125.f - static_cast<float>(S));
+  float t0, t1, j0, j1, f0, f1, p0, p1;
+  fadd2(t0, t1, a0, a1, kM, kM);
+  fadd2(j0, j1, t0, t1, -kM, -kM);  // round(a)
+  fadd2(f0, f1, a0, a1, -j0, -j1);
+  ffma2(p0, p1, 0.009570101276f, 0.009570101276f, f0, f1, 0.05591786281f, 0.05591786281f);
+  ffma2(p0, p1, p0, p1, f0, f1, 0.2402474433f, 0.2402474433f);
+  ffma2(p0, p1, p0, p1, f0, f1, 0.6931217908f, 0.6931217908f);
+  ffma2(p0, p1, p0, p1, f0, f1, 0.9999992847f, 0.9999992847f);
+  y0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+  y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
+}
+
+// The backward filter domain's 2^a with ex2.approx.ftz semantics on the FMA
+// pipe: every a < -126 must give an exact 0.  2^(a + 64) by the packed form
+// above (a clamped to >= -189), then an FTZ multiply by 2^-64: exact for
+// normal results, and anything below 2^-126 flushes to +0.
+__device__ __forceinline__ void ex2_poly_ftz_x2(float& y0, float& y1, float a0, float a1) {
+  float z0, z1;
+  ex2_poly_x2<64>(z0, z1, a0, a1);
+  asm("{\n\t.reg .b64 ra, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\t"
+      "mul.rn.ftz.f32x2 rd, ra, %4;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(y0), "=f"(y1)
+      : "f"(z0), "f"(z1), "l"(0x1f8000001f800000ull));
+}
+
 // Sum of 32 registers as a packed tree (15 FADD2 + 1 FADD, depth 5).
 __device__ __forceinline__ float sum32_x2(const float (&x)[32]) {
   float a[16];

@@ -42,7 +42,7 @@
 #define LF_COMMIT_ALWAYS 1  // backward: release a tile's stage / S buffer by tcgen05.commit even when every G MMA was filtered away
 #endif
 #ifndef LF_POLY_BWD
-#define LF_POLY_BWD 0
+#define LF_POLY_BWD 4  // backward (fast filter domain): exps per 32 on the FMA pipe (packed), even
 #endif
 #ifndef LF_NOSCALE
 #define LF_NOSCALE 1
@@ -244,6 +244,10 @@ constexpr int kPolyFwd = LF_POLY_FWD;
 template <int FLAGS>
 constexpr bool kNoScale = LF_NOSCALE != 0 && !(FLAGS & kTgtIn);
 constexpr int kPolyBwd = LF_POLY_BWD;
+#ifndef LF_POLY_FWDX
+#define LF_POLY_FWDX 8  // fused forward: exps per 32 taken on the FMA pipe (packed), even
+#endif
+constexpr int kPolyFwdx = LF_POLY_FWDX;
 template <int POLY>
 __device__ __forceinline__ float ex2_mix(int c, float a) {
   if ((c & 31) >= 32 - POLY) return ex2_fma(fminf(fmaxf(a, -125.f), 127.f));
@@ -971,7 +975,11 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
                   ffma2(x[c], x[c + 1], __uint_as_float(cur[c]), __uint_as_float(cur[c + 1]), kLog2e, kLog2e,
                         -m, -m);
 #pragma unroll
-                for (int c = 0; c < 32; ++c) x[c] = ex2_approx(x[c]);
+                for (int c = 0; c < 32 - (CHECK ? 0 : kPolyFwdx); ++c) x[c] = ex2_approx(x[c]);
+                if (!CHECK) {  // (branch-free body) the FMA-pipe share of the exps
+#pragma unroll
+                  for (int c = 32 - kPolyFwdx; c < 32; c += 2) ex2_poly_x2<0>(x[c], x[c + 1], x[c], x[c + 1]);
+                }
                 const float sum = sum32_x2(x);
 #else
 #pragma unroll
@@ -1284,26 +1292,19 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
                 for (int c = 0; c < 32; c += 2) ffma2(e[c], e[c + 1], e[c], e[c + 1], kLog2e, kLog2e, bias, bias);
               }
               float x[32];
+              // FMA-pipe share of the exps (fast filter domain only)
+              constexpr int kP = (FLAGS & kFilt) && kNoScale<FLAGS> ? kPolyBwd : 0;
 #pragma unroll
-              for (int c = 0; c < 32; ++c) {
-                if (c >= 32 - kPolyBwd) {  // FMA-pipe share of the exps
-                  if (FLAGS & kFilt) {
-                    // 2^(a + 64) (valid where a >= -126 matters); the fast
-                    // (unscaled) domain takes it back down exactly
-                    const float y = ex2_fma_shl<64>(e[c]);
-                    x[c] = e[c] < kThr<FLAGS> ? 0.f : (kNoScale<FLAGS> ? y * 0x1p-64f : y);
-                  } else {
-                    x[c] = ex2_fma(fmaxf(e[c], -125.f));
-                  }
-                } else {
+              for (int c = 0; c < 32 - kP; ++c) {
 #ifdef LF_DIAG_NOEXP
-                  x[c] = e[c];  // timing diagnostic only: wrong results
+                x[c] = e[c];  // timing diagnostic only: wrong results
 #else
-                  x[c] = ex2_approx(e[c]);
+                x[c] = ex2_approx(e[c]);
 #endif
-                  if ((FLAGS & kFilt) && !kNoScale<FLAGS>) x[c] *= 18446744073709551616.f;  // 2^64
-                }
+                if ((FLAGS & kFilt) && !kNoScale<FLAGS>) x[c] *= 18446744073709551616.f;  // 2^64
               }
+#pragma unroll
+              for (int c = 32 - kP; c < 32; c += 2) ex2_poly_ftz_x2(x[c], x[c + 1], e[c], e[c + 1]);
               // The target is never filtered: g = (s - 1) |scale| (cce.cpp:193-195).
               // Under FILT its softmax is recomputed unflushed from the raw
               // logit still in `cur`: s * 2^-62 / eps = 2^(a + 64).
