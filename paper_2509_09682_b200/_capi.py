@@ -86,9 +86,8 @@ def lib():
         L.lf_ccem_forward.argtypes = [vp, vp, vp, i64, i64, i64, i64, cfgp, dp, dp, dp, vp]
         L.lf_ccem_backward.argtypes = [vp, vp, vp, dp, dp, C.c_double, i64, i64, i64, i64, cfgp,
                                        vp, vp, vp]
-        if hasattr(L, "lf_ccem_forward_backward"):  # (older developer builds lack it)
-            L.lf_ccem_forward_backward.argtypes = [vp, vp, vp, i64, i64, i64, i64, dp, C.c_double,
-                                                   cfgp, dp, dp, dp, vp, vp, vp]
+        L.lf_ccem_forward_backward.argtypes = [vp, vp, vp, i64, i64, i64, i64, dp, C.c_double,
+                                               cfgp, dp, dp, dp, vp, vp, vp]
         L.lf_validate_targets.argtypes = [vp, i64, i64, vp]
         L.lf_validate_inds.argtypes = [vp, i64, i64, i64, vp]
         L.lf_estimate_flops.argtypes = [i64, i64, i64, i64, C.c_int32, C.POINTER(C.c_uint64),
@@ -146,8 +145,7 @@ def lib():
                      "lf_cem_backward", "lf_cce_forward_backward", "lf_cce_fused_supported",
                      "lf_cce_fwdx_shard_begin", "lf_cce_fwdx_shard_end", "lf_cce_work_free",
                      "lf_peer_status", "lf_peer_comm_status", "lf_ccem_forward_backward"):
-            if hasattr(L, name):
-                getattr(L, name).restype = C.c_int
+            getattr(L, name).restype = C.c_int
         if L.lf_abi_version() != 1:
             raise ImportError("liblseforge_b200.so ABI mismatch")
         _lib = L
