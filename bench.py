@@ -385,8 +385,10 @@ def run_ours(args):
                 "traffic": tr.get("dram_bytes_per_launch") if tr else None,
                 "peak_source": mufu_src,
                 "algorithmic_exps_per_launch": exps[dom], "ms_per_launch": dur * 1e3,
-                "note": "one exp per logit per launch (N*V_shard logits); traffic = dram read+write "
-                        "per launch from ncu --set full (profiles/traffic.json)"}
+                "note": "one exp per logit per launch (N*V_shard logits), whether MUFU ex2 or the "
+                        "packed FMA-pipe polynomial computes it (a share of each 32-column chunk); peak = "
+                        "the MUFU rate alone; traffic = dram read+write per launch from ncu --set full "
+                        "(profiles/traffic.json)"}
         ach = flops[dom] / dur / 1e12
         roof_tc = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": peaks["tc_sustained"],
                    "unit": "TFLOP/s", "frac": ach / peaks["tc_sustained"],
