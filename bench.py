@@ -64,7 +64,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-extras", action="store_true", help="skip the cfg3 and filter sub-records")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the cfg3, filter and sharded-config sub-records")
     ap.add_argument("--exchange", choices=["collective", "peer"], default="collective",
                     help="N>1: torch.distributed collectives (NCCL) or the peer-memory exchange "
                          "fused into the producing kernels (CUDA IPC)")
@@ -419,6 +420,7 @@ def run_ours(args):
         del res_box[0], out, res
         extras["filter"] = filter_protocol(lf, X, E, x, Xh, Ch, t, flush, stream, args)
         extras["cfg3"] = cfg3_record(lf, flush, stream, args, peaks, not args.no_cpu_baseline)
+        extras["sharded_configs"] = shard_record(lf, flush, stream, args, peaks)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "positions/s", "n_gpus": world,
@@ -437,7 +439,8 @@ def run_ours(args):
                 "kernels": kern, "gpu_launches": int(launches), "e2e": e2e, "e2e_grads": e2e_grads,
                 "e2e_dropin": extras.get("e2e_dropin"),
                 "cpu_baseline": extras.get("cpu_baseline"), "parity": extras.get("parity"),
-                "filter": extras.get("filter"), "cfg3": extras.get("cfg3"), "clocks": clk}
+                "filter": extras.get("filter"), "cfg3": extras.get("cfg3"),
+                "sharded_configs": extras.get("sharded_configs"), "clocks": clk}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
     return 0
@@ -713,6 +716,48 @@ def cfg3_record(lf, flush, stream, args, peaks, cpu):
     del box[0], o, g, X3, E3, x3, inds
     torch.cuda.synchronize()
     return rec
+
+
+def shard_record(lf, flush, stream, args, peaks):
+    """Per-GPU work of the catalog-sharded configs (BASELINE configs[3],
+    configs[4]) at P = 8, timed on this one GPU: the fused step over one
+    rank's catalog slice (the exchange is not included — one all-gather of
+    N*16 B and one all-reduce of N*D*4 B per step).  Synthetic
+    torch.rand data of the shard's shape, bf16, eps = 6e-8."""
+    import torch
+    dev = torch.device("cuda", torch.cuda.current_device())
+    g = torch.Generator(device=dev).manual_seed(0)
+    out = []
+    for name, n, d, v_total, P in (("cfg4: N=131072, D=128, V=4M over 8 GPUs", 131072, 128, 4_000_000, 8),
+                                   ("cfg5: N=7680 (15% of 256x200), D=256, V=16M over 8 GPUs", 7680, 256,
+                                    16_000_000, 8)):
+        vs = v_total // P
+        X = (torch.rand(n, d, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
+        E = (torch.rand(vs, d, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
+        x = torch.randint(0, vs, (n,), device=dev, generator=g)
+        cfg = lf.CceConfig(filter_eps=EPS)
+        box = [None]
+
+        def step():
+            box[0] = None
+            box[0] = lf.cce_forward_backward(X, E, x, 1.0, cfg, validate=False)
+
+        kern = {}
+        ms = timed_steps(step, max(3, min(args.steps, 5)), 2, stream, flush, kern)
+        flops = 8.0 * n * vs * d
+        tc = flops / (ms / 1e3) / 1e12
+        out.append({"config": name, "shard": {"n": n, "d": d, "v_shard": vs}, "ms_per_step": ms,
+                    "kernel_ms_per_step": kern,
+                    "compute_bound_job_positions_per_s": n / (ms / 1e3),
+                    "roofline": {"bound": "tensor", "achieved": tc, "peak": peaks["tc_sustained"],
+                                 "unit": "TFLOP/s", "frac": tc / peaks["tc_sustained"],
+                                 "algorithmic_flops_per_step": flops}})
+        del box[0], X, E, x
+        torch.cuda.synchronize()
+    return {"shards": out,
+            "note": "one rank's fused CCE step at P = 8 on one B200 (no NVLink exchange: no multi-GPU "
+                    "box in this round); compute_bound_job_positions_per_s = N / t_shard, the 8-GPU "
+                    "job's rate if the two exchanges were free"}
 
 
 def main():
