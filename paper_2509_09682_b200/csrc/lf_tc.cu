@@ -171,7 +171,10 @@ constexpr int bn_items(int D) { return D >= 256 ? 64 : LF_BN_BWD; }
 #define LF_FWDX128_NWG LF_NWG_FWDX
 #endif
 constexpr int nwg_fwdx(int D) { return D >= 256 ? 1 : (D >= 128 ? LF_FWDX128_NWG : LF_NWG_FWDX); }
-constexpr int bn_fwdx(int D) { return D >= 256 ? LF_FWDX256_BN : LF_BN_FWDX; }
+#ifndef LF_FWDX128_BN
+#define LF_FWDX128_BN LF_BN_FWDX
+#endif
+constexpr int bn_fwdx(int D) { return D >= 256 ? LF_FWDX256_BN : (D >= 128 ? LF_FWDX128_BN : LF_BN_FWDX); }
 
 template <int MODE, int D = 64>
 struct Geo {
