@@ -451,14 +451,17 @@ def run_e2e(step, X, E, x, stream, args, world, dev, grads):
     ITS inputs (X, the local E slice, targets) from pinned host memory and
     reads its loss (grads=True: also dX and dE) back on the host.  The copy of
     step k+1 runs on a side stream into the other half of a double buffer
-    while step k computes; with grads, step k's dX / dE go back on a third
-    stream while step k+1 computes."""
+    while step k computes; the host reads step k's loss once step k+1 is
+    enqueued (as a training loop logs it), so the GPU never waits for the
+    host; with grads, step k's dX / dE go back on a third stream while step
+    k+1 computes."""
     import torch
     import torch.distributed as dist
     Xh = X.cpu().pin_memory()
     Eh = E.cpu().pin_memory()
     xh = x.cpu().pin_memory()
-    loss_h = torch.empty((), dtype=torch.float64).pin_memory()
+    loss_h = [torch.empty((), dtype=torch.float64).pin_memory() for _ in range(2)]
+    loss_ev = [torch.cuda.Event() for _ in range(2)]
     dXh = torch.empty((X.shape[0], X.shape[1]), dtype=torch.float32).pin_memory() if grads else None
     dEh = torch.empty((E.shape[0], E.shape[1]), dtype=torch.float32).pin_memory() if grads else None
     bufs = [(torch.empty_like(X), torch.empty_like(E), torch.empty_like(x)) for _ in range(2)]
@@ -489,7 +492,8 @@ def run_e2e(step, X, E, x, stream, args, world, dev, grads):
             consumed[b].record(stream)
             if k + 1 < nsteps:
                 issue_copy(k + 1)
-            loss_h.copy_(o.loss, non_blocking=True)
+            loss_h[b].copy_(o.loss, non_blocking=True)
+            loss_ev[b].record(stream)
             if grads:
                 done = torch.cuda.Event()
                 done.record(stream)
@@ -501,8 +505,11 @@ def run_e2e(step, X, E, x, stream, args, world, dev, grads):
                     dEh.copy_(r.grads.d_classifier, non_blocking=True)
                 keep[b] = r  # hold the device gradients until their copy is done
                 pending = k
-            stream.synchronize()  # the host reads the loss every step
-            _ = float(loss_h)
+            if k > 0:  # the host reads the previous step's loss while this one runs
+                loss_ev[1 - b].synchronize()
+                _ = float(loss_h[1 - b])
+        loss_ev[(nsteps - 1) % 2].synchronize()
+        _ = float(loss_h[(nsteps - 1) % 2])
         if grads:
             ds.synchronize()
 
@@ -523,7 +530,8 @@ def run_e2e(step, X, E, x, stream, args, world, dev, grads):
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "ms_per_step": float(e_ms),
             "api": "ShardedCce.forward_backward -> lf_cce_forward_backward (C-ABI)",
-            "overlap": "step k+1's host->device copy overlaps step k's compute (double buffer)"
+            "overlap": "step k+1's host->device copy overlaps step k's compute (double buffer); the "
+                       "host reads step k's loss while step k+1 runs"
                        + ("; step k's dX/dE device->host copy overlaps step k+1" if grads else "")}
 
 
