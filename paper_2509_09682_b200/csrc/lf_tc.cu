@@ -1829,9 +1829,17 @@ int tc_cce_fwdx_partials(const void* X, const void* E, const int64_t* targets, i
   const int64_t owner_tiles = ceil_div(n, BM);
   const int64_t stream_tiles = ceil_div(v, BN);
 #ifndef LF_FWDX_MAXCHUNKS
-#define LF_FWDX_MAXCHUNKS 4
+#define LF_FWDX_MAXCHUNKS 0  // 0: bounded by the O partials' memory (see below)
 #endif
-  const int64_t chunks = pick_chunks(owner_tiles, stream_tiles, LF_FWDX_MAXCHUNKS);
+  // More V chunks balance the waves when there are few owner tiles (cfg5's
+  // shard: 60), at the price of one n x D fp32 partial per chunk: the
+  // partials may take max(64 MB, 1/8 of the shard's E + dE bytes) — cfg2
+  // keeps 4 chunks, the cfg5 shard gets ~27 (13.4 -> 11.4 ms).
+  const int64_t part_budget = std::max<int64_t>(int64_t(64) << 20, v * D * 6 / 8);
+  const int64_t max_chunks =
+      LF_FWDX_MAXCHUNKS > 0 ? LF_FWDX_MAXCHUNKS
+                            : std::max<int64_t>(4, std::min<int64_t>(64, part_budget / (n * D * 4)));
+  const int64_t chunks = pick_chunks(owner_tiles, stream_tiles, max_chunks);
   const int64_t tiles_per = ceil_div(stream_tiles, chunks);
   const int64_t P = ceil_div(stream_tiles, tiles_per);
   const int64_t n_pad = owner_tiles * BM;
