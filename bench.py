@@ -412,15 +412,29 @@ def run_ours(args):
         e2e_grads = run_e2e(step, X, E, x, stream, args, world, dev, grads=True)
 
     extras = {}
+
+    def sub_record(name, fn):
+        # a sub-record that fails is reported in the line, never fatal to it
+        try:
+            extras[name] = fn()
+        except Exception as e:  # noqa: BLE001
+            extras[name] = {"error": f"{type(e).__name__}: {e}"[:400]}
+            torch.cuda.synchronize()
+
     if rank == 0 and world == 1 and not args.no_e2e:
-        extras["e2e_dropin"] = dropin_e2e()
+        sub_record("e2e_dropin", dropin_e2e)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        extras["cpu_baseline"], extras["parity"] = cfg2_parity(lf, sh, X, E, x, out, res, Xh, Ch, t, cfg)
+        sub_record("cfg2_parity", lambda: cfg2_parity(lf, sh, X, E, x, out, res, Xh, Ch, t, cfg))
+        cp = extras.pop("cfg2_parity")
+        if isinstance(cp, tuple):
+            extras["cpu_baseline"], extras["parity"] = cp
+        else:
+            extras["cpu_baseline"] = extras["parity"] = cp
     if rank == 0 and world == 1 and not args.no_extras:
         del res_box[0], out, res
-        extras["filter"] = filter_protocol(lf, X, E, x, Xh, Ch, t, flush, stream, args)
-        extras["cfg3"] = cfg3_record(lf, flush, stream, args, peaks, not args.no_cpu_baseline)
-        extras["sharded_configs"] = shard_record(lf, flush, stream, args, peaks)
+        sub_record("filter", lambda: filter_protocol(lf, X, E, x, Xh, Ch, t, flush, stream, args))
+        sub_record("cfg3", lambda: cfg3_record(lf, flush, stream, args, peaks, not args.no_cpu_baseline))
+        sub_record("sharded_configs", lambda: shard_record(lf, flush, stream, args, peaks))
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "positions/s", "n_gpus": world,
