@@ -131,6 +131,9 @@ struct TcParams {
   float fix_scale;               // scale = upstream / n (signed, real units)
   const uint32_t* fix_off;       // BWD_ITEMS: [v + 2] offsets into fix_list per local item
   const uint32_t* fix_list;      // BWD_ITEMS: rows sorted by local target
+  const float* tw;               // !kTgtIn: 1 - p_t per row (its target's softmax, full precision)
+  const uint32_t* hit_off;       // BWD_ITEMS !kTgtIn: [item tiles + 1] offsets into hit_list
+  const uint64_t* hit_list;      // rows grouped by their target's item tile, ascending
   float4* part;          // FWD: [n_chunks][n_owner]
   float* out;            // BWD_ROWS: [n_chunks][n_owner][D]; BWD_ITEMS: [n_owner][D]
   unsigned long long* counters;  // [0] skipped elems, [1] skipped tiles, [2] total tiles
@@ -347,7 +350,7 @@ __device__ __noinline__ void tmem_scale_bf16(uint32_t taddr, int nwords, float f
 // in TMEM), stored, and O and the P chunks already written are rescaled by
 // f = 2^(m - m_new).  Returns {m_new, f, sum of the chunk's P}.
 __device__ __noinline__ float4 fwdx_rebase(uint32_t ta, uint32_t o_addr, int D, int q, int nv, float m,
-                                           bool over) {
+                                           bool over, int jt) {
   uint32_t r[32];
   LF_TMEM_LD32(ta + q * 32, r);
   tmem_ld_wait();
@@ -363,6 +366,8 @@ __device__ __noinline__ float4 fwdx_rebase(uint32_t ta, uint32_t o_addr, int D, 
     x[c] = c < nv ? ex2_approx(fma_log2(__uint_as_float(r[c]), mr)) : 0.f;
     a += x[c];
   }
+#pragma unroll
+  for (int c = 0; c < 32; ++c) x[c] = c == jt ? 0.f : x[c];  // the target leaves O (see fwdx_dx)
   uint32_t g[16];
 #pragma unroll
   for (int c = 0; c < 16; ++c) g[c] = pack_bf16x2(x[2 * c], x[2 * c + 1]);
@@ -404,7 +409,7 @@ __device__ __noinline__ float4 fwdx_tile_tail(uint32_t ta, uint32_t o_addr, int 
     tmem_ld_wait();
     const float mm = max32_valid(r, nv) * kLog2e;
     const bool over = mm > (m == -INFINITY ? -INFINITY : m + 64.f);
-    const float4 o = fwdx_rebase(ta, o_addr, D, q, nv, m, over);
+    const float4 o = fwdx_rebase(ta, o_addr, D, q, nv, m, over, lc - q * 32);
     m = o.x;
     s = fmaf(s, o.y, o.z);
   }
@@ -774,6 +779,23 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
       }
       float m = -INFINITY, s = 0.f, tv = 0.f, has = 0.f;
       bool fast = false;  // FWDX: this warp's rows cannot overflow (set with m)
+      // BWD_ITEMS read-out form: the rows whose target lies in this owner tile,
+      // ascending, packed row << 7 | local target; hnext / hnext2 = the next
+      // two (~0 when none is left), loaded a tile-walk ahead of their use;
+      // hti = hnext's stream tile (the per-tile test is one 32-bit compare)
+      uint32_t hptr = 0, hend = 0;
+      uint64_t hnext = ~0ull, hnext2 = ~0ull;
+      int hti = INT_MAX;
+      auto hit_tile = [&](uint64_t h) {
+        return h == ~0ull ? INT_MAX : static_cast<int>((static_cast<int64_t>(h >> 7) - s_begin) / BN);
+      };
+      if (MODE == BWD_ITEMS && !(FLAGS & kTgtIn)) {
+        hptr = p.hit_off[ot];
+        hend = p.hit_off[ot + 1];
+        if (hptr < hend) hnext = p.hit_list[hptr];
+        if (hptr + 1 < hend) hnext2 = p.hit_list[hptr + 1];
+        hti = hit_tile(hnext);
+      }
       float st = 0.f, st_dn = 0.f;  // EVAL: the row's target score
       bool cnt_fma = false;         // EVAL: rank count on the FMA pipe (see below)
       if (MODE == EVAL && run_first) {
@@ -938,7 +960,10 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
             tv = r.z;
             has = r.w;
           } else {
-            if (__any_sync(0xffffffffu, static_cast<unsigned>(lc) < static_cast<unsigned>(BN))) {
+            // a tile holding some row's target: capture the logit, and run the
+            // CHECK body, which leaves the target entry out of P (the rare path)
+            const bool tgt_tile = __any_sync(0xffffffffu, static_cast<unsigned>(lc) < static_cast<unsigned>(BN));
+            if (tgt_tile) {
               const float2 r = fwdx_capture(ta, NQ, lc, tv, has);  // before P overwrites S
               tv = r.x;
               has = r.y;
@@ -1006,11 +1031,18 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
                       waited = true;
                     }
                     tc_fence_after();
-                    const float4 r = fwdx_rebase(ta, o_addr, D, q, 32, m, over);
+                    const float4 r = fwdx_rebase(ta, o_addr, D, q, 32, m, over, lc - q * 32);
                     m = r.x;
                     s = fmaf(s, r.y, r.z);
                     stored = true;
                   }
+                }
+                if (CHECK && !stored) {
+                  // the target entry leaves O (counted in s above; fwdx_dx adds
+                  // -(1 - p_t) E_t back in full precision)
+                  const int jt = lc - q * 32;
+#pragma unroll
+                  for (int c = 0; c < 32; ++c) x[c] = c == jt ? 0.f : x[c];
                 }
                 if (!stored) {
                   s += sum;
@@ -1022,7 +1054,7 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
                 if (q + 1 < NQ) tmem_ld_wait();
               }
             };
-            if (fast) {
+            if (fast && !tgt_tile) {
               body(std::false_type{});
             } else {
               body(std::true_type{});
@@ -1178,6 +1210,41 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
           // headline case — never have one).  Either way the result is exact:
           // the ftz flush zeroes every entry below eps.
           uint32_t live_bits = 0u;  // chunks of G this warp did not skip
+          // The read-out form (!kTgtIn): each row's target entry leaves the
+          // product (fwdx_dx / the read-out add -(1 - p_t) back in full
+          // precision).  Tiles holding a target (~BN / tiles of the other side,
+          // 1.6 % at cfg2) run the TEST body, which masks it in registers:
+          // BWD_ROWS at column lc_t, BWD_ITEMS at the bits of tm[] (this lane's
+          // owner item is the target of those stream rows, from the hit list).
+          bool tgt_tile = false;
+          uint32_t tm[NQ];
+#ifdef LF_DIAG_NOMASK  // timing diagnostic only (wrong results): no target masking
+          if (false) {
+#else
+          if (!(FLAGS & kTgtIn)) {
+#endif
+            if (MODE == BWD_ROWS) {
+              tgt_tile = __any_sync(0xffffffffu, static_cast<unsigned>(lc_t) < static_cast<unsigned>(BN));
+            } else if (hti <= static_cast<int>(i - kPre)) {  // warp-uniform, rare
+              const int ti = static_cast<int>(i - kPre);
+#pragma unroll
+              for (int q = 0; q < NQ; ++q) tm[q] = 0u;
+              // hits in the other warpgroup's tiles (hti < ti) are passed over
+              while (hti <= ti) {
+                if (hti == ti) {
+                  const int c = static_cast<int>(static_cast<int64_t>(hnext >> 7) - col0);
+                  const uint32_t bit = lrow == static_cast<int>(hnext & 127u) ? 1u << (c & 31) : 0u;
+#pragma unroll
+                  for (int q = 0; q < NQ; ++q) tm[q] |= q == (c >> 5) ? bit : 0u;
+                  tgt_tile = true;
+                }
+                ++hptr;
+                hnext = hnext2;
+                hnext2 = hptr + 1 < hend ? p.hit_list[hptr + 1] : ~0ull;
+                hti = hit_tile(hnext);
+              }
+            }
+          }
           auto process = [&](auto test_tag) -> bool {
           constexpr bool TEST = decltype(test_tag)::value;
           bool any_below = false;
@@ -1329,6 +1396,20 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
                   }
                 }
               }
+              if (TEST && !(FLAGS & kTgtIn) && tgt_tile) {
+                if (MODE == BWD_ROWS) {
+                  if (__any_sync(0xffffffffu, static_cast<unsigned>(jt) < 32u)) {
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) x[c] = c == jt ? 0.f : x[c];
+                  }
+                } else {
+                  const uint32_t mk = tm[q];
+                  if (__any_sync(0xffffffffu, mk != 0u)) {
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) x[c] = (mk >> c) & 1u ? 0.f : x[c];
+                  }
+                }
+              }
               uint32_t g[16];
 #pragma unroll
               for (int c = 0; c < 16; ++c) g[c] = pack_bf16x2(x[2 * c], x[2 * c + 1]);
@@ -1340,7 +1421,7 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
           }
           return any_below;
           };
-          skip_on = skip_on ? process(std::true_type{}) : process(std::false_type{});
+          skip_on = skip_on || tgt_tile ? process(std::true_type{}) : process(std::false_type{});
           tmem_st_wait();
           if ((FLAGS & kFilt) && lane == 0) live_mask[b * 4 + quad] = live_bits;
 #ifndef LF_DIAG_EARLY
@@ -1488,8 +1569,9 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
         float* dst = MODE == BWD_ROWS ? p.out + (chunk * p.n_owner + orow) * D
                                       : p.out + orow * D;
         const float os = p.out_scale;
-        // !kTgtIn: the onehot part of softmax - onehot, -scale x (the target's
-        // item row | the rows targeting this item, in sorted = row order)
+        // !kTgtIn: the target entries of softmax - onehot, left out of the
+        // product: -scale (1 - p_t) x (the target's item row | the rows
+        // targeting this item, in sorted = row order)
         uint32_t fb = 0, fe = 0;
         const __nv_bfloat16* frow = nullptr;
         if (!(FLAGS & kTgtIn) && orow < p.n_owner) {
@@ -1516,10 +1598,15 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
 #pragma unroll
               for (int c = 0; c < 16; ++c) fx[c] = 0.f;
               for (uint32_t k = fb; k < fe; ++k) {
-                const __nv_bfloat16* xr =
-                    MODE == BWD_ROWS ? frow : p.fix_rows + static_cast<int64_t>(p.fix_list[k]) * D;
+                const int64_t rr = MODE == BWD_ROWS ? orow : static_cast<int64_t>(p.fix_list[k]);
+                const __nv_bfloat16* xr = MODE == BWD_ROWS ? frow : p.fix_rows + rr * D;
+#ifdef LF_DIAG_NOTW  // timing diagnostic only (wrong results)
+                const float wk = 1.f;
+#else
+                const float wk = p.tw[rr];  // 1 - p_t of that row
+#endif
 #pragma unroll
-                for (int c = 0; c < 16; ++c) fx[c] += __bfloat162float(xr[c0 + c]);
+                for (int c = 0; c < 16; ++c) fx[c] = fmaf(wk, __bfloat162float(xr[c0 + c]), fx[c]);
               }
 #pragma unroll
               for (int c = 0; c < 16; ++c) o[c] = fmaf(-p.fix_scale, fx[c], o[c]);
@@ -1680,10 +1767,40 @@ __global__ void prep_rows(const int64_t* __restrict__ targets, const double* __r
   if (lse2) lse2[i] = l;
 }
 
-__global__ void target_keys(const int32_t* __restrict__ tgt, int64_t n, int64_t v,
-                            int64_t* __restrict__ keys) {
+// Sort keys of the rows by local target item >> shift (out-of-shard targets
+// -> `none`, the last bin).
+__global__ void target_keys(const int32_t* __restrict__ tgt, int64_t n, int64_t none,
+                            int64_t* __restrict__ keys, int shift) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) keys[i] = tgt[i] >= 0 ? tgt[i] : v;
+  if (i < n) keys[i] = tgt[i] >= 0 ? (tgt[i] >> shift) : none;
+}
+
+// The dE pass's hit list: row << 7 | (target & 127) (the local item in its
+// 128-item owner tile), so the epilogue needs no dependent load of tgt[row].
+__global__ void pack_hits(const uint32_t* __restrict__ rows, const int32_t* __restrict__ tgt, int64_t n,
+                          uint64_t* __restrict__ hits) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) hits[i] = static_cast<uint64_t>(rows[i]) << 7 | static_cast<uint32_t>(tgt[rows[i]] & 127);
+}
+
+// Read-out form of the backward: w_i = 1 - p_t,i = -expm1(t_i - lse_i) per
+// row whose target is in the shard (0 otherwise), with the target logit t_i
+// in double from the bf16 rows (warp per row) — full precision however close
+// p_t is to 1.
+__global__ void target_weight(const __nv_bfloat16* __restrict__ X, const __nv_bfloat16* __restrict__ E,
+                              const int32_t* __restrict__ tgt, const double* __restrict__ lse, int64_t n,
+                              int64_t n_pad, int D, float* __restrict__ tw) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= n_pad) return;
+  const int t = row < n ? tgt[row] : -1;
+  double acc = 0.0;
+  if (t >= 0)
+    for (int k = lane; k < D; k += 32)
+      acc += static_cast<double>(__bfloat162float(X[row * D + k])) *
+             static_cast<double>(__bfloat162float(E[static_cast<int64_t>(t) * D + k]));
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) tw[row] = t >= 0 ? static_cast<float>(-expm1(acc - lse[row])) : 0.f;
 }
 
 template <int D, int MODE, int FLAGS>
@@ -1775,17 +1892,20 @@ __global__ void fwdx_dx(const float4* __restrict__ part, const float* __restrict
   const int lane = threadIdx.x & 31;
   const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= n) return;
-  double lse2;
+  double lse2, t = 0.0;
+  for (int p = 0; p < P; ++p) {
+    const float4 q = part[p * n + row];
+    if (q.w != 0.f) t = static_cast<double>(q.z);
+  }
   if (lse_in) {
     lse2 = lse_in[row] * 1.4426950408889634;
   } else {
     double M = -INFINITY;
     for (int p = 0; p < P; ++p) M = fmax(M, static_cast<double>(part[p * n + row].x));
-    double S = 0.0, t = 0.0;
+    double S = 0.0;
     for (int p = 0; p < P; ++p) {
       const float4 q = part[p * n + row];
       if (q.x != -INFINITY) S += static_cast<double>(q.y) * exp2(static_cast<double>(q.x) - M);
-      if (q.w != 0.f) t = static_cast<double>(q.z);
     }
     lse2 = M + log2(S);
     if (lane == 0) {
@@ -1805,11 +1925,13 @@ __global__ void fwdx_dx(const float4* __restrict__ part, const float* __restrict
 #pragma unroll
     for (int k = 0; k < CPL; ++k) acc[k] = fmaf(w, o[lane + 32 * k], acc[k]);
   }
-  const int t = tgt[row];
+  // the target entry was left out of O: its term p_t - 1 in full precision
+  const int ti = tgt[row];
+  const float wt = ti >= 0 ? static_cast<float>(-expm1(t - lse2 * 0.6931471805599453)) : 0.f;
 #pragma unroll
   for (int k = 0; k < CPL; ++k) {
-    const float et = t >= 0 ? __bfloat162float(E[static_cast<int64_t>(t) * D + lane + 32 * k]) : 0.f;
-    dX[row * D + lane + 32 * k] = scale * (acc[k] - et);
+    const float et = ti >= 0 ? __bfloat162float(E[static_cast<int64_t>(ti) * D + lane + 32 * k]) : 0.f;
+    dX[row * D + lane + 32 * k] = scale * fmaf(-wt, et, acc[k]);
   }
 }
 
@@ -2043,6 +2165,16 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
   prep_rows<<<ceil_div(n_pad, 256), 256, 0, st>>>(targets, lse, n, n_pad, v, v_offset, sub,
                                                  tgt.as<int32_t>(), lse2.as<float>());
   LF_LAUNCHED();
+  // read-out form (!tgt_in): 1 - p_t per row, full precision
+  Scratch tw;
+  if (!tgt_in) {
+    rc = tw.alloc(sizeof(float) * n_pad, st);
+    if (rc) return rc;
+    target_weight<<<ceil_div(n_pad, 8), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(X),
+                                                      static_cast<const __nv_bfloat16*>(E), tgt.as<int32_t>(),
+                                                      lse, n, n_pad, static_cast<int>(D), tw.as<float>());
+    LF_LAUNCHED();
+  }
   CUtensorMap mx_own, mx_str, me_own, me_str;  // owner box 128 rows, stream box BN rows
   rc = make_map(&mx_own, X, n, D, BM);
   if (!rc) rc = make_map(&mx_str, X, n, D, BNi);
@@ -2079,6 +2211,7 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
   p.counters = counters;
   p.fix_rows = static_cast<const __nv_bfloat16*>(E);
   p.fix_scale = static_cast<float>(scale);
+  p.tw = tw.as<float>();
   rc = launch_d<BWD_ROWS>(D, flags, mx_own, me_str, mx_own, mx_own, p, st);
   if (rc) return rc;
   if (push) {  // chunk reduction fused with the all-gather of this rank's dX partial
@@ -2106,18 +2239,31 @@ int tc_cce_backward(const void* X, const void* E, const int64_t* targets, const 
   q.counters = counters;
   q.fix_rows = static_cast<const __nv_bfloat16*>(X);
   q.fix_scale = static_cast<float>(scale);
-  Scratch keys, fix_list, fix_off;
+  q.tw = tw.as<float>();
+  Scratch keys, fix_list, fix_off, hit_list, hit_off, hits;
   if (!tgt_in) {
     // rows grouped by local target item (stable, so each item's rows are
     // summed in row order at the dE read-out); out-of-shard targets -> item v
     rc = keys.alloc(sizeof(int64_t) * n, st);
     if (rc) return rc;
-    target_keys<<<ceil_div(n, 256), 256, 0, st>>>(tgt.as<int32_t>(), n, v, keys.as<int64_t>());
+    target_keys<<<ceil_div(n, 256), 256, 0, st>>>(tgt.as<int32_t>(), n, v, keys.as<int64_t>(), 0);
     LF_LAUNCHED();
     rc = sort_by_item(keys.as<int64_t>(), n, v + 1, fix_list, fix_off, st);
     if (rc) return rc;
     q.fix_off = fix_off.as<uint32_t>();
     q.fix_list = fix_list.as<uint32_t>();
+    // ... and by the target's 128-item owner tile, ascending within a tile:
+    // the dE epilogue walks them to leave each target entry out of G
+    target_keys<<<ceil_div(n, 256), 256, 0, st>>>(tgt.as<int32_t>(), n, item_tiles, keys.as<int64_t>(), 7);
+    LF_LAUNCHED();
+    rc = sort_by_item(keys.as<int64_t>(), n, item_tiles + 1, hit_list, hit_off, st);
+    if (!rc) rc = hits.alloc(sizeof(uint64_t) * n, st);
+    if (rc) return rc;
+    pack_hits<<<ceil_div(n, 256), 256, 0, st>>>(hit_list.as<uint32_t>(), tgt.as<int32_t>(), n,
+                                                hits.as<uint64_t>());
+    LF_LAUNCHED();
+    q.hit_off = hit_off.as<uint32_t>();
+    q.hit_list = hits.as<uint64_t>();
   }
   // bias columns folding -lse2 into the dE pass's S MMA (see bias_columns)
   Scratch bias, ones;
