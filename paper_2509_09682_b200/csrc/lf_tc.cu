@@ -29,6 +29,7 @@
 #include <cudaTypedefs.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <type_traits>
 
 #include "lf_internal.cuh"
@@ -122,6 +123,7 @@ struct TcParams {
   int64_t owner_tiles;
   int64_t chunk;         // stream rows per unit (multiple of BN)
   int64_t n_chunks;
+  int64_t c_first;       // EVAL: this launch's first chunk (the seeding pass took the ones before)
   int64_t units;
   const int32_t* tgt;    // FWD/BWD_ROWS: per owner row (local item or -1); BWD_ITEMS: per stream row
   const float* lse2;     // lse*log2e - log2|scale| per row (padded; +inf pad); FWDX: logit bound
@@ -437,8 +439,13 @@ struct Units {
   // EVAL phase-aligned: phase-A units, owner tiles in phase A, the phase-B
   // range's first owner / first chunk, its last owner, and the head run length
   int64_t A = 0, R0 = 0, bo = 0, bj = 0, lo = 0, hl = 0;
+  int64_t cf = 0;  // EVAL: chunk offset of this launch (TcParams::c_first)
   bool aligned = false;
   __device__ Units(const TcParams& p) : P(p.n_chunks), OT(p.owner_tiles) {
+    if (MODE == EVAL) {
+      cf = p.c_first;
+      P -= cf;
+    }
     const int64_t G = gridDim.x, c = blockIdx.x;
     if (MODE == EVAL && LF_EVAL_CONTIG == 2 && OT >= G) {
       aligned = true;
@@ -467,11 +474,11 @@ struct Units {
   }
   __device__ int64_t chunk(int64_t u) const {
     if (MODE == EVAL && aligned) {
-      if (u < A) return u % P;
+      if (u < A) return cf + u % P;
       const int64_t t = u - A;
-      return t < hl ? t : bj + (t - hl);
+      return cf + (t < hl ? t : bj + (t - hl));
     }
-    return MODE == EVAL && LF_EVAL_CONTIG ? u % P : u / OT;
+    return MODE == EVAL ? cf + (LF_EVAL_CONTIG ? u % P : u / OT) : u / OT;
   }
   __device__ int64_t owner(int64_t u) const {
     if (MODE == EVAL && aligned) {
@@ -1159,15 +1166,18 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
                 // saturates to exactly 1.0; equal or lower scores give 0.0.
                 // Summed in pairs with FADD2 — exact (<= 64).
                 const float nk = -thr * 0x1p100f;
-                float f[4] = {0.f, 0.f, 0.f, 0.f};
+                // four independent FADD2 chains (8 deep per 64 columns)
+                float f[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                 for (int g = 0; g < 2; ++g)
 #pragma unroll
-                  for (int c = 0; c < 32; c += 4) {
-                    fadd2(f[0], f[1], f[0], f[1], fma_sat(w[g][c], 0x1p100f, nk), fma_sat(w[g][c + 1], 0x1p100f, nk));
-                    fadd2(f[2], f[3], f[2], f[3], fma_sat(w[g][c + 2], 0x1p100f, nk), fma_sat(w[g][c + 3], 0x1p100f, nk));
+                  for (int c = 0; c < 32; c += 8) {
+#pragma unroll
+                    for (int e = 0; e < 8; e += 2)
+                      fadd2(f[e], f[e + 1], f[e], f[e + 1], fma_sat(w[g][c + e], 0x1p100f, nk),
+                            fma_sat(w[g][c + e + 1], 0x1p100f, nk));
                   }
-                ecnt += static_cast<uint32_t>((f[0] + f[1]) + (f[2] + f[3]));
+                ecnt += static_cast<uint32_t>(((f[0] + f[1]) + (f[2] + f[3])) + ((f[4] + f[5]) + (f[6] + f[7])));
               } else {
                 // 1.0f / 0.0f per compare (FSET.BF, ALU pipe) summed on the FMA
                 // pipe: exact (<= 64), one ALU op per item
@@ -2124,12 +2134,31 @@ int tc_eval_partials(const void* X, const void* E, const void* Et, const int32_t
   p.owner_tiles = owner_tiles;
   p.chunk = tiles_per * BN;
   p.n_chunks = P;
-  p.units = owner_tiles * P;
   p.tgt = tl;
   p.ev_count = cnt.as<uint32_t>();
   p.ev_val = val.as<float>();
   p.ev_idx = idx.as<int32_t>();
   p.ev_floor = floor.as<int32_t>();
+  // Seeding pass: the first S chunks for every row, as a launch of their own.
+  // Each row's k-th score over that subset (published to ev_floor) is a lower
+  // bound of its k-th over the catalog, so the main launch starts every list
+  // from placeholders just below it instead of empty: far fewer slabs reach
+  // the divergent insertion path (an empty list admits every slab).  The
+  // seeding pass's results are the first S chunks' records — no work repeats.
+  // (LSEFORGE_EVAL_SEED_CHUNKS overrides S, 0 = no seeding pass.)
+  int64_t seed_chunks = 1;
+  if (const char* e = std::getenv("LSEFORGE_EVAL_SEED_CHUNKS")) seed_chunks = std::atoll(e);
+  const int64_t S = P > 1 ? std::max<int64_t>(0, std::min<int64_t>(seed_chunks, P - 1)) : 0;
+  if (S > 0) {
+    TcParams q = p;
+    q.n_chunks = S;
+    q.c_first = 0;
+    q.units = owner_tiles * S;
+    rc = launch_d<EVAL>(D, kclass, mo, ms, mt, mo, q, st);
+    if (rc) return rc;
+  }
+  p.c_first = S;
+  p.units = owner_tiles * (P - S);
   rc = launch_d<EVAL>(D, kclass, mo, ms, mt, mo, p, st);
   if (rc) return rc;
   *P_out = static_cast<int>(P);

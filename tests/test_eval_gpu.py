@@ -188,3 +188,28 @@ def test_errors(lf, M):
         M.rank_topk(X, E[:50], tg, 5)
     s = lf.evaluate(X.double()[:, :8], E.double()[:20, :8], tg % 20, 200, pop[:20])  # k_eff = v
     assert s.coverage == 1.0
+
+
+@pytest.mark.parametrize("k", [3, 10, 16])
+@pytest.mark.parametrize("planted", [False, True])
+def test_seeding_pass_is_exact(M, monkeypatch, k, planted):
+    # The seeding launch (the first S V-chunks, whose k-th scores seed the
+    # main launch's lists, lf_tc.cu tc_eval_partials) must not change a single
+    # rank, id or score: S = 0 (no seeding), 1 (default) and 5 agree bitwise,
+    # on uniform scores and with well-ranked (planted) targets and ties.
+    n, d, v = 1024, 64, 300_000
+    g = torch.Generator(device="cpu").manual_seed(11 + k)
+    X = (torch.randn(n, d, generator=g) * 0.4).to(torch.bfloat16).cuda()
+    E = (torch.randn(v, d, generator=g) * 0.4).to(torch.bfloat16).cuda()
+    tg = torch.randint(0, v, (n,), generator=g).cuda()
+    if planted:
+        E[tg[:64]] = X[:64]
+        E[1000:1100] = E[5]  # a block of tied items early in the catalog
+    out = {}
+    for s in ("0", "1", "5"):
+        monkeypatch.setenv("LSEFORGE_EVAL_SEED_CHUNKS", s)
+        out[s] = M.rank_topk(X, E, tg, k)
+    for s in ("1", "5"):
+        for a, b in zip(out["0"], out[s]):
+            assert torch.equal(a, b), s
+    _check_rounded(X, E, tg, *out["1"], k)

@@ -46,7 +46,7 @@ L.lf_profile_enable(0)
 ms = s.elapsed_time(e) / a.iters
 cnt, tot = C.c_uint64(), C.c_double()
 L.lf_profile_read(7, C.byref(cnt), C.byref(tot))
-k_ms = tot.value / max(1, cnt.value)
+k_ms = tot.value / a.iters  # the seeding launch and the main launch
 flops = 2.0 * a.n * a.v * a.d
 peak = None
 try:
@@ -54,5 +54,6 @@ try:
 except OSError:
     pass
 print(json.dumps({"probe": "eval_rank_topk", "n": a.n, "d": a.d, "v": a.v, "k": a.k, "dtype": a.dtype,
-                  "ms_per_call": ms, "kernel_ms": k_ms, "rows_per_s": a.n / ms * 1e3,
+                  "ms_per_call": ms, "kernel_ms": k_ms, "launches_per_call": cnt.value / a.iters,
+                  "seed_chunks": os.environ.get("LSEFORGE_EVAL_SEED_CHUNKS", "default"), "rows_per_s": a.n / ms * 1e3,
                   "tflops_kernel": flops / k_ms * 1e-9, "peaks": peak}))
