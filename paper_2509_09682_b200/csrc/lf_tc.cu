@@ -63,6 +63,9 @@
 #ifndef LF_FWD_MAXCHUNKS
 #define LF_FWD_MAXCHUNKS 64  // forward: most V chunks pick_chunks may choose
 #endif
+#ifndef LF_EVAL_PIPE
+#define LF_EVAL_PIPE 0  // EVAL: 1 = double-buffered 32-column TMEM loads, gate per 32 columns (measured 19.2 vs 13.9 ms at cfg2, k = 10)
+#endif
 #ifndef LF_EVAL_CONTIG
 #define LF_EVAL_CONTIG 1  // EVAL: 1 CTA-contiguous owner-tile-major units, 2 phase-aligned rounds of owner tiles (see Units; E read ~once per round from HBM, measured slower), 0 chunk-major round robin
 #endif
@@ -1122,6 +1125,78 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
           // sees slabs whose max beats its k-th entry (rare after warm-up).
           // The slab loop stays rolled: the epilogue must fit the i-cache.
           const int lc = tgt - static_cast<int>(col0);
+#if LF_EVAL_PIPE
+          // 32-column chunks, double-buffered: chunk q+1's tcgen05.ld is in
+          // flight while chunk q is counted and gated (the loop stays rolled,
+          // two chunks per trip, for the i-cache).
+          auto chunk32 = [&](float (&w)[32], int q) {
+            if (nvalid - q * 32 < 32) {
+#pragma unroll
+              for (int c = 0; c < 32; ++c)
+                if (q * 32 + c >= nvalid) w[c] = -INFINITY;
+            }
+            const int l = lc - q * 32;
+            if (static_cast<unsigned>(l) < 32u) {
+#pragma unroll
+              for (int c = 0; c < 32; ++c) ecnt -= c < l ? set_ge(w[c], st) : (c > l ? set_gt(w[c], st) : 0u);
+            } else {
+              const float thr = l >= 32 ? st_dn : st;
+              float f[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+              if (cnt_fma) {  // see the 64-column form below
+                const float nk = -thr * 0x1p100f;
+#pragma unroll
+                for (int c = 0; c < 32; c += 8) {
+#pragma unroll
+                  for (int e = 0; e < 8; e += 2)
+                    fadd2(f[e], f[e + 1], f[e], f[e + 1], fma_sat(w[c + e], 0x1p100f, nk),
+                          fma_sat(w[c + e + 1], 0x1p100f, nk));
+                }
+              } else {
+#pragma unroll
+                for (int c = 0; c < 32; ++c) f[c & 7] += fset_gt(w[c], thr);
+              }
+              ecnt += static_cast<uint32_t>(((f[0] + f[1]) + (f[2] + f[3])) + ((f[4] + f[5]) + (f[6] + f[7])));
+            }
+#ifndef LF_DIAG_NOTOPK
+            const float g = max32(w);
+            if (g > kv[KK - 1]) {  // divergent, rare once the list has filled
+              const float kth = kv[KK - 1];
+              uint32_t msk = 0;
+#pragma unroll
+              for (int c = 0; c < 32; ++c) msk |= (w[c] > kth ? 1u : 0u) << c;
+              const int base = static_cast<int>(col0) + q * 32;
+              if ((msk & (msk - 1u)) == 0u) {  // the chunk max is the only candidate
+                topk_insert(kv, ki, g, base + __ffs(static_cast<int>(msk)) - 1);
+              } else {
+                do {
+                  const int c = __ffs(static_cast<int>(msk)) - 1;
+                  msk &= msk - 1u;
+                  const float cv = select_reg(w, c);
+                  if (cv > kv[KK - 1]) topk_insert(kv, ki, cv, base + c);
+                } while (msk);
+              }
+            }
+#endif
+          };
+          float wa[32], wb[32];
+          LF_TMEM_LD32(ta, reinterpret_cast<uint32_t*>(wa));
+          tmem_ld_wait();
+#pragma unroll 1
+          for (int q = 0; q < BN / 32; q += 2) {
+            LF_TMEM_LD32(ta + (q + 1) * 32, reinterpret_cast<uint32_t*>(wb));
+            chunk32(wa, q);
+            tmem_ld_wait();
+            if (q + 2 < BN / 32) {
+              LF_TMEM_LD32(ta + (q + 2) * 32, reinterpret_cast<uint32_t*>(wa));
+            } else {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&s_empty[b]);
+            }
+            chunk32(wb, q + 1);
+            if (q + 2 < BN / 32) tmem_ld_wait();
+          }
+#else
 #pragma unroll 1
           for (int h = 0; h < BN / 64; ++h) {
             float w[2][32];
@@ -1217,6 +1292,7 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
             }
 #endif
           }
+#endif
         } else {
           // ---- backward: G = softmax * |scale| (target: minus |scale|), bf16,
           // back into the same TMEM columns (chunk q -> columns 16q..16q+15,
@@ -2142,11 +2218,13 @@ int tc_eval_partials(const void* X, const void* E, const void* Et, const int32_t
   // Seeding pass: the first S chunks for every row, as a launch of their own.
   // Each row's k-th score over that subset (published to ev_floor) is a lower
   // bound of its k-th over the catalog, so the main launch starts every list
-  // from placeholders just below it instead of empty: far fewer slabs reach
-  // the divergent insertion path (an empty list admits every slab).  The
-  // seeding pass's results are the first S chunks' records — no work repeats.
-  // (LSEFORGE_EVAL_SEED_CHUNKS overrides S, 0 = no seeding pass.)
-  int64_t seed_chunks = 1;
+  // from placeholders just below it instead of empty, so fewer slabs reach
+  // the divergent insertion path.  The seeding pass's results are the first
+  // S chunks' records — no work repeats.  Off by default: at cfg2 (k = 10)
+  // S = 1 / 2 / 4 measured 14.3 / 14.4 / 14.1 ms against 13.9 ms without — the
+  // CTA-contiguous order already lets each list see most of V, and the gate
+  // (two max trees per slab) costs the same either way.  S = LSEFORGE_EVAL_SEED_CHUNKS.
+  int64_t seed_chunks = 0;
   if (const char* e = std::getenv("LSEFORGE_EVAL_SEED_CHUNKS")) seed_chunks = std::atoll(e);
   const int64_t S = P > 1 ? std::max<int64_t>(0, std::min<int64_t>(seed_chunks, P - 1)) : 0;
   if (S > 0) {
