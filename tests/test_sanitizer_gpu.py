@@ -5,7 +5,13 @@ list-class instantiation and the rebase path, SIMT f32 / f64, CCE-,
 samplers, CE baselines, Adam, layout converters, the bounded peer
 barrier); memcheck, synccheck and racecheck must report zero errors.  A
 negative control (an out-of-bounds item table on the SIMT path) proves the
-tool instruments this process.  Logs of a full run: profiles/r02_sanitizer_*.log."""
+tool instruments this process.  Logs of a full run: profiles/r02_sanitizer_*.log.
+
+Opt-in (LSEFORGE_RUN_SANITIZER=1): the GPU pool this repo is tested on has
+since closed compute-sanitizer (its runs left other jobs' GPUs needing a
+reset; the wrapper prints a refusal instead of running), so by default these
+tests skip, and they skip on that refusal too.  The logs above are from the
+runs made while it was open."""
 import os
 import shutil
 import subprocess
@@ -13,7 +19,10 @@ import sys
 
 import pytest
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(os.environ.get("LSEFORGE_RUN_SANITIZER") != "1",
+                                 reason="compute-sanitizer runs are opt-in (LSEFORGE_RUN_SANITIZER=1)")]
+CLOSED = "compute-sanitizer is closed"
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
@@ -40,7 +49,10 @@ def sanitize(tool, args, timeout=900, env=None):
     assert os.path.exists(SAN), "compute-sanitizer not found"
     p = subprocess.run([SAN, "--tool", tool, "--error-exitcode", "9", *args], capture_output=True,
                        text=True, timeout=timeout, env=env)
-    return p.returncode, p.stdout + p.stderr
+    log = p.stdout + p.stderr
+    if CLOSED in log:
+        pytest.skip(log.strip().splitlines()[0])
+    return p.returncode, log
 
 
 @pytest.mark.parametrize("tool", ["memcheck", "synccheck", "racecheck"])
