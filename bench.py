@@ -51,6 +51,8 @@ N_ROWS, D, V = 51200, 64, 1_000_000
 EPS = 6e-8  # CceConfig::Fp16SaturationPreset (cce.hpp:26-30)
 SEED = 0xB2000002   # cfg2 (0xB2000000 + cfg#)
 SEED3 = 0xB2000003  # cfg3
+SEED1 = 0xB2000001  # cfg1
+N1, V1 = 2048, 32768  # cfg1: fp32, batch 32 x seq 64, filtering off
 K_NEG = 512
 WORKLOAD = ("cfg2: SASRec-shaped CCE bf16, N=51200 (batch 256 x seq 200), D=64, V=1M items, "
             "saturated-gradient filtering on (eps=6e-8)")
@@ -433,6 +435,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_extras:
         del res_box[0], out, res
         sub_record("filter", lambda: filter_protocol(lf, X, E, x, Xh, Ch, t, flush, stream, args))
+        sub_record("cfg1", lambda: cfg1_record(lf, flush, stream, args, not args.no_cpu_baseline))
         sub_record("cfg3", lambda: cfg3_record(lf, flush, stream, args, peaks, not args.no_cpu_baseline))
         sub_record("sharded_configs", lambda: shard_record(lf, flush, stream, args, peaks))
 
@@ -453,7 +456,7 @@ def run_ours(args):
                 "kernels": kern, "gpu_launches": int(launches), "e2e": e2e, "e2e_grads": e2e_grads,
                 "e2e_dropin": extras.get("e2e_dropin"),
                 "cpu_baseline": extras.get("cpu_baseline"), "parity": extras.get("parity"),
-                "filter": extras.get("filter"), "cfg3": extras.get("cfg3"),
+                "filter": extras.get("filter"), "cfg1": extras.get("cfg1"), "cfg3": extras.get("cfg3"),
                 "sharded_configs": extras.get("sharded_configs"), "clocks": clk}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
@@ -736,6 +739,62 @@ def cfg3_record(lf, flush, stream, args, peaks, cpu):
                          and p["dX_normwise"] < tol["dX_normwise"] and p["dE_normwise"] < tol["dE_normwise"])
         rec["parity"] = p
     del box[0], o, g, X3, E3, x3, inds
+    torch.cuda.synchronize()
+    return rec
+
+
+def cfg1_record(lf, flush, stream, args, cpu):
+    """BASELINE configs[0]: CCE fwd + bwd fp32, N = 2048 (batch 32 x seq 64),
+    D = 64, V = 32768, filtering off — "bit-for-tolerance vs the CPU oracle".
+    The reference itself (oracle/_ref, all host threads) runs the same
+    make_instance inputs at full size; the GPU path is the public
+    cce_forward + cce_backward (fp32: the SIMT kernels, exact exp)."""
+    import numpy as np
+    import torch
+    from paper_2509_09682_b200 import synth
+    dev = torch.device("cuda", torch.cuda.current_device())
+    Xh, Ch, t1 = synth.make_instance(SEED1, N1, D, V1)
+    X1 = torch.from_numpy(np.ascontiguousarray(Xh, np.float32)).to(dev)
+    E1 = torch.from_numpy(np.ascontiguousarray(Ch.T, np.float32)).to(dev)
+    x1 = torch.from_numpy(t1).to(dev)
+    cfg = lf.CceConfig()
+    box = [None]
+
+    def step():
+        box[0] = None
+        o = lf.cce_forward(X1, E1, x1, cfg, validate=False)
+        r = lf.cce_backward(X1, E1, x1, o.lse, 1.0, cfg, validate=False, stats=False)
+        box[0] = (o, r)
+
+    kern = {}
+    ms = timed_steps(step, args.steps, max(3, args.warmup), stream, flush, kern)
+    rec = {"workload": f"cfg1: CCE fp32, N={N1} (batch 32 x seq 64), D={D}, V={V1}, filtering off "
+                       f"(make_instance seed {SEED1:#x})",
+           "value": N1 / (ms / 1e3), "unit": "positions/s", "ms_per_step": ms, "steps": args.steps,
+           "path": "lf_cce_forward + lf_cce_backward (fp32 SIMT kernels)", "kernel_ms_per_step": kern}
+    o, r = box[0]
+    if cpu:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import oracle_bind as ob
+        threads = os.cpu_count() or 1
+        t0 = time.perf_counter()
+        loss, pos, lse = ob.ref_cce_forward(Xh, Ch, t1, workers=threads)
+        rdE, rdC, _ = ob.ref_cce_backward(Xh, Ch, t1, lse, 1.0, 0.0, workers=threads)
+        sec = time.perf_counter() - t0
+        rec["cpu_baseline"] = {"value": N1 / sec, "unit": "positions/s", "cores": threads, "kind": "reference",
+                               "sample": f"reference cce_forward + cce_backward (oracle/_ref) at full cfg1 size, "
+                                         f"workers={threads}"}
+        dXg = r.grads.d_embeddings.double().cpu().numpy()
+        dEg = r.grads.d_classifier.double().cpu().numpy()
+        tol = {"loss_rel": 1e-5, "lse_max_rel": 1e-5, "pos_max_rel": 1e-5, "dX_normwise": 1e-5,
+               "dE_normwise": 1e-5}
+        p = {"rows": N1, "loss_rel": abs(float(o.loss) - loss) / max(1.0, abs(loss)),
+             "lse_max_rel": rel(o.lse.cpu().numpy(), lse), "pos_max_rel": rel(o.pos_logits.cpu().numpy(), pos),
+             "dX_normwise": normwise(dXg, rdE), "dE_normwise": normwise(dEg, rdC.T), "tolerance": tol,
+             "note": "fp32 tolerance of the north star (1e-5 relative); reference accumulates in double"}
+        p["pass"] = all(p[k] < tol[k] for k in tol)
+        rec["parity"] = p
+    del box[0], o, r, X1, E1, x1
     torch.cuda.synchronize()
     return rec
 
