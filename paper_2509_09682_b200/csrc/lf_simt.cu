@@ -90,6 +90,28 @@ struct TileMap {
   }
 };
 
+// Four consecutive smem values (16-byte aligned): one LDS.128 for float.
+template <class T>
+__device__ __forceinline__ void ld4(const T* p, T (&v)[4]) {
+#pragma unroll
+  for (int r = 0; r < 4; ++r) v[r] = p[r];
+}
+template <>
+__device__ __forceinline__ void ld4<float>(const float* p, float (&v)[4]) {
+  const float4 q = *reinterpret_cast<const float4*>(p);
+  v[0] = q.x;
+  v[1] = q.y;
+  v[2] = q.z;
+  v[3] = q.w;
+}
+// Gradient-tile stride (4 owners of one stream element contiguous, rows
+// 16-byte aligned) and the tile's offset, rounded up to 16 bytes.
+constexpr int gstride(int owners) { return owners + 4; }
+template <class T>
+__device__ __host__ constexpr size_t align16(size_t elems) {
+  return (elems * sizeof(T) + 15) / 16 * 16 / sizeof(T);
+}
+
 // Online LSE update, numeric.hpp:19-27 (branch structure kept).
 template <class T>
 __device__ __forceinline__ void lse_update(T& m, T& s, T o) {
@@ -204,9 +226,10 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_dx(
   constexpr int R = 32, C = 64;
   using M = TileMap<T, R, C>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int GS = gstride(R);
   T* Xs = reinterpret_cast<T*>(smem_raw);
   T* Es = Xs + D * (R + 1);
-  T* Gs = Es + D * (C + 1);  // [R][C+1]
+  T* Gs = Xs + align16<T>(static_cast<size_t>(D) * (R + 1 + C + 1));  // [C][GS]: column-major G
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * R;
   const int64_t c_begin = static_cast<int64_t>(blockIdx.y) * chunk;
   const int64_t c_end = min(v, c_begin + chunk);
@@ -220,12 +243,16 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_dx(
     row_lse[i] = row < n ? static_cast<T>(lse[row]) : T(0);
     tgt[i] = row < n ? targets[row] - v_offset : -1;
   }
-  // dX accumulators: row = tid/8, dims (tid%8) + 8q.
-  const int arow = threadIdx.x / 8, adim = threadIdx.x % 8;
-  const int nq = (D - adim + 7) / 8;
-  T acc[32];
+  // dX accumulators: rows 4 (tid / 32) + r (the warp's four rows, one
+  // 16-byte G load per column), dims (tid % 32) + 32 q (conflict-free E
+  // reads): 4 + nq smem loads per 4 nq FMAs.
+  const int arow = (threadIdx.x / 32) * 4, adim = threadIdx.x % 32;
+  const int nq = (D - adim + 31) / 32;
+  T acc[4][8];
 #pragma unroll
-  for (int q = 0; q < 32; ++q) acc[q] = T(0);
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[r][q] = T(0);
   unsigned skips = 0;
 
   for (int64_t c0 = c_begin; c0 < c_end; c0 += C) {
@@ -242,23 +269,31 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_dx(
         const bool valid = col < c_end && (r0 + M::row(i)) < n;
         T g = T(0);
         if (valid) g = coeff(o[i][q], row_lse[i], col == tgt[i], eps, scale, skips);
-        Gs[M::row(i) * (C + 1) + M::col(q)] = g;
+        Gs[M::col(q) * GS + M::row(i)] = g;
       }
     __syncthreads();
     const int cn = static_cast<int>((c_end - c0 < C ? c_end - c0 : C));
     for (int j = 0; j < cn; ++j) {
-      const T gv = Gs[arow * (C + 1) + j];
+      T gv[4];
+      ld4(Gs + j * GS + arow, gv);
 #pragma unroll
-      for (int q = 0; q < 32; ++q)
-        if (q < nq) acc[q] = fma_acc(acc[q], gv, Es[(adim + 8 * q) * (C + 1) + j]);
+      for (int q = 0; q < 8; ++q)
+        if (q < nq) {
+          const T ev = Es[(adim + 32 * q) * (C + 1) + j];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) acc[r][q] = fma_acc(acc[r][q], gv[r], ev);
+        }
     }
   }
-  const int64_t row = r0 + arow;
-  if (row < n) {
-    T* out = dx_part + static_cast<int64_t>(blockIdx.y) * n * D + row * D;
 #pragma unroll
-    for (int q = 0; q < 32; ++q)
-      if (q < nq) out[adim + 8 * q] = acc[q];
+  for (int r = 0; r < 4; ++r) {
+    const int64_t row = r0 + arow + r;
+    if (row < n) {
+      T* out = dx_part + static_cast<int64_t>(blockIdx.y) * n * D + row * D;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q < nq) out[adim + 32 * q] = acc[r][q];
+    }
   }
   if (skip_counter) {
     for (int off = 16; off > 0; off >>= 1) skips += __shfl_xor_sync(0xffffffffu, skips, off);
@@ -277,16 +312,21 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_de(
   constexpr int R = 64, C = 32;
   using M = TileMap<T, R, C>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int GS = gstride(C);
   T* Es = reinterpret_cast<T*>(smem_raw);
   T* Xs = Es + D * (C + 1);
-  T* Gs = Xs + D * (R + 1);  // [R][C+1]
+  T* Gs = Es + align16<T>(static_cast<size_t>(D) * (C + 1 + R + 1));  // [R][GS]
   const int64_t c0 = static_cast<int64_t>(blockIdx.x) * C;
   stage_T<T, C>(Es, E, c0, v, D);
-  const int aitem = threadIdx.x / 8, adim = threadIdx.x % 8;
-  const int nq = (D - adim + 7) / 8;
-  T acc[32];
+  // dE accumulators: items 4 (tid / 32) + r (one 16-byte G load per row),
+  // dims (tid % 32) + 32 q (conflict-free X reads).
+  const int aitem = (threadIdx.x / 32) * 4, adim = threadIdx.x % 32;
+  const int nq = (D - adim + 31) / 32;
+  T acc[4][8];
 #pragma unroll
-  for (int q = 0; q < 32; ++q) acc[q] = T(0);
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[r][q] = T(0);
   unsigned skips = 0;
 
   for (int64_t r0 = 0; r0 < n; r0 += R) {
@@ -306,23 +346,31 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_de(
         const int64_t col = c0 + M::col(q);
         T g = T(0);
         if (rvalid && col < v) g = coeff(o[i][q], rl, col == tg, eps, scale, skips);
-        Gs[M::row(i) * (C + 1) + M::col(q)] = g;
+        Gs[M::row(i) * GS + M::col(q)] = g;
       }
     }
     __syncthreads();
     const int rn = static_cast<int>((n - r0 < R ? n - r0 : R));
     for (int i = 0; i < rn; ++i) {
-      const T gv = Gs[i * (C + 1) + aitem];
+      T gv[4];
+      ld4(Gs + i * GS + aitem, gv);
 #pragma unroll
-      for (int q = 0; q < 32; ++q)
-        if (q < nq) acc[q] = fma_acc(acc[q], gv, Xs[(adim + 8 * q) * (R + 1) + i]);
+      for (int q = 0; q < 8; ++q)
+        if (q < nq) {
+          const T xv = Xs[(adim + 32 * q) * (R + 1) + i];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) acc[r][q] = fma_acc(acc[r][q], gv[r], xv);
+        }
     }
   }
-  const int64_t item = c0 + aitem;
-  if (item < v) {
 #pragma unroll
-    for (int q = 0; q < 32; ++q)
-      if (q < nq) dE[item * D + adim + 8 * q] = acc[q];
+  for (int r = 0; r < 4; ++r) {
+    const int64_t item = c0 + aitem + r;
+    if (item < v) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q < nq) dE[item * D + adim + 32 * q] = acc[r][q];
+    }
   }
 }
 
@@ -394,9 +442,13 @@ int launch_combine_f32log2(const float* part, int P, int64_t n, double* lse, dou
 template <class T>
 static size_t fwd_smem(int D) { return sizeof(T) * D * (32 + 1 + 64 + 1); }
 template <class T>
-static size_t dx_smem(int D) { return sizeof(T) * (D * (32 + 1 + 64 + 1) + 32 * (64 + 1)); }
+static size_t dx_smem(int D) {  // Xs, Es, then the 64 x gstride(32) G tile
+  return sizeof(T) * (align16<T>(static_cast<size_t>(D) * (32 + 1 + 64 + 1)) + 64 * gstride(32));
+}
 template <class T>
-static size_t de_smem(int D) { return sizeof(T) * (D * (32 + 1 + 64 + 1) + 64 * (32 + 1)); }
+static size_t de_smem(int D) {  // Es, Xs, then the 64 x gstride(32) G tile
+  return sizeof(T) * (align16<T>(static_cast<size_t>(D) * (32 + 1 + 64 + 1)) + 64 * gstride(32));
+}
 
 static int64_t pick_chunks(int64_t row_tiles, int64_t v, int64_t min_cols) {
   const int64_t want = 4 * num_sms();
