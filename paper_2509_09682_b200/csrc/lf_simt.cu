@@ -50,46 +50,42 @@ template <class T>
 __device__ __forceinline__ T neg_inf() { return -INFINITY; }
 
 // Stage rows [r0, r0+R) of a row-major [rows x D] matrix into smem laid out
-// [D][R+1] (transposed, padded); rows past `rows` are zero.
-template <class T, int R>
+// [D][R+PAD] (transposed, padded); rows past `rows` are zero.  PAD = 1: one
+// element per thread, k fastest (conflict-free stores).  PAD = 4 (fp32 tile
+// rows 16-byte aligned for vector reads): 16-byte global loads along k with
+// the row fastest, so a warp's four stores per load hit 32 distinct banks.
+template <class T, int R, int PAD = 1>
 __device__ __forceinline__ void stage_T(T* s, const T* __restrict__ g, int64_t r0, int64_t rows,
                                         int D) {
+  constexpr int LD = R + PAD;
+  if constexpr (PAD == 4 && sizeof(T) == 4) {
+    if ((D & 3) == 0 && (reinterpret_cast<uintptr_t>(g) & 15) == 0) {
+      const int nk4 = D / 4;
+      for (int idx = threadIdx.x; idx < R * nk4; idx += kThreads) {
+        const int r = idx % R, kq = idx / R;
+        const int64_t row = r0 + r;
+        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row < rows) q = *reinterpret_cast<const float4*>(g + row * D + 4 * kq);
+        T* c = s + 4 * kq * LD + r;
+        c[0] = q.x;
+        c[LD] = q.y;
+        c[2 * LD] = q.z;
+        c[3 * LD] = q.w;
+      }
+      return;
+    }
+  }
   for (int idx = threadIdx.x; idx < R * D; idx += kThreads) {
     const int r = idx / D, k = idx % D;
     const int64_t row = r0 + r;
-    s[k * (R + 1) + r] = row < rows ? g[row * D + k] : T(0);
+    s[k * LD + r] = row < rows ? g[row * D + k] : T(0);
   }
 }
 
-// R x C logit tile from staged Xs [D][R+1] and Es [D][C+1]; each of the 256
-// threads owns RPT rows x CPT columns (RPT*CPT = 8).  Exact mode: k ascending.
-template <class T, int R, int C>
-struct TileMap {
-  static constexpr int RPT = 2;
-  static constexpr int CPT = 4;
-  static constexpr int CG = C / CPT;
-  static_assert((R / RPT) * CG == kThreads, "tile map must cover 256 threads");
-  __device__ static int row(int i) { return (threadIdx.x / CG) * RPT + i; }
-  __device__ static int col(int q) { return (threadIdx.x % CG) + CG * q; }
-  __device__ static void logits(const T* Xs, const T* Es, int D, T (&o)[RPT][CPT]) {
-#pragma unroll
-    for (int i = 0; i < RPT; ++i)
-#pragma unroll
-      for (int q = 0; q < CPT; ++q) o[i][q] = T(0);
-    for (int k = 0; k < D; ++k) {
-      T xv[RPT], ev[CPT];
-#pragma unroll
-      for (int i = 0; i < RPT; ++i) xv[i] = Xs[k * (R + 1) + row(i)];
-#pragma unroll
-      for (int q = 0; q < CPT; ++q) ev[q] = Es[k * (C + 1) + col(q)];
-#pragma unroll
-      for (int i = 0; i < RPT; ++i)
-#pragma unroll
-        for (int q = 0; q < CPT; ++q) o[i][q] = fma_acc(o[i][q], xv[i], ev[q]);
-    }
-  }
-};
-
+// R x C logit tile from staged Xs [D][R+PAD] and Es [D][C+PAD]; each of the
+// 256 threads owns RPT rows x CPT columns.  PAD = 1: columns CG apart
+// (scalar reads); PAD = 4 (RPT = CPT = 4): four consecutive rows and columns,
+// one 16-byte read of each per k.  Exact mode: k ascending either way.
 // Four consecutive smem values (16-byte aligned): one LDS.128 for float.
 template <class T>
 __device__ __forceinline__ void ld4(const T* p, T (&v)[4]) {
@@ -111,6 +107,59 @@ template <class T>
 __device__ __host__ constexpr size_t align16(size_t elems) {
   return (elems * sizeof(T) + 15) / 16 * 16 / sizeof(T);
 }
+
+template <class T, int R, int C, int RPT_ = 2, int CPT_ = 4, int PAD = 1>
+struct TileMap {
+  static constexpr int RPT = RPT_;
+  static constexpr int CPT = CPT_;
+  static constexpr int CG = C / CPT;
+  static constexpr bool kVec = PAD == 4 && RPT == 4 && CPT == 4;
+  static_assert((R / RPT) * CG == kThreads, "tile map must cover 256 threads");
+  __device__ static int row(int i) { return (threadIdx.x / CG) * RPT + i; }
+  __device__ static int col(int q) { return kVec ? (threadIdx.x % CG) * CPT + q : (threadIdx.x % CG) + CG * q; }
+  __device__ static void logits(const T* Xs, const T* Es, int D, T (&o)[RPT][CPT]) {
+#pragma unroll
+    for (int i = 0; i < RPT; ++i)
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) o[i][q] = T(0);
+    for (int k = 0; k < D; ++k) {
+      T xv[RPT], ev[CPT];
+      if constexpr (kVec) {
+        ld4(Xs + k * (R + PAD) + row(0), xv);
+        ld4(Es + k * (C + PAD) + col(0), ev);
+      } else {
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) xv[i] = Xs[k * (R + PAD) + row(i)];
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) ev[q] = Es[k * (C + PAD) + col(q)];
+      }
+#pragma unroll
+      for (int i = 0; i < RPT; ++i)
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) o[i][q] = fma_acc(o[i][q], xv[i], ev[q]);
+    }
+  }
+};
+
+// Tile geometry per element type.  fp64 (exact mode) keeps 32 x 64 tiles
+// (D = 256 must fit in shared memory); fp32 uses 4 x 4 register tiles with
+// 16-byte operand reads on twice the tile area.
+template <class T>
+struct Lay {
+  static constexpr int RPT = 2, CPT = 4, PAD = 1;
+  static constexpr int FR = 32, FC = 64;  // forward: rows x columns per tile
+  static constexpr int XR = 32, XC = 64;  // dX pass
+  static constexpr int ER = 64, EC = 32;  // dE pass (rows per step x items per block)
+};
+template <>
+struct Lay<float> {
+  static constexpr int RPT = 4, CPT = 4, PAD = 4;
+  static constexpr int FR = 32, FC = 128;
+  static constexpr int XR = 32, XC = 128;
+  static constexpr int ER = 128, EC = 32;
+};
+template <class T, int R, int C>
+using LayMap = TileMap<T, R, C, Lay<T>::RPT, Lay<T>::CPT, Lay<T>::PAD>;
 
 // Online LSE update, numeric.hpp:19-27 (branch structure kept).
 template <class T>
@@ -141,15 +190,15 @@ __global__ void __launch_bounds__(kThreads) cce_simt_fwd(const T* __restrict__ X
                                                          int64_t n, int D, int64_t v,
                                                          int64_t v_offset, int64_t chunk,
                                                          Partial<T>* __restrict__ part) {
-  constexpr int R = 32, C = 64;
-  using M = TileMap<T, R, C>;
+  constexpr int R = Lay<T>::FR, C = Lay<T>::FC, PAD = Lay<T>::PAD;
+  using M = LayMap<T, R, C>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Xs = reinterpret_cast<T*>(smem_raw);
-  T* Es = Xs + D * (R + 1);
+  T* Es = Xs + D * (R + PAD);
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * R;
   const int64_t c_begin = static_cast<int64_t>(blockIdx.y) * chunk;
   const int64_t c_end = min(v, c_begin + chunk);
-  stage_T<T, R>(Xs, X, r0, n, D);
+  stage_T<T, R, PAD>(Xs, X, r0, n, D);
 
   T m[M::RPT], s[M::RPT], t[M::RPT], has[M::RPT];
   int64_t tgt[M::RPT];
@@ -164,7 +213,7 @@ __global__ void __launch_bounds__(kThreads) cce_simt_fwd(const T* __restrict__ X
   }
   for (int64_t c0 = c_begin; c0 < c_end; c0 += C) {
     __syncthreads();
-    stage_T<T, C>(Es, E, c0, c_end, D);
+    stage_T<T, C, PAD>(Es, E, c0, c_end, D);
     __syncthreads();
     T o[M::RPT][M::CPT];
     M::logits(Xs, Es, D, o);
@@ -223,17 +272,17 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_dx(
     const T* __restrict__ X, const T* __restrict__ E, const int64_t* __restrict__ targets,
     const double* __restrict__ lse, int64_t n, int D, int64_t v, int64_t v_offset, int64_t chunk,
     T scale, T eps, T* __restrict__ dx_part, unsigned long long* __restrict__ skip_counter) {
-  constexpr int R = 32, C = 64;
-  using M = TileMap<T, R, C>;
+  constexpr int R = Lay<T>::XR, C = Lay<T>::XC, PAD = Lay<T>::PAD;
+  using M = LayMap<T, R, C>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int GS = gstride(R);
   T* Xs = reinterpret_cast<T*>(smem_raw);
-  T* Es = Xs + D * (R + 1);
-  T* Gs = Xs + align16<T>(static_cast<size_t>(D) * (R + 1 + C + 1));  // [C][GS]: column-major G
+  T* Es = Xs + D * (R + PAD);
+  T* Gs = Xs + align16<T>(static_cast<size_t>(D) * (R + PAD + C + PAD));  // [C][GS]: column-major G
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * R;
   const int64_t c_begin = static_cast<int64_t>(blockIdx.y) * chunk;
   const int64_t c_end = min(v, c_begin + chunk);
-  stage_T<T, R>(Xs, X, r0, n, D);
+  stage_T<T, R, PAD>(Xs, X, r0, n, D);
 
   T row_lse[M::RPT];
   int64_t tgt[M::RPT];
@@ -257,7 +306,7 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_dx(
 
   for (int64_t c0 = c_begin; c0 < c_end; c0 += C) {
     __syncthreads();
-    stage_T<T, C>(Es, E, c0, c_end, D);
+    stage_T<T, C, PAD>(Es, E, c0, c_end, D);
     __syncthreads();
     T o[M::RPT][M::CPT];
     M::logits(Xs, Es, D, o);
@@ -273,16 +322,37 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_dx(
       }
     __syncthreads();
     const int cn = static_cast<int>((c_end - c0 < C ? c_end - c0 : C));
-    for (int j = 0; j < cn; ++j) {
-      T gv[4];
-      ld4(Gs + j * GS + arow, gv);
+    if constexpr (PAD == 4) {
+      // four columns per step (16-byte E reads along the column; a column
+      // past cn has G = 0 and a zero-staged E row, adding exact zeros)
+      for (int j = 0; j < cn; j += 4) {
+        T gv[4][4], ev[8][4];
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (q < nq) {
-          const T ev = Es[(adim + 32 * q) * (C + 1) + j];
+        for (int jj = 0; jj < 4; ++jj) ld4(Gs + (j + jj) * GS + arow, gv[jj]);
 #pragma unroll
-          for (int r = 0; r < 4; ++r) acc[r][q] = fma_acc(acc[r][q], gv[r], ev);
-        }
+        for (int q = 0; q < 8; ++q)
+          if (q < nq) ld4(Es + (adim + 32 * q) * (C + PAD) + j, ev[q]);
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (q < nq) {
+#pragma unroll
+              for (int r = 0; r < 4; ++r) acc[r][q] = fma_acc(acc[r][q], gv[jj][r], ev[q][jj]);
+            }
+      }
+    } else {
+      for (int j = 0; j < cn; ++j) {
+        T gv[4];
+        ld4(Gs + j * GS + arow, gv);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < nq) {
+            const T ev = Es[(adim + 32 * q) * (C + PAD) + j];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) acc[r][q] = fma_acc(acc[r][q], gv[r], ev);
+          }
+      }
     }
   }
 #pragma unroll
@@ -309,15 +379,15 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_de(
     const T* __restrict__ X, const T* __restrict__ E, const int64_t* __restrict__ targets,
     const double* __restrict__ lse, int64_t n, int D, int64_t v, int64_t v_offset, T scale,
     T eps, T* __restrict__ dE) {
-  constexpr int R = 64, C = 32;
-  using M = TileMap<T, R, C>;
+  constexpr int R = Lay<T>::ER, C = Lay<T>::EC, PAD = Lay<T>::PAD;
+  using M = LayMap<T, R, C>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int GS = gstride(C);
   T* Es = reinterpret_cast<T*>(smem_raw);
-  T* Xs = Es + D * (C + 1);
-  T* Gs = Es + align16<T>(static_cast<size_t>(D) * (C + 1 + R + 1));  // [R][GS]
+  T* Xs = Es + D * (C + PAD);
+  T* Gs = Es + align16<T>(static_cast<size_t>(D) * (C + PAD + R + PAD));  // [R][GS]
   const int64_t c0 = static_cast<int64_t>(blockIdx.x) * C;
-  stage_T<T, C>(Es, E, c0, v, D);
+  stage_T<T, C, PAD>(Es, E, c0, v, D);
   // dE accumulators: items 4 (tid / 32) + r (one 16-byte G load per row),
   // dims (tid % 32) + 32 q (conflict-free X reads).
   const int aitem = (threadIdx.x / 32) * 4, adim = threadIdx.x % 32;
@@ -331,7 +401,7 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_de(
 
   for (int64_t r0 = 0; r0 < n; r0 += R) {
     __syncthreads();
-    stage_T<T, R>(Xs, X, r0, n, D);
+    stage_T<T, R, PAD>(Xs, X, r0, n, D);
     __syncthreads();
     T o[M::RPT][M::CPT];
     M::logits(Xs, Es, D, o);
@@ -351,16 +421,37 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_de(
     }
     __syncthreads();
     const int rn = static_cast<int>((n - r0 < R ? n - r0 : R));
-    for (int i = 0; i < rn; ++i) {
-      T gv[4];
-      ld4(Gs + i * GS + aitem, gv);
+    if constexpr (PAD == 4) {
+      // four rows per step (16-byte X reads; a row past rn has G = 0 and a
+      // zero-staged X row, adding exact zeros)
+      for (int i = 0; i < rn; i += 4) {
+        T gv[4][4], xv[8][4];
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (q < nq) {
-          const T xv = Xs[(adim + 32 * q) * (R + 1) + i];
+        for (int ii = 0; ii < 4; ++ii) ld4(Gs + (i + ii) * GS + aitem, gv[ii]);
 #pragma unroll
-          for (int r = 0; r < 4; ++r) acc[r][q] = fma_acc(acc[r][q], gv[r], xv);
-        }
+        for (int q = 0; q < 8; ++q)
+          if (q < nq) ld4(Xs + (adim + 32 * q) * (R + PAD) + i, xv[q]);
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (q < nq) {
+#pragma unroll
+              for (int r = 0; r < 4; ++r) acc[r][q] = fma_acc(acc[r][q], gv[ii][r], xv[q][ii]);
+            }
+      }
+    } else {
+      for (int i = 0; i < rn; ++i) {
+        T gv[4];
+        ld4(Gs + i * GS + aitem, gv);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < nq) {
+            const T xv = Xs[(adim + 32 * q) * (R + PAD) + i];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) acc[r][q] = fma_acc(acc[r][q], gv[r], xv);
+          }
+      }
     }
   }
 #pragma unroll
@@ -440,14 +531,19 @@ int launch_combine_f32log2(const float* part, int P, int64_t n, double* lse, dou
 }
 
 template <class T>
-static size_t fwd_smem(int D) { return sizeof(T) * D * (32 + 1 + 64 + 1); }
-template <class T>
-static size_t dx_smem(int D) {  // Xs, Es, then the 64 x gstride(32) G tile
-  return sizeof(T) * (align16<T>(static_cast<size_t>(D) * (32 + 1 + 64 + 1)) + 64 * gstride(32));
+static size_t fwd_smem(int D) {
+  using L = Lay<T>;
+  return sizeof(T) * D * (L::FR + L::PAD + L::FC + L::PAD);
 }
 template <class T>
-static size_t de_smem(int D) {  // Es, Xs, then the 64 x gstride(32) G tile
-  return sizeof(T) * (align16<T>(static_cast<size_t>(D) * (32 + 1 + 64 + 1)) + 64 * gstride(32));
+static size_t dx_smem(int D) {  // Xs, Es, then the XC x gstride(XR) G tile
+  using L = Lay<T>;
+  return sizeof(T) * (align16<T>(static_cast<size_t>(D) * (L::XR + L::PAD + L::XC + L::PAD)) + L::XC * gstride(L::XR));
+}
+template <class T>
+static size_t de_smem(int D) {  // Es, Xs, then the ER x gstride(EC) G tile
+  using L = Lay<T>;
+  return sizeof(T) * (align16<T>(static_cast<size_t>(D) * (L::EC + L::PAD + L::ER + L::PAD)) + L::ER * gstride(L::EC));
 }
 
 static int64_t pick_chunks(int64_t row_tiles, int64_t v, int64_t min_cols) {
@@ -465,9 +561,9 @@ int simt_cce_forward(const T* X, const T* E, const int64_t* targets, int64_t n, 
   if (smem > 227 * 1024) return fail(LF_EUNSUPPORTED, "simt forward: d too large");
   LF_CUDA(cudaFuncSetAttribute(cce_simt_fwd<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem)));
-  const int64_t rt = ceil_div(n, 32);
+  const int64_t rt = ceil_div(n, Lay<T>::FR);
   const int64_t chunks = pick_chunks(rt, v, 256);
-  const int64_t chunk = ceil_div(ceil_div(v, chunks), 64) * 64;
+  const int64_t chunk = ceil_div(ceil_div(v, chunks), Lay<T>::FC) * Lay<T>::FC;
   const int64_t P = ceil_div(v, chunk);
   int rc = ws.alloc(sizeof(Partial<T>) * P * n, st);
   if (rc) return rc;
@@ -544,9 +640,9 @@ int simt_cce_backward(const T* X, const T* E, const int64_t* targets, const doub
                                static_cast<int>(sdx)));
   LF_CUDA(cudaFuncSetAttribute(cce_simt_bwd_de<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(sde)));
-  const int64_t rt = ceil_div(n, 32);
+  const int64_t rt = ceil_div(n, Lay<T>::XR);
   int64_t chunks = std::min<int64_t>(pick_chunks(rt, v, 1024), 8);
-  const int64_t chunk = ceil_div(ceil_div(v, chunks), 64) * 64;
+  const int64_t chunk = ceil_div(ceil_div(v, chunks), Lay<T>::XC) * Lay<T>::XC;
   const int64_t P = ceil_div(v, chunk);
   Scratch ws;
   T* part = dX;
@@ -565,7 +661,7 @@ int simt_cce_backward(const T* X, const T* E, const int64_t* targets, const doub
         part, static_cast<int>(P), n * D, dX);
     LF_LAUNCHED();
   }
-  cce_simt_bwd_de<T><<<ceil_div(v, 32), kThreads, sde, st>>>(X, E, targets, lse, n, D, v,
+  cce_simt_bwd_de<T><<<ceil_div(v, Lay<T>::EC), kThreads, sde, st>>>(X, E, targets, lse, n, D, v,
                                                            v_offset, T(scale), T(eps), dE);
   LF_LAUNCHED();
   return LF_OK;
