@@ -265,9 +265,10 @@ __device__ __forceinline__ T coeff(T o, T row_lse, bool is_target, T eps, T scal
 }
 
 // ---------------------------------------------------------------------------
-// Backward dX: block = 32 rows x one V chunk; dX partial per chunk.
+// Backward dX: block = 32 rows x one V chunk; dX partial per chunk.  NQ =
+// ceil(D / 32): the dims each thread accumulates (register arrays sized to D).
 // ---------------------------------------------------------------------------
-template <class T>
+template <class T, int NQ>
 __global__ void __launch_bounds__(kThreads) cce_simt_bwd_dx(
     const T* __restrict__ X, const T* __restrict__ E, const int64_t* __restrict__ targets,
     const double* __restrict__ lse, int64_t n, int D, int64_t v, int64_t v_offset, int64_t chunk,
@@ -297,11 +298,11 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_dx(
   // reads): 4 + nq smem loads per 4 nq FMAs.
   const int arow = (threadIdx.x / 32) * 4, adim = threadIdx.x % 32;
   const int nq = (D - adim + 31) / 32;
-  T acc[4][8];
+  T acc[4][NQ];
 #pragma unroll
   for (int r = 0; r < 4; ++r)
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc[r][q] = T(0);
+    for (int q = 0; q < NQ; ++q) acc[r][q] = T(0);
   unsigned skips = 0;
 
   for (int64_t c0 = c_begin; c0 < c_end; c0 += C) {
@@ -326,16 +327,16 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_dx(
       // four columns per step (16-byte E reads along the column; a column
       // past cn has G = 0 and a zero-staged E row, adding exact zeros)
       for (int j = 0; j < cn; j += 4) {
-        T gv[4][4], ev[8][4];
+        T gv[4][4], ev[NQ][4];
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) ld4(Gs + (j + jj) * GS + arow, gv[jj]);
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
+        for (int q = 0; q < NQ; ++q)
           if (q < nq) ld4(Es + (adim + 32 * q) * (C + PAD) + j, ev[q]);
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj)
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
+          for (int q = 0; q < NQ; ++q)
             if (q < nq) {
 #pragma unroll
               for (int r = 0; r < 4; ++r) acc[r][q] = fma_acc(acc[r][q], gv[jj][r], ev[q][jj]);
@@ -346,7 +347,7 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_dx(
         T gv[4];
         ld4(Gs + j * GS + arow, gv);
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
+        for (int q = 0; q < NQ; ++q)
           if (q < nq) {
             const T ev = Es[(adim + 32 * q) * (C + PAD) + j];
 #pragma unroll
@@ -361,7 +362,7 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_dx(
     if (row < n) {
       T* out = dx_part + static_cast<int64_t>(blockIdx.y) * n * D + row * D;
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
+      for (int q = 0; q < NQ; ++q)
         if (q < nq) out[adim + 32 * q] = acc[r][q];
     }
   }
@@ -374,7 +375,7 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_dx(
 // ---------------------------------------------------------------------------
 // Backward dE: block = 32 items, loops over all rows (ascending row tiles).
 // ---------------------------------------------------------------------------
-template <class T>
+template <class T, int NQ>
 __global__ void __launch_bounds__(kThreads) cce_simt_bwd_de(
     const T* __restrict__ X, const T* __restrict__ E, const int64_t* __restrict__ targets,
     const double* __restrict__ lse, int64_t n, int D, int64_t v, int64_t v_offset, T scale,
@@ -392,11 +393,11 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_de(
   // dims (tid % 32) + 32 q (conflict-free X reads).
   const int aitem = (threadIdx.x / 32) * 4, adim = threadIdx.x % 32;
   const int nq = (D - adim + 31) / 32;
-  T acc[4][8];
+  T acc[4][NQ];
 #pragma unroll
   for (int r = 0; r < 4; ++r)
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc[r][q] = T(0);
+    for (int q = 0; q < NQ; ++q) acc[r][q] = T(0);
   unsigned skips = 0;
 
   for (int64_t r0 = 0; r0 < n; r0 += R) {
@@ -425,16 +426,16 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_de(
       // four rows per step (16-byte X reads; a row past rn has G = 0 and a
       // zero-staged X row, adding exact zeros)
       for (int i = 0; i < rn; i += 4) {
-        T gv[4][4], xv[8][4];
+        T gv[4][4], xv[NQ][4];
 #pragma unroll
         for (int ii = 0; ii < 4; ++ii) ld4(Gs + (i + ii) * GS + aitem, gv[ii]);
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
+        for (int q = 0; q < NQ; ++q)
           if (q < nq) ld4(Xs + (adim + 32 * q) * (R + PAD) + i, xv[q]);
 #pragma unroll
         for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
+          for (int q = 0; q < NQ; ++q)
             if (q < nq) {
 #pragma unroll
               for (int r = 0; r < 4; ++r) acc[r][q] = fma_acc(acc[r][q], gv[ii][r], xv[q][ii]);
@@ -445,7 +446,7 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_de(
         T gv[4];
         ld4(Gs + i * GS + aitem, gv);
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
+        for (int q = 0; q < NQ; ++q)
           if (q < nq) {
             const T xv = Xs[(adim + 32 * q) * (R + PAD) + i];
 #pragma unroll
@@ -459,7 +460,7 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_de(
     const int64_t item = c0 + aitem + r;
     if (item < v) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
+      for (int q = 0; q < NQ; ++q)
         if (q < nq) dE[item * D + adim + 32 * q] = acc[r][q];
     }
   }
@@ -553,6 +554,31 @@ static int64_t pick_chunks(int64_t row_tiles, int64_t v, int64_t min_cols) {
   return chunks;
 }
 
+// V chunks for a (row tiles x chunks) grid: the count in [1, max_chunks]
+// (chunks of at least min_cols columns) that minimises the per-SM serial work
+// waves(P) / P, waves = ceil(rt P / (SMs x resident blocks)) — a second
+// wave that is mostly empty costs as much as a full one.
+template <class K>
+static int64_t balanced_chunks(K kernel, size_t smem, int64_t rt, int64_t v, int64_t min_cols,
+                               int64_t max_chunks) {
+  int per_sm = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  const int64_t slots = static_cast<int64_t>(per_sm) * num_sms();
+  const int64_t hi = std::max<int64_t>(1, std::min<int64_t>(max_chunks, ceil_div(v, min_cols)));
+  int64_t best = 1;
+  double best_cost = 1e300;
+  for (int64_t P = 1; P <= hi; ++P) {
+    const double cost = static_cast<double>(ceil_div(rt * P, slots)) / static_cast<double>(P);
+    if (cost < best_cost * (1.0 - 1e-9)) {
+      best_cost = cost;
+      best = P;
+    }
+  }
+  return best;
+}
+
 template <class T>
 int simt_cce_forward(const T* X, const T* E, const int64_t* targets, int64_t n, int D,
                      int64_t v, int64_t v_offset, Partial<T>** part_out, int* P_out,
@@ -562,7 +588,7 @@ int simt_cce_forward(const T* X, const T* E, const int64_t* targets, int64_t n, 
   LF_CUDA(cudaFuncSetAttribute(cce_simt_fwd<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem)));
   const int64_t rt = ceil_div(n, Lay<T>::FR);
-  const int64_t chunks = pick_chunks(rt, v, 256);
+  const int64_t chunks = balanced_chunks(cce_simt_fwd<T>, smem, rt, v, 256, 64);
   const int64_t chunk = ceil_div(ceil_div(v, chunks), Lay<T>::FC) * Lay<T>::FC;
   const int64_t P = ceil_div(v, chunk);
   int rc = ws.alloc(sizeof(Partial<T>) * P * n, st);
@@ -629,19 +655,18 @@ int simt_cce_forward_partial_log2(const T* X, const T* E, const int64_t* targets
   return LF_OK;
 }
 
-template <class T>
-int simt_cce_backward(const T* X, const T* E, const int64_t* targets, const double* lse, double scale,
-                      double eps, int64_t n, int D, int64_t v, int64_t v_offset, T* dX, T* dE,
-                      unsigned long long* skip_counter, cudaStream_t st) {
-  const size_t sdx = dx_smem<T>(D), sde = de_smem<T>(D);
-  if (sdx > 227 * 1024 || sde > 227 * 1024) return fail(LF_EUNSUPPORTED, "simt backward: d too large");
-  if (D > 256) return fail(LF_EUNSUPPORTED, "simt backward: d > 256");
-  LF_CUDA(cudaFuncSetAttribute(cce_simt_bwd_dx<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+template <class T, int NQ>
+static int simt_backward_nq(const T* X, const T* E, const int64_t* targets, const double* lse, double scale,
+                            double eps, int64_t n, int D, int64_t v, int64_t v_offset, T* dX, T* dE,
+                            unsigned long long* skip_counter, size_t sdx, size_t sde, cudaStream_t st) {
+  LF_CUDA(cudaFuncSetAttribute(cce_simt_bwd_dx<T, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(sdx)));
-  LF_CUDA(cudaFuncSetAttribute(cce_simt_bwd_de<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  LF_CUDA(cudaFuncSetAttribute(cce_simt_bwd_de<T, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(sde)));
   const int64_t rt = ceil_div(n, Lay<T>::XR);
-  int64_t chunks = std::min<int64_t>(pick_chunks(rt, v, 1024), 8);
+  // dX partials: P x n x D of scratch, so at most 16 chunks (8 past 64 MB)
+  const int64_t max_p = sizeof(T) * 16 * n * D <= (int64_t(64) << 20) ? 16 : 8;
+  const int64_t chunks = balanced_chunks(cce_simt_bwd_dx<T, NQ>, sdx, rt, v, 1024, max_p);
   const int64_t chunk = ceil_div(ceil_div(v, chunks), Lay<T>::XC) * Lay<T>::XC;
   const int64_t P = ceil_div(v, chunk);
   Scratch ws;
@@ -652,7 +677,7 @@ int simt_cce_backward(const T* X, const T* E, const int64_t* targets, const doub
     part = ws.as<T>();
   }
   ProfScope prof(LF_K_CCE_SIMT, st);
-  cce_simt_bwd_dx<T><<<dim3(rt, P), kThreads, sdx, st>>>(X, E, targets, lse, n, D, v, v_offset,
+  cce_simt_bwd_dx<T, NQ><<<dim3(rt, P), kThreads, sdx, st>>>(X, E, targets, lse, n, D, v, v_offset,
                                                         chunk, T(scale), T(eps), part,
                                                         skip_counter);
   LF_LAUNCHED();
@@ -661,10 +686,29 @@ int simt_cce_backward(const T* X, const T* E, const int64_t* targets, const doub
         part, static_cast<int>(P), n * D, dX);
     LF_LAUNCHED();
   }
-  cce_simt_bwd_de<T><<<ceil_div(v, Lay<T>::EC), kThreads, sde, st>>>(X, E, targets, lse, n, D, v,
+  cce_simt_bwd_de<T, NQ><<<ceil_div(v, Lay<T>::EC), kThreads, sde, st>>>(X, E, targets, lse, n, D, v,
                                                            v_offset, T(scale), T(eps), dE);
   LF_LAUNCHED();
   return LF_OK;
+}
+
+
+template <class T>
+int simt_cce_backward(const T* X, const T* E, const int64_t* targets, const double* lse, double scale,
+                      double eps, int64_t n, int D, int64_t v, int64_t v_offset, T* dX, T* dE,
+                      unsigned long long* skip_counter, cudaStream_t st) {
+  const size_t sdx = dx_smem<T>(D), sde = de_smem<T>(D);
+  if (sdx > 227 * 1024 || sde > 227 * 1024) return fail(LF_EUNSUPPORTED, "simt backward: d too large");
+  if (D > 256) return fail(LF_EUNSUPPORTED, "simt backward: d > 256");
+  const int nq = (D + 31) / 32;
+  return nq <= 1 ? simt_backward_nq<T, 1>(X, E, targets, lse, scale, eps, n, D, v, v_offset, dX, dE,
+                                           skip_counter, sdx, sde, st)
+       : nq <= 2 ? simt_backward_nq<T, 2>(X, E, targets, lse, scale, eps, n, D, v, v_offset, dX, dE,
+                                           skip_counter, sdx, sde, st)
+       : nq <= 4 ? simt_backward_nq<T, 4>(X, E, targets, lse, scale, eps, n, D, v, v_offset, dX, dE,
+                                           skip_counter, sdx, sde, st)
+                 : simt_backward_nq<T, 8>(X, E, targets, lse, scale, eps, n, D, v, v_offset, dX, dE,
+                                           skip_counter, sdx, sde, st);
 }
 
 // ---------------------------------------------------------------------------
