@@ -772,6 +772,14 @@ def cfg1_record(lf, flush, stream, args, cpu):
                        f"(make_instance seed {SEED1:#x})",
            "value": N1 / (ms / 1e3), "unit": "positions/s", "ms_per_step": ms, "steps": args.steps,
            "path": "lf_cce_forward + lf_cce_backward (fp32 SIMT kernels)", "kernel_ms_per_step": kern}
+    # fp32 FMA roofline: algorithmic 8 N V D flops (fwd 2, dX 2 + recompute 2,
+    # dE 2; the SIMT path executes 10 N V D: one more logit recompute) against
+    # the nominal CUDA-core fp32 rate (148 SMs x 128 lanes x 2 flop x max clock)
+    peak32 = 148 * 128 * 2 * 1.965e9 / 1e12
+    ach32 = 8.0 * N1 * V1 * D / (ms / 1e3) / 1e12
+    rec["roofline"] = {"bound": "fp32 FMA (CUDA cores)", "achieved": ach32, "peak": peak32, "unit": "TFLOP/s",
+                       "frac": ach32 / peak32, "traffic": None,
+                       "peak_source": "nominal: 148 SMs x 128 FP32 lanes x 2 x 1.965 GHz (no measured fp32 peak)"}
     o, r = box[0]
     if cpu:
         sys.path.insert(0, os.path.join(ROOT, "tests"))
