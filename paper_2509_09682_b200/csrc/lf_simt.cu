@@ -311,16 +311,25 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_dx(
     __syncthreads();
     T o[M::RPT][M::CPT];
     M::logits(Xs, Es, D, o);
+    T gt[M::RPT][M::CPT];
 #pragma unroll
     for (int i = 0; i < M::RPT; ++i)
 #pragma unroll
       for (int q = 0; q < M::CPT; ++q) {
         const int64_t col = c0 + M::col(q);
         const bool valid = col < c_end && (r0 + M::row(i)) < n;
-        T g = T(0);
-        if (valid) g = coeff(o[i][q], row_lse[i], col == tgt[i], eps, scale, skips);
-        Gs[M::col(q) * GS + M::row(i)] = g;
+        gt[i][q] = valid ? coeff(o[i][q], row_lse[i], col == tgt[i], eps, scale, skips) : T(0);
       }
+#pragma unroll
+    for (int q = 0; q < M::CPT; ++q) {
+      if constexpr (M::kVec) {  // the thread's four rows of column q: one 16-byte store
+        *reinterpret_cast<float4*>(Gs + M::col(q) * GS + M::row(0)) =
+            make_float4(gt[0][q], gt[1][q], gt[2][q], gt[3][q]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < M::RPT; ++i) Gs[M::col(q) * GS + M::row(i)] = gt[i][q];
+      }
+    }
     __syncthreads();
     const int cn = static_cast<int>((c_end - c0 < C ? c_end - c0 : C));
     if constexpr (PAD == 4) {
@@ -412,12 +421,17 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_de(
       const bool rvalid = row < n;
       const T rl = rvalid ? static_cast<T>(lse[row]) : T(0);
       const int64_t tg = rvalid ? targets[row] - v_offset : -1;
+      T gt[M::CPT];
 #pragma unroll
       for (int q = 0; q < M::CPT; ++q) {
         const int64_t col = c0 + M::col(q);
-        T g = T(0);
-        if (rvalid && col < v) g = coeff(o[i][q], rl, col == tg, eps, scale, skips);
-        Gs[M::row(i) * GS + M::col(q)] = g;
+        gt[q] = rvalid && col < v ? coeff(o[i][q], rl, col == tg, eps, scale, skips) : T(0);
+      }
+      if constexpr (M::kVec) {  // four consecutive items of row i: one 16-byte store
+        *reinterpret_cast<float4*>(Gs + M::row(i) * GS + M::col(0)) = make_float4(gt[0], gt[1], gt[2], gt[3]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < M::CPT; ++q) Gs[M::row(i) * GS + M::col(q)] = gt[q];
       }
     }
     __syncthreads();
