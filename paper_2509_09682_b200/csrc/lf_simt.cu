@@ -23,6 +23,10 @@ namespace lf {
 namespace {
 
 constexpr int kThreads = 256;
+#ifndef LF_SIMT_KUNROLL
+#define LF_SIMT_KUNROLL 4  // logit tiles: k steps unrolled (shared-memory reads issued ahead of the FMAs)
+#endif
+constexpr int kKUnroll = LF_SIMT_KUNROLL;
 
 template <class T>
 __device__ __forceinline__ T mul_rn(T a, T b) { return a * b; }
@@ -122,6 +126,7 @@ struct TileMap {
     for (int i = 0; i < RPT; ++i)
 #pragma unroll
       for (int q = 0; q < CPT; ++q) o[i][q] = T(0);
+#pragma unroll kKUnroll
     for (int k = 0; k < D; ++k) {
       T xv[RPT], ev[CPT];
       if constexpr (kVec) {
