@@ -72,6 +72,9 @@
 #ifndef LF_NWG_EVAL
 #define LF_NWG_EVAL 2
 #endif
+#ifndef LF_BN_EVAL
+#define LF_BN_EVAL 128  // EVAL stream tile (64: eight S buffers; the target-rows tile then spans two tiles)
+#endif
 #ifndef LF_BWD_LD64
 #define LF_BWD_LD64 0  // backward: 64-column TMEM loads (two chunks), no prefetch
 #endif
@@ -188,7 +191,7 @@ template <int MODE, int D = 64>
 struct Geo {
   static constexpr int BN = MODE == FWD    ? LF_BN_FWD
                             : MODE == FWDX ? bn_fwdx(D)
-                            : MODE == EVAL ? 128
+                            : MODE == EVAL ? LF_BN_EVAL
                             : MODE == BWD_ITEMS ? bn_items(D)
                                                 : LF_BN_BWD;  // stream tile
   static constexpr int NWG = MODE == FWD    ? LF_NWG_FWD
@@ -601,14 +604,18 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
                       static_cast<int32_t>(ot * BM), pol);
         if (MODE == BWD_ITEMS) tma_load_2d(ones_smem, &map_ones, owner_full, 0, 0, pol);
         if (MODE == EVAL) {
-          // the owner rows' own target items (gathered, row-aligned with the owner tile)
-          unsigned char* stg = stage_smem + rs.i * C::kStageBytes;
-          mbar_wait(&empty[rs.i], rs.ph ^ 1);
-          mbar_arrive_expect_tx(&full[rs.i], C::kTileBytes);
+          // the owner rows' own target items (gathered, row-aligned with the
+          // owner tile), BN rows per tile: BM / BN tiles
+          for (int h = 0; h < BM / BN; ++h) {
+            unsigned char* stg = stage_smem + rs.i * C::kStageBytes;
+            mbar_wait(&empty[rs.i], rs.ph ^ 1);
+            mbar_arrive_expect_tx(&full[rs.i], C::kTileBytes);
 #pragma unroll
-          for (int a = 0; a < C::kAtoms; ++a)
-            tma_load_2d(stg + a * BN * 128, &map_lsex, &full[rs.i], a * 64, static_cast<int32_t>(ot * BM), pol);
-          rs.next();
+            for (int a = 0; a < C::kAtoms; ++a)
+              tma_load_2d(stg + a * BN * 128, &map_lsex, &full[rs.i], a * 64,
+                          static_cast<int32_t>(ot * BM + h * BN), pol);
+            rs.next();
+          }
         }
         for (int64_t s0 = s_begin; s0 < s_end; s0 += BN, rs.next()) {
           unsigned char* stg = stage_smem + rs.i * C::kStageBytes;
@@ -648,7 +655,7 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
       const int64_t chunk = U.chunk(u);
       const int64_t s_begin = chunk * p.chunk;
       const int64_t s_end = min(p.n_stream, s_begin + p.chunk);
-      const int ntile = static_cast<int>(ceil_div(s_end - s_begin, BN)) + (MODE == EVAL ? 1 : 0);
+      const int ntile = static_cast<int>(ceil_div(s_end - s_begin, BN)) + (MODE == EVAL ? BM / BN : 0);
       mbar_wait(owner_full, j & 1);
       tc_fence_after();
       for (int i = 0; i < ntile; ++i, s1.next(), b1.next()) {
@@ -825,7 +832,7 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
           ki[k] = 0x7fffffff;
         }
       }
-      constexpr int kPre = MODE == EVAL ? 1 : 0;  // EVAL: the target-rows tile comes first
+      constexpr int kPre = MODE == EVAL ? BM / BN : 0;  // EVAL: the target-rows tile(s) come first
       const int64_t i_first =
           MODE == EVAL ? 0 : static_cast<int64_t>((static_cast<uint32_t>(wg) + NWG - T0 % NWG) % NWG);
       // The loop's end test doubles as the BWD_ITEMS hit test: lim = the end
@@ -869,6 +876,35 @@ __global__ void __launch_bounds__(Geo<MODE, D>::kThreads, 1)
         const uint32_t T = T0 + static_cast<uint32_t>(i);
         const int tw = static_cast<int>(T % NWG);
         const uint32_t rbi = T % C::kNB, rbph = (T / C::kNB) & 1u;
+        if (MODE == EVAL && kPre > 1 && i < kPre) {
+          // BN < BM: target columns i BN .. i BN + BN - 1 in tile i; the warps
+          // whose rows lie there read their diagonal, every warp of the owner
+          // releases the buffer, and after the last such tile all epilogue
+          // threads meet once (same double buffering by unit parity).
+          float* st_sh = reinterpret_cast<float*>(merge) + (NWG - 1) * BM * C::kEvalStride + (j & 1) * BM;
+          if (tw == wg) {
+            const int b = static_cast<int>(rbi);
+            mbar_wait(&s_full[b], rbph);
+            tc_fence_after();
+            const int c = quad * 32 - static_cast<int>(i) * BN;  // this warp's diagonal column
+            if (c >= 0 && c < BN) {
+              float d[32];
+              LF_TMEM_LD32(tmem + lane_base + b * BN + c, reinterpret_cast<uint32_t*>(d));
+              tmem_ld_wait();
+              st_sh[lrow] = select_reg(d, lane);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[b]);
+          }
+          if (i + 1 == kPre) {
+            named_bar_sync(2, G::kEpiThreads);
+            st = st_sh[lrow];
+            st_dn = next_down(st);
+            cnt_fma = __all_sync(0xffffffffu, fabsf(st) >= 0x1p-60f && fabsf(st) < 0x1p27f);
+          }
+          continue;
+        }
         if (MODE == EVAL && i == 0) {
           // S = owner rows x their target rows: the diagonal is each row's
           // target score, from the same MMA as the scores it is compared with.
@@ -2202,7 +2238,7 @@ int tc_eval_partials(const void* X, const void* E, const void* Et, const int32_t
   CUtensorMap mo, ms, mt;
   rc = make_map(&mo, X, n, D, BM);
   if (!rc) rc = make_map(&ms, E, v, D, BN);
-  if (!rc) rc = make_map(&mt, Et, owner_tiles * BM, D, BM);
+  if (!rc) rc = make_map(&mt, Et, owner_tiles * BM, D, BN);
   if (rc) return rc;
   TcParams p{};
   p.n_owner = n;
