@@ -15,6 +15,10 @@
 #include "lf_internal.cuh"
 #include "lf_kernels.cuh"
 
+#ifndef LF_SIMT_FUSED
+#define LF_SIMT_FUSED 1  // fp32 lf_cce_forward_backward with the filter off: fused SIMT forward + dX
+#endif
+
 namespace lf {
 
 namespace {
@@ -295,6 +299,22 @@ int lf_cce_forward_backward(const void* d_X, const void* d_E, const int64_t* d_t
   if (!rc) rc = check_shapes(n, d, v);
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
+  if (cfg->dtype == LF_F32 && cfg->filter_eps == 0.0 && !(cfg->flags & LF_FLAG_FILTER_DX) &&
+      LF_SIMT_FUSED) {
+    // fp32, filter off: the fused SIMT forward + dX, then the dE pass (no
+    // entry is filtered, so the skip counts are zero)
+    if (!d_lse || !d_pos || !d_dX || !d_dE) return fail(LF_EINVAL, "cce_forward_backward: null output");
+    rc = simt_cce_fused_f32(static_cast<const float*>(d_X), static_cast<const float*>(d_E), d_targets, n,
+                            static_cast<int>(d), v, upstream / static_cast<double>(n), 0.0, d_lse, d_pos,
+                            d_loss, static_cast<float*>(d_dX), static_cast<float*>(d_dE), st);
+    if (rc) return rc;
+    if (stats) {
+      Counters c;
+      rc = c.init(st);
+      if (!rc) rc = read_stats(c, stats, n, v, st);
+    }
+    return rc;
+  }
   if (!lf_cce_fused_supported(cfg, d)) {
     rc = lf_cce_forward(d_X, d_E, d_targets, n, d, v, cfg, d_lse, d_pos, d_loss, stream);
     if (rc) return rc;

@@ -29,6 +29,12 @@ int simt_cce_backward(const T* X, const T* E, const int64_t* targets, const doub
                       double scale, double eps, int64_t n, int D, int64_t v, int64_t v_offset,
                       T* dX, T* dE, unsigned long long* skip_counter, cudaStream_t st);
 
+// Fused forward + dX (fp32, filter off) then the dE pass: lse, pos, loss
+// (optional), dX, dE in one call (lf_cce_forward_backward).
+int simt_cce_fused_f32(const float* X, const float* E, const int64_t* targets, int64_t n, int D, int64_t v,
+                       double scale, double eps, double* lse, double* pos, double* loss, float* dX, float* dE,
+                       cudaStream_t st);
+
 int launch_combine_f32log2(const float* part, int P, int64_t n, double* lse, double* pos,
                            double* loss, cudaStream_t st);
 int launch_reduce_f32(const float* part, int P, int64_t count, float* out, cudaStream_t st);

@@ -393,7 +393,10 @@ template <class T, int NQ>
 __global__ void __launch_bounds__(kThreads) cce_simt_bwd_de(
     const T* __restrict__ X, const T* __restrict__ E, const int64_t* __restrict__ targets,
     const double* __restrict__ lse, int64_t n, int D, int64_t v, int64_t v_offset, T scale,
-    T eps, T* __restrict__ dE) {
+    T eps, T* __restrict__ dE, const double* __restrict__ omp = nullptr) {
+  // omp (optional, the fused fp32 forward's): 1 - p_t per row in full
+  // precision, so a target entry is -(1 - p_t) scale even where exp(o - lse)
+  // rounds to 1 (well-fit rows)
   constexpr int R = Lay<T>::ER, C = Lay<T>::EC, PAD = Lay<T>::PAD;
   using M = LayMap<T, R, C>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -431,6 +434,7 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_de(
       for (int q = 0; q < M::CPT; ++q) {
         const int64_t col = c0 + M::col(q);
         gt[q] = rvalid && col < v ? coeff(o[i][q], rl, col == tg, eps, scale, skips) : T(0);
+        if (omp && rvalid && col == tg) gt[q] = static_cast<T>(-omp[row] * static_cast<double>(scale));
       }
       if constexpr (M::kVec) {  // four consecutive items of row i: one 16-byte store
         *reinterpret_cast<float4*>(Gs + M::row(i) * GS + M::col(0)) = make_float4(gt[0], gt[1], gt[2], gt[3]);
@@ -485,6 +489,195 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_de(
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Fused forward + dX, fp32 (lf_cce_forward_backward with the filter off): one
+// pass over the logits instead of the forward and the dX recompute.  Block =
+// 32 rows x one V chunk on the fp32 4 x 4 tile map, so warp w owns rows
+// 4w..4w+3 of every tile — in the logits and in the dX accumulation alike —
+// and keeps their running max warp-uniform: per tile, P = exp(o - M) (the
+// target entry left out, as in the tensor-core read-out form), the row sums
+// and the O accumulator (O_i = sum_j P_ij E_j) are rescaled by exp(M_old -
+// M_new).  Output per (chunk, row): Partial {M, S, t, has} + the O row; the
+// combine below normalises dX = scale (sum_p O_p e^(M_p - lse) - (1 - p_t) E_t).
+// ---------------------------------------------------------------------------
+template <int NQ>
+__global__ void __launch_bounds__(kThreads) cce_simt_fwdx(const float* __restrict__ X,
+                                                          const float* __restrict__ E,
+                                                          const int64_t* __restrict__ targets,
+                                                          int64_t n, int D, int64_t v, int64_t chunk,
+                                                          Partial<float>* __restrict__ part,
+                                                          float* __restrict__ sxpart,
+                                                          float* __restrict__ opart) {
+  using L = Lay<float>;
+  constexpr int R = L::XR, C = L::XC, PAD = L::PAD;
+  using M = LayMap<float, R, C>;
+  static_assert(M::kVec && M::CG == 32, "a warp owns four whole rows of the tile");
+  constexpr int GS = gstride(R);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* Xs = reinterpret_cast<float*>(smem_raw);
+  float* Es = Xs + D * (R + PAD);
+  float* Gs = Xs + align16<float>(static_cast<size_t>(D) * (R + PAD + C + PAD));  // [C][GS]
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * R;
+  const int64_t c_begin = static_cast<int64_t>(blockIdx.y) * chunk;
+  const int64_t c_end = min(v, c_begin + chunk);
+  stage_T<float, R, PAD>(Xs, X, r0, n, D);
+  const int lane = threadIdx.x % 32, wr = (threadIdx.x / 32) * 4;  // == M::row(0)
+  int64_t tgt[4];
+  float mx[4], sm[4], sx[4], tv[4], has[4];  // sx: the row sum without the target entry
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t row = r0 + wr + i;
+    tgt[i] = row < n ? targets[row] : -1;
+    mx[i] = -INFINITY;
+    sm[i] = 0.f;
+    sx[i] = 0.f;
+    tv[i] = 0.f;
+    has[i] = 0.f;
+  }
+  const int nq = (D - lane + 31) / 32;
+  float acc[4][NQ];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) acc[r][q] = 0.f;
+
+  for (int64_t c0 = c_begin; c0 < c_end; c0 += C) {
+    __syncthreads();
+    stage_T<float, C, PAD>(Es, E, c0, c_end, D);
+    __syncthreads();
+    float o[4][4];
+    M::logits(Xs, Es, D, o);
+    float alpha[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float tm = -INFINITY;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (c0 + M::col(q) >= c_end) o[i][q] = -INFINITY;
+        tm = fmaxf(tm, o[i][q]);
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, off));
+      const float nm = fmaxf(mx[i], tm);  // finite: every tile has a valid column
+      alpha[i] = mx[i] == -INFINITY ? 0.f : expf(mx[i] - nm);
+      mx[i] = nm;
+    }
+    float pe[4][4];  // P with the target entry left out
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float ps = 0.f, pxs = 0.f;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float pv = expf(o[i][q] - mx[i]);  // 0 for a masked column
+        ps += pv;
+        const bool t = c0 + M::col(q) == tgt[i];
+        if (t) {
+          tv[i] = o[i][q];
+          has[i] = 1.f;
+        }
+        pe[i][q] = t ? 0.f : pv;
+        pxs += pe[i][q];
+      }
+      sm[i] = sm[i] * alpha[i] + ps;
+      sx[i] = sx[i] * alpha[i] + pxs;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      *reinterpret_cast<float4*>(Gs + M::col(q) * GS + wr) = make_float4(pe[0][q], pe[1][q], pe[2][q], pe[3][q]);
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) acc[r][q] *= alpha[r];
+    const int cn = static_cast<int>((c_end - c0 < C ? c_end - c0 : C));
+    for (int j = 0; j < cn; j += 4) {
+      float gv[4][4], ev[NQ][4];
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) ld4(Gs + (j + jj) * GS + wr, gv[jj]);
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+        if (q < nq) ld4(Es + (lane + 32 * q) * (C + PAD) + j, ev[q]);
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+          if (q < nq) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) acc[r][q] = fmaf(gv[jj][r], ev[q][jj], acc[r][q]);
+          }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float si = sm[i], xi = sx[i];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      si += __shfl_xor_sync(0xffffffffu, si, off);
+      xi += __shfl_xor_sync(0xffffffffu, xi, off);
+    }
+    const unsigned hb = __ballot_sync(0xffffffffu, has[i] != 0.f);
+    const float ti = __shfl_sync(0xffffffffu, tv[i], hb ? __ffs(hb) - 1 : 0);
+    const int64_t row = r0 + wr + i;
+    if (row < n) {
+      if (lane == 0) {
+        Partial<float> pp;
+        pp.m = mx[i];
+        pp.s = si;
+        pp.t = hb ? ti : 0.f;
+        pp.has = hb ? 1.f : 0.f;
+        part[static_cast<int64_t>(blockIdx.y) * n + row] = pp;
+        sxpart[static_cast<int64_t>(blockIdx.y) * n + row] = xi;
+      }
+      float* out = opart + (static_cast<int64_t>(blockIdx.y) * n + row) * D;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+        if (q < nq) out[lane + 32 * q] = acc[i][q];
+    }
+  }
+}
+
+// Warp per row: lse / pos from the chunk partials, then dX (see above).
+// lse = t + log1p(Sx / e^(t - M)) and 1 - p_t = Sx / (e^(t - M) + Sx) from the
+// sum without the target (Sx), so both keep full precision when the target
+// dominates the row (a total sum rounded to e^(t - M) would lose them).
+__global__ void simt_fwdx_combine(const Partial<float>* __restrict__ part, const float* __restrict__ sxpart,
+                                  const float* __restrict__ opart, int P, int64_t n, int D,
+                                  const float* __restrict__ E, const int64_t* __restrict__ targets,
+                                  double scale, double* __restrict__ lse, double* __restrict__ pos,
+                                  double* __restrict__ omp_out, float* __restrict__ dX) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= n) return;
+  double Mx = -INFINITY;
+  for (int p = 0; p < P; ++p) Mx = fmax(Mx, static_cast<double>(part[p * n + row].m));
+  double Sx = 0.0, t = 0.0;
+  bool found = false;
+  for (int p = 0; p < P; ++p) {
+    const Partial<float> q = part[p * n + row];
+    Sx += static_cast<double>(sxpart[p * n + row]) * exp(static_cast<double>(q.m) - Mx);
+    if (q.has != 0.f) {
+      t = q.t;
+      found = true;
+    }
+  }
+  const double St = found ? exp(t - Mx) : 0.0;  // the target's own term
+  const double l = found ? t + log1p(Sx / St) : Mx + log(Sx);
+  const double omp = found ? Sx / (St + Sx) : 1.0;  // 1 - p_t
+  if (lane == 0) {
+    lse[row] = l;
+    pos[row] = t;
+    omp_out[row] = omp;
+  }
+  const float* et = E + targets[row] * D;
+  for (int k = lane; k < D; k += 32) {
+    double acc = 0.0;
+    for (int p = 0; p < P; ++p)
+      acc += static_cast<double>(opart[(static_cast<int64_t>(p) * n + row) * D + k]) *
+             exp(static_cast<double>(part[p * n + row].m) - l);
+    dX[row * D + k] = static_cast<float>(scale * (acc - omp * static_cast<double>(et[k])));
+  }
+}
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -728,6 +921,63 @@ int simt_cce_backward(const T* X, const T* E, const int64_t* targets, const doub
                                            skip_counter, sdx, sde, st)
                  : simt_backward_nq<T, 8>(X, E, targets, lse, scale, eps, n, D, v, v_offset, dX, dE,
                                            skip_counter, sdx, sde, st);
+}
+
+template <int NQ>
+static int simt_fused_nq(const float* X, const float* E, const int64_t* targets, int64_t n, int D, int64_t v,
+                         double scale, double eps, double* lse, double* pos, double* loss, float* dX, float* dE,
+                         cudaStream_t st) {
+  const size_t sfx = dx_smem<float>(D), sde = de_smem<float>(D);
+  LF_CUDA(cudaFuncSetAttribute(cce_simt_fwdx<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(sfx)));
+  LF_CUDA(cudaFuncSetAttribute(cce_simt_bwd_de<float, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(sde)));
+  const int64_t rt = ceil_div(n, Lay<float>::XR);
+  // O partials: P x n x D floats, so at most 16 chunks (8 past 64 MB)
+  const int64_t max_p = sizeof(float) * 16 * n * D <= (int64_t(64) << 20) ? 16 : 8;
+  const int64_t chunks = balanced_chunks(cce_simt_fwdx<NQ>, sfx, rt, v, 1024, max_p);
+  const int64_t chunk = ceil_div(ceil_div(v, chunks), Lay<float>::XC) * Lay<float>::XC;
+  const int64_t P = ceil_div(v, chunk);
+  Scratch omp;
+  int rc = omp.alloc(sizeof(double) * n, st);
+  if (rc) return rc;
+  {
+    Scratch part, sxpart, opart;
+    rc = part.alloc(sizeof(Partial<float>) * P * n, st);
+    if (!rc) rc = sxpart.alloc(sizeof(float) * P * n, st);
+    if (!rc) rc = opart.alloc(sizeof(float) * P * n * D, st);
+    if (rc) return rc;
+    ProfScope prof(LF_K_CCE_SIMT, st);
+    cce_simt_fwdx<NQ><<<dim3(rt, P), kThreads, sfx, st>>>(X, E, targets, n, D, v, chunk,
+                                                         part.as<Partial<float>>(), sxpart.as<float>(),
+                                                         opart.as<float>());
+    LF_LAUNCHED();
+    simt_fwdx_combine<<<ceil_div(n, 8), 256, 0, st>>>(part.as<Partial<float>>(), sxpart.as<float>(),
+                                                      opart.as<float>(), static_cast<int>(P), n, D, E,
+                                                      targets, scale, lse, pos, omp.as<double>(), dX);
+    LF_LAUNCHED();
+    if (loss) {
+      rc = launch_mean_loss(lse, pos, n, loss, st);
+      if (rc) return rc;
+    }
+  }  // the O partials go back to the pool before the dE pass
+  ProfScope prof(LF_K_CCE_SIMT, st);
+  cce_simt_bwd_de<float, NQ><<<ceil_div(v, Lay<float>::EC), kThreads, sde, st>>>(
+      X, E, targets, lse, n, D, v, 0, static_cast<float>(scale), static_cast<float>(eps), dE, omp.as<double>());
+  LF_LAUNCHED();
+  return LF_OK;
+}
+
+int simt_cce_fused_f32(const float* X, const float* E, const int64_t* targets, int64_t n, int D, int64_t v,
+                       double scale, double eps, double* lse, double* pos, double* loss, float* dX, float* dE,
+                       cudaStream_t st) {
+  const size_t sfx = dx_smem<float>(D), sde = de_smem<float>(D);
+  if (D > 256 || sfx > 227 * 1024 || sde > 227 * 1024) return fail(LF_EUNSUPPORTED, "simt fused: d too large");
+  const int nq = (D + 31) / 32;
+  return nq <= 1 ? simt_fused_nq<1>(X, E, targets, n, D, v, scale, eps, lse, pos, loss, dX, dE, st)
+       : nq <= 2 ? simt_fused_nq<2>(X, E, targets, n, D, v, scale, eps, lse, pos, loss, dX, dE, st)
+       : nq <= 4 ? simt_fused_nq<4>(X, E, targets, n, D, v, scale, eps, lse, pos, loss, dX, dE, st)
+                 : simt_fused_nq<8>(X, E, targets, n, D, v, scale, eps, lse, pos, loss, dX, dE, st);
 }
 
 // ---------------------------------------------------------------------------

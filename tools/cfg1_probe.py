@@ -22,9 +22,16 @@ x = torch.from_numpy(t).cuda()
 cfg = lf.CceConfig()
 
 
-def step():
+def step_separate():
     o = lf.cce_forward(X, E, x, cfg, validate=False)
     return o, lf.cce_backward(X, E, x, o.lse, 1.0, cfg, validate=False, stats=False)
+
+
+def step_fused():
+    return lf.cce_forward_backward(X, E, x, 1.0, cfg, validate=False, stats=False)
+
+
+step = step_fused if os.environ.get("CFG1_PATH", "fused") == "fused" else step_separate
 
 
 for _ in range(3):
@@ -38,5 +45,5 @@ for _ in range(iters):
 e.record()
 torch.cuda.synchronize()
 ms = s.elapsed_time(e) / iters
-print(json.dumps({"probe": "cfg1", "ms_per_step": ms, "positions_per_s": n / ms * 1e3,
+print(json.dumps({"probe": "cfg1", "path": os.environ.get("CFG1_PATH", "fused"), "ms_per_step": ms, "positions_per_s": n / ms * 1e3,
                   "tflops_fp32": 8 * n * v * d / ms * 1e-9}))
