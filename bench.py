@@ -748,7 +748,8 @@ def cfg1_record(lf, flush, stream, args, cpu):
     D = 64, V = 32768, filtering off — "bit-for-tolerance vs the CPU oracle".
     The reference itself (oracle/_ref, all host threads) runs the same
     make_instance inputs at full size; the GPU path is the public
-    cce_forward + cce_backward (fp32: the SIMT kernels, exact exp)."""
+    cce_forward_backward (the trainer's pairing, as for cfg2; fp32: the fused
+    SIMT forward + dX, then the dE pass, exact exp)."""
     import numpy as np
     import torch
     from paper_2509_09682_b200 import synth
@@ -762,18 +763,17 @@ def cfg1_record(lf, flush, stream, args, cpu):
 
     def step():
         box[0] = None
-        o = lf.cce_forward(X1, E1, x1, cfg, validate=False)
-        r = lf.cce_backward(X1, E1, x1, o.lse, 1.0, cfg, validate=False, stats=False)
-        box[0] = (o, r)
+        box[0] = lf.cce_forward_backward(X1, E1, x1, 1.0, cfg, validate=False, stats=False)
 
     kern = {}
     ms = timed_steps(step, args.steps, max(3, args.warmup), stream, flush, kern)
     rec = {"workload": f"cfg1: CCE fp32, N={N1} (batch 32 x seq 64), D={D}, V={V1}, filtering off "
                        f"(make_instance seed {SEED1:#x})",
            "value": N1 / (ms / 1e3), "unit": "positions/s", "ms_per_step": ms, "steps": args.steps,
-           "path": "lf_cce_forward + lf_cce_backward (fp32 SIMT kernels)", "kernel_ms_per_step": kern}
-    # fp32 FMA roofline: algorithmic 8 N V D flops (fwd 2, dX 2 + recompute 2,
-    # dE 2; the SIMT path executes 10 N V D: one more logit recompute) against
+           "path": "lf_cce_forward_backward (fp32 SIMT: fused forward + dX, then the dE pass)",
+           "kernel_ms_per_step": kern}
+    # fp32 FMA roofline: algorithmic 8 N V D flops (logits 2 + dX 2 in the
+    # fused pass, logits 2 + dE 2 in the dE pass; executed = algorithmic) against
     # the nominal CUDA-core fp32 rate (148 SMs x 128 lanes x 2 flop x max clock)
     peak32 = 148 * 128 * 2 * 1.965e9 / 1e12
     ach32 = 8.0 * N1 * V1 * D / (ms / 1e3) / 1e12
