@@ -393,7 +393,9 @@ template <class T, int NQ>
 __global__ void __launch_bounds__(kThreads) cce_simt_bwd_de(
     const T* __restrict__ X, const T* __restrict__ E, const int64_t* __restrict__ targets,
     const double* __restrict__ lse, int64_t n, int D, int64_t v, int64_t v_offset, T scale,
-    T eps, T* __restrict__ dE, const double* __restrict__ omp = nullptr) {
+    T eps, T* __restrict__ dE, int64_t rows_per, const double* __restrict__ omp = nullptr) {
+  // rows_per: the rows this block's y-slice sums (gridDim.y > 1: a partial
+  // dE per slice at dE + y v D, reduced afterwards; fp32 only)
   // omp (optional, the fused fp32 forward's): 1 - p_t per row in full
   // precision, so a target entry is -(1 - p_t) scale even where exp(o - lse)
   // rounds to 1 (well-fit rows)
@@ -417,16 +419,19 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_de(
     for (int q = 0; q < NQ; ++q) acc[r][q] = T(0);
   unsigned skips = 0;
 
-  for (int64_t r0 = 0; r0 < n; r0 += R) {
+  const int64_t r_begin = static_cast<int64_t>(blockIdx.y) * rows_per;
+  const int64_t r_end = min(n, r_begin + rows_per);
+  dE += static_cast<int64_t>(blockIdx.y) * v * D;
+  for (int64_t r0 = r_begin; r0 < r_end; r0 += R) {
     __syncthreads();
-    stage_T<T, R, PAD>(Xs, X, r0, n, D);
+    stage_T<T, R, PAD>(Xs, X, r0, r_end, D);
     __syncthreads();
     T o[M::RPT][M::CPT];
     M::logits(Xs, Es, D, o);
 #pragma unroll
     for (int i = 0; i < M::RPT; ++i) {
       const int64_t row = r0 + M::row(i);
-      const bool rvalid = row < n;
+      const bool rvalid = row < r_end;
       const T rl = rvalid ? static_cast<T>(lse[row]) : T(0);
       const int64_t tg = rvalid ? targets[row] - v_offset : -1;
       T gt[M::CPT];
@@ -444,7 +449,7 @@ __global__ void __launch_bounds__(kThreads) cce_simt_bwd_de(
       }
     }
     __syncthreads();
-    const int rn = static_cast<int>((n - r0 < R ? n - r0 : R));
+    const int rn = static_cast<int>((r_end - r0 < R ? r_end - r0 : R));
     if constexpr (PAD == 4) {
       // four rows per step (16-byte X reads; a row past rn has G = 0 and a
       // zero-staged X row, adding exact zeros)
@@ -867,6 +872,38 @@ int simt_cce_forward_partial_log2(const T* X, const T* E, const int64_t* targets
   return LF_OK;
 }
 
+// The dE pass: one block per 32 items over all rows — fp32 splits the rows
+// into Q slices when that fills the SMs' last wave better (partial dE per
+// slice, then a fixed-order sum); fp64 keeps one slice (reference order).
+template <class T, int NQ>
+static int launch_de(const T* X, const T* E, const int64_t* targets, const double* lse, int64_t n, int D,
+                     int64_t v, int64_t v_offset, T scale, T eps, T* dE, size_t sde, const double* omp,
+                     cudaStream_t st) {
+  constexpr int R = Lay<T>::ER;
+  const int64_t blocks = ceil_div(v, Lay<T>::EC);
+  int64_t Q = 1;
+  if (sizeof(T) == 4 && sizeof(T) * 4 * v * D <= (int64_t(256) << 20))
+    Q = balanced_chunks(cce_simt_bwd_de<T, NQ>, sde, blocks, n, R, 4);
+  const int64_t rows_per = ceil_div(ceil_div(n, R), Q) * R;
+  Q = ceil_div(n, rows_per);
+  Scratch part;
+  T* out = dE;
+  if (Q > 1) {
+    const int rc = part.alloc(sizeof(T) * Q * v * D, st);
+    if (rc) return rc;
+    out = part.as<T>();
+  }
+  cce_simt_bwd_de<T, NQ><<<dim3(blocks, Q), kThreads, sde, st>>>(X, E, targets, lse, n, D, v, v_offset, scale,
+                                                                  eps, out, rows_per, omp);
+  LF_LAUNCHED();
+  if (Q > 1) {
+    reduce_chunks<T, T><<<std::min<int64_t>(ceil_div(v * D, 256), 4 * num_sms()), 256, 0, st>>>(
+        out, static_cast<int>(Q), v * D, dE);
+    LF_LAUNCHED();
+  }
+  return LF_OK;
+}
+
 template <class T, int NQ>
 static int simt_backward_nq(const T* X, const T* E, const int64_t* targets, const double* lse, double scale,
                             double eps, int64_t n, int D, int64_t v, int64_t v_offset, T* dX, T* dE,
@@ -898,10 +935,7 @@ static int simt_backward_nq(const T* X, const T* E, const int64_t* targets, cons
         part, static_cast<int>(P), n * D, dX);
     LF_LAUNCHED();
   }
-  cce_simt_bwd_de<T, NQ><<<ceil_div(v, Lay<T>::EC), kThreads, sde, st>>>(X, E, targets, lse, n, D, v,
-                                                           v_offset, T(scale), T(eps), dE);
-  LF_LAUNCHED();
-  return LF_OK;
+  return launch_de<T, NQ>(X, E, targets, lse, n, D, v, v_offset, T(scale), T(eps), dE, sde, nullptr, st);
 }
 
 
@@ -962,10 +996,8 @@ static int simt_fused_nq(const float* X, const float* E, const int64_t* targets,
     }
   }  // the O partials go back to the pool before the dE pass
   ProfScope prof(LF_K_CCE_SIMT, st);
-  cce_simt_bwd_de<float, NQ><<<ceil_div(v, Lay<float>::EC), kThreads, sde, st>>>(
-      X, E, targets, lse, n, D, v, 0, static_cast<float>(scale), static_cast<float>(eps), dE, omp.as<double>());
-  LF_LAUNCHED();
-  return LF_OK;
+  return launch_de<float, NQ>(X, E, targets, lse, n, D, v, 0, static_cast<float>(scale), static_cast<float>(eps),
+                              dE, sde, omp.as<double>(), st);
 }
 
 int simt_cce_fused_f32(const float* X, const float* E, const int64_t* targets, int64_t n, int D, int64_t v,
