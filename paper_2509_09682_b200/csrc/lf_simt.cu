@@ -274,7 +274,7 @@ __device__ __forceinline__ T coeff(T o, T row_lse, bool is_target, T eps, T scal
 // ceil(D / 32): the dims each thread accumulates (register arrays sized to D).
 // ---------------------------------------------------------------------------
 template <class T, int NQ>
-__global__ void __launch_bounds__(kThreads) cce_simt_bwd_dx(
+__global__ void __launch_bounds__(kThreads, NQ <= 2 ? 3 : 1) cce_simt_bwd_dx(
     const T* __restrict__ X, const T* __restrict__ E, const int64_t* __restrict__ targets,
     const double* __restrict__ lse, int64_t n, int D, int64_t v, int64_t v_offset, int64_t chunk,
     T scale, T eps, T* __restrict__ dx_part, unsigned long long* __restrict__ skip_counter) {
