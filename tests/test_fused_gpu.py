@@ -171,7 +171,7 @@ def test_fused_d256_peaked_rows_and_filter(lf):
 
 @pytest.mark.parametrize("n,d,v", [(1, 64, 2), (127, 64, 129), (300, 64, 5000), (2048, 64, 32768),
                                    (257, 32, 3001), (200, 48, 1000), (257, 128, 3000),
-                                   (130, 256, 1000), (100, 96, 70000)])
+                                   (130, 256, 1000), (100, 96, 70000), (100, 30, 2000), (65, 7, 513)])
 def test_fused_f32_equals_oracle(lf, n, d, v):
     """fp32 with the filter off: the fused SIMT forward + dX (lf_simt.cu
     cce_simt_fwdx + simt_fwdx_combine) and the dE pass, against the oracle at
